@@ -1,0 +1,211 @@
+/*
+ * td_api.h — C ABI of the B200-native tensor-comparison hot path.
+ *
+ * The reference (TTrace `traindiff`, pure Python/numpy) has no native
+ * boundary; its hot path sits behind Python functions.  Each entry point
+ * below replaces the arithmetic of one of those functions:
+ *
+ *   td_segnorm   replaces rel_err_arrays' two norms   (pkg/src/traindiff/tensor.py:158-167)
+ *                fused with merge()'s box copies      (pkg/src/traindiff/canonical.py:182-212)
+ *                and check_replicas' per-copy rel_err  (pkg/src/traindiff/canonical.py:225-247)
+ *                and TraceRecord.values() widening     (pkg/src/traindiff/tracestore.py:84-86)
+ *   td_reduce_slots + td_verdict
+ *                replace check()'s per-id loop         (pkg/src/traindiff/checker.py:312-365)
+ *                and _merge_one's replica verdicts     (pkg/src/traindiff/checker.py:151-198)
+ *   td_perturb   replaces Emulator._apply_perturbation (pkg/src/traindiff/engine.py:351-361)
+ *                = signed_uniforms (generation.py:163-167) + 1+u*eps + quantize_array (tensor.py:64-77)
+ *   td_quantize  replaces quantize_array               (pkg/src/traindiff/tensor.py:64-77)
+ *   td_fingerprint
+ *                order-independent 128-bit digest of a payload, used to decide
+ *                replica equality across GPUs without moving data
+ *   td_box_gather
+ *                materialises merge()'s f64 output on the device (public merge API)
+ *
+ * Conventions: every function returns 0 on success and a nonzero status on
+ * error (td_last_error() then describes it, thread-local).  All pointers to
+ * bulk data are DEVICE pointers owned by the caller; no function allocates
+ * device memory.  `stream` is a cudaStream_t passed as void*; all work is
+ * stream-ordered and re-entrant per stream.  No C++ exceptions cross the ABI.
+ */
+#ifndef TD_API_H
+#define TD_API_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TD_ABI_VERSION 1
+
+/* element types of payload buffers */
+enum td_dtype { TD_F32 = 0, TD_BF16 = 1, TD_F16 = 2, TD_F64 = 3 };
+
+/* storage formats of the reference's FloatFormat (tensor.py:28-61) */
+enum td_format { TD_FMT_NONE = 0, TD_FMT_FP32 = 1, TD_FMT_BF16 = 2, TD_FMT_FP8E4M3 = 3 };
+
+/* verdict codes; order matches checker.VERDICTS (checker.py:36-42) */
+enum td_verdict_code { TD_PASS = 0, TD_FLAG = 1, TD_REPLICA = 2, TD_MERGE = 3, TD_MISSING = 4, TD_NONE = 255 };
+
+/* perturbation generators */
+enum td_generator { TD_GEN_SPLITMIX64 = 0, TD_GEN_PHILOX4x32 = 1 };
+
+#define TD_MAX_Z 7              /* replica copies beside copy 0 per segment */
+#define TD_PARTIAL_STRIDE 10    /* doubles per tile partial: d2, x2, y2, z2[7] */
+#define TD_TILE_UNITS 8192      /* units (8-element vectors or elements) per tile */
+#define TD_SLOT_STRIDE 8        /* doubles per reduced slot */
+
+/* segment flags */
+#define TD_SEG_HAS_X 1u         /* x present: accumulate d2=sum (x-y)^2 and x2=sum x^2 */
+#define TD_SEG_VEC 2u           /* 16-byte vector path legal (alignment + cols%8 proven by host) */
+
+/*
+ * A segment is a 2-D strided block read in lockstep from x (the reference
+ * side), y (candidate copy 0) and z[0..nz) (replica copies laid out like y).
+ * rows x cols elements; row r of operand p starts at p + r*stride elements.
+ * The host planner derives segments from the intersection of candidate and
+ * reference global boxes (one per contiguous run), so the merged tensor is
+ * never materialised.  144 bytes, all fields naturally aligned.
+ */
+typedef struct td_segment {
+    uint64_t x;                 /* device address or 0 */
+    uint64_t y;
+    uint64_t z[TD_MAX_Z];
+    int64_t  x_stride;          /* elements per row in x */
+    int64_t  y_stride;          /* elements per row in y and every z */
+    int64_t  rows;
+    int64_t  cols;
+    int64_t  tile_begin;        /* global index of this segment's first tile */
+    int64_t  n_units;           /* rows*cols/8 (VEC) or rows*cols (scalar); < 2^31 */
+    int32_t  x_dtype;
+    int32_t  y_dtype;           /* dtype of y and of every z */
+    int32_t  nz;
+    uint32_t flags;
+    uint32_t div_m;             /* magic divisor for units-per-row: q = (n*div_m) >> div_p */
+    int32_t  div_p;
+} td_segment;
+
+/* per canonical id: where its partial sums live and what the host already knows */
+typedef struct td_id_desc {
+    int64_t tile_begin;         /* compare tiles [tile_begin, tile_end) */
+    int64_t tile_end;
+    int32_t cgroup_begin;       /* candidate replica-group slots [cgroup_begin, cgroup_end) */
+    int32_t cgroup_end;
+    int32_t rgroup_begin;       /* reference replica-group slots */
+    int32_t rgroup_end;
+    int32_t has_compare;        /* both merges succeed and merged shapes agree */
+    int32_t cand_host;          /* host-known candidate problem: 0, TD_REPLICA (declared size), TD_MERGE */
+    int32_t ref_host;           /* same for the reference side */
+    int32_t pad;
+    double  tolerance;          /* ToleranceMap.get(id) */
+} td_id_desc;                   /* 56 bytes */
+
+typedef struct td_group_desc {
+    int64_t tile_begin;         /* tiles carrying this group's y2/z2 partials */
+    int64_t tile_end;
+    int32_t nz;                 /* copies beside copy 0 */
+    int32_t pad;
+} td_group_desc;                /* 24 bytes */
+
+typedef struct td_id_result {
+    double  observed;           /* rel_err(ref, cand) or NaN when not computed */
+    double  threshold;          /* kappa * max(tol, eps) */
+    int32_t verdict;            /* td_verdict_code */
+    int32_t cand_kind;          /* 0, TD_REPLICA or TD_MERGE */
+    int32_t ref_kind;
+    int32_t near_tie;           /* |obs - thr| <= 1e-12 * thr */
+} td_id_result;                 /* 32 bytes */
+
+typedef struct td_group_result {
+    double  worst;              /* max_i rel_err(copy0, copy_i), strict > (NaN ignored) */
+    int32_t worst_index;        /* i of the worst copy, -1 when none exceeded 0 */
+    int32_t mismatch;           /* worst > replica eps */
+} td_group_result;              /* 16 bytes */
+
+/* ---- library ---- */
+int         td_version(void);
+const char* td_last_error(void);
+int         td_sm_count(int device);
+
+/* A tile class: the tiles (global tile indices, device array) whose segments
+ * share one walker.  Vector classes (vec=1) require every operand to have
+ * `dtype` (bf16, f16 or f32); everything else runs the generic walker. */
+typedef struct td_class {
+    const int32_t* tiles;       /* device */
+    int64_t n_tiles;
+    int32_t dtype;
+    int32_t nz;
+    int32_t has_x;
+    int32_t vec;
+    int32_t mode;               /* TD_MODE_NORMS, or TD_MODE_STATIC (generic walker only) */
+    int32_t pad;
+    double  atol;               /* static mode: count |y - x| > atol + rtol*|x| into d2 */
+    double  rtol;
+} td_class;                     /* 56 bytes */
+
+#define TD_MODE_NORMS 0
+#define TD_MODE_STATIC 1        /* compare_static's elementwise test (checker.py:403-443) */
+
+/* ---- kernel 1: fused canonicalise + relative-difference norms ----
+ * One persistent launch per class (classes is a HOST array).  tile_seg maps
+ * every global tile index to its segment.  partials: n_tiles_total *
+ * TD_PARTIAL_STRIDE doubles; each tile's row is written (not accumulated).
+ * blocks_per_sm <= 0 selects 4 CTAs of 256 threads per SM. */
+int td_segnorm(const td_segment* segs, const int32_t* tile_seg,
+               const td_class* classes, int32_t n_classes,
+               double* partials, int32_t blocks_per_sm, void* stream);
+
+/* deterministic per-slot sums of tile partials.
+ * id_sums:    n_ids    * 2 doubles  (d2, x2)
+ * group_sums: n_groups * TD_SLOT_STRIDE doubles (y2, z2[0..6]) */
+int td_reduce_slots(const td_id_desc* ids, int32_t n_ids,
+                    const td_group_desc* groups, int32_t n_groups,
+                    const double* partials,
+                    double* id_sums, double* group_sums, void* stream);
+
+/* ---- kernel 3: batched threshold compare -> per-id verdicts ----
+ * eps = fmt.eps (threshold floor); replica_eps = fmt.eps for check_replicas.
+ * near_ties: one device uint64 counter, incremented. */
+int td_verdict(const td_id_desc* ids, int32_t n_ids,
+               const td_group_desc* groups, int32_t n_groups,
+               const double* id_sums, const double* group_sums,
+               double kappa, double eps, double replica_eps,
+               td_id_result* id_out, td_group_result* group_out,
+               unsigned long long* near_ties, void* stream);
+
+/* ---- kernel 2: eps-scaled perturbation fused with the storage cast ----
+ * y[i, j] = Q_fmt(x[i, j] * (1 + u_k * eps)),  k = pos(i) * full_cols + col0 + j,
+ * u_k = 2 * U53(word k of the stream seeded by `seed`) - 1.
+ * pos(i) = row_pos[i] when row_pos != NULL, else row0 + i.
+ * x and y are contiguous (rows, cols); x == y (in place) is allowed.
+ * nonfinite: device uint64 counter incremented for each non-finite product
+ * (the reference raises NonFinite, tensor.py:66-67). */
+int td_perturb(const void* x, void* y, int32_t dtype_in, int32_t dtype_out,
+               int64_t rows, int64_t cols, int64_t full_cols, int64_t col0,
+               const int64_t* row_pos, int64_t row0,
+               uint64_t seed, double eps, int32_t fmt, int32_t generator,
+               unsigned long long* nonfinite, void* stream);
+
+/* raw stream words / signed uniforms for n consecutive counters from k0 */
+int td_signed_uniforms(double* out, int64_t n, uint64_t seed, int64_t k0,
+                       int32_t generator, void* stream);
+
+/* quantize_array on the device: y = Q_fmt(x) elementwise (f64 in, dtype_out out) */
+int td_quantize(const double* x, void* y, int32_t dtype_out, int64_t n, int32_t fmt,
+                unsigned long long* nonfinite, void* stream);
+
+/* ---- replica digests for multi-GPU replica groups ----
+ * out[0..1] += order-independent 128-bit digest of n elements (bit patterns). */
+int td_fingerprint(const void* x, int32_t dtype, int64_t n,
+                   unsigned long long* out, void* stream);
+
+/* ---- merge() materialisation: copy a strided box of src into dst (f64) ----
+ * boxes: n_boxes rows of {src_off, dst_off, rows, cols, src_stride, dst_stride} int64 */
+int td_box_gather(const void* src, int32_t src_dtype, double* dst,
+                  const int64_t* boxes, int32_t n_boxes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TD_API_H */

@@ -1,0 +1,440 @@
+"""Trace comparison under perturbation-estimated tolerances — the drop-in
+for pkg/src/traindiff/checker.py.
+
+Same public surface and semantics: ToleranceMap (checker.py:49-99),
+estimate_tolerance (:102-138), check (:312-365), CheckEntry / CheckReport /
+render_report (:221-309, 446-489), compare_static (:403-443).  The
+difference is where the arithmetic happens: metadata (grouping, hulls,
+merge witnesses) is planned on the host by `plan`, and every norm, replica
+check and threshold compare runs in the sm_100a kernels over payloads
+resident in HBM.  `CheckPlan` exposes the plan so a layout that repeats
+every step is planned once and re-run on fresh payloads.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+
+from . import _native as N
+from .device import resolve_operands
+from .errors import (ConfigInvalid, DigestMismatch, FormatError, ShapeMismatch,
+                     TraindiffError)
+from .perturb import PerturbSpec
+from .plan import Plan, PlanEntry, merge_view
+from .tensor import FloatFormat
+from .tracestore import Trace, canonical_json
+
+VERDICT_PASS = "pass"
+VERDICT_FLAG = "flag"
+VERDICT_REPLICA = "replica-mismatch"
+VERDICT_MERGE = "merge-error"
+VERDICT_MISSING = "missing"
+VERDICTS = (VERDICT_PASS, VERDICT_FLAG, VERDICT_REPLICA, VERDICT_MERGE, VERDICT_MISSING)
+_NAME = {N.PASS: VERDICT_PASS, N.FLAG: VERDICT_FLAG, N.REPLICA: VERDICT_REPLICA,
+         N.MERGE: VERDICT_MERGE}
+
+Runner = Callable[[PerturbSpec | None], Trace]
+
+
+@dataclass(frozen=True)
+class ToleranceMap:
+    """Per-id perturbation responses used as tolerances (checker.py:49-99)."""
+
+    responses: dict
+    n_samples: int
+    eps_p: float
+    aggregation: str = "max"
+
+    def __post_init__(self):
+        if self.n_samples < 1:
+            raise ConfigInvalid("n_samples must be >= 1")
+        if self.aggregation not in ("max", "mean"):
+            raise ConfigInvalid(f"unknown aggregation {self.aggregation!r}")
+        if not (self.eps_p >= 0.0 and math.isfinite(self.eps_p)):
+            raise ConfigInvalid("eps_p must be finite and >= 0")
+        for ident, resp in self.responses.items():
+            if not (math.isfinite(resp) and resp >= 0.0):
+                raise ConfigInvalid(f"response for {ident} must be finite and >= 0")
+
+    def get(self, ident: str) -> float:
+        """Never-estimated ids get 0.0, so the eps floor governs them."""
+        return self.responses.get(ident, 0.0)
+
+    def to_json(self) -> bytes:
+        return canonical_json({"tolerance_version": 1, "n_samples": self.n_samples,
+                               "eps_p": self.eps_p, "aggregation": self.aggregation,
+                               "responses": self.responses})
+
+    @classmethod
+    def from_json(cls, blob) -> "ToleranceMap":
+        try:
+            doc = json.loads(blob)
+        except (json.JSONDecodeError, UnicodeDecodeError) as exc:
+            raise FormatError(f"tolerance file is not valid JSON: {exc}")
+        if not isinstance(doc, dict) or doc.get("tolerance_version") != 1:
+            raise FormatError("unsupported tolerance file version")
+        try:
+            return cls(responses={str(k): float(v) for k, v in doc["responses"].items()},
+                       n_samples=int(doc["n_samples"]), eps_p=float(doc["eps_p"]),
+                       aggregation=str(doc["aggregation"]))
+        except (KeyError, TypeError, ValueError, AttributeError) as exc:
+            raise FormatError(f"malformed tolerance file: {exc}")
+
+
+@dataclass(frozen=True)
+class CheckEntry:
+    ident: str
+    verdict: str
+    observed: float | None
+    tolerance: float | None
+    threshold: float | None
+    detail: str = ""
+
+
+def _jsonable(value):
+    if value is None:
+        return None
+    if not math.isfinite(value):
+        return "inf" if value > 0 else ("-inf" if value < 0 else "nan")
+    return value
+
+
+def _entry_dicts(entries) -> list[dict]:
+    return [{"id": e.ident, "verdict": e.verdict, "observed": _jsonable(e.observed),
+             "tolerance": _jsonable(e.tolerance), "threshold": _jsonable(e.threshold),
+             "detail": e.detail} for e in entries]
+
+
+def _count(entries) -> dict[str, int]:
+    counts = dict.fromkeys(VERDICTS, 0)
+    for e in entries:
+        counts[e.verdict] += 1
+    return counts
+
+
+def _first_with(entries, verdicts) -> str | None:
+    return next((e.ident for e in entries if e.verdict in verdicts), None)
+
+
+@dataclass(frozen=True)
+class CheckReport:
+    """Per-id outcomes in candidate execution order, reference-only ids last."""
+
+    entries: tuple
+    mode: str
+    kappa: float
+    fmt: FloatFormat
+    near_ties: int = field(default=0, compare=False)
+
+    @property
+    def counts(self) -> dict[str, int]:
+        return _count(self.entries)
+
+    @property
+    def earliest_flag(self) -> str | None:
+        return _first_with(self.entries, (VERDICT_FLAG,))
+
+    @property
+    def earliest_divergence(self) -> str | None:
+        return _first_with(self.entries, (VERDICT_FLAG, VERDICT_REPLICA, VERDICT_MERGE))
+
+    def exit_code(self) -> int:
+        """3 replica/merge failures, else 2 flags, else 0 (missing never gates)."""
+        c = self.counts
+        if c[VERDICT_REPLICA] or c[VERDICT_MERGE]:
+            return 3
+        return 2 if c[VERDICT_FLAG] else 0
+
+    def to_dict(self) -> dict:
+        return {"report_version": 1, "kind": "check", "mode": self.mode, "kappa": self.kappa,
+                "format": self.fmt.value, "summary": self.counts,
+                "earliest_flag": self.earliest_flag,
+                "earliest_divergence": self.earliest_divergence,
+                "exit_code": self.exit_code(), "entries": _entry_dicts(self.entries)}
+
+
+def _require_same_setup(ref: Trace, cand: Trace) -> None:
+    for key in ("digest", "mode"):
+        a, b = ref.header.get(key), cand.header.get(key)
+        if a != b:
+            raise DigestMismatch(f"traces disagree on {key}: {a!r} vs {b!r}")
+
+
+def _side_detail(meta, group_rows) -> str:
+    """The first problem of one side in _merge_one's order: per group the
+    declared-size or numeric replica problem, then the merge problem."""
+    for gi, g in enumerate(meta.groups):
+        if g.declared_detail is not None:
+            return g.declared_detail
+        row = group_rows.get(gi)
+        if row is not None and row["mismatch"]:
+            return (f"replicas diverge: rel_err {float(row['worst']):.6g} between ranks "
+                    f"0 and {int(row['worst_index'])}")
+    return meta.merge_detail or ""
+
+
+class CheckPlan:
+    """check() split into plan (metadata, once per layout) and run (GPU)."""
+
+    def __init__(self, ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float = 3.0, *,
+                 fmt: FloatFormat):
+        if kappa <= 0:
+            raise ConfigInvalid("kappa must be positive")
+        _require_same_setup(ref, cand)
+        self.ref, self.cand, self.tol, self.kappa, self.fmt = ref, cand, tol, kappa, fmt
+        self.ref_view = merge_view(ref)
+        self.cand_view = merge_view(cand)
+        self.common = [i for i in self.cand_view if i in self.ref_view]
+        self.plan = Plan([PlanEntry(i, x=self.ref_view[i], y=self.cand_view[i], x_rep=True,
+                                    y_rep=True, tolerance=tol.get(i)) for i in self.common])
+        self.mode = str(cand.header.get("mode", ""))
+
+    @property
+    def algorithmic_bytes(self) -> int:
+        return self.plan.algorithmic_bytes
+
+    def execute(self, timing: dict | None = None):
+        """Device part only: resolve payloads, launch, fetch raw results."""
+        ptrs, keep = resolve_operands(self.plan.operands, self.plan.operand_dtypes)
+        out = self.plan.run(ptrs, kappa=self.kappa, eps=self.fmt.eps, replica_eps=self.fmt.eps,
+                            timing=timing)
+        del keep
+        return out
+
+    def run(self, timing: dict | None = None) -> CheckReport:
+        idres, gres, ties = self.execute(timing)
+        return self.report(idres, gres, ties)
+
+    def report(self, idres, gres, ties) -> CheckReport:
+        per_entry: dict = {}
+        for row, (ei, side, gi) in zip(gres, self.plan.group_owner):
+            per_entry.setdefault((ei, side), {})[gi] = row
+        kappa, eps = self.kappa, self.fmt.eps
+        index = {ident: k for k, ident in enumerate(self.common)}
+        entries = []
+        for ident, got in self.cand_view.items():
+            tolerance = self.tol.get(ident)
+            threshold = kappa * max(tolerance, eps)
+            k = index.get(ident)
+            if k is None:
+                entries.append(CheckEntry(ident, VERDICT_MISSING, None, tolerance, threshold,
+                                          "only in candidate trace"))
+                continue
+            r = idres[k]
+            want = self.ref_view[ident]
+            has_compare = bool(self.plan.ids[k]["has_compare"])
+            observed = float(r["observed"]) if has_compare else None
+            verdict = _NAME[int(r["verdict"])]
+            if int(r["cand_kind"]):
+                detail = _side_detail(got, per_entry.get((k, 0), {}))
+            elif int(r["ref_kind"]):
+                detail = "reference side: " + _side_detail(want, per_entry.get((k, 1), {}))
+            elif not has_compare:
+                detail = (f"merged shapes differ: reference {want.global_shape} vs "
+                          f"candidate {got.global_shape}")
+            else:
+                detail = ""
+            entries.append(CheckEntry(ident, verdict, observed, tolerance, threshold, detail))
+        for ident in self.ref_view:
+            if ident in self.cand_view:
+                continue
+            tolerance = self.tol.get(ident)
+            entries.append(CheckEntry(ident, VERDICT_MISSING, None, tolerance,
+                                      kappa * max(tolerance, eps), "only in reference trace"))
+        return CheckReport(entries=tuple(entries), mode=self.mode, kappa=kappa, fmt=self.fmt,
+                           near_ties=ties)
+
+
+def check(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float = 3.0, *,
+          fmt: FloatFormat) -> CheckReport:
+    """Compare a candidate trace against the reference (checker.py:312-365):
+    replica copies must agree to fmt precision, shards are merged (never
+    materialised here), and an id flags when rel_err(ref, cand) exceeds
+    kappa * max(tolerance, fmt.eps)."""
+    return CheckPlan(ref, cand, tol, kappa, fmt=fmt).run()
+
+
+def _strict_problem(view, plan: Plan, gres, side_of_entry: dict) -> str | None:
+    """First id (view order) with a merge/replica problem, as 'id: detail'."""
+    per_entry: dict = {}
+    for row, (ei, side, gi) in zip(gres, plan.group_owner):
+        per_entry.setdefault((ei, side), {})[gi] = row
+    for ident, meta in view.items():
+        rows = per_entry.get(side_of_entry[ident], {})
+        numeric = any(r["mismatch"] for r in rows.values())
+        if meta.declared_problem is not None or numeric or not meta.merge_ok:
+            return f"{ident}: {_side_detail(meta, rows)}"
+    return None
+
+
+def estimate_tolerance(runner: Runner, *, n_samples: int = 5, eps_p: float,
+                       aggregation: str = "max") -> ToleranceMap:
+    """Per-id response to an eps_p input nudge (checker.py:102-138).
+
+    runner(None) replays the trusted run; runner(PerturbSpec(s, eps_p))
+    replays it perturbed (the B200 runner applies td_perturb in a hook).
+    Merges are strict with FP32 replica tolerance, as in the reference."""
+    if n_samples < 1:
+        raise ConfigInvalid("n_samples must be >= 1")
+    if aggregation not in ("max", "mean"):
+        raise ConfigInvalid(f"unknown aggregation {aggregation!r}")
+    rep_eps = FloatFormat.FP32.eps
+    base_trace = runner(None)
+    base = merge_view(base_trace)
+    plan = Plan([PlanEntry(i, x=None, y=m, x_rep=False, y_rep=True) for i, m in base.items()])
+    ptrs, keep = resolve_operands(plan.operands, plan.operand_dtypes)
+    _, gres, _ = plan.run(ptrs, replica_eps=rep_eps)
+    del keep
+    problem = _strict_problem(base, plan, gres, {i: (k, 0) for k, i in enumerate(base)})
+    if problem is not None:
+        raise TraindiffError(problem)
+    samples: dict = {ident: [] for ident in base}
+    for s in range(n_samples):
+        pert = merge_view(runner(PerturbSpec(sample=s, eps=eps_p)))
+        entries = []
+        for ident, meta in pert.items():
+            b = base.get(ident)
+            entries.append(PlanEntry(ident, x=b, y=meta, x_rep=False, y_rep=True))
+        plan = Plan(entries)
+        ptrs, keep = resolve_operands(plan.operands, plan.operand_dtypes)
+        idres, gres, _ = plan.run(ptrs, replica_eps=rep_eps)
+        del keep
+        problem = _strict_problem(pert, plan, gres, {i: (k, 0) for k, i in enumerate(pert)})
+        if problem is not None:
+            raise TraindiffError(problem)
+        index = {ident: k for k, ident in enumerate(pert)}
+        for ident, meta in base.items():
+            k = index.get(ident)
+            if k is None:
+                continue
+            moved = pert[ident]
+            if meta.global_shape != moved.global_shape:
+                raise ShapeMismatch(f"rel_err: {meta.global_shape} vs {moved.global_shape}")
+            resp = float(idres[k]["observed"])
+            samples[ident].append(resp if math.isfinite(resp) else 0.0)
+    responses = {}
+    for ident, resp in samples.items():
+        if not resp:
+            responses[ident] = 0.0
+        elif aggregation == "max":
+            responses[ident] = max(resp)
+        else:
+            responses[ident] = sum(resp) / len(resp)
+    return ToleranceMap(responses=responses, n_samples=n_samples, eps_p=eps_p,
+                        aggregation=aggregation)
+
+
+# ---------------------------------------------------------------------------
+# static-threshold ablation and rendering
+
+@dataclass(frozen=True)
+class StaticReport:
+    """Fixed-threshold baseline outcome (checker.py:368-400)."""
+
+    entries: tuple
+    atol: float
+    rtol: float
+
+    @property
+    def counts(self) -> dict[str, int]:
+        return _count(self.entries)
+
+    @property
+    def earliest_flag(self) -> str | None:
+        return _first_with(self.entries, (VERDICT_FLAG,))
+
+    def exit_code(self) -> int:
+        c = self.counts
+        if c[VERDICT_MERGE]:
+            return 3
+        return 2 if c[VERDICT_FLAG] else 0
+
+    def to_dict(self) -> dict:
+        return {"report_version": 1, "kind": "static", "atol": self.atol, "rtol": self.rtol,
+                "summary": self.counts, "earliest_flag": self.earliest_flag,
+                "exit_code": self.exit_code(), "entries": _entry_dicts(self.entries)}
+
+
+def compare_static(ref: Trace, cand: Trace, atol: float, rtol: float) -> StaticReport:
+    """Elementwise |cand - ref| <= atol + rtol*|ref| per id, no replica
+    checks (checker.py:403-443); the elementwise test runs in td_segnorm's
+    static mode."""
+    if atol < 0 or rtol < 0:
+        raise ConfigInvalid("atol and rtol must be nonnegative")
+    _require_same_setup(ref, cand)
+    ref_view = merge_view(ref, replica_check=False)
+    cand_view = merge_view(cand, replica_check=False)
+    common = [i for i in cand_view if i in ref_view]
+    plan = Plan([PlanEntry(i, x=ref_view[i], y=cand_view[i], x_rep=False, y_rep=False)
+                 for i in common], static=(float(atol), float(rtol)))
+    ptrs, keep = resolve_operands(plan.operands, plan.operand_dtypes)
+    sums: dict = {}
+    plan.run(ptrs, sums=sums)
+    del keep
+    index = {ident: k for k, ident in enumerate(common)}
+    entries = []
+    for ident, got in cand_view.items():
+        k = index.get(ident)
+        if k is None:
+            entries.append(CheckEntry(ident, VERDICT_MISSING, None, None, None,
+                                      "only in candidate trace"))
+            continue
+        want = ref_view[ident]
+        if not got.merge_ok:
+            entries.append(CheckEntry(ident, VERDICT_MERGE, None, None, None, got.merge_detail))
+        elif not want.merge_ok:
+            entries.append(CheckEntry(ident, VERDICT_MERGE, None, None, None,
+                                      f"reference side: {want.merge_detail}"))
+        elif want.global_shape != got.global_shape:
+            entries.append(CheckEntry(ident, VERDICT_MERGE, None, None, None,
+                                      f"merged shapes differ: reference {want.global_shape} vs "
+                                      f"candidate {got.global_shape}"))
+        else:
+            failing = sums["id"][k, 0]
+            entries.append(CheckEntry(ident, VERDICT_PASS if failing == 0 else VERDICT_FLAG,
+                                      None, None, None))
+    for ident in ref_view:
+        if ident not in cand_view:
+            entries.append(CheckEntry(ident, VERDICT_MISSING, None, None, None,
+                                      "only in reference trace"))
+    return StaticReport(entries=tuple(entries), atol=atol, rtol=rtol)
+
+
+def _fmt_value(value) -> str:
+    return "-" if value is None else f"{value:.6g}"
+
+
+def _render_text(report) -> str:
+    doc = report.to_dict()
+    if doc["kind"] == "check":
+        lines = [f"check mode={doc['mode']} kappa={doc['kappa']:g} format={doc['format']}"]
+    else:
+        lines = [f"static check atol={doc['atol']:g} rtol={doc['rtol']:g}"]
+    earliest = doc["earliest_flag"]
+    for e in report.entries:
+        mark = ">" if earliest is not None and e.ident == earliest else " "
+        line = (f"{mark} {e.verdict:<16} obs={_fmt_value(e.observed):>12} "
+                f"tol={_fmt_value(e.tolerance):>12} thr={_fmt_value(e.threshold):>12}  {e.ident}")
+        if e.detail:
+            line += f"  [{e.detail}]"
+        lines.append(line)
+    counts = report.counts
+    lines.append("summary: " + ", ".join(f"{counts[v]} {v}" for v in VERDICTS))
+    lines.append(f"earliest flag: {earliest if earliest else '(none)'}")
+    divergence = doc.get("earliest_divergence")
+    if divergence is not None and divergence != earliest:
+        lines.append(f"earliest divergence: {divergence}")
+    return "\n".join(lines) + "\n"
+
+
+def render_report(report, format: str = "text") -> str:
+    if format == "json":
+        return canonical_json(report.to_dict()).decode("utf-8")
+    if format == "text":
+        return _render_text(report)
+    raise ConfigInvalid(f"unknown report format {format!r}")

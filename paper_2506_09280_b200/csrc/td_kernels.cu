@@ -1,0 +1,770 @@
+// td_kernels.cu — sm_100a kernels behind include/td_api.h.
+//
+// Kernel 1 (k_segnorm): one persistent pass over a flat tile list.  Each tile
+// is a fixed slice of one segment (a 2-D strided block read in lockstep from
+// the reference side x, candidate copy 0 y and up to seven replica copies z).
+// It accumulates, in fp64:
+//     d2 = sum (x - y)^2      x2 = sum x^2                 (rel_err(ref, cand))
+//     y2 = sum y^2            z2[j] = sum (y - z_j)^2       (rel_err(copy0, copy_j))
+// and writes the tile's block-reduced partials; no atomics, so the result is
+// bit-reproducible for a given plan, independent of grid size.
+// Reference semantics: tensor.py:158-167 (norms), canonical.py:182-212 (merge,
+// never materialised here), canonical.py:225-247 (replica rel_err),
+// tracestore.py:84-86 (f32 -> f64 widening).
+//
+// Kernel 3 (k_reduce_slots + k_verdict): deterministic per-id / per-group sums
+// of tile partials, then checker.check's verdict precedence (checker.py:328-354)
+// and check_replicas' strict-> worst tracking (canonical.py:236-247).
+//
+// Kernel 2 (k_perturb): Emulator._apply_perturbation (engine.py:351-361):
+// y = Q(x * (1 + u*eps)) with the splitmix64 stream of generation.py:49-78 and
+// the RNE-to-p-bits quantiser of tensor.py:64-77, each fp64 op rounded
+// separately (__dmul_rn / __dadd_rn: numpy never contracts to FMA).
+
+#include "td_api.h"
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return 1;
+}
+
+int check_launch(const char* what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail("%s: %s", what, cudaGetErrorString(e));
+    return 0;
+}
+
+constexpr int BLOCK = 256;
+constexpr int NWARP = BLOCK / 32;
+
+// ---------------------------------------------------------------------------
+// loads and widening
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+// words (u32) per 8-element vector, and their widening to fp64
+template <int DT> struct Vec;
+
+template <> struct Vec<TD_BF16> {
+    static constexpr int Q = 1;  // uint4 loads per 8 elements
+    __device__ __forceinline__ static double at(const uint4* q, int e) {
+        const uint32_t w = (&q[0].x)[e >> 1];
+        const uint32_t b = (e & 1) ? (w & 0xffff0000u) : (w << 16);
+        return (double)__uint_as_float(b);
+    }
+};
+template <> struct Vec<TD_F16> {
+    static constexpr int Q = 1;
+    __device__ __forceinline__ static double at(const uint4* q, int e) {
+        const uint32_t w = (&q[0].x)[e >> 1];
+        const unsigned short h = (e & 1) ? (unsigned short)(w >> 16) : (unsigned short)(w & 0xffffu);
+        return (double)__half2float(__ushort_as_half(h));
+    }
+};
+template <> struct Vec<TD_F32> {
+    static constexpr int Q = 2;
+    __device__ __forceinline__ static double at(const uint4* q, int e) {
+        return (double)__uint_as_float((&q[0].x)[e]);
+    }
+};
+template <> struct Vec<TD_F64> {
+    static constexpr int Q = 4;
+    __device__ __forceinline__ static double at(const uint4* q, int e) {
+        const uint32_t* w = &q[0].x;
+        return __hiloint2double((int)w[2 * e + 1], (int)w[2 * e]);
+    }
+};
+
+__host__ __device__ __forceinline__ int dtype_size(int dt) {
+    return dt == TD_F32 ? 4 : (dt == TD_F64 ? 8 : 2);
+}
+
+__device__ __forceinline__ double load_elem(const char* base, int dt, int64_t idx) {
+    switch (dt) {
+        case TD_F32: return (double)__ldg(reinterpret_cast<const float*>(base) + idx);
+        case TD_BF16: {
+            unsigned short h = __ldg(reinterpret_cast<const unsigned short*>(base) + idx);
+            return (double)__uint_as_float(((uint32_t)h) << 16);
+        }
+        case TD_F16: {
+            unsigned short h = __ldg(reinterpret_cast<const unsigned short*>(base) + idx);
+            return (double)__half2float(__ushort_as_half(h));
+        }
+        default: return __ldg(reinterpret_cast<const double*>(base) + idx);
+    }
+}
+
+struct Acc {
+    double d2, x2, y2, z[TD_MAX_Z];
+    __device__ __forceinline__ void zero() {
+        d2 = x2 = y2 = 0.0;
+#pragma unroll
+        for (int j = 0; j < TD_MAX_Z; ++j) z[j] = 0.0;
+    }
+};
+
+struct SegView {
+    const char* x;
+    const char* y;
+    const char* z[TD_MAX_Z];
+    int64_t xs, ys, cols;
+    uint32_t vpr;      // units per row
+    uint32_t div_m;
+    int div_p;
+};
+
+__device__ __forceinline__ uint32_t udiv(uint32_t n, uint32_t m, int p) {
+    return (uint32_t)(((uint64_t)n * (uint64_t)m) >> p);
+}
+
+// ---------------------------------------------------------------------------
+// tile walkers.  Every (dtype, nz, has_x) class is its own __global__ so ptxas
+// allocates registers for exactly one loop; the host launches one persistent
+// kernel per class present in the plan (usually 1-3).
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ __forceinline__ void load_view(const td_segment* __restrict__ g, SegView& S, int nz_max) {
+    S.x = reinterpret_cast<const char*>(__ldg(&g->x));
+    S.y = reinterpret_cast<const char*>(__ldg(&g->y));
+#pragma unroll
+    for (int j = 0; j < TD_MAX_Z; ++j)
+        S.z[j] = j < nz_max ? reinterpret_cast<const char*>(__ldg(&g->z[j])) : nullptr;
+    S.xs = __ldg(&g->x_stride);
+    S.ys = __ldg(&g->y_stride);
+    S.cols = __ldg(&g->cols);
+    S.div_m = __ldg(&g->div_m);
+    S.div_p = __ldg(&g->div_p);
+}
+
+// Fixed-order block reduction of the first `used` accumulators -> one tile
+// partial.  Deterministic: the element->thread map and the tree are fixed.
+__device__ __forceinline__ void write_partial(const Acc& a, int used, double (*red)[TD_PARTIAL_STRIDE],
+                                              double* __restrict__ out) {
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const double v[TD_PARTIAL_STRIDE] = {a.d2, a.x2, a.y2, a.z[0], a.z[1], a.z[2],
+                                         a.z[3], a.z[4], a.z[5], a.z[6]};
+#pragma unroll
+    for (int k = 0; k < TD_PARTIAL_STRIDE; ++k) {
+        if (k < used) {
+            const double s = warp_sum(v[k]);
+            if (lane == 0) red[warp][k] = s;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < TD_PARTIAL_STRIDE) {
+        double s = 0.0;
+        if ((int)threadIdx.x < used) {
+#pragma unroll
+            for (int w = 0; w < NWARP; ++w) s += red[w][threadIdx.x];
+        }
+        out[threadIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+// vector class: every operand has dtype DT, rows 16-byte aligned, cols % 8 == 0
+template <int DT, int NZ, bool HX, int U, int MINB>
+__global__ void __launch_bounds__(BLOCK, MINB)
+k_segnorm_vec(const td_segment* __restrict__ segs, const int32_t* __restrict__ tile_seg,
+              const int32_t* __restrict__ tiles, int64_t n, double* __restrict__ partials) {
+    __shared__ double red[NWARP][TD_PARTIAL_STRIDE];
+    constexpr int Q = Vec<DT>::Q;
+    constexpr int ES = (DT == TD_F32) ? 4 : 2;
+    constexpr int USED = NZ > 0 ? 3 + NZ : 2;
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const int64_t t = __ldg(tiles + i);
+        const td_segment* g = segs + __ldg(tile_seg + t);
+        SegView S;
+        load_view(g, S, NZ);
+        const uint32_t vpr = (uint32_t)(S.cols >> 3);
+        const int64_t first = (t - __ldg(&g->tile_begin)) * (int64_t)TD_TILE_UNITS;
+        const uint32_t u0 = (uint32_t)first;
+        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, __ldg(&g->n_units));
+        Acc a;
+        a.zero();
+        for (uint32_t base = u0 + threadIdx.x; base < u1; base += BLOCK * U) {
+            uint4 xr[U][Q];
+            uint4 yr[U][Q];
+            uint4 zr[NZ > 0 ? NZ : 1][U][Q];
+            bool ok[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t u = base + k * BLOCK;
+                ok[k] = u < u1;
+                if (ok[k]) {
+                    const uint32_t row = udiv(u, S.div_m, S.div_p);
+                    const uint32_t cv = u - row * vpr;
+                    const int64_t yo = ((int64_t)row * S.ys + (int64_t)cv * 8) * ES;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        if (HX) xr[k][q] = ld_stream(S.x + ((int64_t)row * S.xs + (int64_t)cv * 8) * ES + 16 * q);
+                        yr[k][q] = ld_stream(S.y + yo + 16 * q);
+#pragma unroll
+                        for (int j = 0; j < NZ; ++j) zr[j][k][q] = ld_stream(S.z[j] + yo + 16 * q);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                if (!ok[k]) continue;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const double yv = Vec<DT>::at(yr[k], e);
+                    if (HX) {
+                        const double xv = Vec<DT>::at(xr[k], e);
+                        const double d = xv - yv;
+                        a.d2 = fma(d, d, a.d2);
+                        a.x2 = fma(xv, xv, a.x2);
+                    }
+                    if (NZ > 0) {
+                        a.y2 = fma(yv, yv, a.y2);
+#pragma unroll
+                        for (int j = 0; j < NZ; ++j) {
+                            const double dz = yv - Vec<DT>::at(zr[j][k], e);
+                            a.z[j] = fma(dz, dz, a.z[j]);
+                        }
+                    }
+                }
+            }
+        }
+        write_partial(a, USED, red, partials + t * TD_PARTIAL_STRIDE);
+    }
+}
+
+// generic class: per element, runtime dtypes, any alignment, any nz (<= 7)
+// mode TD_MODE_STATIC replaces d2 by the count of cells failing
+// |y - x| <= atol + rtol*|x| (numpy's elementwise test, each op rounded once;
+// NaN fails) and leaves x2 at 0.
+__global__ void __launch_bounds__(BLOCK, 4)
+k_segnorm_generic(const td_segment* __restrict__ segs, const int32_t* __restrict__ tile_seg,
+                  const int32_t* __restrict__ tiles, int64_t n, double* __restrict__ partials,
+                  int mode, double atol, double rtol) {
+    __shared__ double red[NWARP][TD_PARTIAL_STRIDE];
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const int64_t t = __ldg(tiles + i);
+        const td_segment* g = segs + __ldg(tile_seg + t);
+        const int nz = __ldg(&g->nz);
+        const bool hx = (__ldg(&g->flags) & TD_SEG_HAS_X) != 0;
+        const int xdt = __ldg(&g->x_dtype);
+        const int ydt = __ldg(&g->y_dtype);
+        SegView S;
+        load_view(g, S, nz);
+        const uint32_t cols = (uint32_t)S.cols;
+        const int64_t first = (t - __ldg(&g->tile_begin)) * (int64_t)TD_TILE_UNITS;
+        const uint32_t u0 = (uint32_t)first;
+        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, __ldg(&g->n_units));
+        Acc a;
+        a.zero();
+        for (uint32_t u = u0 + threadIdx.x; u < u1; u += BLOCK) {
+            const uint32_t row = udiv(u, S.div_m, S.div_p);
+            const uint32_t col = u - row * cols;
+            const int64_t yi = (int64_t)row * S.ys + col;
+            const double yv = load_elem(S.y, ydt, yi);
+            if (hx) {
+                const double xv = load_elem(S.x, xdt, (int64_t)row * S.xs + col);
+                if (mode == TD_MODE_STATIC) {
+                    const double lim = __dadd_rn(atol, __dmul_rn(rtol, fabs(xv)));
+                    if (!(fabs(__dsub_rn(yv, xv)) <= lim)) a.d2 += 1.0;
+                } else {
+                    const double d = xv - yv;
+                    a.d2 = fma(d, d, a.d2);
+                    a.x2 = fma(xv, xv, a.x2);
+                }
+            }
+            if (nz > 0) {
+                a.y2 = fma(yv, yv, a.y2);
+#pragma unroll
+                for (int j = 0; j < TD_MAX_Z; ++j) {
+                    if (j < nz) {
+                        const double dz = yv - load_elem(S.z[j], ydt, yi);
+                        a.z[j] = fma(dz, dz, a.z[j]);
+                    }
+                }
+            }
+        }
+        write_partial(a, nz > 0 ? 3 + nz : 2, red, partials + t * TD_PARTIAL_STRIDE);
+    }
+}
+
+typedef void (*segnorm_fn)(const td_segment*, const int32_t*, const int32_t*, int64_t, double*);
+
+static_assert(sizeof(td_segment) == 144, "td_segment layout");
+static_assert(sizeof(td_id_desc) == 56, "td_id_desc layout");
+static_assert(sizeof(td_group_desc) == 24, "td_group_desc layout");
+static_assert(sizeof(td_id_result) == 32, "td_id_result layout");
+static_assert(sizeof(td_group_result) == 16, "td_group_result layout");
+static_assert(sizeof(td_class) == 56, "td_class layout");
+
+// U keeps ~4-8 16-byte loads in flight per thread; wide replica classes trade
+// occupancy (2 CTAs/SM, 128 registers) for no spills.
+template <int DT>
+segnorm_fn pick_vec(int nz, bool hx) {
+    constexpr int Q = Vec<DT>::Q;
+    constexpr int U4 = 4 / Q > 0 ? 4 / Q : 1;
+    constexpr int U2 = 2 / Q > 0 ? 2 / Q : 1;
+    if (hx) {
+        switch (nz) {
+            case 0: return k_segnorm_vec<DT, 0, true, U4, 4>;
+            case 1: return k_segnorm_vec<DT, 1, true, U2, 4>;
+            case 2: return k_segnorm_vec<DT, 2, true, 1, 4>;
+            case 3: return k_segnorm_vec<DT, 3, true, 1, 4>;
+            case 4: return k_segnorm_vec<DT, 4, true, 1, 2>;
+            case 5: return k_segnorm_vec<DT, 5, true, 1, 2>;
+            case 6: return k_segnorm_vec<DT, 6, true, 1, 2>;
+            case 7: return k_segnorm_vec<DT, 7, true, 1, 2>;
+            default: return nullptr;
+        }
+    }
+    switch (nz) {
+        case 1: return k_segnorm_vec<DT, 1, false, U4, 4>;
+        case 2: return k_segnorm_vec<DT, 2, false, U2, 4>;
+        case 3: return k_segnorm_vec<DT, 3, false, 1, 4>;
+        case 4: return k_segnorm_vec<DT, 4, false, 1, 4>;
+        case 5: return k_segnorm_vec<DT, 5, false, 1, 2>;
+        case 6: return k_segnorm_vec<DT, 6, false, 1, 2>;
+        case 7: return k_segnorm_vec<DT, 7, false, 1, 2>;
+        default: return nullptr;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// slot reduction: one warp per id / group, fixed lane-strided order + butterfly
+
+__global__ void k_reduce_slots(const td_id_desc* __restrict__ ids, int n_ids,
+                               const td_group_desc* __restrict__ groups, int n_groups,
+                               const double* __restrict__ partials,
+                               double* __restrict__ id_sums, double* __restrict__ group_sums) {
+    const int lane = threadIdx.x & 31;
+    const int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (slot >= (int64_t)n_ids + n_groups) return;
+    if (slot < n_ids) {
+        const int64_t tb = ids[slot].tile_begin, te = ids[slot].tile_end;
+        double d2 = 0.0, x2 = 0.0;
+        for (int64_t t = tb + lane; t < te; t += 32) {
+            d2 += partials[t * TD_PARTIAL_STRIDE + 0];
+            x2 += partials[t * TD_PARTIAL_STRIDE + 1];
+        }
+        d2 = warp_sum(d2);
+        x2 = warp_sum(x2);
+        if (lane == 0) {
+            id_sums[2 * slot + 0] = d2;
+            id_sums[2 * slot + 1] = x2;
+        }
+    } else {
+        const int64_t g = slot - n_ids;
+        const int64_t tb = groups[g].tile_begin, te = groups[g].tile_end;
+        const int nz = groups[g].nz;
+        double s[TD_SLOT_STRIDE];
+#pragma unroll
+        for (int k = 0; k < TD_SLOT_STRIDE; ++k) s[k] = 0.0;
+        for (int64_t t = tb + lane; t < te; t += 32) {
+#pragma unroll
+            for (int k = 0; k < TD_SLOT_STRIDE; ++k)
+                if (k <= nz) s[k] += partials[t * TD_PARTIAL_STRIDE + 2 + k];
+        }
+#pragma unroll
+        for (int k = 0; k < TD_SLOT_STRIDE; ++k) {
+            const double v = warp_sum(s[k]);
+            if (lane == 0) group_sums[g * TD_SLOT_STRIDE + k] = v;
+        }
+    }
+}
+
+// rel_err_arrays' tail (tensor.py:163-167): two square roots, then a divide
+__device__ __forceinline__ double rel_from_sums(double d2, double r2) {
+    const double diff = __dsqrt_rn(d2);
+    const double ref = __dsqrt_rn(r2);
+    if (ref == 0.0) return diff == 0.0 ? 0.0 : __longlong_as_double(0x7ff0000000000000LL);
+    return __ddiv_rn(diff, ref);
+}
+
+__global__ void k_verdict(const td_id_desc* __restrict__ ids, int n_ids,
+                          const td_group_desc* __restrict__ groups,
+                          const double* __restrict__ id_sums, const double* __restrict__ group_sums,
+                          double kappa, double eps, double replica_eps,
+                          td_id_result* __restrict__ id_out, td_group_result* __restrict__ group_out,
+                          unsigned long long* __restrict__ near_ties) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_ids) return;
+    const td_id_desc D = ids[i];
+    int kinds[2] = {D.cand_host, D.ref_host};
+    const int gb[2] = {D.cgroup_begin, D.rgroup_begin};
+    const int ge[2] = {D.cgroup_end, D.rgroup_end};
+    for (int side = 0; side < 2; ++side) {
+        bool any = false;
+        for (int g = gb[side]; g < ge[side]; ++g) {
+            const double* s = group_sums + (int64_t)g * TD_SLOT_STRIDE;
+            const int nz = groups[g].nz;
+            double worst = 0.0;
+            int widx = -1;
+            for (int j = 0; j < nz && j < TD_MAX_Z; ++j) {
+                const double err = rel_from_sums(s[1 + j], s[0]);
+                if (err > worst) { worst = err; widx = j + 1; }  // NaN never wins
+            }
+            const int mm = worst > replica_eps;
+            group_out[g].worst = worst;
+            group_out[g].worst_index = widx;
+            group_out[g].mismatch = mm;
+            any |= (mm != 0);
+        }
+        // replica problems (declared-size or numeric) precede the merge problem
+        if (kinds[side] != TD_REPLICA && any) kinds[side] = TD_REPLICA;
+    }
+    // threshold = kappa * max(tol, eps) (checker.py:330-331)
+    const double m = (eps > D.tolerance) ? eps : D.tolerance;
+    const double thr = __dmul_rn(kappa, m);
+    double obs = __longlong_as_double(0x7ff8000000000000LL);
+    int tie = 0;
+    int verdict;
+    if (D.has_compare) obs = rel_from_sums(id_sums[2 * i + 0], id_sums[2 * i + 1]);
+    if (kinds[0]) verdict = kinds[0];
+    else if (kinds[1]) verdict = kinds[1];
+    else if (!D.has_compare) verdict = TD_MERGE;
+    else {
+        verdict = (obs > thr) ? TD_FLAG : TD_PASS;   // NaN -> pass (reference quirk)
+        if (fabs(obs - thr) <= 1e-12 * thr) {
+            tie = 1;
+            atomicAdd(near_ties, 1ull);
+        }
+    }
+    id_out[i].observed = obs;
+    id_out[i].threshold = thr;
+    id_out[i].verdict = verdict;
+    id_out[i].cand_kind = kinds[0];
+    id_out[i].ref_kind = kinds[1];
+    id_out[i].near_tie = tie;
+}
+
+// ---------------------------------------------------------------------------
+// RNG streams
+
+constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t MIX1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t MIX2 = 0x94D049BB133111EBull;
+
+// word k (0-based) of the splitmix64 stream: mix(seed + (k+1)*gamma)  (generation.py:67-78)
+__device__ __forceinline__ uint64_t splitmix_word(uint64_t seed, uint64_t k) {
+    uint64_t z = seed + (k + 1) * GAMMA;
+    z = (z ^ (z >> 30)) * MIX1;
+    z = (z ^ (z >> 27)) * MIX2;
+    return z ^ (z >> 31);
+}
+
+// Philox4x32-10 keyed by the seed, counter = k; the 64-bit word is (out1:out0)
+__device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t k) {
+    uint32_t c0 = (uint32_t)k, c1 = (uint32_t)(k >> 32), c2 = 0, c3 = 0;
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    return ((uint64_t)c1 << 32) | c0;
+}
+
+__device__ __forceinline__ double signed_uniform(uint64_t seed, uint64_t k, int gen) {
+    const uint64_t w = gen == TD_GEN_PHILOX4x32 ? philox_word(seed, k) : splitmix_word(seed, k);
+    const double u = __dmul_rn((double)(w >> 11), 0x1p-53);   // exact
+    return __dsub_rn(__dmul_rn(2.0, u), 1.0);                  // 2u - 1 (generation.py:166)
+}
+
+// quantize_array (tensor.py:64-77): RNE to p significand bits, unbounded
+// exponent, clip to +-max_finite.  Done on the fp64 bit pattern: never via f32.
+__device__ __forceinline__ double quantize_p(double y, int p, double maxf) {
+    double s = y;
+    bool scaled = false;
+    if (fabs(s) < 0x1p-1000 && s != 0.0) { s = s * 0x1p200; scaled = true; }   // exact
+    long long b = __double_as_longlong(s);
+    const int drop = 53 - p;
+    const long long mask = (1ll << drop) - 1;
+    const long long lsb = (b >> drop) & 1ll;
+    const long long sign = b & (long long)0x8000000000000000ull;
+    long long mag = b & 0x7fffffffffffffffll;
+    mag = (mag + (mask >> 1) + lsb) & ~mask;
+    double r = __longlong_as_double(mag | sign);
+    if (scaled) r = r * 0x1p-200;   // one IEEE rounding, as numpy's ldexp
+    if (fabs(r) > maxf) r = copysign(maxf, r);
+    return r;
+}
+
+__device__ __forceinline__ double apply_format(double y, int fmt) {
+    switch (fmt) {
+        case TD_FMT_BF16: return quantize_p(y, 8, 0x1.fep127);
+        case TD_FMT_FP8E4M3: return quantize_p(y, 4, 448.0);
+        case TD_FMT_FP32: return quantize_p(y, 24, 0x1.fffffep127);
+        default: return y;
+    }
+}
+
+__device__ __forceinline__ void store_elem(void* base, int dt, int64_t idx, double v) {
+    switch (dt) {
+        case TD_F32: reinterpret_cast<float*>(base)[idx] = (float)v; break;
+        case TD_BF16: {
+            // round f64 straight to 8 significand bits (no f64->f32->bf16 double rounding);
+            // only the bf16 subnormal range goes through f32
+            const double q = (isfinite(v) && fabs(v) >= 0x1p-126) ? quantize_p(v, 8, __longlong_as_double(0x7ff0000000000000LL)) : v;
+            reinterpret_cast<__nv_bfloat16*>(base)[idx] = __float2bfloat16_rn((float)q);
+            break;
+        }
+        case TD_F16: reinterpret_cast<__half*>(base)[idx] = __double2half(v); break;
+        default: reinterpret_cast<double*>(base)[idx] = v; break;
+    }
+}
+
+__global__ void k_perturb(const char* x, char* y, int dt_in, int dt_out,
+                          int64_t rows, int64_t cols, int64_t full_cols, int64_t col0,
+                          const int64_t* __restrict__ row_pos, int64_t row0,
+                          uint64_t seed, double eps, int fmt, int gen,
+                          unsigned long long* __restrict__ nonfinite) {
+    int bad = 0;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const int64_t pos = row_pos ? row_pos[r] : row0 + r;
+        const uint64_t kbase = (uint64_t)(pos * full_cols + col0);
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+             c += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t idx = r * cols + c;
+            const double xv = load_elem(x, dt_in, idx);
+            const double u = signed_uniform(seed, kbase + (uint64_t)c, gen);
+            const double f = __dadd_rn(1.0, __dmul_rn(u, eps));   // 1.0 + u*eps
+            double v = __dmul_rn(xv, f);
+            if (!isfinite(v)) bad = 1;
+            v = apply_format(v, fmt);
+            store_elem(y, dt_out, idx, v);
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(nonfinite, 1ull);
+}
+
+__global__ void k_signed_uniforms(double* __restrict__ out, int64_t n, uint64_t seed, int64_t k0, int gen) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = signed_uniform(seed, (uint64_t)(k0 + i), gen);
+}
+
+__global__ void k_quantize(const double* __restrict__ x, char* __restrict__ y, int dt_out, int64_t n,
+                           int fmt, unsigned long long* __restrict__ nonfinite) {
+    int bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = x[i];
+        if (!isfinite(v)) bad = 1;
+        store_elem(y, dt_out, i, apply_format(v, fmt));
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(nonfinite, 1ull);
+}
+
+// ---------------------------------------------------------------------------
+// order-independent 128-bit digest: sum_i mix(i, bits_i) in two lanes
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * MIX1;
+    z = (z ^ (z >> 27)) * MIX2;
+    return z ^ (z >> 31);
+}
+
+__global__ void k_fingerprint(const char* __restrict__ x, int dt, int64_t n,
+                              unsigned long long* __restrict__ out) {
+    uint64_t h0 = 0, h1 = 0;
+    const int es = dtype_size(dt);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t b;
+        if (es == 2) b = reinterpret_cast<const unsigned short*>(x)[i];
+        else if (es == 4) b = reinterpret_cast<const uint32_t*>(x)[i];
+        else b = reinterpret_cast<const uint64_t*>(x)[i];
+        const uint64_t k = mix64((uint64_t)i * GAMMA + 0x632BE59BD9B4E019ull);
+        h0 += mix64(k ^ b);
+        h1 += mix64((k + 0x8CB92BA72F3D8DD7ull) ^ (b * 0xD6E8FEB86659FD93ull));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        h0 += __shfl_xor_sync(0xffffffffu, h0, o);
+        h1 += __shfl_xor_sync(0xffffffffu, h1, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out + 0, (unsigned long long)h0);
+        atomicAdd(out + 1, (unsigned long long)h1);
+    }
+}
+
+__global__ void k_box_gather(const char* __restrict__ src, int dt, double* __restrict__ dst,
+                             const int64_t* __restrict__ boxes) {
+    const int64_t* b = boxes + 6 * (int64_t)blockIdx.y;
+    const int64_t so = b[0], dof = b[1], rows = b[2], cols = b[3], ss = b[4], ds = b[5];
+    const int64_t n = rows * cols;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / cols, c = e - r * cols;
+        dst[dof + r * ds + c] = load_elem(src, dt, so + r * ss + c);
+    }
+}
+
+int grid_for(int64_t n, int per_block, int cap) {
+    int64_t g = (n + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (int)g;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+
+extern "C" {
+
+int td_version(void) { return TD_ABI_VERSION; }
+
+const char* td_last_error(void) { return g_err; }
+
+int td_sm_count(int device) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+    return n;
+}
+
+int td_segnorm(const td_segment* segs, const int32_t* tile_seg, const td_class* classes, int32_t n_classes,
+               double* partials, int32_t blocks_per_sm, void* stream) {
+    if (n_classes == 0) return 0;
+    if (!segs || !tile_seg || !classes || !partials || n_classes < 0)
+        return fail("td_segnorm: invalid arguments (n_classes=%d)", n_classes);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = blocks_per_sm > 0 ? blocks_per_sm : 4;
+    for (int c = 0; c < n_classes; ++c) {
+        const td_class& C = classes[c];
+        if (C.n_tiles == 0) continue;
+        if (!C.tiles || C.n_tiles < 0 || C.nz < 0 || C.nz > TD_MAX_Z)
+            return fail("td_segnorm: invalid class %d", c);
+        int64_t grid = (int64_t)sms * per_sm;
+        if (grid > C.n_tiles) grid = C.n_tiles;
+        if (!C.vec || C.mode != TD_MODE_NORMS) {
+            k_segnorm_generic<<<(unsigned)grid, BLOCK, 0, (cudaStream_t)stream>>>(
+                segs, tile_seg, C.tiles, C.n_tiles, partials, C.mode, C.atol, C.rtol);
+            if (int rc = check_launch("td_segnorm")) return rc;
+            continue;
+        }
+        segnorm_fn fn = nullptr;
+        {
+            switch (C.dtype) {
+                case TD_BF16: fn = pick_vec<TD_BF16>(C.nz, C.has_x != 0); break;
+                case TD_F16: fn = pick_vec<TD_F16>(C.nz, C.has_x != 0); break;
+                case TD_F32: fn = pick_vec<TD_F32>(C.nz, C.has_x != 0); break;
+                default: break;
+            }
+            if (!fn) return fail("td_segnorm: no vector walker for class %d (dtype=%d nz=%d has_x=%d)", c,
+                                 C.dtype, C.nz, C.has_x);
+        }
+        fn<<<(unsigned)grid, BLOCK, 0, (cudaStream_t)stream>>>(segs, tile_seg, C.tiles, C.n_tiles, partials);
+        if (int rc = check_launch("td_segnorm")) return rc;
+    }
+    return 0;
+}
+
+int td_reduce_slots(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups, int32_t n_groups,
+                    const double* partials, double* id_sums, double* group_sums, void* stream) {
+    const int64_t slots = (int64_t)n_ids + n_groups;
+    if (slots == 0) return 0;
+    if (n_ids < 0 || n_groups < 0 || (n_ids && (!ids || !id_sums)) || (n_groups && (!groups || !group_sums)))
+        return fail("td_reduce_slots: invalid arguments");
+    const int threads = 256;
+    const int64_t blocks = (slots * 32 + threads - 1) / threads;
+    k_reduce_slots<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(ids, n_ids, groups, n_groups,
+                                                                          partials, id_sums, group_sums);
+    return check_launch("td_reduce_slots");
+}
+
+int td_verdict(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups, int32_t n_groups,
+               const double* id_sums, const double* group_sums, double kappa, double eps,
+               double replica_eps, td_id_result* id_out, td_group_result* group_out,
+               unsigned long long* near_ties, void* stream) {
+    if (n_ids == 0) return 0;
+    if (n_ids < 0 || !ids || !id_sums || !id_out || !near_ties || (n_groups && (!groups || !group_sums || !group_out)))
+        return fail("td_verdict: invalid arguments");
+    const int threads = 128;
+    k_verdict<<<(n_ids + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(
+        ids, n_ids, groups, id_sums, group_sums, kappa, eps, replica_eps, id_out, group_out, near_ties);
+    return check_launch("td_verdict");
+}
+
+int td_perturb(const void* x, void* y, int32_t dtype_in, int32_t dtype_out, int64_t rows, int64_t cols,
+               int64_t full_cols, int64_t col0, const int64_t* row_pos, int64_t row0, uint64_t seed,
+               double eps, int32_t fmt, int32_t generator, unsigned long long* nonfinite, void* stream) {
+    if (rows == 0 || cols == 0) return 0;
+    if (!x || !y || !nonfinite || rows < 0 || cols < 0 || dtype_in < 0 || dtype_in > 3 || dtype_out < 0 ||
+        dtype_out > 3 || fmt < 0 || fmt > 3 || col0 < 0 || col0 + cols > full_cols)
+        return fail("td_perturb: invalid arguments");
+    const int threads = 256;
+    dim3 grid((unsigned)grid_for(cols, threads, 64), (unsigned)(rows < 65535 ? rows : 65535));
+    k_perturb<<<grid, threads, 0, (cudaStream_t)stream>>>(
+        static_cast<const char*>(x), static_cast<char*>(y), dtype_in, dtype_out, rows, cols, full_cols, col0,
+        row_pos, row0, seed, eps, fmt, generator, nonfinite);
+    return check_launch("td_perturb");
+}
+
+int td_signed_uniforms(double* out, int64_t n, uint64_t seed, int64_t k0, int32_t generator, void* stream) {
+    if (n == 0) return 0;
+    if (!out || n < 0) return fail("td_signed_uniforms: invalid arguments");
+    k_signed_uniforms<<<grid_for(n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(out, n, seed, k0, generator);
+    return check_launch("td_signed_uniforms");
+}
+
+int td_quantize(const double* x, void* y, int32_t dtype_out, int64_t n, int32_t fmt,
+                unsigned long long* nonfinite, void* stream) {
+    if (n == 0) return 0;
+    if (!x || !y || !nonfinite || n < 0 || fmt < 0 || fmt > 3) return fail("td_quantize: invalid arguments");
+    k_quantize<<<grid_for(n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(x, static_cast<char*>(y), dtype_out,
+                                                                           n, fmt, nonfinite);
+    return check_launch("td_quantize");
+}
+
+int td_fingerprint(const void* x, int32_t dtype, int64_t n, unsigned long long* out, void* stream) {
+    if (n == 0) return 0;
+    if (!x || !out || n < 0) return fail("td_fingerprint: invalid arguments");
+    k_fingerprint<<<grid_for(n, 256 * 8, 148 * 8), 256, 0, (cudaStream_t)stream>>>(static_cast<const char*>(x),
+                                                                                 dtype, n, out);
+    return check_launch("td_fingerprint");
+}
+
+int td_box_gather(const void* src, int32_t src_dtype, double* dst, const int64_t* boxes, int32_t n_boxes,
+                  void* stream) {
+    if (n_boxes == 0) return 0;
+    if (!src || !dst || !boxes || n_boxes < 0 || n_boxes > 65535) return fail("td_box_gather: invalid arguments");
+    dim3 grid(64, (unsigned)n_boxes);
+    k_box_gather<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<const char*>(src), src_dtype, dst, boxes);
+    return check_launch("td_box_gather");
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+"""Device residency and the small single-purpose device entry points.
+
+`resolve_operands` turns a plan's operand table (trace records or raw
+arrays) into 16-byte-aligned CUDA buffers: payloads already in HBM are used
+in place, host payloads (numpy, pinned or pageable torch CPU tensors) are
+copied up on the current stream.  Everything numeric goes through the
+kernels in libtdb200.so; there is no CPU arithmetic fallback.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+
+
+def is_torch(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor)
+
+
+def _payload_of(owner):
+    return getattr(owner, "payload", owner)
+
+
+def to_device(x, stream=None):
+    """A contiguous, 16-byte-aligned CUDA tensor holding x's values in x's
+    own dtype (numpy arrays keep their dtype; f64 stays f64)."""
+    import torch
+    if not torch.cuda.is_available():
+        raise N.NativeError("no CUDA device: the B200 compare path cannot run here")
+    if not is_torch(x):
+        arr = np.ascontiguousarray(x)
+        if arr.dtype not in (np.float32, np.float64, np.float16):
+            arr = arr.astype(np.float64)
+        x = torch.from_numpy(arr)
+    if x.device.type != "cuda":
+        x = x.contiguous().to("cuda", non_blocking=x.is_pinned())
+    elif not x.is_contiguous():
+        x = x.contiguous()
+    if x.data_ptr() % 16 != 0:
+        x = x.clone()
+    return x
+
+
+_TORCH_DTYPES = None
+
+
+def resolve_operands(operands, dtypes=None) -> tuple[np.ndarray, list]:
+    """(device addresses as uint64 array, keep-alive list of tensors).
+
+    dtypes[k], when given, is the td_dtype operand k must be presented as;
+    a differing payload is widened on the device (exact: bf16/f16 < f32 < f64)."""
+    global _TORCH_DTYPES
+    import torch
+    if _TORCH_DTYPES is None:
+        _TORCH_DTYPES = {N.F32: torch.float32, N.BF16: torch.bfloat16,
+                         N.F16: torch.float16, N.F64: torch.float64}
+    keep = []
+    ptrs = np.zeros(len(operands), np.uint64)
+    memo: dict = {}
+    for k, owner in enumerate(operands):
+        t = memo.get(id(owner))
+        if t is None:
+            dev = getattr(owner, "device_payload", None)
+            t = dev() if dev is not None else to_device(_payload_of(owner))
+            memo[id(owner)] = t
+        if dtypes is not None and N.dtype_code(t) != dtypes[k]:
+            t = t.to(_TORCH_DTYPES[dtypes[k]])
+        keep.append(t)
+        ptrs[k] = t.data_ptr()
+    return ptrs, keep
+
+
+class _Raw:
+    """A bare array presented as a one-box identity-mapped record."""
+
+    __slots__ = ("tensor", "dtype_code", "shape", "mapping", "replica_group_size")
+
+    def __init__(self, tensor, replicas: int = 1):
+        from .canonical import identity_mapping
+        self.tensor = tensor
+        self.dtype_code = N.dtype_code(tensor)
+        self.shape = tuple(tensor.shape)
+        self.mapping = identity_mapping(self.shape)
+        self.replica_group_size = replicas
+
+    def device_payload(self):
+        return self.tensor
+
+
+def _one_group(ident, records, numeric):
+    from .plan import GroupMeta, IdMeta
+    meta = IdMeta(ident=ident, exec_index=0, global_shape=records[0].shape)
+    meta.groups.append(GroupMeta(records=list(records), declared_detail=None, numeric=numeric))
+    return meta
+
+
+def rel_err_pair(a, b) -> float:
+    """rel_err_arrays(a, b) on the GPU: ||a - b|| / ||a|| with the reference's
+    zero conventions (tensor.py:158-167).  Shapes must already agree."""
+    from .plan import Plan, PlanEntry
+    ra, rb = _Raw(to_device(a).reshape(-1)), _Raw(to_device(b).reshape(-1))
+    plan = Plan([PlanEntry("pair", x=_one_group("pair", [ra], False),
+                           y=_one_group("pair", [rb], False), x_rep=False, y_rep=False)])
+    ptrs, keep = resolve_operands(plan.operands, plan.operand_dtypes)
+    idres, _, _ = plan.run(ptrs)
+    return float(idres["observed"][0])
+
+
+def replica_worst(copies) -> tuple[float, int | None]:
+    """(worst, index) of max_i rel_err(copy0, copy_i), strict > so NaN never
+    wins (canonical.py:236-242); computed by td_segnorm + td_verdict."""
+    from .plan import Plan, PlanEntry
+    raws = [_Raw(to_device(c).reshape(-1), replicas=len(copies)) for c in copies]
+    worst, index = 0.0, None
+    # chunks of at most MAX_Z extra copies, each re-reading copy 0 once
+    for k in range(1, len(raws), N.MAX_Z):
+        chunk = [raws[0]] + raws[k:k + N.MAX_Z]
+        plan = Plan([PlanEntry("replicas", x=None, y=_one_group("replicas", chunk, True),
+                               x_rep=False, y_rep=True)])
+        ptrs, keep = resolve_operands(plan.operands, plan.operand_dtypes)
+        _, gres, _ = plan.run(ptrs, replica_eps=float("inf"))
+        w, i = float(gres["worst"][0]), int(gres["worst_index"][0])
+        if i > 0 and w > worst:
+            worst, index = w, k + i - 1
+    return worst, index
+
+
+def merge_boxes(shards, global_shape):
+    """td_box_gather: assemble the merged f64 tensor on the device."""
+    import torch
+    from .plan import _blocks
+    out = torch.zeros(tuple(global_shape), dtype=torch.float64, device="cuda")
+    gstrides = out.stride() if out.dim() else ()
+    for mapping, data in shards:
+        src = to_device(data)
+        code = N.dtype_code(src)
+        rows = []
+        for loc, glob in mapping.pairs:
+            for so, do, r, c, rs, ds in _blocks(loc.extents, loc.start, mapping.local_shape,
+                                                glob.start, tuple(global_shape)):
+                rows.append((so, do, r, c, rs, ds))
+        if not rows:
+            continue
+        boxes = torch.tensor(np.array(rows, np.int64).reshape(-1), dtype=torch.int64).to("cuda")
+        for k in range(0, len(rows), 65535):
+            n = min(65535, len(rows) - k)
+            N.call("td_box_gather", src.data_ptr(), code, out.data_ptr(),
+                   boxes.data_ptr() + 8 * 6 * k, n, N.stream_handle())
+    return out

@@ -1,0 +1,605 @@
+"""Host planner + executor of the compare hot path.
+
+Planning is metadata only.  For each canonical id it reproduces
+checker._merge_one (pkg/src/traindiff/checker.py:151-198) up to the
+arithmetic: rank agreement, per-axis hull, grouping of records by
+(local shape, pairs), the declared replica-group size, mapping validation
+and the merge witnesses (data-free, see canonical.py).  It then lays the
+arithmetic out as *segments* — 2-D strided blocks read in lockstep from the
+reference side (x), candidate copy 0 (y) and the candidate's replica copies
+(z) — cut from the intersections of candidate and reference global boxes, so
+the merged tensors are never materialised and every payload byte is read
+once.  Segments are split into fixed-size tiles; one persistent kernel per
+tile class (dtype x replica count) walks them (td_segnorm), then
+td_reduce_slots and td_verdict turn tile partials into per-id verdicts.
+
+A `Plan` captures structure only: it holds (record, byte offset) for every
+operand and patches device addresses in at `run()` time, so a plan built
+once for a layout can be re-run on every step's fresh payloads.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .canonical import ShardMapping, merge_problem
+from .errors import MappingInvalid, MergeConflict, ShapeMismatch
+
+VERDICT_NAMES = {N.PASS: "pass", N.FLAG: "flag", N.REPLICA: "replica-mismatch",
+                 N.MERGE: "merge-error", N.MISSING: "missing"}
+MAX_UNITS = 1 << 30          # per-segment unit cap (kernel uses 32-bit unit indices)
+_VEC_DTYPES = (N.F32, N.BF16, N.F16)
+
+
+# ---------------------------------------------------------------------------
+# merge metadata (checker.py:151-198 without the arithmetic)
+
+@dataclass
+class GroupMeta:
+    records: list                 # copies of one shard, record order
+    declared_detail: str | None   # replica-size declaration problem, if any
+    numeric: bool                 # copies need the device rel_err check
+
+
+@dataclass
+class IdMeta:
+    ident: str
+    exec_index: int
+    groups: list = field(default_factory=list)
+    global_shape: tuple | None = None
+    rank_problem: bool = False
+    merge_detail: str | None = None
+
+    @property
+    def merge_ok(self) -> bool:
+        return not self.rank_problem and self.merge_detail is None
+
+    @property
+    def declared_problem(self) -> str | None:
+        for g in self.groups:
+            if g.declared_detail is not None:
+                return g.declared_detail
+        return None
+
+
+def id_meta(ident: str, entries: list, replica_check: bool = True) -> IdMeta:
+    """entries: [(exec index, TraceRecord)] sorted by exec index."""
+    meta = IdMeta(ident=ident, exec_index=entries[0][0])
+    ranks = {len(rec.mapping.global_shape) for _, rec in entries}
+    if len(ranks) != 1:
+        meta.rank_problem = True
+        meta.merge_detail = "records disagree on tensor rank"
+        return meta
+    (ndim,) = ranks
+    hull = tuple(max(rec.mapping.global_shape[a] for _, rec in entries) for a in range(ndim))
+    meta.global_shape = hull
+    buckets: dict[tuple, list] = {}
+    for _, rec in entries:
+        key = (rec.mapping.local_shape,
+               tuple((loc.bounds, glob.bounds) for loc, glob in rec.mapping.pairs))
+        buckets.setdefault(key, []).append(rec)
+    for recs in buckets.values():
+        detail = None
+        numeric = False
+        if replica_check:
+            declared = {rec.replica_group_size for rec in recs}
+            if declared != {len(recs)}:
+                detail = (f"{len(recs)} copies of one shard, declared replica group size "
+                          f"{sorted(declared)}")
+            else:
+                numeric = len(recs) > 1
+        meta.groups.append(GroupMeta(records=recs, declared_detail=detail, numeric=numeric))
+    mappings = [ShardMapping(g.records[0].mapping.local_shape, hull, g.records[0].mapping.pairs)
+                for g in meta.groups]
+    err = merge_problem(mappings, hull, [tuple(g.records[0].shape) for g in meta.groups])
+    if err is not None:
+        meta.merge_detail = str(err)
+    return meta
+
+
+def merge_view(trace, replica_check: bool = True) -> dict[str, IdMeta]:
+    """Per-id merge metadata in first-appearance order (checker.py:201-211)."""
+    view = {}
+    for ident, entries in trace.by_id().items():
+        view[ident] = id_meta(ident, sorted(entries, key=lambda p: p[0]), replica_check)
+    return view
+
+
+# ---------------------------------------------------------------------------
+# segment construction
+
+def _magic(d: int) -> tuple[int, int]:
+    """(m, p) with floor(n / d) == (n * m) >> p for 0 <= n < 2^31."""
+    l = (d - 1).bit_length()
+    p = 31 + l
+    return (1 << p) // d + (1 if (1 << p) % d else 0), p
+
+
+def _strides(shape: tuple) -> list[int]:
+    out, acc = [0] * len(shape), 1
+    for a in range(len(shape) - 1, -1, -1):
+        out[a] = acc
+        acc *= shape[a]
+    return out
+
+
+def _blocks(ext, x_start, x_shape, y_start, y_shape):
+    """Decompose an N-d box (extents `ext`) read at x_start in an array of
+    x_shape and at y_start in y_shape into 2-D strided blocks:
+    yields (x_off, y_off, rows, cols, x_row_stride, y_row_stride) in elements."""
+    d = len(ext)
+    if any(e == 0 for e in ext):
+        return
+    if d == 0:
+        yield 0, 0, 1, 1, 1, 1
+        return
+    xs, ys = _strides(x_shape), _strides(y_shape)
+    k = d - 1
+    while k > 0 and ext[k] == x_shape[k] and ext[k] == y_shape[k]:
+        k -= 1
+    cols = math.prod(ext[k:])
+    if k == 0:
+        rows, rx, ry, outer = 1, cols, cols, []
+    else:
+        rows, rx, ry, outer = ext[k - 1], xs[k - 1], ys[k - 1], list(range(k - 1))
+    base_x = sum(x_start[a] * xs[a] for a in range(d) if a not in outer)
+    base_y = sum(y_start[a] * ys[a] for a in range(d) if a not in outer)
+    for combo in np.ndindex(*[ext[a] for a in outer]) if outer else [()]:
+        ox = base_x + sum((x_start[a] + i) * xs[a] for a, i in zip(outer, combo))
+        oy = base_y + sum((y_start[a] + i) * ys[a] for a, i in zip(outer, combo))
+        yield ox, oy, rows, cols, rx, ry
+
+
+@dataclass
+class _Operand:
+    slot: int        # index into the plan's operand table
+    dtype: int
+    esize: int
+
+
+class PlanBuilder:
+    """Accumulates segments; operands are registered payloads (records)."""
+
+    def __init__(self, force_generic: bool = False):
+        self.force_generic = force_generic
+        self.operands: list = []          # payload owners (records or raw tensors)
+        self.operand_dtypes: list = []    # dtype each operand is read as
+        self._operand_index: dict = {}
+        self.seg_rows: list = []          # (xs, xoff, ys, yoff, zs, rows, cols, rx, ry, tile_begin, n_units, vec_ok)
+        self.n_tiles = 0
+        self.classes: dict = {}           # class key -> list of (tile_begin, n_tiles)
+
+    def operand(self, owner, dtype: int) -> _Operand:
+        """Register `owner`'s payload, to be presented to the kernel as `dtype`
+        (a widening cast at resolution time when the stored dtype differs)."""
+        key = (id(owner), dtype)
+        slot = self._operand_index.get(key)
+        if slot is None:
+            slot = len(self.operands)
+            self.operands.append(owner)
+            self.operand_dtypes.append(dtype)
+            self._operand_index[key] = slot
+        return _Operand(slot, dtype, N.DTYPE_SIZE[dtype])
+
+    def add(self, x: _Operand | None, x_off: int, y: _Operand, y_off: int, zs: list,
+            rows: int, cols: int, rx: int, ry: int) -> None:
+        if rows == 0 or cols == 0:
+            return
+        same = [y.dtype] + [z.dtype for z in zs] + ([x.dtype] if x is not None else [])
+        vec_dtype = (not self.force_generic and same[0] in _VEC_DTYPES
+                     and all(d == same[0] for d in same))
+        esize = y.esize
+        # row-stride alignment is a property of the layout; base alignment is
+        # re-checked against live addresses at run time
+        vec = (vec_dtype and cols % 8 == 0
+               and (rows == 1 or ((ry * esize) % 16 == 0
+                                  and (x is None or (rx * x.esize) % 16 == 0)))
+               and (x_off * (x.esize if x else 0)) % 16 == 0 and (y_off * esize) % 16 == 0)
+        unit = 8 if vec else 1
+        upr = cols // unit
+        if rows == 1:
+            step = max(unit, (MAX_UNITS // 1) * unit)
+            for c0 in range(0, cols, step):
+                cc = min(step, cols - c0)
+                self._emit(x, x_off + c0, y, y_off + c0, zs, 1, cc, rx, ry, vec)
+            return
+        rows_per = max(1, MAX_UNITS // max(upr, 1))
+        if upr > MAX_UNITS:
+            for r in range(rows):
+                self.add(x, x_off + r * rx, y, y_off + r * ry, zs, 1, cols, rx, ry)
+            return
+        for r0 in range(0, rows, rows_per):
+            rr = min(rows_per, rows - r0)
+            self._emit(x, x_off + r0 * rx, y, y_off + r0 * ry, zs, rr, cols, rx, ry, vec)
+
+    def _emit(self, x, x_off, y, y_off, zs, rows, cols, rx, ry, vec):
+        unit = 8 if vec else 1
+        n_units = rows * cols // unit
+        n_tiles = -(-n_units // N.TILE_UNITS)
+        self.seg_rows.append((x, x_off, y, y_off, list(zs), rows, cols, rx, ry,
+                              self.n_tiles, n_units, vec))
+        self.n_tiles += n_tiles
+
+    @property
+    def tile_cursor(self) -> int:
+        return self.n_tiles
+
+
+# ---------------------------------------------------------------------------
+# plans
+
+@dataclass
+class PlanEntry:
+    ident: str
+    x: IdMeta | None          # reference side (or base in tolerance estimation)
+    y: IdMeta | None          # candidate side
+    x_rep: bool               # run numeric replica checks on x's groups
+    y_rep: bool
+    tolerance: float = 0.0
+
+
+class Plan:
+    """Frozen layout of one comparison; `run()` executes it on the GPU."""
+
+    def __init__(self, entries: list[PlanEntry], static: tuple[float, float] | None = None):
+        """static=(atol, rtol) builds compare_static's plan: the elementwise
+        failure count replaces d2 (generic walker, no replica checks)."""
+        self.entries = entries
+        self.static = static
+        b = PlanBuilder(force_generic=static is not None)
+        id_rows = []
+        group_rows = []
+        self.group_owner = []     # (entry index, side, group index)
+        for ei, e in enumerate(entries):
+            t0 = b.tile_cursor
+            has_compare = (e.x is not None and e.y is not None and e.x.merge_ok and e.y.merge_ok
+                           and e.x.global_shape == e.y.global_shape)
+            cg0 = len(group_rows)
+            if e.y is not None and not e.y.rank_problem:
+                for gi, g in enumerate(e.y.groups):
+                    rep = e.y_rep and g.numeric
+                    if len(g.records) - 1 > N.MAX_Z and rep:
+                        raise NotImplementedError(
+                            f"{e.ident}: replica groups of more than {N.MAX_Z + 1} copies")
+                    s0 = b.tile_cursor
+                    y0 = g.records[0]
+                    gdt = _group_dtype(g.records) if rep else y0.dtype_code
+                    yop = b.operand(y0, gdt)
+                    zops = [b.operand(r, gdt) for r in g.records[1:]] if rep else []
+                    if has_compare:
+                        self._compare_runs(b, e.x, y0, yop, zops)
+                        if zops:
+                            self._replica_remainder(b, y0, yop, zops)
+                    elif zops:
+                        n = math.prod(y0.shape)
+                        b.add(None, 0, yop, 0, zops, 1, n, n, n)
+                    if zops:
+                        group_rows.append((s0, b.tile_cursor, len(zops)))
+                        self.group_owner.append((ei, 0, gi))
+            cg1 = len(group_rows)
+            rg0 = len(group_rows)
+            if e.x is not None and e.x_rep and not e.x.rank_problem:
+                for gi, g in enumerate(e.x.groups):
+                    if not g.numeric:
+                        continue
+                    if len(g.records) - 1 > N.MAX_Z:
+                        raise NotImplementedError(
+                            f"{e.ident}: replica groups of more than {N.MAX_Z + 1} copies")
+                    s0 = b.tile_cursor
+                    x0 = g.records[0]
+                    gdt = _group_dtype(g.records)
+                    yop = b.operand(x0, gdt)
+                    zops = [b.operand(r, gdt) for r in g.records[1:]]
+                    n = math.prod(x0.shape)
+                    b.add(None, 0, yop, 0, zops, 1, n, n, n)
+                    group_rows.append((s0, b.tile_cursor, len(zops)))
+                    self.group_owner.append((ei, 1, gi))
+            rg1 = len(group_rows)
+            cand_host = 0
+            if e.y is not None:
+                if e.y.declared_problem is not None:
+                    cand_host = N.REPLICA
+                elif not e.y.merge_ok:
+                    cand_host = N.MERGE
+            ref_host = 0
+            if e.x is not None:
+                if e.x.declared_problem is not None:
+                    ref_host = N.REPLICA
+                elif not e.x.merge_ok:
+                    ref_host = N.MERGE
+            id_rows.append((t0, b.tile_cursor, cg0, cg1, rg0, rg1, int(has_compare),
+                            cand_host, ref_host, 0, float(e.tolerance)))
+        self.builder = b
+        self.n_tiles = b.n_tiles
+        self.ids = np.array(id_rows, dtype=N.ID_DESC) if id_rows else np.zeros(0, N.ID_DESC)
+        self.groups = (np.array(group_rows, dtype=[("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")])
+                       if group_rows else np.zeros(0, [("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")]))
+        self._freeze_segments()
+
+    # -- geometry -------------------------------------------------------------
+
+    @staticmethod
+    def _compare_runs(b: PlanBuilder, xmeta: IdMeta, y0, yop, zops) -> None:
+        """Runs = candidate global boxes cut by reference global boxes."""
+        for yl, yg in y0.mapping.pairs:
+            for h in xmeta.groups:
+                x0 = h.records[0]
+                xop = None
+                for xl, xg in x0.mapping.pairs:
+                    cut = []
+                    for (a0, a1), (b0, b1) in zip(yg.bounds, xg.bounds):
+                        lo, hi = max(a0, b0), min(a1, b1)
+                        if lo >= hi:
+                            cut = None
+                            break
+                        cut.append((lo, hi))
+                    if cut is None:
+                        continue
+                    if xop is None:
+                        xop = b.operand(x0, x0.dtype_code)
+                    ext = tuple(hi - lo for lo, hi in cut)
+                    ys = tuple(l0 + (c0 - g0) for (l0, _), (g0, _), (c0, _) in zip(yl.bounds, yg.bounds, cut))
+                    xs = tuple(l0 + (c0 - g0) for (l0, _), (g0, _), (c0, _) in zip(xl.bounds, xg.bounds, cut))
+                    for xo, yo, rows, cols, rx, ry in _blocks(ext, xs, x0.mapping.local_shape,
+                                                              ys, y0.mapping.local_shape):
+                        b.add(xop, xo, yop, yo, zops, rows, cols, rx, ry)
+        if not y0.mapping.pairs:
+            return
+
+    @staticmethod
+    def _replica_remainder(b: PlanBuilder, y0, yop, zops) -> None:
+        """Replica sums over payload cells no local box covers (usually none)."""
+        shape = y0.mapping.local_shape
+        covered = sum(loc.volume for loc, _ in y0.mapping.pairs)
+        if covered == math.prod(shape):
+            return
+        pieces = [tuple((0, n) for n in shape)]
+        for loc, _ in y0.mapping.pairs:
+            nxt = []
+            for p in pieces:
+                nxt.extend(_subtract(p, loc.bounds))
+            pieces = nxt
+        for p in pieces:
+            ext = tuple(hi - lo for lo, hi in p)
+            st = tuple(lo for lo, _ in p)
+            for _, yo, rows, cols, _, ry in _blocks(ext, st, shape, st, shape):
+                b.add(None, 0, yop, yo, zops, rows, cols, ry, ry)
+
+    # -- device tables ----------------------------------------------------------
+
+    def _freeze_segments(self) -> None:
+        rows = self.builder.seg_rows
+        n = len(rows)
+        segs = np.zeros(n, dtype=N.SEGMENT)
+        self.seg_xslot = np.full(n, -1, np.int64)
+        self.seg_xoff = np.zeros(n, np.int64)     # bytes
+        self.seg_yslot = np.zeros(n, np.int64)
+        self.seg_yoff = np.zeros(n, np.int64)
+        self.seg_zslot = np.full((n, N.MAX_Z), -1, np.int64)
+        tile_seg = np.zeros(self.n_tiles, np.int32)
+        class_tiles: dict = {}
+        for i, (x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec) in enumerate(rows):
+            s = segs[i]
+            s["x_stride"], s["y_stride"], s["rows"], s["cols"] = rx, ry, r, c
+            s["tile_begin"], s["n_units"] = tb, nu
+            s["x_dtype"] = x.dtype if x is not None else y.dtype
+            s["y_dtype"], s["nz"] = y.dtype, len(zs)
+            s["flags"] = (N.SEG_HAS_X if x is not None else 0) | (N.SEG_VEC if vec else 0)
+            m, p = _magic(c // 8 if vec else c)
+            s["div_m"], s["div_p"] = m, p
+            if x is not None:
+                self.seg_xslot[i], self.seg_xoff[i] = x.slot, xo * x.esize
+            self.seg_yslot[i], self.seg_yoff[i] = y.slot, yo * y.esize
+            for j, z in enumerate(zs):
+                self.seg_zslot[i, j] = z.slot
+            nt = -(-nu // N.TILE_UNITS)
+            tile_seg[tb:tb + nt] = i
+            key = (bool(vec), y.dtype, len(zs), x is not None)
+            class_tiles.setdefault(key, []).append((tb, nt))
+        self.segs = segs
+        self.tile_seg = tile_seg
+        self.class_keys = sorted(class_tiles)
+        self.class_lists = [np.concatenate([np.arange(tb, tb + nt, dtype=np.int32)
+                                            for tb, nt in class_tiles[k]]) for k in self.class_keys]
+        self.operands = self.builder.operands
+        self.operand_dtypes = self.builder.operand_dtypes
+        self.algorithmic_bytes = 0
+        for x, _, y, _, zs, r, c, *_ in rows:
+            per = y.esize * (1 + len(zs)) + (x.esize if x is not None else 0)
+            self.algorithmic_bytes += r * c * per
+
+    # -- execution ----------------------------------------------------------------
+
+    def run(self, pointers: np.ndarray, *, kappa: float = 3.0, eps: float = 0.0,
+            replica_eps: float = 0.0, stream=None, timing: dict | None = None,
+            sums: dict | None = None):
+        """Execute once on the current CUDA device; pointers[k] is the device
+        address of operand k.  Returns (id results, group results, near ties)."""
+        prep = self.prepare(pointers, kappa=kappa, eps=eps, replica_eps=replica_eps, stream=stream)
+        prep.launch(timing=timing)
+        out = prep.fetch()
+        if timing is not None:
+            prep.read_timing(timing)
+        if sums is not None:
+            sums.update(prep.sums())
+        return out
+
+    def prepare(self, pointers: np.ndarray, *, kappa: float = 3.0, eps: float = 0.0,
+                replica_eps: float = 0.0, stream=None) -> "Prepared":
+        """Patch live addresses into the segment table and stage every
+        device-side table and workspace; the result can be launched repeatedly."""
+        return Prepared(self, pointers, kappa, eps, replica_eps, stream)
+
+
+class Prepared:
+    """A plan bound to payload addresses, with its tables resident in HBM."""
+
+    def __init__(self, plan: Plan, pointers, kappa, eps, replica_eps, stream):
+        import torch
+        self.plan = plan
+        self.kappa, self.eps, self.replica_eps = float(kappa), float(eps), float(replica_eps)
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        n_ids, n_groups = len(plan.ids), len(plan.groups)
+        self.n_ids, self.n_groups = n_ids, n_groups
+        segs = plan.segs.copy()
+        pointers = np.asarray(pointers, dtype=np.uint64)
+        has_x = plan.seg_xslot >= 0
+        segs["x"][has_x] = pointers[plan.seg_xslot[has_x]] + plan.seg_xoff[has_x].astype(np.uint64)
+        segs["y"] = pointers[plan.seg_yslot] + plan.seg_yoff.astype(np.uint64)
+        zmask = plan.seg_zslot >= 0
+        zaddr = np.zeros(plan.seg_zslot.shape, dtype=np.uint64)
+        zaddr[zmask] = pointers[plan.seg_zslot[zmask]] + \
+            np.repeat(plan.seg_yoff[:, None], N.MAX_Z, 1)[zmask].astype(np.uint64)
+        segs["z"] = zaddr
+        # vector walkers need 16-byte aligned bases; operand resolution
+        # (device.resolve_operands) guarantees it, so a violation is a bug
+        if len(segs):
+            vec = (segs["flags"] & N.SEG_VEC) != 0
+            mis = ((segs["y"] % 16) != 0) | (has_x & ((segs["x"] % 16) != 0)) | \
+                  (zmask & ((zaddr % 16) != 0)).any(axis=1)
+            if (vec & mis).any():
+                raise N.NativeError("vector segment with a misaligned operand address")
+        dev = torch.device("cuda", torch.cuda.current_device())
+        parts, offsets = [], []
+        cursor = 0
+
+        def put(arr):
+            nonlocal cursor
+            raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+            pad = (-cursor) % 16
+            if pad:
+                parts.append(np.zeros(pad, np.uint8))
+                cursor += pad
+            offsets.append(cursor)
+            parts.append(raw)
+            cursor += raw.size
+
+        gdesc = np.zeros(n_groups, N.GROUP_DESC)
+        if n_groups:
+            gdesc["tile_begin"] = plan.groups["tile_begin"]
+            gdesc["tile_end"] = plan.groups["tile_end"]
+            gdesc["nz"] = plan.groups["nz"]
+        put(segs)
+        put(plan.tile_seg)
+        for lst in plan.class_lists:
+            put(lst)
+        put(plan.ids)
+        put(gdesc)
+        blob = np.concatenate(parts) if parts else np.zeros(16, np.uint8)
+        host = torch.from_numpy(blob).pin_memory()
+        self.tables = torch.empty(blob.size, dtype=torch.uint8, device=dev)
+        with torch.cuda.stream(self.stream):
+            self.tables.copy_(host, non_blocking=True)
+        self._host_blob = host                    # keep the pinned source alive
+        base = self.tables.data_ptr()
+        self.seg_ptr, self.tseg_ptr = base + offsets[0], base + offsets[1]
+        n_cls = len(plan.class_lists)
+        self.ids_ptr = base + offsets[2 + n_cls]
+        self.grp_ptr = base + offsets[3 + n_cls]
+        self.n_part = max(1, plan.n_tiles * N.PARTIAL_STRIDE)
+        self.work = torch.empty(self.n_part + 2 * n_ids + N.SLOT_STRIDE * n_groups,
+                                dtype=torch.float64, device=dev)
+        self.part_ptr = self.work.data_ptr()
+        self.idsum_ptr = self.part_ptr + 8 * self.n_part
+        self.gsum_ptr = self.idsum_ptr + 8 * 2 * n_ids
+        self.res_bytes = N.ID_RESULT.itemsize * n_ids + N.GROUP_RESULT.itemsize * n_groups + 8
+        self.res = torch.zeros(self.res_bytes, dtype=torch.uint8, device=dev)
+        self.idres_ptr = self.res.data_ptr()
+        self.gres_ptr = self.idres_ptr + N.ID_RESULT.itemsize * n_ids
+        self.tie_ptr = self.gres_ptr + N.GROUP_RESULT.itemsize * n_groups
+        mode = N.MODE_STATIC if plan.static else N.MODE_NORMS
+        atol, rtol = plan.static if plan.static else (0.0, 0.0)
+        self.classes = np.zeros(len(plan.class_keys), N.CLASS)
+        for k, (vec, dt, nz, hx) in enumerate(plan.class_keys):
+            self.classes[k] = (base + offsets[2 + k], len(plan.class_lists[k]), dt, nz, int(hx),
+                               int(vec), mode, 0, atol, rtol)
+        self.launches_per_run = len(self.classes) + 2
+        self._events = None
+
+    def launch(self, timing: dict | None = None) -> None:
+        """Enqueue td_segnorm (one launch per tile class), td_reduce_slots
+        and td_verdict on the plan's stream; no host synchronisation."""
+        import torch
+        sh = N.stream_handle(self.stream)
+        self.res[-8:].zero_()
+        ev = None
+        if timing is not None:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            ev[0].record(self.stream)
+        if len(self.classes):
+            N.call("td_segnorm", self.seg_ptr, self.tseg_ptr, self.classes.ctypes.data,
+                   len(self.classes), self.part_ptr, 0, sh)
+        if ev:
+            ev[1].record(self.stream)
+        N.call("td_reduce_slots", self.ids_ptr, self.n_ids, self.grp_ptr, self.n_groups,
+               self.part_ptr, self.idsum_ptr, self.gsum_ptr, sh)
+        N.call("td_verdict", self.ids_ptr, self.n_ids, self.grp_ptr, self.n_groups,
+               self.idsum_ptr, self.gsum_ptr, self.kappa, self.eps, self.replica_eps,
+               self.idres_ptr, self.gres_ptr, self.tie_ptr, sh)
+        if ev:
+            ev[2].record(self.stream)
+        self._events = ev
+
+    def read_timing(self, timing: dict) -> None:
+        ev = self._events
+        if ev:
+            ev[2].synchronize()
+            timing["segnorm_ms"] = ev[0].elapsed_time(ev[1])
+            timing["verdict_ms"] = ev[1].elapsed_time(ev[2])
+
+    def fetch(self):
+        """D2H of the packed results (synchronises the stream)."""
+        import torch
+        with torch.cuda.stream(self.stream):
+            raw = self.res.cpu().numpy()
+        n_ids, n_groups = self.n_ids, self.n_groups
+        idres = raw[:N.ID_RESULT.itemsize * n_ids].view(N.ID_RESULT)
+        lo = N.ID_RESULT.itemsize * n_ids
+        gres = raw[lo:lo + N.GROUP_RESULT.itemsize * n_groups].view(N.GROUP_RESULT)
+        ties = int(raw[-8:].view(np.uint64)[0])
+        return idres, gres, ties
+
+    def sums(self) -> dict:
+        """Per-id (d2, x2) and per-group (y2, z2...) sums, as reduced on the device."""
+        with __import__("torch").cuda.stream(self.stream):
+            flat = self.work[self.n_part:].cpu().numpy()
+        return {"id": flat[:2 * self.n_ids].reshape(self.n_ids, 2),
+                "group": flat[2 * self.n_ids:].reshape(self.n_groups, N.SLOT_STRIDE)}
+
+
+def _group_dtype(records) -> int:
+    """One dtype every copy of a replica group can be read as without loss."""
+    codes = {r.dtype_code for r in records}
+    if len(codes) == 1:
+        return codes.pop()
+    if N.F64 in codes:
+        return N.F64
+    return N.F32
+
+
+def _subtract(box: tuple, cut: tuple) -> list:
+    """box minus cut as disjoint boxes (bound tuples)."""
+    inter = []
+    for (a0, a1), (b0, b1) in zip(box, cut):
+        lo, hi = max(a0, b0), min(a1, b1)
+        if lo >= hi:
+            return [box]
+        inter.append((lo, hi))
+    out = []
+    rest = list(box)
+    for axis, (lo, hi) in enumerate(inter):
+        a0, a1 = rest[axis]
+        if a0 < lo:
+            piece = list(rest)
+            piece[axis] = (a0, lo)
+            out.append(tuple(piece))
+        if hi < a1:
+            piece = list(rest)
+            piece[axis] = (hi, a1)
+            out.append(tuple(piece))
+        rest[axis] = (lo, hi)
+    return out

@@ -1,0 +1,146 @@
+"""Synthetic traces of the named model shapes, built directly in HBM.
+
+The reference is the single-device layout (identity mappings) of `model`;
+the candidate is `pcfg`'s layout from layout.emit_records.  Values: the
+reference tensor of each id is N(0, sigma_kind) rounded to the storage
+dtype; the candidate's logical tensor is Q(ref * (1 + eps*u)) with u from
+the counter-based stream tagged "cand|{id}" (td_perturb — simulated
+round-off), and each candidate record holds its shard of it, laid out
+through its own ShardMapping (replicas are separate allocations, so every
+copy is real memory traffic).  Optional bugs corrupt chosen ids the way the
+config-3 injections do (wrong shard order, missing allreduce, scale error).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from .canonical import identity_mapping, parse_canonical
+from .layout import ModelShape, ParallelConfig, emit_records
+from .perturb import PerturbSpec, apply_perturbation
+from .tracestore import RankMeta, Trace, TraceRecord
+
+SIGMA = {"Param": 0.02, "MainGrad": 1e-3, "ParamGrad": 1e-3, "ActivationGradIn": 1e-3,
+         "ActivationGradOut": 1e-3}
+
+
+def _sigma(kind: str) -> float:
+    return SIGMA.get(kind, 1.0)
+
+
+def _fill(shape, kind, vocab, gen, dtype):
+    import torch
+    if kind == "ActivationIn" and len(shape) == 1:
+        # token ids entering the embedding
+        return torch.randint(0, vocab, shape, generator=gen, device="cuda").to(dtype)
+    return (torch.randn(shape, generator=gen, device="cuda") * _sigma(kind)).to(dtype)
+
+
+def _shard(full, mapping):
+    import torch
+    out = torch.empty(mapping.local_shape, dtype=full.dtype, device=full.device)
+    for loc, glob in mapping.pairs:
+        out[loc.as_slices()] = full[glob.as_slices()]
+    return out
+
+
+def build(model: ModelShape, pcfg: ParallelConfig, *, dtype=None, seed: int = 0,
+          eps: float = 2.0 ** -8, bugs: dict | None = None, header: dict | None = None):
+    """(reference trace, candidate trace), payloads resident in HBM.
+
+    bugs: {id_string: "scale" | "order" | "partial"} corruptions of the
+    candidate (scale error x tp; TP shards swapped under unchanged maps;
+    per-rank partial sums left unreduced)."""
+    import torch
+    dtype = dtype or torch.bfloat16
+    bugs = bugs or {}
+    hdr = header or {"digest": f"synthetic-{model}-{seed}", "mode": "cascade"}
+    ref_specs = emit_records(model, ParallelConfig(microbatches=pcfg.microbatches))
+    cand_specs = emit_records(model, pcfg)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    ref = Trace(header=dict(hdr))
+    full: dict = {}
+    policy = "bf16" if dtype == torch.bfloat16 else "fp32"
+    for s in ref_specs:
+        kind = s.ident.split("|")[2][5:]
+        x = _fill(s.mapping.global_shape, kind, model.vocab, gen, dtype)
+        ref.records.append(TraceRecord(parse_canonical(s.ident), RankMeta(*s.rank), s.mapping,
+                                       s.replica, x, s.module_class))
+        full[s.ident] = x
+    cand = Trace(header=dict(hdr))
+    cand_full: dict = {}
+    order: dict = {}
+    for s in cand_specs:
+        if s.ident not in cand_full:
+            x = full.get(s.ident)
+            if x is None:
+                kind = s.ident.split("|")[2][5:]
+                x = _fill(s.mapping.global_shape, kind, model.vocab, gen, dtype)
+            shape = x.shape
+            y = x if x.dim() == 0 else apply_perturbation(
+                x.reshape(-1, shape[-1]) if x.dim() > 1 else x.reshape(1, -1),
+                "cand|" + s.ident, PerturbSpec(0, eps), policy=policy).reshape(shape)
+            if bugs.get(s.ident) == "scale":
+                y = (y.float() * pcfg.tp).to(dtype)
+            cand_full[s.ident] = y
+        y = cand_full[s.ident]
+        payload = _shard(y, s.mapping)
+        bug = bugs.get(s.ident)
+        if bug == "order":
+            order.setdefault(s.ident, []).append(len(cand.records))
+        if bug == "partial" and payload.numel():
+            payload = (payload.float() / pcfg.tp * (1 + s.rank[1])).to(dtype)
+        cand.records.append(TraceRecord(parse_canonical(s.ident), RankMeta(*s.rank), s.mapping,
+                                        s.replica, payload, s.module_class))
+    for ident, idx in order.items():
+        # swap the first two TP shards' payloads under unchanged maps
+        if len(idx) >= 2:
+            a, b = cand.records[idx[0]], cand.records[idx[1]]
+            if a.shape == b.shape:
+                a.payload, b.payload = b.payload, a.payload
+    return ref, cand
+
+
+def flat_tolerances(trace, value: float) -> dict:
+    return {rec.id.encode(): value for rec in trace.records}
+
+
+def sweep_pair(n_bytes: int, *, maps: str = "identity", g: int = 1, dtype=None, seed: int = 0,
+               eps: float = 2.0 ** -8):
+    """Config 5: one id of n_bytes per tensor, shape (N/4096, 4096), candidate
+    split `g` ways by columns ("columns") or CP-striped in 2 pairs ("stripes")."""
+    import torch
+    from .canonical import CanonicalId, ShardMapping, SliceBox, TensorKind
+    dtype = dtype or torch.bfloat16
+    esize = torch.tensor([], dtype=dtype).element_size()
+    cols = 4096
+    rows = max(1, n_bytes // esize // cols)
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randn((rows, cols), generator=gen, device="cuda").to(dtype)
+    ident = CanonicalId(0, 0, TensorKind.ACTIVATION_OUT, f"sweep.{n_bytes}")
+    hdr = {"digest": "sweep", "mode": "cascade"}
+    ref = Trace(hdr, [TraceRecord(ident, RankMeta(), identity_mapping((rows, cols)), 1, x, "Sweep")])
+    y = apply_perturbation(x, "cand|" + ident.encode(), PerturbSpec(0, eps),
+                           policy="bf16" if dtype == torch.bfloat16 else "fp32")
+    cand = Trace(hdr, [])
+    if maps == "identity":
+        cand.records.append(TraceRecord(ident, RankMeta(), identity_mapping((rows, cols)), 1, y, "Sweep"))
+    elif maps == "columns":
+        w = cols // g
+        for t in range(g):
+            m = ShardMapping((rows, w), (rows, cols),
+                             ((SliceBox(((0, rows), (0, w))), SliceBox(((0, rows), (t * w, (t + 1) * w)))),))
+            cand.records.append(TraceRecord(ident, RankMeta(tp=t), m, 1, _shard(y, m), "Sweep"))
+    elif maps == "stripes":
+        ch = rows // (2 * g)
+        for c in range(g):
+            pieces = [((0, ch), (c * ch, (c + 1) * ch)),
+                      ((ch, 2 * ch), ((2 * g - 1 - c) * ch, (2 * g - c) * ch))]
+            pairs = tuple((SliceBox((l, (0, cols))), SliceBox((gg, (0, cols)))) for l, gg in pieces)
+            m = ShardMapping((2 * ch, cols), (rows, cols), pairs)
+            cand.records.append(TraceRecord(ident, RankMeta(cp=c), m, 1, _shard(y, m), "Sweep"))
+    else:
+        raise ValueError(maps)
+    return ref, cand

@@ -1,0 +1,291 @@
+"""GPU parity: the sm_100a path against the golden reference outputs and
+the CPU oracle.  Norms agree within 1e-12 relative (fp64 accumulation in a
+different order than numpy's pairwise sum); verdicts, details, witnesses,
+quantised values and random streams agree exactly."""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import traindiff_oracle as O  # noqa: E402
+import paper_2506_09280_b200 as td  # noqa: E402
+from paper_2506_09280_b200.canonical import (CanonicalId, ShardMapping, SliceBox,  # noqa: E402
+                                             TensorKind, identity_mapping)
+from paper_2506_09280_b200.tracestore import RankMeta, Trace, TraceRecord, trace_from_bytes  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+REL = 1e-12
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _close(a, b, rel=REL):
+    if a is None or b is None:
+        return a is None and b is None
+    if isinstance(a, str) or isinstance(b, str):
+        return a == b
+    if math.isnan(a) or math.isnan(b):
+        return math.isnan(a) and math.isnan(b)
+    if math.isinf(a) or math.isinf(b):
+        return a == b
+    return abs(a - b) <= rel * max(abs(a), abs(b)) or a == b
+
+
+def assert_reports_match(got: dict, want: dict, label=""):
+    assert got["summary"] == want["summary"], label
+    assert got["earliest_flag"] == want["earliest_flag"], label
+    assert got["earliest_divergence"] == want["earliest_divergence"], label
+    assert got["exit_code"] == want["exit_code"], label
+    assert got["mode"] == want["mode"] and got["format"] == want["format"], label
+    assert len(got["entries"]) == len(want["entries"]), label
+    for g, w in zip(got["entries"], want["entries"]):
+        assert g["id"] == w["id"], label
+        assert g["verdict"] == w["verdict"], (label, g["id"], g, w)
+        assert g["detail"] == w["detail"], (label, g["id"])
+        assert g["tolerance"] == w["tolerance"] and g["threshold"] == w["threshold"], (label, g["id"])
+        assert _close(g["observed"], w["observed"]), (label, g["id"], g["observed"], w["observed"])
+
+
+def _bf16_device(trace):
+    """Same trace with payloads moved to HBM as bf16 (exact: bf16-grid values)."""
+    out = Trace(header=trace.header, raw_header=trace.raw_header)
+    for r in trace.records:
+        t = torch.from_numpy(r.payload).cuda()
+        b = t.to(torch.bfloat16)
+        assert torch.equal(b.float(), t)
+        out.records.append(TraceRecord(r.id, r.rank_meta, r.mapping, r.replica_group_size, b,
+                                       r.module_class))
+    return out
+
+
+@pytest.mark.parametrize("payloads", ["host-f32", "device-bf16"])
+def test_check_reproduces_reference_reports(cases, golden_trace_bytes, payloads):
+    near = 0
+    for case in cases["checks"]:
+        if payloads == "device-bf16" and case["fmt"] != "BF16":
+            continue
+        ref = trace_from_bytes(golden_trace_bytes(case["ref"]))
+        cand = trace_from_bytes(golden_trace_bytes(case["cand"]))
+        if payloads == "device-bf16":
+            ref, cand = _bf16_device(ref), _bf16_device(cand)
+        tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+        rep = td.check(ref, cand, tol, case["kappa"], fmt=td.FloatFormat(case["fmt"]))
+        near += rep.near_ties
+        got = json.loads(td.render_report(rep, "json"))
+        assert_reports_match(got, json.loads(case["report"]), case["name"])
+    assert near == 0
+
+
+def test_estimate_tolerance_reproduces_reference(cases, golden_trace_bytes):
+    for est in cases["estimates"]:
+        base = trace_from_bytes(golden_trace_bytes(est["base"]), device="cuda")
+        pert = [trace_from_bytes(golden_trace_bytes(p), device="cuda") for p in est["perturbed"]]
+
+        def runner(spec):
+            return base if spec is None else pert[spec.sample]
+        tol = td.estimate_tolerance(runner, n_samples=len(pert), eps_p=est["eps_p"],
+                                    aggregation=est["aggregation"])
+        want = json.loads(est["tol"])
+        assert tol.n_samples == want["n_samples"] and tol.aggregation == want["aggregation"]
+        assert list(tol.responses) == list(want["responses"])
+        for k, v in want["responses"].items():
+            assert _close(tol.responses[k], v), (est["name"], k)
+
+
+def test_rel_err_vectors(vectors):
+    for r in vectors["rel_err"]:
+        a = np.array([float.fromhex(h) for h in r["a_hex"]])
+        b = np.array([float.fromhex(h) for h in r["b_hex"]])
+        assert _close(td.rel_err_arrays(a, b), float.fromhex(r["rel"]), 1e-15)
+        # f32 carriers take the vector path
+        assert _close(td.rel_err_arrays(a.astype(np.float32), b.astype(np.float32)),
+                      float.fromhex(r["rel"]), 1e-15)
+
+
+def test_rel_err_definition_cases():
+    one = np.array([1.0, 1.0])
+    assert td.rel_err_arrays(one, np.array([2.0, 2.0])) == 1.0
+    assert td.rel_err_arrays(one, one) == 0.0
+    assert td.rel_err_arrays(np.zeros(2), np.zeros(2)) == 0.0
+    assert td.rel_err_arrays(np.zeros(2), one) == math.inf
+    assert td.rel_err_arrays(one, np.zeros(2)) == 1.0
+    assert math.isnan(td.rel_err_arrays(one, np.array([np.nan, 1.0])))
+    with pytest.raises(td.ShapeMismatch):
+        td.rel_err_arrays(np.zeros(2), np.zeros(3))
+    assert td.frobenius_norm(td.Tensor(np.array([[3.0, 0.0], [0.0, 4.0]]))) == 5.0
+
+
+def test_quantize_vectors_bit_exact(vectors):
+    for fmt, v in vectors["quantize"].items():
+        x = np.array([float.fromhex(h) for h in v["x_hex"]])
+        y = td.quantize_array(x, td.FloatFormat(fmt))
+        assert [float(a).hex() for a in y] == v["y_hex"], fmt
+    with pytest.raises(td.NonFinite):
+        td.quantize_array(np.array([1.0, np.nan]), td.FloatFormat.BF16)
+    assert td.quantize_array(np.array(0.2), td.FloatFormat.BF16) == 0.2001953125
+    assert td.quantize_array(np.array(257.0), td.FloatFormat.BF16) == 256.0
+
+
+def test_signed_uniforms_bit_exact(vectors):
+    for u in vectors["signed_uniforms"]:
+        got = td.signed_uniforms(u["tag"], (u["n"],))
+        assert [float(x).hex() for x in got] == u["values_hex"]
+    from paper_2506_09280_b200.generation import signed_uniforms_device, seed_from
+    tag = "perturb|s=0|iter=0|mb=0|kind=ActivationOut|mod=model.embedding"
+    window = signed_uniforms_device(tag, 1000, k0=123_456_789).cpu().numpy()
+    assert np.array_equal(window, O.signed_uniforms(seed_from(tag), 1000, 123_456_789))
+    ph = signed_uniforms_device(tag, 5000, k0=(1 << 33) - 7, generator="philox").cpu().numpy()
+    assert np.array_equal(ph, O.signed_uniforms(seed_from(tag), 5000, (1 << 33) - 7, "philox"))
+
+
+@pytest.mark.parametrize("dtype", ["f64", "bf16"])
+def test_perturbation_bit_exact(vectors, dtype):
+    for p in vectors["perturb"]:
+        x = np.array([float.fromhex(h) for h in p["x_hex"]]).reshape(p["rows"], p["cols"])
+        want = np.array([float.fromhex(h) for h in p["y_hex"]]).reshape(x.shape)
+        ident = p["tag"].split("|", 2)[2]
+        sample = int(p["tag"].split("|")[1][2:])
+        spec = td.PerturbSpec(sample, p["eps"])
+        policy = "bf16" if p["fmt"] == "BF16" else "fp32"
+        if dtype == "f64":
+            y = td.apply_perturbation(torch.from_numpy(x).cuda(), ident, spec, policy=policy,
+                                      row_positions=p["pos"])
+            assert np.array_equal(y.cpu().numpy(), want), (p["eps"], p["fmt"])
+        elif p["fmt"] == "BF16":
+            xb = torch.from_numpy(x).cuda().to(torch.bfloat16)
+            y = td.apply_perturbation(xb, ident, spec, policy=policy, row_positions=p["pos"])
+            # Q_bf16 values above 2^-126 are exactly representable in bf16
+            assert np.array_equal(y.double().cpu().numpy(), want)
+
+
+def test_perturbation_rank_slices_compose():
+    """Counter-based stream: each CP rank's rows equal the slice of the full
+    perturbation (engine.py:351-361, test_engine.py:443-450)."""
+    g = torch.Generator().manual_seed(0)
+    full = torch.randn(64, 96, generator=g, dtype=torch.float64).cuda()
+    spec = td.PerturbSpec(4, 2.0 ** -8)
+    ident = "iter=0|mb=2|kind=ActivationOut|mod=model.embedding"
+    whole = td.apply_perturbation(full, ident, spec, policy="bf16")
+    rows = [5, 6, 7, 56, 57, 58]
+    part = td.apply_perturbation(full[rows].contiguous(), ident, spec, policy="bf16", row_positions=rows)
+    assert torch.equal(part, whole[rows])
+    assert td.apply_perturbation(full, ident, td.PerturbSpec(0, 0.0)) is full
+
+
+def _random_trace_pair(rng, case, dtype, corrupt):
+    shape = tuple(case["shape"])
+    x = rng.standard_normal(shape).astype(np.float32)
+    if dtype == "bf16":
+        x = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+    ident = CanonicalId(0, 0, TensorKind.ACTIVATION_OUT, "model.layers.0.attn")
+    hdr = {"digest": "d", "mode": "cascade"}
+    ref = Trace(hdr, [TraceRecord(ident, RankMeta(), identity_mapping(shape), 1, x, "Block")])
+    recs = []
+    copies = int(rng.integers(1, 4))
+    for k, s in enumerate(case["shards"]):
+        pairs = tuple((SliceBox(tuple(map(tuple, l))), SliceBox(tuple(map(tuple, g))))
+                      for l, g in s["pairs"])
+        m = ShardMapping(tuple(s["local_shape"]), shape, pairs)
+        payload = np.empty(m.local_shape, np.float32)
+        for l, g in pairs:
+            payload[l.as_slices()] = x[g.as_slices()]
+        for c in range(copies):
+            p = payload.copy()
+            if corrupt == "value" and k == 0 and c == 0 and p.size:
+                p.reshape(-1)[0] += 1.0
+            if corrupt == "replica" and k == 0 and c == copies - 1 and copies > 1 and p.size:
+                p.reshape(-1)[-1] *= 3.0
+            recs.append(TraceRecord(ident, RankMeta(tp=k, dp=c), m, copies, p, "Block"))
+    return ref, Trace(hdr, recs)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_randomized_shardings_match_oracle(shardings, dtype):
+    rng = np.random.default_rng(11)
+    for i, case in enumerate(shardings[:300]):
+        corrupt = ("none", "value", "replica")[i % 3]
+        ref, cand = _random_trace_pair(rng, case, dtype, corrupt)
+        if dtype == "bf16":
+            ref, cand = _bf16_device(ref), _bf16_device(cand)
+        tol = td.ToleranceMap({}, n_samples=1, eps_p=0.0)
+        rep = td.check(ref, cand, tol, fmt=td.FloatFormat.BF16)
+        oref = [O.Rec(r.id.encode(), r.rank_meta.as_tuple(), r.mapping.local_shape,
+                      r.mapping.global_shape, [(l.bounds, g.bounds) for l, g in r.mapping.pairs],
+                      r.replica_group_size, np.asarray(r.values(), np.float32)) for r in ref.records]
+        ocand = [O.Rec(r.id.encode(), r.rank_meta.as_tuple(), r.mapping.local_shape,
+                       r.mapping.global_shape, [(l.bounds, g.bounds) for l, g in r.mapping.pairs],
+                       r.replica_group_size, np.asarray(r.values(), np.float32)) for r in cand.records]
+        want = O.check(oref, ocand, ref.header, cand.header, {}, 3.0, "BF16")
+        assert_reports_match(json.loads(td.render_report(rep, "json")), want, f"case {i}")
+
+
+def test_merge_and_check_replicas_api():
+    full = np.arange(12.0).reshape(3, 4)
+    left = ShardMapping((3, 2), (3, 4), ((td.whole_box((3, 2)), SliceBox(((0, 3), (0, 2)))),))
+    right = ShardMapping((3, 2), (3, 4), ((td.whole_box((3, 2)), SliceBox(((0, 3), (2, 4)))),))
+    out = td.merge([(left, td.Tensor(full[:, :2])), (right, td.Tensor(full[:, 2:]))], (3, 4))
+    assert np.array_equal(out.data, full)
+    with pytest.raises(td.MergeConflict) as info:
+        td.merge([(left, td.Tensor(full[:, :2]))], (3, 4))
+    assert info.value.witness == (0, 2)
+    a, b = td.Tensor(np.array([1.0, 1.0])), td.Tensor(np.array([2.0, 2.0]))
+    with pytest.raises(td.ReplicaMismatch) as rinfo:
+        td.check_replicas([a, b], td.ReplicaGroup((0, 1)), td.FloatFormat.BF16)
+    assert rinfo.value.max_rel_err == 1.0 and rinfo.value.witness == (0, 1)
+    c = td.Tensor(np.array([1.0 + 2.0 ** -10, 1.0]))
+    td.check_replicas([a, c], td.ReplicaGroup((0, 1)), td.FloatFormat.BF16)
+    with pytest.raises(td.ReplicaMismatch):
+        td.check_replicas([a, c], td.ReplicaGroup((0, 1)), td.FloatFormat.FP32)
+    many = [a] * 9 + [b]
+    with pytest.raises(td.ReplicaMismatch) as minfo:
+        td.check_replicas(many, td.ReplicaGroup(tuple(range(10))), td.FloatFormat.BF16)
+    assert minfo.value.witness == (0, 9)
+
+
+def test_compare_static_matches_oracle(cases, golden_trace_bytes):
+    case = next(c for c in cases["checks"] if c["name"] == "clean_tp2_cp2_k3")
+    ref = trace_from_bytes(golden_trace_bytes(case["ref"]))
+    cand = trace_from_bytes(golden_trace_bytes(case["cand"]))
+    _, rr = O.read_ttrc(golden_trace_bytes(case["ref"]))
+    _, cr = O.read_ttrc(golden_trace_bytes(case["cand"]))
+    for atol, rtol in ((0.0, 1e-5), (1e-2, 1e-1), (0.0, 0.0), (10.0, 10.0)):
+        rep = td.compare_static(ref, cand, atol, rtol)
+        want = O.compare_static(rr, cr, atol, rtol)
+        assert [(e.ident, e.verdict) for e in rep.entries] == want, (atol, rtol)
+
+
+@pytest.mark.parametrize("mib", [1, 64, 1024])
+def test_large_tensor_norms_against_torch_fp64(mib):
+    """Config-5 sizes: TP=4 column shards of a (N/4096, 4096) bf16 tensor vs
+    an identity reference; norms against a torch fp64 reduction."""
+    cols = 4096
+    rows = mib * (1 << 20) // 2 // cols
+    g = torch.Generator(device="cuda").manual_seed(mib)
+    ref = torch.randn(rows, cols, device="cuda", generator=g).to(torch.bfloat16)
+    noise = (torch.randn(rows, cols, device="cuda", generator=g) * 1e-2).to(torch.bfloat16)
+    cand_full = (ref.float() + noise.float()).to(torch.bfloat16)
+    ident = CanonicalId(0, 0, TensorKind.ACTIVATION_OUT, "model.lm_head")
+    hdr = {"digest": "d", "mode": "cascade"}
+    rt = Trace(hdr, [TraceRecord(ident, RankMeta(), identity_mapping((rows, cols)), 1, ref, "H")])
+    ct = Trace(hdr, [])
+    w = cols // 4
+    for t in range(4):
+        m = ShardMapping((rows, w), (rows, cols), ((td.whole_box((rows, w)),
+                                                    SliceBox(((0, rows), (t * w, (t + 1) * w)))),))
+        ct.records.append(TraceRecord(ident, RankMeta(tp=t), m, 1,
+                                      cand_full[:, t * w:(t + 1) * w].contiguous(), "H"))
+    rep = td.check(rt, ct, td.ToleranceMap({}, n_samples=1, eps_p=0.0), fmt=td.FloatFormat.BF16)
+    r64, c64 = ref.double(), cand_full.double()
+    want = math.sqrt(float(((r64 - c64) ** 2).sum())) / math.sqrt(float((r64 ** 2).sum()))
+    assert _close(rep.entries[0].observed, want, 1e-12)
+    # identity property: a trace against itself is exactly 0
+    same = td.check(rt, rt, td.ToleranceMap({}, n_samples=1, eps_p=0.0), fmt=td.FloatFormat.BF16)
+    assert same.entries[0].observed == 0.0 and same.entries[0].verdict == "pass"

@@ -1,0 +1,131 @@
+"""CPU-only tests of the host side: data-free merge witnesses, the TTRC
+codec, report rendering and plan metadata, checked against the golden
+fixtures the reference produced and against the oracle."""
+
+import json
+import math
+
+import numpy as np
+import pytest
+
+from oracle import traindiff_oracle as O
+from paper_2506_09280_b200 import canonical as C
+from paper_2506_09280_b200.canonical import ShardMapping, SliceBox
+from paper_2506_09280_b200.checker import (CheckEntry, CheckReport, ToleranceMap,
+                                           render_report)
+from paper_2506_09280_b200.errors import ConfigInvalid, FormatError, MergeConflict
+from paper_2506_09280_b200.plan import merge_view
+from paper_2506_09280_b200.tensor import FloatFormat
+from paper_2506_09280_b200.tracestore import trace_from_bytes, trace_to_bytes
+
+
+def _mapping(sig):
+    pairs = tuple((SliceBox(tuple(map(tuple, l))), SliceBox(tuple(map(tuple, g))))
+                  for l, g in sig["pairs"])
+    return ShardMapping(tuple(sig["local_shape"]), tuple(sig["global_shape"]), pairs)
+
+
+def test_data_free_witnesses_match_reference(shardings):
+    """The boxes-only overlap/gap witnesses equal the reference merge's
+    count-array witnesses on the 1000 randomized shardings (x3 variants)."""
+    for case in shardings:
+        shape = tuple(case["shape"])
+        maps = [_mapping(s) for s in case["shards"]]
+        v = case["victim"]
+        for key, ms in (("ok", maps), ("omitted", maps[:v] + maps[v + 1:]),
+                        ("doubled", maps + [maps[v]])):
+            err = C.merge_problem(ms, shape)
+            want = case[key]
+            if want is None:
+                assert err is None
+            else:
+                assert isinstance(err, MergeConflict)
+                assert str(err) == want["message"]
+                assert list(err.witness) == want["witness"]
+
+
+def test_mapping_problem_matches_count_array_oracle():
+    rng = np.random.default_rng(3)
+    for _ in range(2000):
+        nd = int(rng.integers(0, 4))
+        local = tuple(int(rng.integers(0, 5)) for _ in range(nd))
+        pairs = []
+        for _ in range(int(rng.integers(0, 4))):
+            lb = []
+            gb = []
+            for n in local:
+                a = int(rng.integers(0, n + 2))
+                b = a + int(rng.integers(0, 3))
+                lb.append((a, b))
+                g0 = int(rng.integers(0, 3))
+                gb.append((g0, g0 + (b - a) + (1 if rng.random() < 0.1 else 0)))
+            pairs.append((tuple(lb), tuple(gb)))
+        glob = tuple(n + 2 for n in local)
+        want = O.validate_mapping(local, glob, pairs)
+        m = ShardMapping(local, glob, tuple((SliceBox(l), SliceBox(g)) for l, g in pairs))
+        assert C.mapping_problem(m) == want
+
+
+def test_ttrc_round_trip_is_byte_identical(cases, golden_trace_bytes):
+    for name in cases["traces"]:
+        raw = golden_trace_bytes(name)
+        trace = trace_from_bytes(raw)
+        assert trace_to_bytes(trace) == raw, name
+
+
+@pytest.mark.parametrize("bad,offset", [(b"XXXX", 0)])
+def test_ttrc_rejects_bad_magic(bad, offset, golden_trace_bytes):
+    raw = bad + golden_trace_bytes("fp32_ref_m1")[4:]
+    with pytest.raises(FormatError) as info:
+        trace_from_bytes(raw)
+    assert info.value.offset == offset
+
+
+def test_ttrc_truncation_is_a_format_error(golden_trace_bytes):
+    raw = golden_trace_bytes("fp32_ref_m1")
+    for cut in range(0, len(raw) - 1, max(1, len(raw) // 97)):
+        with pytest.raises(FormatError):
+            trace_from_bytes(raw[:cut])
+
+
+def test_render_matches_reference_text(cases):
+    """Our renderer reproduces the reference's text and JSON reports byte for
+    byte when fed the reference's own entries."""
+    for case in cases["checks"]:
+        doc = json.loads(case["report"])
+        entries = tuple(CheckEntry(e["id"], e["verdict"],
+                                   None if e["observed"] is None else float(e["observed"]),
+                                   None if e["tolerance"] is None else float(e["tolerance"]),
+                                   None if e["threshold"] is None else float(e["threshold"]),
+                                   e["detail"]) for e in doc["entries"])
+        rep = CheckReport(entries=entries, mode=doc["mode"], kappa=doc["kappa"],
+                          fmt=FloatFormat(doc["format"]))
+        assert render_report(rep, "text") == case["text"], case["name"]
+        assert render_report(rep, "json") == case["report"], case["name"]
+
+
+def test_tolerance_map_json(cases):
+    for blob in cases["tols"].values():
+        tol = ToleranceMap.from_json(blob)
+        assert tol.to_json().decode() == blob
+    with pytest.raises(FormatError):
+        ToleranceMap.from_json(b"TTRC\x01\x00\x00\x00\xbc\xfe")
+    with pytest.raises(ConfigInvalid):
+        ToleranceMap({"a": math.inf}, n_samples=1, eps_p=0.1)
+
+
+def test_host_metadata_agrees_with_oracle(cases, golden_trace_bytes):
+    """Declared-size and merge problems are decided on the host; they must
+    match the oracle's _merge_one for every id of every golden trace."""
+    for name in cases["traces"]:
+        raw = golden_trace_bytes(name)
+        view = merge_view(trace_from_bytes(raw))
+        _, recs = O.read_ttrc(raw)
+        ov = O.merge_trace(recs, float("inf"))   # numeric replica problems cannot fire
+        assert list(view) == list(ov)
+        for ident, meta in view.items():
+            o = ov[ident]
+            host = meta.declared_problem or meta.merge_detail
+            assert (host or None) == (o["detail"] or None), (name, ident)
+            if meta.merge_ok:
+                assert tuple(o["values"].shape) == meta.global_shape

@@ -1,0 +1,69 @@
+"""The C-ABI library builds for sm_100a, loads without a GPU and exports
+every function include/td_api.h declares (no compute calls here)."""
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2506_09280_b200 import _native as N
+from paper_2506_09280_b200 import build
+
+HEADER = os.path.join(os.path.dirname(N.HERE), "include", "td_api.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(td_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_builds_and_loads():
+    path = build.build()
+    assert os.path.exists(path)
+    lib = N.load_library()
+    assert lib.td_version() == 1
+
+
+def test_every_declared_symbol_is_exported_and_typed():
+    lib = N.load_library()
+    declared = _declared()
+    assert declared, "no declarations parsed"
+    for name in declared:
+        assert hasattr(lib, name), name
+        assert name in N.SIGNATURES, f"{name} lacks a ctypes signature"
+    assert set(N.SIGNATURES) == set(declared)
+
+
+def test_exports_are_extern_c():
+    out = subprocess.run(["nm", "-D", "--defined-only", N.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("nm unavailable")
+    exported = set(re.findall(r"\bT (td_[a-z_0-9]+)\b", out.stdout))
+    assert set(_declared()) <= exported
+
+
+def test_cubin_is_sm_100a():
+    out = subprocess.run(["cuobjdump", "--list-elf", N.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_last_error_reports_bad_arguments():
+    lib = N.load_library()
+    # argument validation happens before any CUDA call, so this is CPU-safe
+    rc = lib.td_verdict(None, 5, None, 0, None, None, 3.0, 0.1, 0.1, None, None, None, None)
+    assert rc != 0
+    assert b"td_verdict" in lib.td_last_error()
+
+
+def test_struct_layouts_match_header():
+    assert N.SEGMENT.itemsize == 144
+    assert N.ID_DESC.itemsize == 56
+    assert N.GROUP_DESC.itemsize == 24
+    assert N.ID_RESULT.itemsize == 32
+    assert N.GROUP_RESULT.itemsize == 16
+    assert N.CLASS.itemsize == 56
