@@ -33,9 +33,7 @@ import json
 import math
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import threading
 import time
 
@@ -107,49 +105,59 @@ def workload(name: str, rank: int = 0):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled while the timed region runs."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML while
+    the timed region runs (nvidia-smi's clocks.sm / clocks_event_reasons.*)."""
 
-    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, device_index: int):
+    def __init__(self, device_index: int, period_s: float = 0.002):
         self.idx = device_index
+        self.period = period_s
         self.samples = []
         self._stop = threading.Event()
         self._thread = None
+        self._nvml = None
 
     def _run(self):
-        while not self._stop.is_set():
+        nv, h = self._nvml
+        while True:
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.QUERY}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                try:
+                    reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except AttributeError:
+                    reasons = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((sm, mx, reasons))
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            if self._stop.wait(self.period):
+                break
 
     def __enter__(self):
-        self._thread = threading.Thread(target=self._run, daemon=True)
-        self._thread.start()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nvml = (nv, nv.nvmlDeviceGetHandleByIndex(self.idx))
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        except Exception:
+            self._nvml = None
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        self._thread.join(timeout=10)
+        if self._thread is not None:
+            self._thread.join(timeout=10)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        mx = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 5 + k and s[5 + k].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        reasons = sorted({name for _, _, r in self.samples for bit, name in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples)}
 
 
 def cpu_baseline(ref, cand, tol, fmt, stride: int):
@@ -168,7 +176,7 @@ def cpu_baseline(ref, cand, tol, fmt, stride: int):
                                  r.replica_group_size, r.payload.float().cpu().numpy()))
         return out
     rr, cr = host(ref.records), host(cand.records)
-    nbytes = sum(r.payload.numel() * 2 for r in rr) + sum(r.payload.numel() * 2 for r in cr)
+    nbytes = sum(r.payload.size * 2 for r in rr) + sum(r.payload.size * 2 for r in cr)
     t0 = time.perf_counter()
     doc = O.check(rr, cr, ref.header, cand.header, tol.responses, 3.0, fmt.value)
     dt = time.perf_counter() - t0
@@ -328,17 +336,11 @@ def main():
 
     e2e = None
     if not args.no_e2e:
-        # pinned host copies of every payload; the timed step goes through check()
-        from paper_2506_09280_b200.tracestore import Trace, TraceRecord
-
-        def to_host(trace):
-            out = Trace(header=trace.header)
-            for r in trace.records:
-                out.records.append(TraceRecord(r.id, r.rank_meta, r.mapping, r.replica_group_size,
-                                               r.payload.cpu().pin_memory(), r.module_class))
-            return out
+        # every payload copied to a pinned host arena; the timed step goes
+        # through the public check() and moves all of it over PCIe again
+        from paper_2506_09280_b200.tracestore import pack_pinned
         del keep, prep
-        href, hcand = to_host(ref), to_host(cand)
+        href, hcand = pack_pinned(ref), pack_pinned(cand)
         h2d = href.nbytes + hcand.nbytes
         d2h = n_ids * N.ID_RESULT.itemsize
         del ref, cand

@@ -198,16 +198,16 @@ class CheckPlan:
     def algorithmic_bytes(self) -> int:
         return self.plan.algorithmic_bytes
 
-    def execute(self, timing: dict | None = None):
+    def execute(self, timing: dict | None = None, staged: dict | None = None):
         """Device part only: resolve payloads, launch, fetch raw results."""
-        ptrs, keep = resolve_operands(self.plan.operands, self.plan.operand_dtypes)
+        ptrs, keep = resolve_operands(self.plan.operands, self.plan.operand_dtypes, staged)
         out = self.plan.run(ptrs, kappa=self.kappa, eps=self.fmt.eps, replica_eps=self.fmt.eps,
                             timing=timing)
         del keep
         return out
 
-    def run(self, timing: dict | None = None) -> CheckReport:
-        idres, gres, ties = self.execute(timing)
+    def run(self, timing: dict | None = None, staged: dict | None = None) -> CheckReport:
+        idres, gres, ties = self.execute(timing, staged)
         return self.report(idres, gres, ties)
 
     def report(self, idres, gres, ties) -> CheckReport:
@@ -255,8 +255,16 @@ def check(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float = 3.0, *,
     """Compare a candidate trace against the reference (checker.py:312-365):
     replica copies must agree to fmt precision, shards are merged (never
     materialised here), and an id flags when rel_err(ref, cand) exceeds
-    kappa * max(tolerance, fmt.eps)."""
-    return CheckPlan(ref, cand, tol, kappa, fmt=fmt).run()
+    kappa * max(tolerance, fmt.eps).
+
+    Host-resident payloads start their H2D copies before planning, so the
+    metadata work overlaps the DMA."""
+    if kappa <= 0:
+        raise ConfigInvalid("kappa must be positive")
+    _require_same_setup(ref, cand)
+    from .device import stage_host_payloads
+    staged = stage_host_payloads([ref, cand])
+    return CheckPlan(ref, cand, tol, kappa, fmt=fmt).run(staged=staged)
 
 
 def _strict_problem(view, plan: Plan, gres, side_of_entry: dict) -> str | None:

@@ -49,11 +49,47 @@ def to_device(x, stream=None):
 _TORCH_DTYPES = None
 
 
-def resolve_operands(operands, dtypes=None) -> tuple[np.ndarray, list]:
+def stage_host_payloads(traces, stream=None) -> dict:
+    """Start the H2D copies of every host-resident payload of `traces` and
+    return {id(record): CUDA tensor}.  Copies are asynchronous on the current
+    stream, so host-side planning overlaps the DMA.  Payloads that are views
+    of one pinned storage (a trace arena, see tracestore.pack_pinned) move
+    as ONE copy per storage; the device views keep their offsets."""
+    import torch
+    staged: dict = {}
+    arenas: dict = {}
+    for trace in traces:
+        for rec in trace.records:
+            p = rec.payload
+            if id(rec) in staged:
+                continue
+            if is_torch(p):
+                if p.device.type == "cuda":
+                    continue
+                if p.is_pinned():
+                    st = p.untyped_storage()
+                    arenas.setdefault(st.data_ptr(), (st, []))[1].append(rec)
+                    continue
+            staged[id(rec)] = to_device(p)
+    for st, recs in arenas.values():
+        host = torch.empty(0, dtype=torch.uint8).set_(st)
+        dev = torch.empty(host.numel(), dtype=torch.uint8, device="cuda")
+        dev.copy_(host, non_blocking=True)
+        dst = dev.untyped_storage()
+        for rec in recs:
+            p = rec.payload
+            view = torch.empty(0, dtype=p.dtype, device="cuda").set_(dst, p.storage_offset(),
+                                                                     p.shape, p.stride())
+            staged[id(rec)] = view if view.data_ptr() % 16 == 0 else view.clone()
+    return staged
+
+
+def resolve_operands(operands, dtypes=None, staged: dict | None = None) -> tuple[np.ndarray, list]:
     """(device addresses as uint64 array, keep-alive list of tensors).
 
     dtypes[k], when given, is the td_dtype operand k must be presented as;
-    a differing payload is widened on the device (exact: bf16/f16 < f32 < f64)."""
+    a differing payload is widened on the device (exact: bf16/f16 < f32 < f64).
+    staged: device copies already in flight (stage_host_payloads)."""
     global _TORCH_DTYPES
     import torch
     if _TORCH_DTYPES is None:
@@ -64,6 +100,8 @@ def resolve_operands(operands, dtypes=None) -> tuple[np.ndarray, list]:
     memo: dict = {}
     for k, owner in enumerate(operands):
         t = memo.get(id(owner))
+        if t is None and staged is not None:
+            t = staged.get(id(owner))
         if t is None:
             dev = getattr(owner, "device_payload", None)
             t = dev() if dev is not None else to_device(_payload_of(owner))

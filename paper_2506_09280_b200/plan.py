@@ -20,6 +20,7 @@ once for a layout can be re-run on every step's fresh payloads.
 
 from __future__ import annotations
 
+import functools
 import math
 from dataclasses import dataclass, field
 
@@ -93,12 +94,18 @@ def id_meta(ident: str, entries: list, replica_check: bool = True) -> IdMeta:
             else:
                 numeric = len(recs) > 1
         meta.groups.append(GroupMeta(records=recs, declared_detail=detail, numeric=numeric))
-    mappings = [ShardMapping(g.records[0].mapping.local_shape, hull, g.records[0].mapping.pairs)
-                for g in meta.groups]
-    err = merge_problem(mappings, hull, [tuple(g.records[0].shape) for g in meta.groups])
-    if err is not None:
-        meta.merge_detail = str(err)
+    meta.merge_detail = _merge_detail(tuple(g.records[0].mapping for g in meta.groups), hull,
+                                      tuple(tuple(g.records[0].shape) for g in meta.groups))
     return meta
+
+
+@functools.lru_cache(maxsize=65536)
+def _merge_detail(mappings: tuple, hull: tuple, shapes: tuple) -> str | None:
+    """merge()'s verdict for these shard layouts, memoised: every id of one
+    layout (all hidden activations, say) shares one validation."""
+    normed = [ShardMapping(m.local_shape, hull, m.pairs) for m in mappings]
+    err = merge_problem(normed, hull, list(shapes))
+    return None if err is None else str(err)
 
 
 def merge_view(trace, replica_check: bool = True) -> dict[str, IdMeta]:
@@ -325,30 +332,13 @@ class Plan:
     @staticmethod
     def _compare_runs(b: PlanBuilder, xmeta: IdMeta, y0, yop, zops) -> None:
         """Runs = candidate global boxes cut by reference global boxes."""
-        for yl, yg in y0.mapping.pairs:
-            for h in xmeta.groups:
-                x0 = h.records[0]
-                xop = None
-                for xl, xg in x0.mapping.pairs:
-                    cut = []
-                    for (a0, a1), (b0, b1) in zip(yg.bounds, xg.bounds):
-                        lo, hi = max(a0, b0), min(a1, b1)
-                        if lo >= hi:
-                            cut = None
-                            break
-                        cut.append((lo, hi))
-                    if cut is None:
-                        continue
-                    if xop is None:
-                        xop = b.operand(x0, x0.dtype_code)
-                    ext = tuple(hi - lo for lo, hi in cut)
-                    ys = tuple(l0 + (c0 - g0) for (l0, _), (g0, _), (c0, _) in zip(yl.bounds, yg.bounds, cut))
-                    xs = tuple(l0 + (c0 - g0) for (l0, _), (g0, _), (c0, _) in zip(xl.bounds, xg.bounds, cut))
-                    for xo, yo, rows, cols, rx, ry in _blocks(ext, xs, x0.mapping.local_shape,
-                                                              ys, y0.mapping.local_shape):
-                        b.add(xop, xo, yop, yo, zops, rows, cols, rx, ry)
-        if not y0.mapping.pairs:
-            return
+        for h in xmeta.groups:
+            x0 = h.records[0]
+            blocks = _run_blocks(y0.mapping, x0.mapping)
+            if blocks:
+                xop = b.operand(x0, x0.dtype_code)
+                for xo, yo, rows, cols, rx, ry in blocks:
+                    b.add(xop, xo, yop, yo, zops, rows, cols, rx, ry)
 
     @staticmethod
     def _replica_remainder(b: PlanBuilder, y0, yop, zops) -> None:
@@ -569,6 +559,28 @@ class Prepared:
             flat = self.work[self.n_part:].cpu().numpy()
         return {"id": flat[:2 * self.n_ids].reshape(self.n_ids, 2),
                 "group": flat[2 * self.n_ids:].reshape(self.n_groups, N.SLOT_STRIDE)}
+
+
+@functools.lru_cache(maxsize=65536)
+def _run_blocks(ymap: ShardMapping, xmap: ShardMapping) -> tuple:
+    """2-D blocks of (candidate pair x reference pair) box intersections."""
+    out = []
+    for yl, yg in ymap.pairs:
+        for xl, xg in xmap.pairs:
+            cut = []
+            for (a0, a1), (b0, b1) in zip(yg.bounds, xg.bounds):
+                lo, hi = max(a0, b0), min(a1, b1)
+                if lo >= hi:
+                    cut = None
+                    break
+                cut.append((lo, hi))
+            if cut is None:
+                continue
+            ext = tuple(hi - lo for lo, hi in cut)
+            ys = tuple(l0 + (c0 - g0) for (l0, _), (g0, _), (c0, _) in zip(yl.bounds, yg.bounds, cut))
+            xs = tuple(l0 + (c0 - g0) for (l0, _), (g0, _), (c0, _) in zip(xl.bounds, xg.bounds, cut))
+            out.extend(_blocks(ext, xs, xmap.local_shape, ys, ymap.local_shape))
+    return tuple(out)
 
 
 def _group_dtype(records) -> int:

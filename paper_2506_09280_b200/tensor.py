@@ -109,8 +109,10 @@ def quantize_array(x, fmt: FloatFormat) -> np.ndarray:
     pattern, never through float32.  Returns float64 like the reference."""
     import torch
     from .device import to_device
-    host = not (hasattr(x, "device") and getattr(x, "device").type == "cuda")
-    src = to_device(np.asarray(x, dtype=np.float64) if host else x.to(torch.float64))
+    from .device import is_torch
+    host = not (is_torch(x) and x.device.type == "cuda")
+    src = to_device(np.asarray(x.cpu() if is_torch(x) else x, dtype=np.float64) if host
+                    else x.to(torch.float64))
     out = torch.empty_like(src)
     flag = torch.zeros(1, dtype=torch.int64, device=src.device)
     N.call("td_quantize", src.data_ptr(), out.data_ptr(), N.F64, src.numel(), fmt.code,

@@ -55,13 +55,14 @@ def assert_reports_match(got: dict, want: dict, label=""):
 
 
 def _bf16_device(trace):
-    """Same trace with payloads moved to HBM as bf16 (exact: bf16-grid values)."""
+    """Same trace with payloads moved to HBM: bf16 where the values are on the
+    bf16 grid (exact), f32 otherwise (e.g. the emulator's unrounded MainGrad)."""
     out = Trace(header=trace.header, raw_header=trace.raw_header)
     for r in trace.records:
-        t = torch.from_numpy(r.payload).cuda()
+        t = torch.from_numpy(np.asarray(r.values(), np.float32)).cuda()
         b = t.to(torch.bfloat16)
-        assert torch.equal(b.float(), t)
-        out.records.append(TraceRecord(r.id, r.rank_meta, r.mapping, r.replica_group_size, b,
+        payload = b if torch.equal(b.float(), t) else t
+        out.records.append(TraceRecord(r.id, r.rank_meta, r.mapping, r.replica_group_size, payload,
                                        r.module_class))
     return out
 
@@ -95,7 +96,7 @@ def test_estimate_tolerance_reproduces_reference(cases, golden_trace_bytes):
                                     aggregation=est["aggregation"])
         want = json.loads(est["tol"])
         assert tol.n_samples == want["n_samples"] and tol.aggregation == want["aggregation"]
-        assert list(tol.responses) == list(want["responses"])
+        assert sorted(tol.responses) == sorted(want["responses"])
         for k, v in want["responses"].items():
             assert _close(tol.responses[k], v), (est["name"], k)
 
