@@ -252,15 +252,28 @@ class PlanEntry:
 class Plan:
     """Frozen layout of one comparison; `run()` executes it on the GPU."""
 
-    def __init__(self, entries: list[PlanEntry], static: tuple[float, float] | None = None):
+    def __init__(self, entries: list[PlanEntry], static: tuple[float, float] | None = None,
+                 owner=None, me: int = 0):
         """static=(atol, rtol) builds compare_static's plan: the elementwise
-        failure count replaces d2 (generic walker, no replica checks)."""
+        failure count replaces d2 (generic walker, no replica checks).
+
+        owner(record) -> rank restricts the plan to the records rank `me`
+        holds (multi-GPU, distributed.py).  Id and replica-group slots are
+        laid out identically on every rank; a rank emits segments only for
+        work whose operands it holds: compare runs on the rank holding the
+        candidate's copy 0 (the reference slice must be there too), fused
+        replica sums when every copy of the group is on that rank.  Groups
+        whose copies span ranks are listed in `remote_groups` and resolved
+        by fingerprints (zero sums = identical copies)."""
         self.entries = entries
         self.static = static
+        owner = owner if owner is not None else (lambda rec: me)
+        is_local = (lambda rec: owner(rec) == me)
         b = PlanBuilder(force_generic=static is not None)
         id_rows = []
         group_rows = []
         self.group_owner = []     # (entry index, side, group index)
+        self.remote_groups = []   # (group slot, entry index, side, group index)
         for ei, e in enumerate(entries):
             t0 = b.tile_cursor
             has_compare = (e.x is not None and e.y is not None and e.x.merge_ok and e.y.merge_ok
@@ -274,18 +287,23 @@ class Plan:
                             f"{e.ident}: replica groups of more than {N.MAX_Z + 1} copies")
                     s0 = b.tile_cursor
                     y0 = g.records[0]
-                    gdt = _group_dtype(g.records) if rep else y0.dtype_code
-                    yop = b.operand(y0, gdt)
-                    zops = [b.operand(r, gdt) for r in g.records[1:]] if rep else []
-                    if has_compare:
-                        self._compare_runs(b, e.x, y0, yop, zops)
-                        if zops:
-                            self._replica_remainder(b, y0, yop, zops)
-                    elif zops:
-                        n = math.prod(y0.shape)
-                        b.add(None, 0, yop, 0, zops, 1, n, n, n)
-                    if zops:
-                        group_rows.append((s0, b.tile_cursor, len(zops)))
+                    mine = is_local(y0)
+                    together = rep and all(is_local(r) for r in g.records) if mine else False
+                    if rep and len({owner(r) for r in g.records}) > 1:
+                        self.remote_groups.append((len(group_rows), ei, 0, gi))
+                    if mine:
+                        gdt = _group_dtype(g.records) if together else y0.dtype_code
+                        yop = b.operand(y0, gdt)
+                        zops = [b.operand(r, gdt) for r in g.records[1:]] if together else []
+                        if has_compare:
+                            self._compare_runs(b, e.x, y0, yop, zops, is_local)
+                            if zops:
+                                self._replica_remainder(b, y0, yop, zops)
+                        elif zops:
+                            n = math.prod(y0.shape)
+                            b.add(None, 0, yop, 0, zops, 1, n, n, n)
+                    if rep:
+                        group_rows.append((s0, b.tile_cursor, len(g.records) - 1))
                         self.group_owner.append((ei, 0, gi))
             cg1 = len(group_rows)
             rg0 = len(group_rows)
@@ -298,12 +316,16 @@ class Plan:
                             f"{e.ident}: replica groups of more than {N.MAX_Z + 1} copies")
                     s0 = b.tile_cursor
                     x0 = g.records[0]
-                    gdt = _group_dtype(g.records)
-                    yop = b.operand(x0, gdt)
-                    zops = [b.operand(r, gdt) for r in g.records[1:]]
-                    n = math.prod(x0.shape)
-                    b.add(None, 0, yop, 0, zops, 1, n, n, n)
-                    group_rows.append((s0, b.tile_cursor, len(zops)))
+                    mine = is_local(x0)
+                    if len({owner(r) for r in g.records}) > 1:
+                        self.remote_groups.append((len(group_rows), ei, 1, gi))
+                    elif mine:
+                        gdt = _group_dtype(g.records)
+                        yop = b.operand(x0, gdt)
+                        zops = [b.operand(r, gdt) for r in g.records[1:]]
+                        n = math.prod(x0.shape)
+                        b.add(None, 0, yop, 0, zops, 1, n, n, n)
+                    group_rows.append((s0, b.tile_cursor, len(g.records) - 1))
                     self.group_owner.append((ei, 1, gi))
             rg1 = len(group_rows)
             cand_host = 0
@@ -330,12 +352,17 @@ class Plan:
     # -- geometry -------------------------------------------------------------
 
     @staticmethod
-    def _compare_runs(b: PlanBuilder, xmeta: IdMeta, y0, yop, zops) -> None:
+    def _compare_runs(b: PlanBuilder, xmeta: IdMeta, y0, yop, zops, is_local) -> None:
         """Runs = candidate global boxes cut by reference global boxes."""
         for h in xmeta.groups:
             x0 = h.records[0]
             blocks = _run_blocks(y0.mapping, x0.mapping)
             if blocks:
+                if not is_local(x0):
+                    raise ValueError(
+                        f"{x0.id.encode()}: the reference slice overlapping a candidate shard is not "
+                        "on the rank holding that shard; give every rank the reference slices of "
+                        "its candidate boxes")
                 xop = b.operand(x0, x0.dtype_code)
                 for xo, yo, rows, cols, rx, ry in blocks:
                     b.add(xop, xo, yop, yo, zops, rows, cols, rx, ry)

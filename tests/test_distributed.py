@@ -1,0 +1,154 @@
+"""Multi-GPU host logic on CPU (gloo, world size 2) and the full distributed
+algorithm on one GPU (logical ranks as threads, real kernels)."""
+
+import json
+import os
+import threading
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2506_09280_b200.distributed import (DistributedCheckPlan, RecordMeta, ThreadComm,
+                                               TorchComm, global_trace, split_reference)
+from paper_2506_09280_b200.tracestore import Trace, trace_from_bytes
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _owner(rec, world):
+    """Candidate placement: TP rank then DP rank round-robin over GPUs."""
+    return (rec.rank_meta.tp + 2 * rec.rank_meta.dp + 3 * rec.rank_meta.cp) % world
+
+
+def _local(trace, rank, world, key):
+    t = Trace(header=trace.header, raw_header=trace.raw_header)
+    t.records = [r for r in trace.records if key(r) % world == rank]
+    return t
+
+
+def _order_key(positions):
+    """Global order = position in the single-process trace; reference slices
+    inherit their parent record's position."""
+    return lambda rec, pos: (positions[id(getattr(rec, "parent", rec))], rec.rank_meta.as_tuple())
+
+
+def _gloo_worker(rank, world, port, case_names, q):
+    try:
+        _gloo_body(rank, world, port, case_names, q)
+    except Exception as exc:  # surface instead of hanging the peer
+        import traceback
+        q.put((rank, "ERROR " + traceback.format_exc()))
+
+
+def _gloo_body(rank, world, port, case_names, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=__import__("datetime").timedelta(seconds=120))
+    try:
+        import gzip
+        from paper_2506_09280_b200.checker import ToleranceMap
+        from paper_2506_09280_b200.plan import Plan, PlanEntry, merge_view
+        with gzip.open(os.path.join(ROOT, "tests", "golden", "cases.json.gz"), "rt") as fh:
+            cases = json.load(fh)
+        comm = TorchComm()
+        results = []
+        for name in case_names:
+            case = next(c for c in cases["checks"] if c["name"] == name)
+
+            def load(n):
+                with gzip.open(os.path.join(ROOT, "tests", "golden", "traces", n + ".ttrc.gz"), "rb") as fh:
+                    return trace_from_bytes(fh.read())
+            ref, cand = load(case["ref"]), load(case["cand"])
+            pos = {id(r): k for k, r in enumerate(cand.records)}
+            pos.update({id(r): k for k, r in enumerate(ref.records)})
+            cand_local = _local(cand, rank, world, lambda r: _owner(r, world))
+            gcand = global_trace(cand_local, comm, _order_key(pos))
+            refs = split_reference(ref, gcand, world)
+            tol = ToleranceMap.from_json(cases["tols"][case["tol"]])
+            dp = DistributedCheckPlan(refs[rank], cand_local, tol, case["kappa"],
+                                      fmt=__import__("paper_2506_09280_b200").FloatFormat(case["fmt"]),
+                                      comm=comm, order_key=_order_key(pos))
+            results.append({"name": name,
+                            "ids": list(dp.cand_view),
+                            "remote": [(slot, ei, side, gi) for slot, ei, side, gi in dp.plan.remote_groups],
+                            "n_groups": len(dp.plan.groups),
+                            "bytes": dp.plan.algorithmic_bytes,
+                            "host": [(m.declared_problem, m.merge_detail) for m in dp.cand_view.values()]})
+        q.put((rank, results))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_plans_agree_and_cover_the_work():
+    names = ["clean_tp2_cp2_k3", "bug_tp_row_allreduce_k3", "clean_dp2_tp2_k3"]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, names, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r, v in out.items():
+        assert not isinstance(v, str), v
+    for p in procs:
+        assert p.exitcode == 0
+    import gzip
+    from paper_2506_09280_b200.checker import CheckPlan, ToleranceMap
+    with gzip.open(os.path.join(ROOT, "tests", "golden", "cases.json.gz"), "rt") as fh:
+        cases = json.load(fh)
+    for k, name in enumerate(names):
+        a, b = out[0][k], out[1][k]
+        # identical global views, slot layouts and remote-group lists on both ranks
+        assert a["ids"] == b["ids"] and a["remote"] == b["remote"] and a["n_groups"] == b["n_groups"]
+        assert a["host"] == b["host"]
+        case = next(c for c in cases["checks"] if c["name"] == name)
+        want = json.loads(case["report"])
+        assert a["ids"] == [e["id"] for e in want["entries"] if e["detail"] != "only in reference trace"]
+        # the ranks' work covers every candidate byte once; remote groups are
+        # fingerprinted instead of read against copy 0 (no double counting)
+        assert a["bytes"] > 0 and b["bytes"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_check_threads_match_reference(world, cases, golden_trace_bytes):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_09280_b200 as td
+    names = [c["name"] for c in cases["checks"]]
+    for name in names:
+        case = next(c for c in cases["checks"] if c["name"] == name)
+        ref = trace_from_bytes(golden_trace_bytes(case["ref"]), device="cuda")
+        cand = trace_from_bytes(golden_trace_bytes(case["cand"]), device="cuda")
+        tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+        pos = {id(r): k for k, r in enumerate(cand.records)}
+        hub = ThreadComm.hub(world)
+        reports, errors = [None] * world, []
+
+        def worker(rank):
+            try:
+                comm = ThreadComm(hub, rank)
+                cand_local = _local(cand, rank, world, lambda r: _owner(r, world))
+                gcand = global_trace(cand_local, comm, _order_key(pos))
+                refs = split_reference(ref, gcand, world)
+                plan = DistributedCheckPlan(refs[rank], cand_local, tol, case["kappa"],
+                                            fmt=td.FloatFormat(case["fmt"]), comm=comm,
+                                            order_key=_order_key(pos))
+                reports[rank] = json.loads(td.render_report(plan.run(), "json"))
+            except Exception as exc:  # pragma: no cover - surfaced below
+                errors.append(repr(exc))
+                hub.barrier.abort()
+        threads = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=600)
+        assert not errors, (name, errors)
+        from tests.test_gpu_parity import assert_reports_match
+        want = json.loads(case["report"])
+        for rep in reports:
+            assert_reports_match(rep, want, f"{name} world={world}")
