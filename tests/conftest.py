@@ -55,3 +55,8 @@ def golden_trace_bytes():
             cache[name] = trace_bytes(name)
         return cache[name]
     return get
+
+
+@pytest.fixture(scope="session")
+def torchtap_golden():
+    return _load_gz_json("torchtap.json.gz")

@@ -14,6 +14,7 @@ Everything it writes under tests/golden/ is small and committed:
   layouts.json.gz       id emission / shard-map signatures over the 60-layout
                         grid (test_acceptance.py:118-148) — index-map parity
   vectors.json.gz       RNG, quantizer, perturbation and rel_err known answers
+  torchtap.json.gz      the reference torchtap adapter's flushed bytes for small models
 """
 
 from __future__ import annotations
@@ -292,17 +293,45 @@ def vectors() -> dict:
     return v
 
 
+def torchtap_golden() -> dict:
+    """The reference adapter's own capture of small torch models
+    (pkg/adapter/tests/test_torchtap.py:10-19 setup), as flushed bytes."""
+    sys.path.insert(0, os.path.join(REF, "pkg", "adapter", "src"))
+    import torch
+    import torchtap
+    out = {}
+    torch.manual_seed(7)
+    net = torch.nn.Sequential(torch.nn.Linear(8, 16, bias=False), torch.nn.Linear(16, 4, bias=False))
+    x = torch.randn(5, 8)
+    h = torchtap.attach(net, torchtap.TapConfig(patterns=("*",)))
+    net(x).square().sum().backward()
+    out["two_linear"] = {"seed": 7, "bytes_hex": torchtap.to_bytes(h).hex(),
+                         "idents": [r.ident for r in h.records]}
+    torch.manual_seed(3)
+    mlp = torch.nn.Sequential(torch.nn.LayerNorm(16), torch.nn.Linear(16, 32), torch.nn.GELU(),
+                              torch.nn.Linear(32, 16))
+    xb = torch.randn(4, 16)
+    h = torchtap.attach(mlp, torchtap.TapConfig(patterns=("*",), iteration=2, microbatch=1,
+                                                precision="bf16"))
+    mlp(xb).sum().backward()
+    out["layernorm_mlp"] = {"seed": 3, "bytes_hex": torchtap.to_bytes(h).hex(),
+                            "idents": [r.ident for r in h.records]}
+    return out
+
+
+def _dump_gz(name: str, obj, sort_keys: bool = False) -> None:
+    with open(os.path.join(HERE, name), "wb") as raw, \
+            gzip.GzipFile(fileobj=raw, mode="wb", compresslevel=9, mtime=0) as fh:
+        fh.write(json.dumps(obj, sort_keys=sort_keys).encode())
+
+
 def main():
     os.makedirs(HERE, exist_ok=True)
-    cases = scenarios()
-    with gzip.open(os.path.join(HERE, "cases.json.gz"), "wt", compresslevel=9) as fh:
-        json.dump(cases, fh, sort_keys=True)
-    with gzip.open(os.path.join(HERE, "shardings.json.gz"), "wt", compresslevel=9) as fh:
-        json.dump(shardings(), fh)
-    with gzip.open(os.path.join(HERE, "layouts.json.gz"), "wt", compresslevel=9) as fh:
-        json.dump(layouts(), fh)
-    with gzip.open(os.path.join(HERE, "vectors.json.gz"), "wt", compresslevel=9) as fh:
-        json.dump(vectors(), fh, sort_keys=True)
+    _dump_gz("cases.json.gz", scenarios(), sort_keys=True)
+    _dump_gz("shardings.json.gz", shardings())
+    _dump_gz("layouts.json.gz", layouts())
+    _dump_gz("vectors.json.gz", vectors(), sort_keys=True)
+    _dump_gz("torchtap.json.gz", torchtap_golden(), sort_keys=True)
     print("wrote golden fixtures to", HERE)
 
 

@@ -126,6 +126,7 @@ def test_distributed_check_threads_match_reference(world, cases, golden_trace_by
         cand = trace_from_bytes(golden_trace_bytes(case["cand"]), device="cuda")
         tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
         pos = {id(r): k for k, r in enumerate(cand.records)}
+        pos.update({id(r): k for k, r in enumerate(ref.records)})
         hub = ThreadComm.hub(world)
         reports, errors = [None] * world, []
 

@@ -1,0 +1,128 @@
+"""estimate_tolerance on a real bf16 PyTorch model (GPU): the perturbation
+proxy through td_perturb in a forward hook, traces captured in HBM by the
+device-resident torchtap, responses reduced by td_segnorm."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+class Block(torch.nn.Module):
+    def __init__(self, d, h):
+        super().__init__()
+        self.norm = torch.nn.LayerNorm(d)
+        self.qkv = torch.nn.Linear(d, 3 * d, bias=False)
+        self.wo = torch.nn.Linear(d, d, bias=False)
+        self.h = h
+
+    def forward(self, x):
+        s, d = x.shape
+        q, k, v = self.qkv(self.norm(x)).view(s, 3, self.h, d // self.h).unbind(1)
+        o = torch.nn.functional.scaled_dot_product_attention(
+            q.transpose(0, 1), k.transpose(0, 1), v.transpose(0, 1), is_causal=True)
+        return x + self.wo(o.transpose(0, 1).reshape(s, d))
+
+
+class Mlp(torch.nn.Module):
+    def __init__(self, d, ff):
+        super().__init__()
+        self.norm = torch.nn.LayerNorm(d)
+        self.w1 = torch.nn.Linear(d, ff, bias=False)
+        self.w2 = torch.nn.Linear(ff, d, bias=False)
+
+    def forward(self, x):
+        return x + self.w2(torch.nn.functional.gelu(self.w1(self.norm(x))))
+
+
+class Tiny(torch.nn.Module):
+    def __init__(self, vocab=256, d=64, h=4, ff=256, layers=4, seq=64):
+        super().__init__()
+        self.embedding = torch.nn.Embedding(vocab, d)
+        self.pos = torch.nn.Parameter(torch.randn(seq, d) * 0.02)
+        self.layers = torch.nn.ModuleList()
+        for _ in range(layers):
+            self.layers.append(Block(d, h))
+            self.layers.append(Mlp(d, ff))
+        self.final_norm = torch.nn.LayerNorm(d)
+        self.head = torch.nn.Linear(d, vocab, bias=False)
+
+    def forward(self, ids):
+        x = self.embedding(ids) + self.pos
+        for layer in self.layers:
+            x = layer(x)
+        return self.head(self.final_norm(x))
+
+
+@pytest.fixture(scope="module")
+def setup():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.manual_seed(0)
+    model = Tiny().cuda().bfloat16()
+    ids = torch.randint(0, 256, (64,), device="cuda")
+    labels = torch.roll(ids, -1)
+
+    def step(m):
+        logits = m(ids)
+        torch.nn.functional.cross_entropy(logits.float(), labels).backward()
+    return model, step
+
+
+def _runner(model, step, **kw):
+    from paper_2506_09280_b200.runner import torch_runner
+    from paper_2506_09280_b200.torchtap import TapConfig
+    return torch_runner(model, step, embedding="embedding",
+                        tap=TapConfig(patterns=("embedding", "layers.*", "final_norm", "head"),
+                                      precision="bf16"), **kw)
+
+
+def test_tolerance_estimate_on_torch_model(setup):
+    import paper_2506_09280_b200 as td
+    model, step = setup
+    eps = td.FloatFormat.BF16.eps
+    runner = _runner(model, step)
+    tol = td.estimate_tolerance(runner, n_samples=3, eps_p=eps)
+    again = td.estimate_tolerance(runner, n_samples=3, eps_p=eps)
+    assert tol == again                                   # deterministic
+    token_in = "iter=0|mb=0|kind=ActivationIn|mod=model.embedding"
+    assert tol.responses[token_in] == 0.0                 # upstream of the perturbation
+    acts = [v for k, v in tol.responses.items() if "kind=ActivationOut|mod=model.layers" in k]
+    assert acts and all(0.01 * eps <= v <= 100 * eps for v in acts), acts
+    assert all(v >= 0 and math.isfinite(v) for v in tol.responses.values())
+
+
+def test_clean_rerun_passes_and_bug_is_flagged(setup):
+    import paper_2506_09280_b200 as td
+    model, step = setup
+    eps = td.FloatFormat.BF16.eps
+    runner = _runner(model, step)
+    tol = td.estimate_tolerance(runner, n_samples=3, eps_p=eps)
+    ref = runner(None)
+    cand = runner(None)
+    rep = td.check(ref, cand, tol, fmt=td.FloatFormat.BF16)
+    assert rep.exit_code() == 0, rep.counts
+    # silent bug: layer 3 (an Mlp) output scaled by 1.01
+    hook = model.layers[3].register_forward_hook(lambda m, a, o: o * 1.01)
+    try:
+        bad = runner(None)
+    finally:
+        hook.remove()
+    rep = td.check(ref, bad, tol, fmt=td.FloatFormat.BF16)
+    assert rep.exit_code() == 2
+    assert rep.earliest_flag == "iter=0|mb=0|kind=ActivationOut|mod=model.layers.3"
+
+
+def test_module_wise_perturbation_hits_every_listed_input(setup):
+    import paper_2506_09280_b200 as td
+    model, step = setup
+    names = tuple(f"layers.{i}" for i in range(8))
+    runner = _runner(model, step, module_inputs=names)
+    base, pert = runner(None), runner(td.PerturbSpec(0, td.FloatFormat.BF16.eps))
+    assert pert.header["mode"] == "module-wise"
+    moved = {r.id.encode() for r, s in zip(base.records, pert.records)
+             if not torch.equal(r.payload, s.payload)}
+    for i in range(8):
+        assert f"iter=0|mb=0|kind=ActivationIn|mod=model.layers.{i}" in moved
