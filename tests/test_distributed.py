@@ -149,7 +149,7 @@ def test_distributed_check_threads_match_reference(world, cases, golden_trace_by
         for t in threads:
             t.join(timeout=600)
         assert not errors, (name, errors)
-        from tests.test_gpu_parity import assert_reports_match
+        from tests.test_gpu_parity import assert_reports_match  # noqa: E402
         want = json.loads(case["report"])
         for rep in reports:
             assert_reports_match(rep, want, f"{name} world={world}")
