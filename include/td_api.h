@@ -20,6 +20,9 @@
  *                replica equality across GPUs without moving data
  *   td_box_gather
  *                materialises merge()'s f64 output on the device (public merge API)
+ *   td_gather_bytes
+ *                unpacks TTRC payloads from a file image in HBM into an aligned
+ *                arena (device-side trace reader, tracestore.py:225-284)
  *
  * Conventions: every function returns 0 on success and a nonzero status on
  * error (td_last_error() then describes it, thread-local).  All pointers to
@@ -203,6 +206,10 @@ int td_fingerprint(const void* x, int32_t dtype, int64_t n,
  * boxes: n_boxes rows of {src_off, dst_off, rows, cols, src_stride, dst_stride} int64 */
 int td_box_gather(const void* src, int32_t src_dtype, double* dst,
                   const int64_t* boxes, int32_t n_boxes, void* stream);
+
+/* ---- device TTRC reader: byte ranges of a file image -> aligned arena ----
+ * ranges: n rows of {src_off, dst_off, nbytes} int64 (device); any alignment. */
+int td_gather_bytes(const void* src, void* dst, const int64_t* ranges, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

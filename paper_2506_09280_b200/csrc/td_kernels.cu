@@ -162,6 +162,48 @@ __device__ __forceinline__ void load_view(const td_segment* __restrict__ g, SegV
     S.div_p = __ldg(&g->div_p);
 }
 
+// Each CTA walks a CONTIGUOUS share of its class's tile list (balanced to
+// +-1 tile): consecutive tiles are consecutive slices of one segment, so the
+// descriptor is loaded once per segment, not once per tile, and the next
+// tile index is prefetched while the current tile streams.
+struct TileWalk {
+    int64_t i, i1, t;
+    int seg = -1;
+    int64_t st0 = 0, st1 = 0, nu = 0;
+
+    __device__ __forceinline__ explicit TileWalk(int64_t n) {
+        const int64_t per = n / gridDim.x, rem = n % gridDim.x;
+        const int64_t b = blockIdx.x;
+        i = b * per + (b < rem ? b : rem);
+        i1 = i + per + (b < rem ? 1 : 0);
+        t = 0;
+    }
+    __device__ __forceinline__ void advance(const int32_t* __restrict__ tiles) { ++i; t = next; load_next(tiles); }
+    __device__ __forceinline__ void load_next(const int32_t* __restrict__ tiles) {
+        next = (i + 1 < i1) ? __ldg(tiles + i + 1) : 0;
+    }
+    // true when tile t starts a new segment (descriptor must be (re)loaded)
+    __device__ __forceinline__ bool enter(int64_t tt, const td_segment* __restrict__ segs,
+                                          const int32_t* __restrict__ tile_seg) {
+        if (tt >= st0 && tt < st1) return false;
+        seg = __ldg(tile_seg + tt);
+        const td_segment* g = segs + seg;
+        nu = __ldg(&g->n_units);
+        st0 = __ldg(&g->tile_begin);
+        st1 = st0 + (nu + TD_TILE_UNITS - 1) / TD_TILE_UNITS;
+        return true;
+    }
+    int64_t next = 0;
+};
+
+__device__ __forceinline__ TileWalk& start(TileWalk& w, const int32_t* __restrict__ tiles) {
+    if (w.i < w.i1) {
+        w.t = __ldg(tiles + w.i);
+        w.load_next(tiles);
+    }
+    return w;
+}
+
 // Fixed-order block reduction of the first `used` accumulators -> one tile
 // partial.  Deterministic: the element->thread map and the tree are fixed.
 __device__ __forceinline__ void write_partial(const Acc& a, int used, double (*red)[TD_PARTIAL_STRIDE],
@@ -198,15 +240,19 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int32_t* __restrict__ t
     constexpr int Q = Vec<DT>::Q;
     constexpr int ES = (DT == TD_F32) ? 4 : 2;
     constexpr int USED = NZ > 0 ? 3 + NZ : 2;
-    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const int64_t t = __ldg(tiles + i);
-        const td_segment* g = segs + __ldg(tile_seg + t);
-        SegView S;
-        load_view(g, S, NZ);
-        const uint32_t vpr = (uint32_t)(S.cols >> 3);
-        const int64_t first = (t - __ldg(&g->tile_begin)) * (int64_t)TD_TILE_UNITS;
+    TileWalk w(n);
+    start(w, tiles);
+    SegView S;
+    uint32_t vpr = 0;
+    for (; w.i < w.i1; w.advance(tiles)) {
+        const int64_t t = w.t;
+        if (w.enter(t, segs, tile_seg)) {
+            load_view(segs + w.seg, S, NZ);
+            vpr = (uint32_t)(S.cols >> 3);
+        }
+        const int64_t first = (t - w.st0) * (int64_t)TD_TILE_UNITS;
         const uint32_t u0 = (uint32_t)first;
-        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, __ldg(&g->n_units));
+        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, w.nu);
         Acc a;
         a.zero();
         for (uint32_t base = u0 + threadIdx.x; base < u1; base += BLOCK * U) {
@@ -267,19 +313,25 @@ k_segnorm_generic(const td_segment* __restrict__ segs, const int32_t* __restrict
                   const int32_t* __restrict__ tiles, int64_t n, double* __restrict__ partials,
                   int mode, double atol, double rtol) {
     __shared__ double red[NWARP][TD_PARTIAL_STRIDE];
-    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const int64_t t = __ldg(tiles + i);
-        const td_segment* g = segs + __ldg(tile_seg + t);
-        const int nz = __ldg(&g->nz);
-        const bool hx = (__ldg(&g->flags) & TD_SEG_HAS_X) != 0;
-        const int xdt = __ldg(&g->x_dtype);
-        const int ydt = __ldg(&g->y_dtype);
-        SegView S;
-        load_view(g, S, nz);
+    TileWalk w(n);
+    start(w, tiles);
+    SegView S;
+    int nz = 0, xdt = 0, ydt = 0;
+    bool hx = false;
+    for (; w.i < w.i1; w.advance(tiles)) {
+        const int64_t t = w.t;
+        if (w.enter(t, segs, tile_seg)) {
+            const td_segment* g = segs + w.seg;
+            nz = __ldg(&g->nz);
+            hx = (__ldg(&g->flags) & TD_SEG_HAS_X) != 0;
+            xdt = __ldg(&g->x_dtype);
+            ydt = __ldg(&g->y_dtype);
+            load_view(g, S, nz);
+        }
         const uint32_t cols = (uint32_t)S.cols;
-        const int64_t first = (t - __ldg(&g->tile_begin)) * (int64_t)TD_TILE_UNITS;
+        const int64_t first = (t - w.st0) * (int64_t)TD_TILE_UNITS;
         const uint32_t u0 = (uint32_t)first;
-        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, __ldg(&g->n_units));
+        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, w.nu);
         Acc a;
         a.zero();
         for (uint32_t u = u0 + threadIdx.x; u < u1; u += BLOCK) {
@@ -630,6 +682,28 @@ __global__ void k_box_gather(const char* __restrict__ src, int dt, double* __res
     }
 }
 
+// one CTA per range (grid-strided); bytes move 4 at a time when source and
+// destination agree mod 4, else one at a time (file payloads are unaligned)
+__global__ void k_gather_bytes(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
+                               const int64_t* __restrict__ ranges, int64_t n) {
+    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        const int64_t so = ranges[3 * r], dof = ranges[3 * r + 1], nb = ranges[3 * r + 2];
+        const unsigned char* s = src + so;
+        unsigned char* d = dst + dof;
+        const int64_t head = (4 - (dof & 3)) & 3;
+        if (((so - dof) & 3) == 0 && nb > head) {
+            for (int64_t i = threadIdx.x; i < head; i += blockDim.x) d[i] = s[i];
+            const int64_t words = (nb - head) >> 2;
+            const uint32_t* s4 = reinterpret_cast<const uint32_t*>(s + head);
+            uint32_t* d4 = reinterpret_cast<uint32_t*>(d + head);
+            for (int64_t i = threadIdx.x; i < words; i += blockDim.x) d4[i] = s4[i];
+            for (int64_t i = head + 4 * words + threadIdx.x; i < nb; i += blockDim.x) d[i] = s[i];
+        } else {
+            for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) d[i] = s[i];
+        }
+    }
+}
+
 int grid_for(int64_t n, int per_block, int cap) {
     int64_t g = (n + per_block - 1) / per_block;
     if (g < 1) g = 1;
@@ -765,6 +839,15 @@ int td_box_gather(const void* src, int32_t src_dtype, double* dst, const int64_t
     dim3 grid(64, (unsigned)n_boxes);
     k_box_gather<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<const char*>(src), src_dtype, dst, boxes);
     return check_launch("td_box_gather");
+}
+
+int td_gather_bytes(const void* src, void* dst, const int64_t* ranges, int64_t n, void* stream) {
+    if (n == 0) return 0;
+    if (!src || !dst || !ranges || n < 0) return fail("td_gather_bytes: invalid arguments");
+    const int grid = (int)(n < 148 * 32 ? n : 148 * 32);
+    k_gather_bytes<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<const unsigned char*>(src),
+                                                           static_cast<unsigned char*>(dst), ranges, n);
+    return check_launch("td_gather_bytes");
 }
 
 }  // extern "C"

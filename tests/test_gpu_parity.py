@@ -290,3 +290,21 @@ def test_large_tensor_norms_against_torch_fp64(mib):
     # identity property: a trace against itself is exactly 0
     same = td.check(rt, rt, td.ToleranceMap({}, n_samples=1, eps_p=0.0), fmt=td.FloatFormat.BF16)
     assert same.entries[0].observed == 0.0 and same.entries[0].verdict == "pass"
+
+
+def test_device_ttrc_reader_matches_host_reader(tmp_path, cases, golden_trace_bytes):
+    """read_trace(device="cuda"): one DMA of the file image + td_gather_bytes
+    unpacking every (unaligned) payload into an aligned HBM arena."""
+    from paper_2506_09280_b200.tracestore import read_trace, trace_to_bytes
+    for name in cases["traces"][:6]:
+        raw = golden_trace_bytes(name)
+        path = tmp_path / (name + ".ttrc")
+        path.write_bytes(raw)
+        host = trace_from_bytes(raw)
+        dev = read_trace(path, device="cuda")
+        assert len(dev.records) == len(host.records)
+        for a, b in zip(dev.records, host.records):
+            assert a.payload.is_cuda and a.payload.data_ptr() % 256 == 0
+            assert np.array_equal(a.payload.cpu().numpy(), b.payload)
+            assert a.mapping.signature() == b.mapping.signature()
+        assert trace_to_bytes(dev) == raw

@@ -104,8 +104,8 @@ def test_clean_rerun_passes_and_bug_is_flagged(setup):
     cand = runner(None)
     rep = td.check(ref, cand, tol, fmt=td.FloatFormat.BF16)
     assert rep.exit_code() == 0, rep.counts
-    # silent bug: layer 3 (an Mlp) output scaled by 1.01
-    hook = model.layers[3].register_forward_hook(lambda m, a, o: o * 1.01)
+    # silent bug: layer 3 (an Mlp) output scaled by 1.1
+    hook = model.layers[3].register_forward_hook(lambda m, a, o: o * 1.1)
     try:
         bad = runner(None)
     finally:
