@@ -291,7 +291,7 @@ def main():
         if seg_events is not None:
             seg_events[0].record(stream)
         if len(prep.classes):
-            N.call("td_segnorm", prep.seg_ptr, prep.tseg_ptr, prep.classes.ctypes.data, len(prep.classes),
+            N.call("td_segnorm", prep.seg_ptr, prep.classes.ctypes.data, len(prep.classes),
                    prep.part_ptr, 0, N.stream_handle(stream))
         if seg_events is not None:
             seg_events[1].record(stream)

@@ -130,11 +130,12 @@ int         td_version(void);
 const char* td_last_error(void);
 int         td_sm_count(int device);
 
-/* A tile class: the tiles (global tile indices, device array) whose segments
- * share one walker.  Vector classes (vec=1) require every operand to have
- * `dtype` (bf16, f16 or f32); everything else runs the generic walker. */
+/* A tile class: the tiles whose segments share one walker.  Each entry of
+ * `tiles` (device) packs (segment index << 32) | global tile index.  Vector
+ * classes (vec=1) require every operand to have `dtype` (bf16, f16 or f32);
+ * everything else runs the generic walker. */
 typedef struct td_class {
-    const int32_t* tiles;       /* device */
+    const int64_t* tiles;       /* device, packed (segment << 32 | tile) */
     int64_t n_tiles;
     int32_t dtype;
     int32_t nz;
@@ -150,12 +151,10 @@ typedef struct td_class {
 #define TD_MODE_STATIC 1        /* compare_static's elementwise test (checker.py:403-443) */
 
 /* ---- kernel 1: fused canonicalise + relative-difference norms ----
- * One persistent launch per class (classes is a HOST array).  tile_seg maps
- * every global tile index to its segment.  partials: n_tiles_total *
- * TD_PARTIAL_STRIDE doubles; each tile's row is written (not accumulated).
- * blocks_per_sm <= 0 selects 4 CTAs of 256 threads per SM. */
-int td_segnorm(const td_segment* segs, const int32_t* tile_seg,
-               const td_class* classes, int32_t n_classes,
+ * One persistent launch per class (classes is a HOST array).  partials:
+ * n_tiles_total * TD_PARTIAL_STRIDE doubles; each tile's row is written (not
+ * accumulated).  blocks_per_sm <= 0 selects 4 CTAs of 256 threads per SM. */
+int td_segnorm(const td_segment* segs, const td_class* classes, int32_t n_classes,
                double* partials, int32_t blocks_per_sm, void* stream);
 
 /* deterministic per-slot sums of tile partials.

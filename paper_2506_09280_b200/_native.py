@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtdb200.so")
+LIB_PATH = os.environ.get("TD_LIB", os.path.join(HERE, "libtdb200.so"))  # TD_LIB: tuning experiments
 
 # enums (td_api.h)
 F32, BF16, F16, F64 = 0, 1, 2, 3
@@ -63,7 +63,7 @@ SIGNATURES = {
     "td_version": (ctypes.c_int, []),
     "td_last_error": (ctypes.c_char_p, []),
     "td_sm_count": (ctypes.c_int, [ctypes.c_int]),
-    "td_segnorm": (ctypes.c_int, [_P, _P, _P, _I32, _P, _I32, _P]),
+    "td_segnorm": (ctypes.c_int, [_P, _P, _I32, _P, _I32, _P]),
     "td_reduce_slots": (ctypes.c_int, [_P, _I32, _P, _I32, _P, _P, _P, _P]),
     "td_verdict": (ctypes.c_int, [_P, _I32, _P, _I32, _P, _P, _D, _D, _D, _P, _P, _P, _P]),
     "td_perturb": (ctypes.c_int, [_P, _P, _I32, _I32, _I64, _I64, _I64, _I64, _P, _I64, _U64, _D,

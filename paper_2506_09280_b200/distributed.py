@@ -318,7 +318,7 @@ class DistributedCheckPlan:
                                  replica_eps=self.fmt.eps)
         sh = N.stream_handle(prep.stream)
         if len(prep.classes):
-            N.call("td_segnorm", prep.seg_ptr, prep.tseg_ptr, prep.classes.ctypes.data,
+            N.call("td_segnorm", prep.seg_ptr, prep.classes.ctypes.data,
                    len(prep.classes), prep.part_ptr, 0, sh)
         N.call("td_reduce_slots", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups,
                prep.part_ptr, prep.idsum_ptr, prep.gsum_ptr, sh)

@@ -420,7 +420,8 @@ class Plan:
         self.segs = segs
         self.tile_seg = tile_seg
         self.class_keys = sorted(class_tiles)
-        self.class_lists = [np.concatenate([np.arange(tb, tb + nt, dtype=np.int32)
+        # packed (segment << 32 | tile) entries, grid-stride walked by the kernels
+        self.class_lists = [np.concatenate([(np.int64(tile_seg[tb]) << 32) + np.arange(tb, tb + nt, dtype=np.int64)
                                             for tb, nt in class_tiles[k]]) for k in self.class_keys]
         self.operands = self.builder.operands
         self.operand_dtypes = self.builder.operand_dtypes
@@ -501,7 +502,6 @@ class Prepared:
             gdesc["tile_end"] = plan.groups["tile_end"]
             gdesc["nz"] = plan.groups["nz"]
         put(segs)
-        put(plan.tile_seg)
         for lst in plan.class_lists:
             put(lst)
         put(plan.ids)
@@ -513,10 +513,10 @@ class Prepared:
             self.tables.copy_(host, non_blocking=True)
         self._host_blob = host                    # keep the pinned source alive
         base = self.tables.data_ptr()
-        self.seg_ptr, self.tseg_ptr = base + offsets[0], base + offsets[1]
+        self.seg_ptr = base + offsets[0]
         n_cls = len(plan.class_lists)
-        self.ids_ptr = base + offsets[2 + n_cls]
-        self.grp_ptr = base + offsets[3 + n_cls]
+        self.ids_ptr = base + offsets[1 + n_cls]
+        self.grp_ptr = base + offsets[2 + n_cls]
         self.n_part = max(1, plan.n_tiles * N.PARTIAL_STRIDE)
         self.work = torch.empty(self.n_part + 2 * n_ids + N.SLOT_STRIDE * n_groups,
                                 dtype=torch.float64, device=dev)
@@ -532,7 +532,7 @@ class Prepared:
         atol, rtol = plan.static if plan.static else (0.0, 0.0)
         self.classes = np.zeros(len(plan.class_keys), N.CLASS)
         for k, (vec, dt, nz, hx) in enumerate(plan.class_keys):
-            self.classes[k] = (base + offsets[2 + k], len(plan.class_lists[k]), dt, nz, int(hx),
+            self.classes[k] = (base + offsets[1 + k], len(plan.class_lists[k]), dt, nz, int(hx),
                                int(vec), mode, 0, atol, rtol)
         self.launches_per_run = len(self.classes) + 2
         self._events = None
@@ -548,7 +548,7 @@ class Prepared:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             ev[0].record(self.stream)
         if len(self.classes):
-            N.call("td_segnorm", self.seg_ptr, self.tseg_ptr, self.classes.ctypes.data,
+            N.call("td_segnorm", self.seg_ptr, self.classes.ctypes.data,
                    len(self.classes), self.part_ptr, 0, sh)
         if ev:
             ev[1].record(self.stream)

@@ -44,7 +44,7 @@ def main():
                 flush.zero_()
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 ev[0].record()
-                N.call("td_segnorm", prep.seg_ptr, prep.tseg_ptr, prep.classes.ctypes.data,
+                N.call("td_segnorm", prep.seg_ptr, prep.classes.ctypes.data,
                        len(prep.classes), prep.part_ptr, 0, N.stream_handle())
                 ev[1].record()
                 N.call("td_reduce_slots", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups,
