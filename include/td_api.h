@@ -54,7 +54,8 @@ enum td_verdict_code { TD_PASS = 0, TD_FLAG = 1, TD_REPLICA = 2, TD_MERGE = 3, T
 enum td_generator { TD_GEN_SPLITMIX64 = 0, TD_GEN_PHILOX4x32 = 1 };
 
 #define TD_MAX_Z 7              /* replica copies beside copy 0 per segment */
-#define TD_PARTIAL_STRIDE 10    /* doubles per tile partial: d2, x2, y2, z2[7] */
+#define TD_PARTIAL_STRIDE 10    /* doubles per partial row: d2, x2, y2, z2[7] */
+#define TD_WARPS_PER_TILE 8     /* partial rows per tile (one per warp of a 256-thread CTA) */
 #define TD_TILE_UNITS 8192      /* units (8-element vectors or elements) per tile */
 #define TD_SLOT_STRIDE 8        /* doubles per reduced slot */
 
@@ -152,8 +153,8 @@ typedef struct td_class {
 
 /* ---- kernel 1: fused canonicalise + relative-difference norms ----
  * One persistent launch per class (classes is a HOST array).  partials:
- * n_tiles_total * TD_PARTIAL_STRIDE doubles; each tile's row is written (not
- * accumulated).  blocks_per_sm <= 0 selects 4 CTAs of 256 threads per SM. */
+ * n_tiles_total * TD_WARPS_PER_TILE * TD_PARTIAL_STRIDE doubles; each warp
+ * of a tile writes its own row (not accumulated).  blocks_per_sm <= 0 selects 4 CTAs of 256 threads per SM. */
 int td_segnorm(const td_segment* segs, const td_class* classes, int32_t n_classes,
                double* partials, int32_t blocks_per_sm, void* stream);
 

@@ -22,6 +22,7 @@ PASS, FLAG, REPLICA, MERGE, MISSING = 0, 1, 2, 3, 4
 GEN_SPLITMIX64, GEN_PHILOX4x32 = 0, 1
 MAX_Z = 7
 PARTIAL_STRIDE = 10
+WARPS_PER_TILE = 8
 TILE_UNITS = 8192
 SLOT_STRIDE = 8
 SEG_HAS_X = 1

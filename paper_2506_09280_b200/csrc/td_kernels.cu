@@ -29,6 +29,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace {
@@ -145,100 +146,39 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // Tiles are dealt to CTAs grid-stride (neighbouring CTAs stream neighbouring
 // tiles: DRAM row locality; a contiguous share per CTA measured 17% slower).
-// A class-list entry packs (segment << 32 | tile), so no tile->segment lookup
-// is needed, and the NEXT tile's 144-byte descriptor is fetched into shared
-// memory with cp.async while the current tile streams: the per-tile descriptor
-// latency (~1 us, dependent loads) is hidden.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-__device__ __forceinline__ void prefetch_desc(td_segment* dst, const td_segment* __restrict__ src) {
-    static_assert(sizeof(td_segment) % 16 == 0, "descriptor must be 16-byte chunks");
-    if (threadIdx.x < sizeof(td_segment) / 16) {
-        cp_async16(reinterpret_cast<char*>(dst) + 16 * threadIdx.x,
-                   reinterpret_cast<const char*>(src) + 16 * threadIdx.x);
-        cp_async_commit();
-    }
-}
-
+// A class-list entry packs (segment << 32 | tile) so no tile->segment lookup
+// is needed.  Warps are independent: each warp reduces its own slice of a
+// tile and writes its own partial row, so there is no CTA barrier anywhere —
+// a warp that finishes a tile starts loading the next one while its
+// neighbours still drain theirs (a per-tile __syncthreads measured ~9% of
+// the stream).  Rows: partials[(tile * TD_WARPS_PER_TILE + warp) * 10 + k].
 __device__ __forceinline__ int entry_seg(int64_t e) { return (int)(e >> 32); }
 __device__ __forceinline__ int64_t entry_tile(int64_t e) { return e & 0xffffffffll; }
 
-struct TileWalk {
-    int64_t i, n, stride;
-    int64_t cur, next;
-    int buf;
-
-    __device__ __forceinline__ TileWalk(const int64_t* __restrict__ tiles, int64_t n_,
-                                        const td_segment* __restrict__ segs, td_segment* sdesc)
-        : i(blockIdx.x), n(n_), stride(gridDim.x), cur(0), next(0), buf(0) {
-        if (i < n) {
-            cur = __ldg(tiles + i);
-            prefetch_desc(&sdesc[0], segs + entry_seg(cur));
-        }
-        if (i + stride < n) next = __ldg(tiles + i + stride);
-        if (threadIdx.x < sizeof(td_segment) / 16) cp_async_wait_all();
-        __syncthreads();
-    }
-    // call at the start of a tile: prefetch the next tile's descriptor
-    __device__ __forceinline__ int64_t begin(const int64_t* __restrict__ tiles,
-                                             const td_segment* __restrict__ segs, td_segment* sdesc,
-                                             int64_t& after) {
-        if (i + stride < n) prefetch_desc(&sdesc[buf ^ 1], segs + entry_seg(next));
-        after = (i + 2 * stride < n) ? __ldg(tiles + i + 2 * stride) : 0;
-        return entry_tile(cur);
-    }
-    // call after the tile's partial is written (the partial's barriers publish sdesc)
-    __device__ __forceinline__ void end(int64_t after) {
-        i += stride;
-        cur = next;
-        next = after;
-        buf ^= 1;
-    }
-};
-
-__device__ __forceinline__ void view_from(const td_segment& D, SegView& S, int nz_max) {
-    S.x = reinterpret_cast<const char*>(D.x);
-    S.y = reinterpret_cast<const char*>(D.y);
+__device__ __forceinline__ void load_desc(const td_segment* __restrict__ g, SegView& S, int nz_max) {
+    S.x = reinterpret_cast<const char*>(__ldg(&g->x));
+    S.y = reinterpret_cast<const char*>(__ldg(&g->y));
 #pragma unroll
     for (int j = 0; j < TD_MAX_Z; ++j)
-        S.z[j] = j < nz_max ? reinterpret_cast<const char*>(D.z[j]) : nullptr;
-    S.xs = D.x_stride;
-    S.ys = D.y_stride;
-    S.cols = D.cols;
-    S.div_m = D.div_m;
-    S.div_p = D.div_p;
+        S.z[j] = j < nz_max ? reinterpret_cast<const char*>(__ldg(&g->z[j])) : nullptr;
+    S.xs = __ldg(&g->x_stride);
+    S.ys = __ldg(&g->y_stride);
+    S.cols = __ldg(&g->cols);
+    S.div_m = __ldg(&g->div_m);
+    S.div_p = __ldg(&g->div_p);
 }
 
-// Fixed-order block reduction of the first `used` accumulators -> one tile
-// partial.  Deterministic: the element->thread map and the tree are fixed.
-__device__ __forceinline__ void write_partial(const Acc& a, int used, double (*red)[TD_PARTIAL_STRIDE],
-                                              double* __restrict__ out) {
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+// warp-level partial: lane 0 writes the first `used` fixed-order sums
+__device__ __forceinline__ void write_warp_partial(const Acc& a, int used, double* __restrict__ out) {
     const double v[TD_PARTIAL_STRIDE] = {a.d2, a.x2, a.y2, a.z[0], a.z[1], a.z[2],
                                          a.z[3], a.z[4], a.z[5], a.z[6]};
+    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int k = 0; k < TD_PARTIAL_STRIDE; ++k) {
-        if (k < used) {
-            const double s = warp_sum(v[k]);
-            if (lane == 0) red[warp][k] = s;
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x < TD_PARTIAL_STRIDE) {
         double s = 0.0;
-        if ((int)threadIdx.x < used) {
-#pragma unroll
-            for (int w = 0; w < NWARP; ++w) s += red[w][threadIdx.x];
-        }
-        out[threadIdx.x] = s;
+        if (k < used) s = warp_sum(v[k]);
+        if (lane == 0) out[k] = s;
     }
-    __syncthreads();
 }
 
 // vector class: every operand has dtype DT, rows 16-byte aligned, cols % 8 == 0
@@ -246,22 +186,20 @@ template <int DT, int NZ, bool HX, int U, int MINB>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ tiles, int64_t n,
               double* __restrict__ partials) {
-    __shared__ double red[NWARP][TD_PARTIAL_STRIDE];
-    __shared__ __align__(16) td_segment sdesc[2];
     constexpr int Q = Vec<DT>::Q;
     constexpr int ES = (DT == TD_F32) ? 4 : 2;
     constexpr int USED = NZ > 0 ? 3 + NZ : 2;
-    TileWalk w(tiles, n, segs, sdesc);
-    for (; w.i < w.n;) {
-        int64_t after;
-        const int64_t t = w.begin(tiles, segs, sdesc, after);
-        const td_segment& D = sdesc[w.buf];
+    const int warp = threadIdx.x >> 5;
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const int64_t e = __ldg(tiles + i);
+        const int64_t t = entry_tile(e);
+        const td_segment* g = segs + entry_seg(e);
         SegView S;
-        view_from(D, S, NZ);
+        load_desc(g, S, NZ);
         const uint32_t vpr = (uint32_t)(S.cols >> 3);
-        const int64_t first = (t - D.tile_begin) * (int64_t)TD_TILE_UNITS;
+        const int64_t first = (t - __ldg(&g->tile_begin)) * (int64_t)TD_TILE_UNITS;
         const uint32_t u0 = (uint32_t)first;
-        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, D.n_units);
+        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, __ldg(&g->n_units));
         Acc a;
         a.zero();
         for (uint32_t base = u0 + threadIdx.x; base < u1; base += BLOCK * U) {
@@ -290,10 +228,10 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
             for (int k = 0; k < U; ++k) {
                 if (!ok[k]) continue;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const double yv = Vec<DT>::at(yr[k], e);
+                for (int e8 = 0; e8 < 8; ++e8) {
+                    const double yv = Vec<DT>::at(yr[k], e8);
                     if (HX) {
-                        const double xv = Vec<DT>::at(xr[k], e);
+                        const double xv = Vec<DT>::at(xr[k], e8);
                         const double d = xv - yv;
                         a.d2 = fma(d, d, a.d2);
                         a.x2 = fma(xv, xv, a.x2);
@@ -302,43 +240,39 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
                         a.y2 = fma(yv, yv, a.y2);
 #pragma unroll
                         for (int j = 0; j < NZ; ++j) {
-                            const double dz = yv - Vec<DT>::at(zr[j][k], e);
+                            const double dz = yv - Vec<DT>::at(zr[j][k], e8);
                             a.z[j] = fma(dz, dz, a.z[j]);
                         }
                     }
                 }
             }
         }
-        if (threadIdx.x < sizeof(td_segment) / 16) cp_async_wait_all();
-        write_partial(a, USED, red, partials + t * TD_PARTIAL_STRIDE);
-        w.end(after);
+        write_warp_partial(a, USED, partials + (t * TD_WARPS_PER_TILE + warp) * TD_PARTIAL_STRIDE);
     }
 }
 
-// generic class: per element, runtime dtypes, any alignment, any nz (<= 7)
+// generic class: per element, runtime dtypes, any alignment, any nz (<= 7).
 // mode TD_MODE_STATIC replaces d2 by the count of cells failing
 // |y - x| <= atol + rtol*|x| (numpy's elementwise test, each op rounded once;
 // NaN fails) and leaves x2 at 0.
 __global__ void __launch_bounds__(BLOCK, 4)
 k_segnorm_generic(const td_segment* __restrict__ segs, const int64_t* __restrict__ tiles, int64_t n,
                   double* __restrict__ partials, int mode, double atol, double rtol) {
-    __shared__ double red[NWARP][TD_PARTIAL_STRIDE];
-    __shared__ __align__(16) td_segment sdesc[2];
-    TileWalk w(tiles, n, segs, sdesc);
-    for (; w.i < w.n;) {
-        int64_t after;
-        const int64_t t = w.begin(tiles, segs, sdesc, after);
-        const td_segment& D = sdesc[w.buf];
-        const int nz = D.nz;
-        const bool hx = (D.flags & TD_SEG_HAS_X) != 0;
-        const int xdt = D.x_dtype;
-        const int ydt = D.y_dtype;
+    const int warp = threadIdx.x >> 5;
+    for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const int64_t e = __ldg(tiles + i);
+        const int64_t t = entry_tile(e);
+        const td_segment* g = segs + entry_seg(e);
+        const int nz = __ldg(&g->nz);
+        const bool hx = (__ldg(&g->flags) & TD_SEG_HAS_X) != 0;
+        const int xdt = __ldg(&g->x_dtype);
+        const int ydt = __ldg(&g->y_dtype);
         SegView S;
-        view_from(D, S, nz);
+        load_desc(g, S, nz);
         const uint32_t cols = (uint32_t)S.cols;
-        const int64_t first = (t - D.tile_begin) * (int64_t)TD_TILE_UNITS;
+        const int64_t first = (t - __ldg(&g->tile_begin)) * (int64_t)TD_TILE_UNITS;
         const uint32_t u0 = (uint32_t)first;
-        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, D.n_units);
+        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, __ldg(&g->n_units));
         Acc a;
         a.zero();
         for (uint32_t u = u0 + threadIdx.x; u < u1; u += BLOCK) {
@@ -368,15 +302,15 @@ k_segnorm_generic(const td_segment* __restrict__ segs, const int64_t* __restrict
                 }
             }
         }
-        if (threadIdx.x < sizeof(td_segment) / 16) cp_async_wait_all();
-        write_partial(a, nz > 0 ? 3 + nz : 2, red, partials + t * TD_PARTIAL_STRIDE);
-        w.end(after);
+        write_warp_partial(a, nz > 0 ? 3 + nz : 2,
+                           partials + (t * TD_WARPS_PER_TILE + warp) * TD_PARTIAL_STRIDE);
     }
 }
 
 typedef void (*segnorm_fn)(const td_segment*, const int64_t*, int64_t, double*);
 
 static_assert(sizeof(td_segment) == 144, "td_segment layout");
+static_assert(BLOCK / 32 == TD_WARPS_PER_TILE, "one partial row per warp of a tile");
 static_assert(sizeof(td_id_desc) == 56, "td_id_desc layout");
 static_assert(sizeof(td_group_desc) == 24, "td_group_desc layout");
 static_assert(sizeof(td_id_result) == 32, "td_id_result layout");
@@ -435,9 +369,9 @@ __global__ void k_reduce_slots(const td_id_desc* __restrict__ ids, int n_ids,
     if (slot < n_ids) {
         const int64_t tb = ids[slot].tile_begin, te = ids[slot].tile_end;
         double d2 = 0.0, x2 = 0.0;
-        for (int64_t t = tb + lane; t < te; t += 32) {
-            d2 += partials[t * TD_PARTIAL_STRIDE + 0];
-            x2 += partials[t * TD_PARTIAL_STRIDE + 1];
+        for (int64_t r = tb * TD_WARPS_PER_TILE + lane; r < te * TD_WARPS_PER_TILE; r += 32) {
+            d2 += partials[r * TD_PARTIAL_STRIDE + 0];
+            x2 += partials[r * TD_PARTIAL_STRIDE + 1];
         }
         d2 = warp_sum(d2);
         x2 = warp_sum(x2);
@@ -452,10 +386,10 @@ __global__ void k_reduce_slots(const td_id_desc* __restrict__ ids, int n_ids,
         double s[TD_SLOT_STRIDE];
 #pragma unroll
         for (int k = 0; k < TD_SLOT_STRIDE; ++k) s[k] = 0.0;
-        for (int64_t t = tb + lane; t < te; t += 32) {
+        for (int64_t r = tb * TD_WARPS_PER_TILE + lane; r < te * TD_WARPS_PER_TILE; r += 32) {
 #pragma unroll
             for (int k = 0; k < TD_SLOT_STRIDE; ++k)
-                if (k <= nz) s[k] += partials[t * TD_PARTIAL_STRIDE + 2 + k];
+                if (k <= nz) s[k] += partials[r * TD_PARTIAL_STRIDE + 2 + k];
         }
 #pragma unroll
         for (int k = 0; k < TD_SLOT_STRIDE; ++k) {
@@ -720,6 +654,43 @@ __global__ void k_gather_bytes(const unsigned char* __restrict__ src, unsigned c
     }
 }
 
+// per-host-thread, per-device auxiliary streams for concurrent class launches
+struct AuxStreams {
+    static constexpr int N = 7;
+    cudaStream_t stream[N];
+    cudaEvent_t join[N];
+    cudaEvent_t fork;
+    bool ready = false;
+};
+
+AuxStreams* aux_streams(int dev) {
+    thread_local AuxStreams pool[16];
+    if (dev < 0 || dev >= 16) return nullptr;
+    AuxStreams& a = pool[dev];
+    if (!a.ready) {
+        for (int k = 0; k < AuxStreams::N; ++k) {
+            if (cudaStreamCreateWithFlags(&a.stream[k], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+            if (cudaEventCreateWithFlags(&a.join[k], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        }
+        if (cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        a.ready = true;
+    }
+    return &a;
+}
+
+void join_aux(AuxStreams* a, int k, cudaStream_t main_stream) {
+    cudaEventRecord(a->join[k], a->stream[k]);
+    cudaStreamWaitEvent(main_stream, a->join[k], 0);
+}
+
+bool serial_classes() {
+    static const bool serial = [] {
+        const char* e = getenv("TD_SERIAL_CLASSES");
+        return e != nullptr && e[0] == '1';
+    }();
+    return serial;
+}
+
 int grid_for(int64_t n, int per_block, int cap) {
     int64_t g = (n + per_block - 1) / per_block;
     if (g < 1) g = 1;
@@ -753,17 +724,37 @@ int td_segnorm(const td_segment* segs, const td_class* classes, int32_t n_classe
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int per_sm = blocks_per_sm > 0 ? blocks_per_sm : 4;
-    for (int c = 0; c < n_classes; ++c) {
+    // Classes run concurrently: the largest on the caller's stream, the others
+    // forked onto this thread's auxiliary streams, so each kernel's tail is
+    // filled by the next kernel's CTAs instead of idling SMs (joined below).
+    int order[64];
+    const int nc = n_classes < 64 ? n_classes : 64;
+    for (int c = 0; c < nc; ++c) order[c] = c;
+    for (int a = 1; a < nc; ++a)
+        for (int b = a; b > 0 && classes[order[b]].n_tiles > classes[order[b - 1]].n_tiles; --b) {
+            const int t = order[b]; order[b] = order[b - 1]; order[b - 1] = t;
+        }
+    AuxStreams* aux = (nc > 1 && !serial_classes()) ? aux_streams(dev) : nullptr;
+    cudaStream_t main_stream = (cudaStream_t)stream;
+    if (aux && cudaEventRecord(aux->fork, main_stream) != cudaSuccess) aux = nullptr;
+    for (int k = 0; k < n_classes; ++k) {
+        const int c = k < nc ? order[k] : k;
         const td_class& C = classes[c];
+        cudaStream_t st = main_stream;
+        if (aux && k > 0 && k <= AuxStreams::N) {
+            st = aux->stream[k - 1];
+            cudaStreamWaitEvent(st, aux->fork, 0);
+        }
         if (C.n_tiles == 0) continue;
         if (!C.tiles || C.n_tiles < 0 || C.nz < 0 || C.nz > TD_MAX_Z)
             return fail("td_segnorm: invalid class %d", c);
         int64_t grid = (int64_t)sms * per_sm;
         if (grid > C.n_tiles) grid = C.n_tiles;
         if (!C.vec || C.mode != TD_MODE_NORMS) {
-            k_segnorm_generic<<<(unsigned)grid, BLOCK, 0, (cudaStream_t)stream>>>(
+            k_segnorm_generic<<<(unsigned)grid, BLOCK, 0, st>>>(
                 segs, C.tiles, C.n_tiles, partials, C.mode, C.atol, C.rtol);
             if (int rc = check_launch("td_segnorm")) return rc;
+            if (st != main_stream) join_aux(aux, k - 1, main_stream);
             continue;
         }
         segnorm_fn fn = nullptr;
@@ -777,8 +768,9 @@ int td_segnorm(const td_segment* segs, const td_class* classes, int32_t n_classe
             if (!fn) return fail("td_segnorm: no vector walker for class %d (dtype=%d nz=%d has_x=%d)", c,
                                  C.dtype, C.nz, C.has_x);
         }
-        fn<<<(unsigned)grid, BLOCK, 0, (cudaStream_t)stream>>>(segs, C.tiles, C.n_tiles, partials);
+        fn<<<(unsigned)grid, BLOCK, 0, st>>>(segs, C.tiles, C.n_tiles, partials);
         if (int rc = check_launch("td_segnorm")) return rc;
+        if (st != main_stream) join_aux(aux, k - 1, main_stream);
     }
     return 0;
 }

@@ -517,7 +517,7 @@ class Prepared:
         n_cls = len(plan.class_lists)
         self.ids_ptr = base + offsets[1 + n_cls]
         self.grp_ptr = base + offsets[2 + n_cls]
-        self.n_part = max(1, plan.n_tiles * N.PARTIAL_STRIDE)
+        self.n_part = max(1, plan.n_tiles * N.WARPS_PER_TILE * N.PARTIAL_STRIDE)
         self.work = torch.empty(self.n_part + 2 * n_ids + N.SLOT_STRIDE * n_groups,
                                 dtype=torch.float64, device=dev)
         self.part_ptr = self.work.data_ptr()
