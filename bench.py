@@ -299,7 +299,6 @@ def main():
                prep.idsum_ptr, prep.gsum_ptr, N.stream_handle(stream))
         if world > 1:
             allreduce_partials(prep)
-        prep.res[-8:].zero_()
         N.call("td_verdict", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups, prep.idsum_ptr,
                prep.gsum_ptr, prep.kappa, prep.eps, prep.replica_eps, prep.idres_ptr, prep.gres_ptr,
                prep.tie_ptr, N.stream_handle(stream))

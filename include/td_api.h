@@ -168,7 +168,7 @@ int td_reduce_slots(const td_id_desc* ids, int32_t n_ids,
 
 /* ---- kernel 3: batched threshold compare -> per-id verdicts ----
  * eps = fmt.eps (threshold floor); replica_eps = fmt.eps for check_replicas.
- * near_ties: one device uint64 counter, incremented. */
+ * near_ties: one device uint64 counter, reset and then counted. */
 int td_verdict(const td_id_desc* ids, int32_t n_ids,
                const td_group_desc* groups, int32_t n_groups,
                const double* id_sums, const double* group_sums,

@@ -796,6 +796,8 @@ int td_verdict(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups
     if (n_ids < 0 || !ids || !id_sums || !id_out || !near_ties || (n_groups && (!groups || !group_sums || !group_out)))
         return fail("td_verdict: invalid arguments");
     const int threads = 128;
+    if (cudaMemsetAsync(near_ties, 0, sizeof(unsigned long long), (cudaStream_t)stream) != cudaSuccess)
+        return fail("td_verdict: cannot reset the near-tie counter");
     k_verdict<<<(n_ids + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(
         ids, n_ids, groups, id_sums, group_sums, kappa, eps, replica_eps, id_out, group_out, near_ties);
     return check_launch("td_verdict");

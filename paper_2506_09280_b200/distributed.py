@@ -327,7 +327,6 @@ class DistributedCheckPlan:
             for slot, vals in extra.items():
                 gsum[slot] += torch.from_numpy(vals).to(gsum.device)
         allreduce_partials(prep, self.comm)
-        prep.res[-8:].zero_()
         N.call("td_verdict", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups,
                prep.idsum_ptr, prep.gsum_ptr, prep.kappa, prep.eps, prep.replica_eps,
                prep.idres_ptr, prep.gres_ptr, prep.tie_ptr, sh)
