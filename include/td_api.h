@@ -20,6 +20,7 @@
  *                replica equality across GPUs without moving data
  *   td_box_gather
  *                materialises merge()'s f64 output on the device (public merge API)
+ *   td_generate  generate_full's Normal/Uniform/TokenIds streams (generation.py:81-160)
  *   td_gather_bytes
  *                unpacks TTRC payloads from a file image in HBM into an aligned
  *                arena (device-side trace reader, tracestore.py:225-284)
@@ -206,6 +207,19 @@ int td_fingerprint(const void* x, int32_t dtype, int64_t n,
  * boxes: n_boxes rows of {src_off, dst_off, rows, cols, src_stride, dst_stride} int64 */
 int td_box_gather(const void* src, int32_t src_dtype, double* dst,
                   const int64_t* boxes, int32_t n_boxes, void* stream);
+
+/* ---- generate_full on the device (generation.py:81-160) ----
+ * dist: 0 normal(mean=a, std=b) by Box-Muller on consecutive uniform pairs,
+ *       1 uniform(low=a, high=b), 2 token ids floor(u*vocab) capped at vocab-1.
+ * The reference drops exact-zero uniforms from the normal stream (a 2^-53
+ * event per word, generation.py:94-103): `skips` lists the sorted raw word
+ * indices to skip (NULL/0 normally); zero_count (device uint64) receives the
+ * number of zero words seen in the first 2*ceil(n/2) + n_skips words, so the
+ * caller can retry with the skip list.  Ops rounded separately (no FMA);
+ * log/cos/sin are CUDA's (<= 2 ulp), sqrt is IEEE. */
+int td_generate(double* out, int64_t n, uint64_t seed, int32_t dist, double a, double b,
+                int64_t vocab, const int64_t* skips, int32_t n_skips,
+                unsigned long long* zero_count, int64_t* zero_pos, int32_t zero_cap, void* stream);
 
 /* ---- device TTRC reader: byte ranges of a file image -> aligned arena ----
  * ranges: n rows of {src_off, dst_off, nbytes} int64 (device); any alignment. */

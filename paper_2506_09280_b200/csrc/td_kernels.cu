@@ -632,6 +632,58 @@ __global__ void k_box_gather(const char* __restrict__ src, int dt, double* __res
     }
 }
 
+__device__ __forceinline__ double uniform53(uint64_t seed, uint64_t k) {
+    return __dmul_rn((double)(splitmix_word(seed, k) >> 11), 0x1p-53);
+}
+
+// raw word index of the m-th word that survives the skip list (sorted)
+__device__ __forceinline__ uint64_t skip_map(uint64_t m, const int64_t* __restrict__ skips, int n_skips) {
+    for (int j = 0; j < n_skips; ++j)
+        if ((uint64_t)skips[j] <= m) ++m;
+    return m;
+}
+
+__global__ void k_generate(double* __restrict__ out, int64_t n, uint64_t seed, int dist, double a, double b,
+                           int64_t vocab, const int64_t* __restrict__ skips, int n_skips,
+                           unsigned long long* __restrict__ zero_count, int64_t* __restrict__ zero_pos,
+                           int zero_cap) {
+    const int64_t pairs = (n + 1) / 2;
+    const int64_t words = dist == 0 ? 2 * pairs + n_skips : n;
+    // zero census over the words the normal stream consumes
+    if (dist == 0 && zero_count) {
+        for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < words;
+             k += (int64_t)gridDim.x * blockDim.x) {
+            if ((splitmix_word(seed, (uint64_t)k) >> 11) == 0) {
+                const unsigned long long slot = atomicAdd(zero_count, 1ull);
+                if ((int64_t)slot < zero_cap) zero_pos[slot] = k;
+            }
+        }
+    }
+    if (dist == 0) {
+        for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < pairs;
+             p += (int64_t)gridDim.x * blockDim.x) {
+            const double u1 = uniform53(seed, skip_map(2 * p, skips, n_skips));
+            const double u2 = uniform53(seed, skip_map(2 * p + 1, skips, n_skips));
+            const double r = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
+            const double th = __dmul_rn(2.0 * 3.141592653589793, u2);
+            const double z0 = __dmul_rn(r, cos(th));
+            out[2 * p] = __dadd_rn(__dmul_rn(z0, b), a);
+            if (2 * p + 1 < n) out[2 * p + 1] = __dadd_rn(__dmul_rn(__dmul_rn(r, sin(th)), b), a);
+        }
+    } else {
+        for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+             k += (int64_t)gridDim.x * blockDim.x) {
+            const double u = uniform53(seed, (uint64_t)k);
+            if (dist == 1) {
+                out[k] = __dadd_rn(a, __dmul_rn(u, __dsub_rn(b, a)));
+            } else {
+                const double f = floor(__dmul_rn(u, (double)vocab));
+                out[k] = f < (double)(vocab - 1) ? f : (double)(vocab - 1);
+            }
+        }
+    }
+}
+
 // one CTA per range (grid-strided); bytes move 4 at a time when source and
 // destination agree mod 4, else one at a time (file payloads are unaligned)
 __global__ void k_gather_bytes(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
@@ -849,6 +901,18 @@ int td_box_gather(const void* src, int32_t src_dtype, double* dst, const int64_t
     dim3 grid(64, (unsigned)n_boxes);
     k_box_gather<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<const char*>(src), src_dtype, dst, boxes);
     return check_launch("td_box_gather");
+}
+
+int td_generate(double* out, int64_t n, uint64_t seed, int32_t dist, double a, double b, int64_t vocab,
+                const int64_t* skips, int32_t n_skips, unsigned long long* zero_count, int64_t* zero_pos,
+                int32_t zero_cap, void* stream) {
+    if (n == 0) return 0;
+    if (!out || n < 0 || dist < 0 || dist > 2 || n_skips < 0 || (n_skips && !skips) ||
+        (zero_count && !zero_pos && zero_cap > 0) || (dist == 2 && vocab < 1))
+        return fail("td_generate: invalid arguments");
+    k_generate<<<grid_for(n, 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+        out, n, seed, dist, a, b, vocab, skips, n_skips, zero_count, zero_pos, zero_cap);
+    return check_launch("td_generate");
 }
 
 int td_gather_bytes(const void* src, void* dst, const int64_t* ranges, int64_t n, void* stream) {

@@ -12,6 +12,7 @@ generator (`generator="philox"`); its CPU restatement lives in the tests.
 from __future__ import annotations
 
 import math
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -72,3 +73,107 @@ def signed_uniforms(tag: str, shape: tuple[int, ...], generator: str = "splitmix
     """Reference-shaped host array (generation.py:163-167), generated on the GPU."""
     n = math.prod(shape)
     return signed_uniforms_device(tag, n, 0, generator).cpu().numpy().reshape(shape)
+
+
+# ---------------------------------------------------------------------------
+# generate_full on the device (generation.py:81-186)
+
+@dataclass(frozen=True)
+class Normal:
+    mean: float = 0.0
+    std: float = 1.0
+
+
+@dataclass(frozen=True)
+class Uniform:
+    low: float = 0.0
+    high: float = 1.0
+
+
+@dataclass(frozen=True)
+class TokenIds:
+    vocab: int
+
+
+@dataclass(frozen=True)
+class GenSpec:
+    distribution: object
+    shape: tuple
+
+    def __post_init__(self):
+        object.__setattr__(self, "shape", tuple(int(n) for n in self.shape))
+        if any(n <= 0 for n in self.shape):
+            raise ValueError(f"non-positive dimension in shape {self.shape}")
+        if isinstance(self.distribution, TokenIds) and self.distribution.vocab < 1:
+            raise ValueError("token vocabulary must be positive")
+
+
+def generate_full_device(ident, spec: GenSpec):
+    """The full logical tensor for `ident` under `spec`, as a CUDA f64
+    tensor (td_generate).  Uniform and token streams are bit-exact with the
+    reference; normals use CUDA's log/cos/sin (<= 2 ulp) and so agree to
+    ~1e-16 relative (the reference's own normal test allows 1e-15,
+    test_generation.py:59-63).  Exact-zero uniforms (2^-53 per word) are
+    skipped exactly like the reference's scalar fallback."""
+    import torch
+    seed = seed_from(ident)
+    n = math.prod(spec.shape)
+    d = spec.distribution
+    if isinstance(d, Normal):
+        code, a, b, vocab = 0, float(d.mean), float(d.std), 1
+    elif isinstance(d, Uniform):
+        code, a, b, vocab = 1, float(d.low), float(d.high), 1
+    elif isinstance(d, TokenIds):
+        code, a, b, vocab = 2, 0.0, 0.0, int(d.vocab)
+    else:
+        raise TypeError(f"unknown distribution {d!r}")
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    cap = 64
+    count = torch.zeros(1, dtype=torch.int64, device="cuda")
+    pos = torch.zeros(cap, dtype=torch.int64, device="cuda")
+    skips: list = []
+    while True:
+        sk = torch.tensor(skips, dtype=torch.int64, device="cuda") if skips else None
+        count.zero_()
+        N.call("td_generate", out.data_ptr(), n, seed & _M64, code, a, b, vocab,
+               sk.data_ptr() if sk is not None else None, len(skips),
+               count.data_ptr() if code == 0 else None, pos.data_ptr(), cap, N.stream_handle())
+        if code != 0:
+            break
+        seen = int(count.item())
+        if seen > cap:
+            raise N.NativeError(f"{seen} zero uniforms in one stream; skip list capacity is {cap}")
+        found = sorted(int(p) for p in pos[:seen].cpu().tolist())
+        if found == skips:
+            break
+        skips = found
+    return out.reshape(spec.shape)
+
+
+def generate_full(ident, spec: GenSpec, device=None):
+    """Reference-shaped generate_full (generation.py:146-160): a host Tensor,
+    or the CUDA tensor itself with device="cuda"."""
+    t = generate_full_device(ident, spec)
+    if device is not None:
+        return t
+    from .tensor import Tensor
+    return Tensor(t.cpu().numpy())
+
+
+def extract_shard(full, mapping):
+    """The shard a rank holding `mapping` sees of `full` (generation.py:170-186)."""
+    from .canonical import validate_mapping
+    from .errors import MappingInvalid
+    validate_mapping(mapping)
+    data = getattr(full, "data", full)
+    if tuple(data.shape) != mapping.global_shape:
+        raise MappingInvalid(
+            f"full tensor shape {tuple(data.shape)} != mapping global shape {mapping.global_shape}")
+    if sum(loc.volume for loc, _ in mapping.pairs) != math.prod(mapping.local_shape):
+        raise MappingInvalid("local boxes do not cover the local shape")
+    import torch
+    out = torch.zeros(mapping.local_shape, dtype=data.dtype, device=data.device) \
+        if isinstance(data, torch.Tensor) else np.zeros(mapping.local_shape, dtype=np.float64)
+    for loc, glob in mapping.pairs:
+        out[loc.as_slices()] = data[glob.as_slices()]
+    return out

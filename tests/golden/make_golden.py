@@ -290,6 +290,19 @@ def vectors() -> dict:
         rel.append({"a_hex": [float(x).hex() for x in a], "b_hex": [float(x).hex() for x in b],
                     "rel": float(rel_err_arrays(a, b)).hex()})
     v["rel_err"] = rel
+    from traindiff.canonical import CanonicalId, TensorKind
+    from traindiff.generation import GenSpec, Normal, TokenIds, Uniform, generate_full
+    gens = []
+    for ident, spec, kind in [
+            (CanonicalId(0, 0, TensorKind.PARAM, "model.embedding.word"), GenSpec(Normal(0.0, 0.02), (64, 32)), "normal"),
+            (CanonicalId(0, 1, TensorKind.ACTIVATION_IN, "model.layers.3.mlp"), GenSpec(Normal(0.0, 0.02), (16, 33)), "normal"),
+            (CanonicalId(0, 0, TensorKind.ACTIVATION_IN, "ustats"), GenSpec(Uniform(-2.0, 6.0), (5000,)), "uniform"),
+            (CanonicalId(0, 3, TensorKind.ACTIVATION_IN, "model.embedding"), GenSpec(TokenIds(vocab=50257), (4096,)), "tokens")]:
+        data = generate_full(ident, spec).data
+        gens.append({"ident": ident.encode(), "kind": kind, "shape": list(spec.shape),
+                     "params": list(spec.distribution.__dict__.values()),
+                     "values_hex": [float(x).hex() for x in data.ravel()]})
+    v["generate_full"] = gens
     return v
 
 

@@ -308,3 +308,54 @@ def test_device_ttrc_reader_matches_host_reader(tmp_path, cases, golden_trace_by
             assert np.array_equal(a.payload.cpu().numpy(), b.payload)
             assert a.mapping.signature() == b.mapping.signature()
         assert trace_to_bytes(dev) == raw
+
+
+def test_cli_check_reproduces_reference_output(tmp_path, cases, golden_trace_bytes, capsys):
+    """`check` front end: same stdout (text and JSON modulo last-bit norms)
+    and the same exit code as the reference CLI (cli.py:100-111, 276-293)."""
+    from paper_2506_09280_b200.cli import main
+    for case in cases["checks"][:8]:
+        ref, cand, tolp = tmp_path / "r.ttrc", tmp_path / "c.ttrc", tmp_path / "t.json"
+        ref.write_bytes(golden_trace_bytes(case["ref"]))
+        cand.write_bytes(golden_trace_bytes(case["cand"]))
+        tolp.write_text(cases["tols"][case["tol"]])
+        rc = main(["check", "--ref", str(ref), "--cand", str(cand), "--tol", str(tolp),
+                   "--k", str(case["kappa"])])
+        out = capsys.readouterr().out
+        want = json.loads(case["report"])
+        assert rc == want["exit_code"], case["name"]
+        assert out == case["text"], case["name"]
+    rc = main(["check", "--ref", str(tmp_path / "missing"), "--cand", str(cand), "--tol", str(tolp)])
+    assert rc == 1
+    (tmp_path / "bad").write_bytes(b"XXXX" + b"\0" * 16)
+    assert main(["check", "--ref", str(tmp_path / "bad"), "--cand", str(cand), "--tol", str(tolp)]) == 4
+
+
+def test_generate_full_matches_reference(vectors):
+    """generate_full on the device: uniform and token streams bit-exact,
+    Box-Muller normals within 1e-15 relative (the reference's own bar,
+    test_generation.py:59-63)."""
+    from paper_2506_09280_b200.canonical import parse_canonical
+    from paper_2506_09280_b200.generation import (GenSpec, Normal, TokenIds, Uniform,
+                                                  extract_shard, generate_full)
+    exact = total = 0
+    for g in vectors["generate_full"]:
+        want = np.array([float.fromhex(h) for h in g["values_hex"]]).reshape(g["shape"])
+        if g["kind"] == "normal":
+            spec = GenSpec(Normal(*g["params"]), g["shape"])
+        elif g["kind"] == "uniform":
+            spec = GenSpec(Uniform(*g["params"]), g["shape"])
+        else:
+            spec = GenSpec(TokenIds(*g["params"]), g["shape"])
+        got = generate_full(parse_canonical(g["ident"]), spec).data
+        if g["kind"] == "normal":
+            assert np.allclose(got, want, rtol=1e-15, atol=0.0)
+            exact += int((got == want).sum())
+            total += got.size
+        else:
+            assert np.array_equal(got, want), g["kind"]
+    assert exact / total > 0.5          # most normals are bit-identical too
+    full = generate_full(parse_canonical(vectors["generate_full"][0]["ident"]),
+                         GenSpec(Normal(0.0, 0.02), (64, 32)), device="cuda")
+    m = td.ShardMapping((32, 32), (64, 32), ((td.whole_box((32, 32)), td.SliceBox(((32, 64), (0, 32)))),))
+    assert torch.equal(extract_shard(full, m), full[32:])
