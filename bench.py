@@ -267,9 +267,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TD_BENCH_BACKEND=gloo TD_BENCH_SAME_DEVICE=1 validates the multi-rank
+    # code path with several ranks sharing one GPU (timings then meaningless)
+    if os.environ.get("TD_BENCH_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("TD_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2506_09280_b200 import _native as N
     from paper_2506_09280_b200.checker import CheckPlan, check
     from paper_2506_09280_b200.device import resolve_operands
