@@ -236,29 +236,12 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
                         a.d2 = fma(d, d, a.d2);
                         a.x2 = fma(xv, xv, a.x2);
                     }
-                    if (NZ > 0) a.y2 = fma(yv, yv, a.y2);
-                }
-                // Replica diffs word by word: a 32-bit word equal in copy 0 and
-                // copy j contributes exactly 0 to sum (y - z_j)^2 unless it holds
-                // inf/NaN — and then y2 itself is inf/NaN, so rel_err(copy0,
-                // copy_j) is 0 or NaN either way and never wins the strict `>`
-                // of check_replicas (canonical.py:239-242).  Clean replicas (the
-                // common case) therefore cost loads and integer compares only.
-                constexpr int WORDS = 4 * Q;
-                constexpr int PER_WORD = 8 / WORDS;
+                    if (NZ > 0) {
+                        a.y2 = fma(yv, yv, a.y2);
 #pragma unroll
-                for (int j = 0; j < NZ; ++j) {
-#pragma unroll
-                    for (int wd = 0; wd < WORDS; ++wd) {
-                        const uint32_t yw = (&yr[k][0].x)[wd];
-                        const uint32_t zw = (&zr[j][k][0].x)[wd];
-                        if (yw != zw) {
-#pragma unroll
-                            for (int h = 0; h < PER_WORD; ++h) {
-                                const int e8 = wd * PER_WORD + h;
-                                const double dz = Vec<DT>::at(yr[k], e8) - Vec<DT>::at(zr[j][k], e8);
-                                a.z[j] = fma(dz, dz, a.z[j]);
-                            }
+                        for (int j = 0; j < NZ; ++j) {
+                            const double dz = yv - Vec<DT>::at(zr[j][k], e8);
+                            a.z[j] = fma(dz, dz, a.z[j]);
                         }
                     }
                 }

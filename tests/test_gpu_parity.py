@@ -359,3 +359,15 @@ def test_generate_full_matches_reference(vectors):
                          GenSpec(Normal(0.0, 0.02), (64, 32)), device="cuda")
     m = td.ShardMapping((32, 32), (64, 32), ((td.whole_box((32, 32)), td.SliceBox(((32, 64), (0, 32)))),))
     assert torch.equal(extract_shard(full, m), full[32:])
+
+
+def test_reports_are_byte_deterministic(cases, golden_trace_bytes):
+    """Fixed-order reductions: repeating check() reproduces the report bytes
+    (the reference's CLI determinism contract, test_cli.py:55-67)."""
+    case = next(c for c in cases["checks"] if c["name"] == "bug_tp_row_allreduce_k3")
+    ref = trace_from_bytes(golden_trace_bytes(case["ref"]), device="cuda")
+    cand = trace_from_bytes(golden_trace_bytes(case["cand"]), device="cuda")
+    tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+    a = td.render_report(td.check(ref, cand, tol, fmt=td.FloatFormat.BF16), "json")
+    b = td.render_report(td.check(ref, cand, tol, fmt=td.FloatFormat.BF16), "json")
+    assert a == b

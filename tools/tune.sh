@@ -1,8 +1,9 @@
 #!/bin/bash
-# run the cfg2 bench (device path only) against each library variant in tools/
+# A/B the cfg2 bench (device path only) across library variants in tools/,
+# twice in alternating order to expose box drift
+for pass in 1 2; do
 for lib in tools/libtd_*.so; do
-  echo "== $lib"
-  TD_LIB=$PWD/$lib timeout 600 python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu 2>&1 | python3 tools/summarize_bench.py
+  echo "== pass $pass $lib"
+  TD_LIB=$PWD/$lib timeout 600 python bench.py --steps 30 --warmup 5 --no-e2e --no-cpu 2>&1 | python3 tools/summarize_bench.py
 done
-echo "== default lib, classes serialised"
-TD_SERIAL_CLASSES=1 timeout 600 python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu 2>&1 | python3 tools/summarize_bench.py
+done
