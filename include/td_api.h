@@ -57,7 +57,9 @@ enum td_generator { TD_GEN_SPLITMIX64 = 0, TD_GEN_PHILOX4x32 = 1 };
 #define TD_MAX_Z 7              /* replica copies beside copy 0 per segment */
 #define TD_PARTIAL_STRIDE 10    /* doubles per partial row: d2, x2, y2, z2[7] */
 #define TD_WARPS_PER_TILE 8     /* partial rows per tile (one per warp of a 256-thread CTA) */
+#ifndef TD_TILE_UNITS
 #define TD_TILE_UNITS 8192      /* units (8-element vectors or elements) per tile */
+#endif
 #define TD_SLOT_STRIDE 8        /* doubles per reduced slot */
 
 /* segment flags */

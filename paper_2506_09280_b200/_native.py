@@ -23,7 +23,7 @@ GEN_SPLITMIX64, GEN_PHILOX4x32 = 0, 1
 MAX_Z = 7
 PARTIAL_STRIDE = 10
 WARPS_PER_TILE = 8
-TILE_UNITS = 8192
+TILE_UNITS = int(os.environ.get("TD_TILE_UNITS", "8192"))  # must match the library build
 SLOT_STRIDE = 8
 SEG_HAS_X = 1
 SEG_VEC = 2

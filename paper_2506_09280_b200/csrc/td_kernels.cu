@@ -50,6 +50,10 @@ int check_launch(const char* what) {
     return 0;
 }
 
+#ifndef TD_LDG_STREAM
+#define TD_LDG_STREAM "ld.global.nc.L1::no_allocate.L2::256B.v4.u32"
+#endif
+
 constexpr int BLOCK = 256;
 constexpr int NWARP = BLOCK / 32;
 
@@ -58,7 +62,7 @@ constexpr int NWARP = BLOCK / 32;
 
 __device__ __forceinline__ uint4 ld_stream(const void* p) {
     uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile(TD_LDG_STREAM " {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
@@ -317,6 +321,12 @@ static_assert(sizeof(td_id_result) == 32, "td_id_result layout");
 static_assert(sizeof(td_group_result) == 16, "td_group_result layout");
 static_assert(sizeof(td_class) == 56, "td_class layout");
 
+#ifndef TD_NZ3_U
+#define TD_NZ3_U 1
+#endif
+#ifndef TD_NZ3_MINB
+#define TD_NZ3_MINB 4
+#endif
 #ifndef TD_NZ0_U
 #define TD_NZ0_U 4
 #endif
@@ -336,7 +346,7 @@ segnorm_fn pick_vec(int nz, bool hx) {
             case 0: return k_segnorm_vec<DT, 0, true, (TD_NZ0_U / Q > 0 ? TD_NZ0_U / Q : 1), TD_NZ0_MINB>;
             case 1: return k_segnorm_vec<DT, 1, true, U2, 4>;
             case 2: return k_segnorm_vec<DT, 2, true, 1, 4>;
-            case 3: return k_segnorm_vec<DT, 3, true, 1, 4>;
+            case 3: return k_segnorm_vec<DT, 3, true, TD_NZ3_U, TD_NZ3_MINB>;
             case 4: return k_segnorm_vec<DT, 4, true, 1, 2>;
             case 5: return k_segnorm_vec<DT, 5, true, 1, 2>;
             case 6: return k_segnorm_vec<DT, 6, true, 1, 2>;
@@ -495,10 +505,15 @@ __device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t k) {
     return ((uint64_t)c1 << 32) | c0;
 }
 
+// 2u - 1 with u = (w >> 11) * 2^-53 (generation.py:74-78, 166), without an
+// int->double conversion (XU pipe): t = 2u = m * 2^-52 for the 53-bit m is
+// exact as (1.m52 as a double) - (m < 2^52 ? 1 : 0); then t - 1 rounds once,
+// exactly like numpy's 2.0*u - 1.0.  Folded: (1.m52) - (m < 2^52 ? 2 : 1).
 __device__ __forceinline__ double signed_uniform(uint64_t seed, uint64_t k, int gen) {
     const uint64_t w = gen == TD_GEN_PHILOX4x32 ? philox_word(seed, k) : splitmix_word(seed, k);
-    const double u = __dmul_rn((double)(w >> 11), 0x1p-53);   // exact
-    return __dsub_rn(__dmul_rn(2.0, u), 1.0);                  // 2u - 1 (generation.py:166)
+    const uint64_t m = w >> 11;
+    const double one_m = __longlong_as_double((long long)(0x3FF0000000000000ull | (m & 0xFFFFFFFFFFFFFull)));
+    return __dsub_rn(one_m, (m >> 52) ? 1.0 : 2.0);
 }
 
 // quantize_array (tensor.py:64-77): RNE to p significand bits, unbounded
@@ -529,6 +544,17 @@ __device__ __forceinline__ double apply_format(double y, int fmt) {
     }
 }
 
+// bf16 bits of a double that already has <= 8 significant bits; integer ops
+// only (no F2F) for the normal bf16 range, exact conversion otherwise
+__device__ __forceinline__ unsigned short bf16_bits_q8(double v) {
+    const uint32_t hi = (uint32_t)((unsigned long long)__double_as_longlong(v) >> 32);
+    const uint32_t sign = (hi >> 16) & 0x8000u;
+    const uint32_t e = (hi >> 20) & 0x7ffu;
+    if (e >= 897u && e <= 1150u) return (unsigned short)(sign | ((e - 896u) << 7) | ((hi >> 13) & 0x7fu));
+    if (v == 0.0) return (unsigned short)sign;
+    return __bfloat16_as_ushort(__float2bfloat16_rn((float)v));
+}
+
 __device__ __forceinline__ void store_elem(void* base, int dt, int64_t idx, double v) {
     switch (dt) {
         case TD_F32: reinterpret_cast<float*>(base)[idx] = (float)v; break;
@@ -544,6 +570,57 @@ __device__ __forceinline__ void store_elem(void* base, int dt, int64_t idx, doub
     }
 }
 
+__device__ __forceinline__ double perturb_one(double xv, uint64_t seed, uint64_t k, double eps, int gen, int& bad) {
+    const double u = signed_uniform(seed, k, gen);
+    const double f = __dadd_rn(1.0, __dmul_rn(u, eps));   // 1.0 + u*eps
+    const double v = __dmul_rn(xv, f);                     // x * factor
+    bad |= !isfinite(v);
+    return v;
+}
+
+// One thread per group of 8 consecutive elements of a row (cols % 8 == 0,
+// 16-byte aligned rows): 16-byte loads/stores for bf16, one division per group.
+template <bool BF16_Q8>
+__global__ void __launch_bounds__(256)
+k_perturb_vec8(const char* x, char* y, int dt_in, int dt_out, int64_t rows, int64_t cols,
+               int64_t full_cols, int64_t col0, const int64_t* __restrict__ row_pos, int64_t row0,
+               uint64_t seed, double eps, int fmt, int gen, uint32_t div_m, int div_p,
+               unsigned long long* __restrict__ nonfinite) {
+    const int64_t groups = rows * (cols >> 3);
+    const uint32_t gpr = (uint32_t)(cols >> 3);
+    int bad = 0;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = groups < (1ll << 31) ? (int64_t)udiv((uint32_t)g, div_m, div_p) : g / gpr;
+        const int64_t c = (g - r * gpr) * 8;
+        const int64_t pos = row_pos ? __ldg(row_pos + r) : row0 + r;
+        const uint64_t kb = (uint64_t)(pos * full_cols + col0 + c);
+        const int64_t idx = r * cols + c;
+        if (BF16_Q8) {
+            const uint4 in = *reinterpret_cast<const uint4*>(x + idx * 2);
+            const uint32_t* iw = &in.x;
+            uint4 out;
+            uint32_t* ow = &out.x;
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                const double x0 = (double)__uint_as_float(iw[h] << 16);
+                const double x1 = (double)__uint_as_float(iw[h] & 0xffff0000u);
+                const double v0 = quantize_p(perturb_one(x0, seed, kb + 2 * h, eps, gen, bad), 8, 0x1.fep127);
+                const double v1 = quantize_p(perturb_one(x1, seed, kb + 2 * h + 1, eps, gen, bad), 8, 0x1.fep127);
+                ow[h] = (uint32_t)bf16_bits_q8(v0) | ((uint32_t)bf16_bits_q8(v1) << 16);
+            }
+            *reinterpret_cast<uint4*>(y + idx * 2) = out;
+        } else {
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+                const double v = perturb_one(load_elem(x, dt_in, idx + h), seed, kb + h, eps, gen, bad);
+                store_elem(y, dt_out, idx + h, apply_format(v, fmt));
+            }
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(nonfinite, 1ull);
+}
+
 __global__ void k_perturb(const char* x, char* y, int dt_in, int dt_out,
                           int64_t rows, int64_t cols, int64_t full_cols, int64_t col0,
                           const int64_t* __restrict__ row_pos, int64_t row0,
@@ -556,13 +633,8 @@ __global__ void k_perturb(const char* x, char* y, int dt_in, int dt_out,
         for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
              c += (int64_t)gridDim.x * blockDim.x) {
             const int64_t idx = r * cols + c;
-            const double xv = load_elem(x, dt_in, idx);
-            const double u = signed_uniform(seed, kbase + (uint64_t)c, gen);
-            const double f = __dadd_rn(1.0, __dmul_rn(u, eps));   // 1.0 + u*eps
-            double v = __dmul_rn(xv, f);
-            if (!isfinite(v)) bad = 1;
-            v = apply_format(v, fmt);
-            store_elem(y, dt_out, idx, v);
+            const double v = perturb_one(load_elem(x, dt_in, idx), seed, kbase + (uint64_t)c, eps, gen, bad);
+            store_elem(y, dt_out, idx, apply_format(v, fmt));
         }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(nonfinite, 1ull);
@@ -863,10 +935,32 @@ int td_perturb(const void* x, void* y, int32_t dtype_in, int32_t dtype_out, int6
         dtype_out > 3 || fmt < 0 || fmt > 3 || col0 < 0 || col0 + cols > full_cols)
         return fail("td_perturb: invalid arguments");
     const int threads = 256;
-    dim3 grid((unsigned)grid_for(cols, threads, 64), (unsigned)(rows < 65535 ? rows : 65535));
-    k_perturb<<<grid, threads, 0, (cudaStream_t)stream>>>(
-        static_cast<const char*>(x), static_cast<char*>(y), dtype_in, dtype_out, rows, cols, full_cols, col0,
-        row_pos, row0, seed, eps, fmt, generator, nonfinite);
+    const int esz_in = dtype_in == TD_F32 ? 4 : (dtype_in == TD_F64 ? 8 : 2);
+    const int esz_out = dtype_out == TD_F32 ? 4 : (dtype_out == TD_F64 ? 8 : 2);
+    const bool vec = cols % 8 == 0 && ((uintptr_t)x % 16) == 0 && ((uintptr_t)y % 16) == 0 &&
+                     (cols * esz_in) % 16 == 0 && (cols * esz_out) % 16 == 0;
+    if (vec) {
+        const int64_t groups = rows * (cols / 8);
+        const uint32_t gpr = (uint32_t)(cols / 8);
+        const int l = gpr > 1 ? 32 - __builtin_clz(gpr - 1) : 0;
+        const int p = 31 + l;
+        const uint32_t m = (uint32_t)(((1ull << p) + gpr - 1) / gpr);
+        const int grid = grid_for(groups, threads, 148 * 8);
+        const bool q8 = dtype_in == TD_BF16 && dtype_out == TD_BF16 && fmt == TD_FMT_BF16;
+        if (q8)
+            k_perturb_vec8<true><<<grid, threads, 0, (cudaStream_t)stream>>>(
+                static_cast<const char*>(x), static_cast<char*>(y), dtype_in, dtype_out, rows, cols, full_cols,
+                col0, row_pos, row0, seed, eps, fmt, generator, m, p, nonfinite);
+        else
+            k_perturb_vec8<false><<<grid, threads, 0, (cudaStream_t)stream>>>(
+                static_cast<const char*>(x), static_cast<char*>(y), dtype_in, dtype_out, rows, cols, full_cols,
+                col0, row_pos, row0, seed, eps, fmt, generator, m, p, nonfinite);
+    } else {
+        dim3 grid((unsigned)grid_for(cols, threads, 64), (unsigned)(rows < 65535 ? rows : 65535));
+        k_perturb<<<grid, threads, 0, (cudaStream_t)stream>>>(
+            static_cast<const char*>(x), static_cast<char*>(y), dtype_in, dtype_out, rows, cols, full_cols, col0,
+            row_pos, row0, seed, eps, fmt, generator, nonfinite);
+    }
     return check_launch("td_perturb");
 }
 
