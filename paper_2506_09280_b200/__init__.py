@@ -15,11 +15,12 @@ from .checker import (CheckEntry, CheckPlan, CheckReport, StaticReport, Toleranc
                       compare_static, estimate_tolerance, render_report)
 from .errors import (ConfigInvalid, DigestMismatch, FormatError, MappingInvalid, MergeConflict,
                      NonFinite, ReplicaMismatch, ShapeMismatch, TraindiffError, UnknownBugId)
-from .generation import SplitMix64, fnv1a_64, seed_from, signed_uniforms
+from .generation import (GenSpec, Normal, SplitMix64, TokenIds, Uniform, extract_shard, fnv1a_64,
+                         generate_full, seed_from, signed_uniforms)
 from .perturb import PerturbSpec, apply_perturbation
 from .tensor import (POLICIES, FloatFormat, PrecisionPolicy, Tensor, frobenius_norm, quantize,
                      quantize_array, rel_err, rel_err_arrays)
-from .tracestore import (RankMeta, Trace, TraceCollector, TraceFilter, TraceRecord, read_trace,
-                         trace_from_bytes, trace_to_bytes, write_trace)
+from .tracestore import (RankMeta, Trace, TraceCollector, TraceFilter, TraceRecord, pack_pinned,
+                         read_trace, trace_from_bytes, trace_to_bytes, write_trace)
 
 __version__ = "0.1.0"
