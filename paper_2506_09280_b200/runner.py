@@ -20,8 +20,9 @@ from .torchtap.writer import encode_id
 
 
 def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
-                 module_inputs: tuple = (), policy: str = "bf16",
-                 generator: str = "splitmix64", header: dict | None = None) -> Callable:
+                 module_inputs: tuple = (), rewrite: bool = False, rewrite_std: float = 0.02,
+                 policy: str = "bf16", generator: str = "splitmix64",
+                 header: dict | None = None) -> Callable:
     """runner(spec) for estimate_tolerance.
 
     model:     the torch module (already on the GPU)
@@ -29,17 +30,37 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
     embedding: torch name of the module whose output is perturbed
     tap:       which modules to trace and how to name them
     module_inputs: torch names whose first input is perturbed too (module-wise)
+    rewrite:   module-wise mode proper (engine.py:363-377): each listed
+               module's input is first REGENERATED from its canonical id —
+               generate_full(ActivationIn id, Normal(0, rewrite_std)) on the
+               GPU, rounded to the storage format — so every module sees a
+               fixed input and only its own perturbation, then perturbed
     """
     emb = model.get_submodule(embedding)
     emb_id = encode_id(tap.iteration, tap.microbatch, "ActivationOut", tap.canonical_name(embedding))
 
     def runner(spec: PerturbSpec | None):
         hooks = []
+        if rewrite:
+            for name in module_inputs:
+                ident = encode_id(tap.iteration, tap.microbatch, "ActivationIn", tap.canonical_name(name))
+
+                def regen(module, args, _ident=ident):
+                    if not args:
+                        return None
+                    x = args[0]
+                    value = _regenerate(_ident, tuple(x.shape), rewrite_std, policy).to(x.dtype)
+                    if spec is not None and spec.eps != 0.0:
+                        value = apply_perturbation(value, _ident, spec, policy=policy, generator=generator)
+                    # the module reads `value`; its input gradient still flows
+                    # back to the chain unchanged (engine.py:383-385)
+                    return (_replace(x, value),) + tuple(args[1:])
+                hooks.append(model.get_submodule(name).register_forward_pre_hook(regen, prepend=True))
         if spec is not None and spec.eps != 0.0:
             def out_hook(module, args, output):
                 return apply_perturbation(output, emb_id, spec, policy=policy, generator=generator)
             hooks.append(emb.register_forward_hook(out_hook, prepend=True))
-            for name in module_inputs:
+            for name in (() if rewrite else module_inputs):
                 ident = encode_id(tap.iteration, tap.microbatch, "ActivationIn", tap.canonical_name(name))
 
                 def pre_hook(module, args, _ident=ident):
@@ -59,3 +80,37 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
         hdr = header if header is not None else dict(handle.header(), mode="module-wise" if module_inputs else "cascade")
         return handle.trace(hdr)
     return runner
+
+
+_REPLACE = None
+
+
+def _replace(x, value):
+    """autograd-aware substitution: forward yields `value`, backward hands the
+    gradient to the replaced input `x` unchanged."""
+    global _REPLACE
+    if _REPLACE is None:
+        import torch
+
+        class Replace(torch.autograd.Function):
+            @staticmethod
+            def forward(ctx, inp, val):
+                return val.clone()
+
+            @staticmethod
+            def backward(ctx, grad):
+                return grad, None
+        _REPLACE = Replace.apply
+    return _REPLACE(x, value)
+
+
+def _regenerate(ident: str, shape: tuple, std: float, policy: str):
+    """generate_full(ident, Normal(0, std), shape) on the GPU, quantised to the
+    storage format with the reference's RNE (tensor.py:64-77) — fp64 result."""
+    from .canonical import parse_canonical
+    from .generation import GenSpec, Normal, generate_full_device
+    from .tensor import FloatFormat, quantize_array
+    full = generate_full_device(parse_canonical(ident), GenSpec(Normal(0.0, std), shape))
+    if policy == "fp32":
+        return full
+    return quantize_array(full, FloatFormat.BF16)

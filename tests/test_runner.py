@@ -126,3 +126,27 @@ def test_module_wise_perturbation_hits_every_listed_input(setup):
              if not torch.equal(r.payload, s.payload)}
     for i in range(8):
         assert f"iter=0|mb=0|kind=ActivationIn|mod=model.layers.{i}" in moved
+
+
+def test_rewrite_mode_regenerates_inputs_and_localises_a_bug(setup):
+    """Module-wise mode (engine.py:363-377): every listed module's input is
+    regenerated from its id on the GPU, so a corrupted block flags at its own
+    output while downstream blocks stay clean (test_checker.py:358-372)."""
+    import paper_2506_09280_b200 as td
+    model, step = setup
+    names = tuple(f"layers.{i}" for i in range(8))
+    runner = _runner(model, step, module_inputs=names, rewrite=True)
+    eps = td.FloatFormat.BF16.eps
+    tol = td.estimate_tolerance(runner, n_samples=3, eps_p=eps)
+    ref = runner(None)
+    again = runner(None)
+    assert td.check(ref, again, tol, fmt=td.FloatFormat.BF16).exit_code() == 0
+    hook = model.layers[2].register_forward_hook(lambda m, a, o: o * 1.1)
+    try:
+        bad = runner(None)
+    finally:
+        hook.remove()
+    rep = td.check(ref, bad, tol, fmt=td.FloatFormat.BF16)
+    flagged_fwd = {e.ident for e in rep.entries if e.verdict == "flag" and "kind=Activation" in e.ident
+                   and "Grad" not in e.ident}
+    assert flagged_fwd == {"iter=0|mb=0|kind=ActivationOut|mod=model.layers.2"}
