@@ -86,15 +86,22 @@ def workload(name: str, rank: int = 0):
             model, pcfg, dtype, fmt = L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), torch.float32, FloatFormat.FP32
             label = "config1 GPT-2-small-shape L=2 fp32 traces, TP=2 candidate vs single-device reference"
         elif name == "cfg3":
-            model = L.ModelShape(layers=16, d_model=2048, n_heads=32, d_ff=8192, seq_len=2048, vocab=128256,
-                                 n_kv_heads=8, gated_mlp=True, norm_bias=False, position_table=False)
+            model = L.LLAMA3_1B
             pcfg, dtype, fmt = L.ParallelConfig(tp=8), torch.bfloat16, FloatFormat.BF16
-            label = "config3 Llama-3-1B-shape bf16 traces (S=2048), TP=8 candidate vs single-device reference"
+            label = ("config3 Llama-3-1B-shape bf16 traces (L=16 d=2048 GQA 32/8 ff=8192 SwiGLU S=8192 "
+                     "V=128256), TP=8 candidate vs single-device reference, injected bugs: wrong shard "
+                     "order (lm_head logits), missing row-parallel allreduce (layers.7.attn output), "
+                     "scale error (embedding output)")
         else:
             model, pcfg, dtype, fmt = L.GPT2_MEDIUM, L.ParallelConfig(tp=4), torch.bfloat16, FloatFormat.BF16
             label = ("config2 GPT-2-medium-shape bf16 traces (L=24 d=1024 ff=4096 S=1024 V=50304), TP=4 "
                      "candidate vs single-device reference, activations+grads+MainGrad+Param")
-        ref, cand = synthetic.build(model, pcfg, dtype=dtype, seed=rank)
+        bugs = None
+        if name == "cfg3":
+            bugs = {"iter=0|mb=0|kind=ActivationOut|mod=model.lm_head": "order",
+                    "iter=0|mb=0|kind=ActivationOut|mod=model.layers.7.attn": "partial",
+                    "iter=0|mb=0|kind=ActivationOut|mod=model.embedding": "scale"}
+        ref, cand = synthetic.build(model, pcfg, dtype=dtype, seed=rank, eps=fmt.eps, bugs=bugs)
         desc = {"workload": label, "model": f"layers={model.layers} d={model.d_model} ff={model.d_ff} "
                                            f"S={model.seq_len} V={model.vocab}",
                 "candidate_layout": f"tp={pcfg.tp} dp={pcfg.dp} cp={pcfg.cp} sp={pcfg.sp}",

@@ -144,3 +144,63 @@ def sweep_pair(n_bytes: int, *, maps: str = "identity", g: int = 1, dtype=None, 
     else:
         raise ValueError(maps)
     return ref, cand
+
+
+def build_rank_share(model: ModelShape, pcfg: ParallelConfig, world: int, rank: int, *,
+                     owner=None, dtype=None, seed: int = 0, eps: float = 2.0 ** -8,
+                     header: dict | None = None):
+    """One GPU's share of a multi-GPU job, built without materialising the
+    others': the candidate records `owner(spec) == rank` (default: candidate
+    rank (dp, tp) -> dp*tp_size + tp, mod world) and, from the same logical
+    tensors, the reference slices covering the global boxes of the copy-0
+    shards this rank compares (what distributed.split_reference hands it).
+
+    Returns (ref_local, cand_local, all candidate RecordSpecs, owner function)
+    so a caller can build the global plan (plan.Plan(owner=..., me=rank))."""
+    import torch
+    from .canonical import ShardMapping, SliceBox
+    dtype = dtype or torch.bfloat16
+    owner = owner or (lambda s: (s.rank[0] * pcfg.tp + s.rank[1] + pcfg.tp * pcfg.dp * s.rank[4]) % world)
+    hdr = header or {"digest": f"synthetic-{model}-{seed}", "mode": "cascade"}
+    ref_specs = {s.ident: s for s in emit_records(model, ParallelConfig(microbatches=pcfg.microbatches))}
+    cand_specs = emit_records(model, pcfg)
+    by_id: dict = {}
+    for s in cand_specs:
+        by_id.setdefault(s.ident, []).append(s)
+    policy = "bf16" if dtype == torch.bfloat16 else "fp32"
+    ref, cand = Trace(header=dict(hdr)), Trace(header=dict(hdr))
+    gen = torch.Generator(device="cuda")
+    for n, (ident, specs) in enumerate(by_id.items()):
+        mine = [s for s in specs if owner(s) == rank]
+        # copy 0 of each shard layout = first record with that (local shape, pairs)
+        seen, copy0 = set(), []
+        for s in specs:
+            key = (s.mapping.local_shape, tuple((l.bounds, g.bounds) for l, g in s.mapping.pairs))
+            if key not in seen:
+                seen.add(key)
+                copy0.append(s)
+        compares = [s for s in copy0 if owner(s) == rank]
+        if not mine:
+            continue
+        gen.manual_seed(seed * 1000003 + n)
+        rspec = ref_specs.get(ident)
+        shape = rspec.mapping.global_shape if rspec else specs[0].mapping.global_shape
+        kind = ident.split("|")[2][5:]
+        x = _fill(shape, kind, model.vocab, gen, dtype)
+        y = x if x.dim() == 0 else apply_perturbation(
+            x.reshape(-1, shape[-1]) if x.dim() > 1 else x.reshape(1, -1),
+            "cand|" + ident, PerturbSpec(0, eps), policy=policy).reshape(shape)
+        for s in mine:
+            cand.records.append(TraceRecord(parse_canonical(ident), RankMeta(*s.rank), s.mapping,
+                                            s.replica, _shard(y, s.mapping), s.module_class))
+        if rspec is None:
+            continue
+        for k, s in enumerate(compares):
+            for _, gbox in s.mapping.pairs:
+                ext = gbox.extents
+                local = SliceBox(tuple((0, e) for e in ext))
+                m = ShardMapping(ext, shape, ((local, gbox),))
+                ref.records.append(TraceRecord(parse_canonical(ident), RankMeta(0, len(ref.records), 0, 0, 0, 0),
+                                               m, 1, x[gbox.as_slices()].contiguous(), rspec.module_class))
+        del x, y
+    return ref, cand, cand_specs, owner

@@ -129,7 +129,7 @@ def main():
     per_layer = []
     for l in range(args.layers):
         keys = [k for k in tol.responses if "kind=ParamGrad" in k and
-                (f"mod=model.layers.{2 * l}." in k or f"mod=model.layers.{2 * l + 1}.") in k]
+                (f"mod=model.layers.{2 * l}." in k or f"mod=model.layers.{2 * l + 1}." in k)]
         vals = [tol.responses[k] for k in keys]
         per_layer.append(math.sqrt(sum(v * v for v in vals) / len(vals)) if vals else 0.0)
     L = args.layers
