@@ -18,8 +18,6 @@ import math
 from dataclasses import dataclass, field
 from typing import Callable
 
-import numpy as np
-
 from . import _native as N
 from .device import resolve_operands
 from .errors import (ConfigInvalid, DigestMismatch, FormatError, ShapeMismatch,

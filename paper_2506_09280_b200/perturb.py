@@ -17,8 +17,6 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-import numpy as np
-
 from . import _native as N
 from .canonical import CanonicalId
 from .errors import NonFinite

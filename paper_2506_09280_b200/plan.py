@@ -28,7 +28,6 @@ import numpy as np
 
 from . import _native as N
 from .canonical import ShardMapping, merge_problem
-from .errors import MappingInvalid, MergeConflict, ShapeMismatch
 
 VERDICT_NAMES = {N.PASS: "pass", N.FLAG: "flag", N.REPLICA: "replica-mismatch",
                  N.MERGE: "merge-error", N.MISSING: "missing"}

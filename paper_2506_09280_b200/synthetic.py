@@ -13,10 +13,6 @@ config-3 injections do (wrong shard order, missing allreduce, scale error).
 
 from __future__ import annotations
 
-import math
-
-import numpy as np
-
 from .canonical import identity_mapping, parse_canonical
 from .layout import ModelShape, ParallelConfig, emit_records
 from .perturb import PerturbSpec, apply_perturbation

@@ -5,7 +5,6 @@ within 1e-12."""
 
 import json
 
-import numpy as np
 import pytest
 import torch
 

@@ -5,14 +5,13 @@ import json
 import os
 import threading
 
-import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2506_09280_b200.distributed import (DistributedCheckPlan, RecordMeta, ThreadComm,
-                                               TorchComm, global_trace, split_reference)
+from paper_2506_09280_b200.distributed import (DistributedCheckPlan, ThreadComm, TorchComm,
+                                               global_trace, split_reference)
 from paper_2506_09280_b200.tracestore import Trace, trace_from_bytes
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -49,7 +48,6 @@ def _gloo_body(rank, world, port, case_names, q):
     try:
         import gzip
         from paper_2506_09280_b200.checker import ToleranceMap
-        from paper_2506_09280_b200.plan import Plan, PlanEntry, merge_view
         with gzip.open(os.path.join(ROOT, "tests", "golden", "cases.json.gz"), "rt") as fh:
             cases = json.load(fh)
         comm = TorchComm()
@@ -97,7 +95,6 @@ def test_gloo_world2_plans_agree_and_cover_the_work():
     for p in procs:
         assert p.exitcode == 0
     import gzip
-    from paper_2506_09280_b200.checker import CheckPlan, ToleranceMap
     with gzip.open(os.path.join(ROOT, "tests", "golden", "cases.json.gz"), "rt") as fh:
         cases = json.load(fh)
     for k, name in enumerate(names):

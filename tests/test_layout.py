@@ -3,9 +3,7 @@ for every layout of the reference's 60-layout grid, exactly the records the
 reference emulator traced — same ids in the same order, same RankMeta,
 replica sizes, module classes and ShardMapping signatures."""
 
-import pytest
-
-from paper_2506_09280_b200.layout import (GPT2_MEDIUM, LLAMA3_1B, ModelShape, ParallelConfig,
+from paper_2506_09280_b200.layout import (GPT2_MEDIUM, ModelShape, ParallelConfig,
                                           emit_records, piece_positions, seq_pieces, sub_pieces)
 
 

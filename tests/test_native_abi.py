@@ -1,7 +1,6 @@
 """The C-ABI library builds for sm_100a, loads without a GPU and exports
 every function include/td_api.h declares (no compute calls here)."""
 
-import ctypes
 import os
 import re
 import subprocess
