@@ -213,33 +213,83 @@ def _reference_worker(args):
 _REF_SHARED = None
 
 
+def host_sample(name: str, stride: int):
+    """The reference arm's input, built on the host with numpy only (no GPU,
+    none of our kernels): every `stride`-th candidate id of the workload,
+    reference = N(0, sigma) rounded to the storage format, candidate =
+    Q(ref * (1 + eps*u)) with the reference's own stream semantics (oracle),
+    sharded and replicated through the candidate layout's maps."""
+    import numpy as np
+    from oracle import traindiff_oracle as O
+    from paper_2506_09280_b200 import layout as L
+    from paper_2506_09280_b200.synthetic import SIGMA
+    if name.startswith("cfg5"):
+        parts = name.split(":")
+        mib = int(parts[1]) if len(parts) > 1 else 1024
+        rows = (mib << 20) // 2 // 4096
+        rng = np.random.default_rng(0)
+        x = O.quantize(rng.standard_normal((rows, 4096)), "BF16")
+        u = O.signed_uniforms(O.seed_of("cand|sweep"), x.size).reshape(x.shape)
+        y = O.quantize(x * (1.0 + u * 2.0 ** -8), "BF16")
+        box = (((0, rows), (0, 4096)),)
+        rr = [O.Rec("sweep", (0,) * 6, x.shape, x.shape, [(box[0], box[0])], 1, x)]
+        cr = [O.Rec("sweep", (0,) * 6, y.shape, y.shape, [(box[0], box[0])], 1, y)]
+        return rr, cr, "BF16", 1
+    if name == "cfg1":
+        model, pcfg, fmt = L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), "FP32"
+    elif name == "cfg3":
+        model, pcfg, fmt = L.LLAMA3_1B, L.ParallelConfig(tp=8), "BF16"
+    else:
+        model, pcfg, fmt = L.GPT2_MEDIUM, L.ParallelConfig(tp=4), "BF16"
+    eps = 2.0 ** -24 if fmt == "FP32" else 2.0 ** -8
+    ref_specs = {s.ident: s for s in L.emit_records(model, L.ParallelConfig(microbatches=pcfg.microbatches))}
+    cand_specs = L.emit_records(model, pcfg)
+    ids = list(dict.fromkeys(s.ident for s in cand_specs))
+    sample = set(ids[::stride])
+    rng = np.random.default_rng(0)
+    rr, cr = [], []
+    for ident in ids:
+        if ident not in sample:
+            continue
+        rs = ref_specs[ident]
+        kind = ident.split("|")[2][5:]
+        shape = rs.mapping.global_shape
+        x = rng.standard_normal(shape) * SIGMA.get(kind, 1.0)
+        x = O.quantize(x, fmt) if fmt != "FP32" else x.astype(np.float32).astype(np.float64)
+        u = O.signed_uniforms(O.seed_of("cand|" + ident), x.size).reshape(shape)
+        y = x * (1.0 + u * eps)
+        y = O.quantize(y, fmt) if fmt != "FP32" else y.astype(np.float32).astype(np.float64)
+        pairs = [(l.bounds, g.bounds) for l, g in rs.mapping.pairs]
+        rr.append(O.Rec(ident, rs.rank, rs.mapping.local_shape, shape, pairs, rs.replica, x))
+        for s in cand_specs:
+            if s.ident != ident:
+                continue
+            local = np.empty(s.mapping.local_shape, dtype=np.float32)
+            for l, g in s.mapping.pairs:
+                local[l.as_slices()] = y[g.as_slices()]
+            cr.append(O.Rec(ident, s.rank, s.mapping.local_shape, s.mapping.global_shape,
+                            [(l.bounds, g.bounds) for l, g in s.mapping.pairs], s.replica, local))
+    return rr, cr, fmt, len(sample)
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm on the CPU (the oracle port;
-    the reference is pure Python and cannot travel to the GPU box), on all
-    host cores, each step a bounded id sample of the same workload."""
+    the reference is pure Python and /root/reference does not travel to the
+    GPU box), on all host cores (ids partitioned over processes), each step a
+    bounded id sample of the same workload.  No GPU is touched."""
     global _REF_SHARED
     import multiprocessing as mp
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import torch
-    from oracle import traindiff_oracle as O
-    desc, ref, cand, tol, fmt = workload(args.config)
-    ids = list(dict.fromkeys(r.id.encode() for r in cand.records))
     stride = max(1, args.cpu_stride * 4)
-    sample = set(ids[::stride])
-
-    def host(recs):
-        return [O.Rec(r.id.encode(), r.rank_meta.as_tuple(), r.mapping.local_shape, r.mapping.global_shape,
-                      [(l.bounds, g.bounds) for l, g in r.mapping.pairs], r.replica_group_size,
-                      r.payload.float().cpu().numpy()) for r in recs if r.id.encode() in sample]
-    rr, cr = host(ref.records), host(cand.records)
-    del ref, cand
-    torch.cuda.empty_cache()
+    rr, cr, fmt, n_sample = host_sample(args.config, stride)
     nbytes = sum(r.payload.size * 2 for r in rr) + sum(r.payload.size * 2 for r in cr)
     cores = os.cpu_count() or 1
-    _REF_SHARED = (rr, cr, fmt.eps)
-    chunks = [sorted(sample)[k::cores] for k in range(cores)]
+    eps = 2.0 ** -24 if fmt == "FP32" else 2.0 ** -8
+    _REF_SHARED = (rr, cr, eps)
+    sample = sorted({r.ident for r in cr})
+    chunks = [sample[k::cores] for k in range(cores)]
     ctx = mp.get_context("fork")
     times = []
     with ctx.Pool(cores) as pool:
@@ -251,13 +301,15 @@ def run_reference(args):
                 times.append(dt)
     t = sum(times) / len(times)
     value = nbytes / t / 1e9
-    line = {"impl": "reference", "metric": "traced-tensor compare GB/s", "value": value, "unit": "GB/s",
+    line = {"impl": "reference", "metric": "traced-tensor compare GB/s vs HBM roofline; layer-checks/sec",
+            "value": value, "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": desc,
-            "layer_checks_per_s": len(sample) / t,
+            "data": "synthetic (host numpy, same shapes/layout as the GPU arm)",
+            "config": {"workload": f"{args.config} (see the GPU arm's line)", "sampled_ids": n_sample},
+            "layer_checks_per_s": n_sample / t,
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
-                             "sample": f"every {stride}th id of the workload ({len(sample)} ids, "
+                             "sample": f"every {stride}th id of the workload ({n_sample} ids, "
                                        f"{nbytes / 1e9:.3f} GB at 2 B/elem), merge+rel_err per id on "
                                        f"{cores} processes"},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
