@@ -321,6 +321,12 @@ static_assert(sizeof(td_id_result) == 32, "td_id_result layout");
 static_assert(sizeof(td_group_result) == 16, "td_group_result layout");
 static_assert(sizeof(td_class) == 56, "td_class layout");
 
+#ifndef TD_NZ7_U
+#define TD_NZ7_U 1
+#endif
+#ifndef TD_NZ7_MINB
+#define TD_NZ7_MINB 2
+#endif
 #ifndef TD_NZ3_U
 #define TD_NZ3_U 1
 #endif
@@ -350,7 +356,7 @@ segnorm_fn pick_vec(int nz, bool hx) {
             case 4: return k_segnorm_vec<DT, 4, true, 1, 2>;
             case 5: return k_segnorm_vec<DT, 5, true, 1, 2>;
             case 6: return k_segnorm_vec<DT, 6, true, 1, 2>;
-            case 7: return k_segnorm_vec<DT, 7, true, 1, 2>;
+            case 7: return k_segnorm_vec<DT, 7, true, TD_NZ7_U, TD_NZ7_MINB>;
             default: return nullptr;
         }
     }

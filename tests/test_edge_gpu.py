@@ -1,0 +1,130 @@
+"""Edge cases and size-independent properties on the GPU: empty, 0-d and
+ragged tensors, misaligned payload views, maximum sizes (exact identities
+at 4 GiB per tensor), power-of-two scale invariance, record-order
+independence."""
+
+import json
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import traindiff_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _rec(shape, payload, mapping=None, mb=0, rank=None, replica=1, module="model.x"):
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200.tracestore import RankMeta, TraceRecord
+    return TraceRecord(td.CanonicalId(0, mb, td.TensorKind.ACTIVATION_OUT, module), rank or RankMeta(),
+                       mapping or td.identity_mapping(shape), replica, payload, "M")
+
+
+def _orecs(trace):
+    return [O.Rec(r.id.encode(), r.rank_meta.as_tuple(), r.mapping.local_shape, r.mapping.global_shape,
+                  [(l.bounds, g.bounds) for l, g in r.mapping.pairs], r.replica_group_size,
+                  np.asarray(r.values(), np.float32)) for r in trace.records]
+
+
+def _check_vs_oracle(ref, cand, fmt="BF16"):
+    import paper_2506_09280_b200 as td
+    from tests.test_gpu_parity import assert_reports_match
+    tol = td.ToleranceMap({}, n_samples=1, eps_p=0.0)
+    rep = td.check(ref, cand, tol, fmt=td.FloatFormat(fmt))
+    want = O.check(_orecs(ref), _orecs(cand), ref.header, cand.header, {}, 3.0, fmt)
+    assert_reports_match(json.loads(td.render_report(rep, "json")), want)
+    return rep
+
+
+def test_empty_zero_d_and_ragged_tensors():
+    import paper_2506_09280_b200 as td
+    H = {"digest": "d", "mode": "cascade"}
+    g = np.random.default_rng(0)
+    ref = td.Trace(H, [_rec((0, 4), np.zeros((0, 4), np.float32), mb=0),
+                       _rec((), np.array(2.5, np.float32), mb=1),
+                       _rec((3, 7), g.standard_normal((3, 7)).astype(np.float32), mb=2),
+                       _rec((5,), np.zeros(5, np.float32), mb=3)])
+    cand = td.Trace(H, [_rec((0, 4), np.zeros((0, 4), np.float32), mb=0),
+                        _rec((), np.array(2.75, np.float32), mb=1),
+                        _rec((3, 7), ref.records[2].payload * np.float32(1.001), mb=2),
+                        _rec((5,), np.array([0, 0, 1e-30, 0, 0], np.float32), mb=3)])
+    rep = _check_vs_oracle(ref, cand)
+    v = {e.ident.split("|")[1]: e for e in rep.entries}
+    assert v["mb=0"].observed == 0.0 and v["mb=0"].verdict == "pass"
+    assert v["mb=1"].observed == pytest.approx(0.1) and v["mb=1"].verdict == "flag"
+    assert v["mb=3"].observed == math.inf and v["mb=3"].verdict == "flag"
+
+
+def test_misaligned_and_strided_payload_views_match_oracle():
+    import paper_2506_09280_b200 as td
+    H = {"digest": "d", "mode": "cascade"}
+    base = torch.randn(4097, device="cuda").to(torch.bfloat16)
+    x = base[1:].reshape(64, 64)              # storage offset 2 bytes: not 16-byte aligned
+    y = (x.float() * 1.01).to(torch.bfloat16)
+    wide = torch.randn(64, 80, device="cuda").to(torch.bfloat16)
+    ref = td.Trace(H, [_rec((64, 64), x, mb=0), _rec((64, 64), wide[:, 8:72], mb=1)])
+    cand = td.Trace(H, [_rec((64, 64), y, mb=0), _rec((64, 64), wide[:, 8:72].contiguous(), mb=1)])
+    rep = _check_vs_oracle(ref, cand)
+    assert rep.entries[1].observed == 0.0
+
+
+def test_power_of_two_scaling_and_record_order_are_exact():
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200 import layout as L, synthetic
+    m = L.ModelShape(layers=2, d_model=128, n_heads=8, d_ff=256, seq_len=64, vocab=512)
+    ref, cand = synthetic.build(m, L.ParallelConfig(tp=4))
+    tol = td.ToleranceMap({}, n_samples=1, eps_p=0.0)
+    base = td.check(ref, cand, tol, fmt=td.FloatFormat.BF16)
+    scaled_ref, scaled_cand = td.Trace(ref.header), td.Trace(cand.header)
+    for src, dst in ((ref, scaled_ref), (cand, scaled_cand)):
+        for r in src.records:
+            dst.records.append(type(r)(r.id, r.rank_meta, r.mapping, r.replica_group_size,
+                                       r.payload * 4, r.module_class))
+    scaled = td.check(scaled_ref, scaled_cand, tol, fmt=td.FloatFormat.BF16)
+    assert [e.observed for e in scaled.entries] == [e.observed for e in base.entries]
+    # shuffling records WITHIN each id (not across ids) keeps every norm
+    shuffled = td.Trace(cand.header, [])
+    groups = {}
+    for r in cand.records:
+        groups.setdefault(r.id.encode(), []).append(r)
+    for recs in groups.values():
+        shuffled.records.extend(reversed(recs))
+    again = td.check(ref, shuffled, tol, fmt=td.FloatFormat.BF16)
+    for a, b in zip(again.entries, base.entries):
+        assert a.ident == b.ident
+        assert a.observed == pytest.approx(b.observed, rel=1e-12, abs=0.0)
+
+
+@pytest.mark.parametrize("gib", [4])
+def test_maximum_size_identities(gib):
+    """check(x, x) == 0 and check(x, 2x) == 1 exactly at 4 GiB per tensor
+    (the partial sums of x^2 and (x-2x)^2 are the same numbers in the same
+    order), with a 4-way column-sharded candidate."""
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200 import synthetic
+    ref, _ = synthetic.sweep_pair(gib << 30, maps="identity")
+    x = ref.records[0].payload
+    rows, cols = x.shape
+    H = ref.header
+    w = cols // 4
+    for factor, want in ((1, 0.0), (2, 1.0)):
+        y = x if factor == 1 else (x * 2)
+        cand = td.Trace(H, [])
+        for t in range(4):
+            mp = td.ShardMapping((rows, w), (rows, cols),
+                                 ((td.whole_box((rows, w)), td.SliceBox(((0, rows), (t * w, (t + 1) * w)))),))
+            cand.records.append(_rec((rows, w), y[:, t * w:(t + 1) * w].contiguous(), mp,
+                                     rank=td.RankMeta(tp=t), module=ref.records[0].id.module_name))
+        cand.records = [type(r)(ref.records[0].id, r.rank_meta, r.mapping, 1, r.payload, "M") for r in cand.records]
+        rep = td.check(ref, cand, td.ToleranceMap({}, n_samples=1, eps_p=0.0), fmt=td.FloatFormat.BF16)
+        assert rep.entries[0].observed == want
+        del cand, y
+        torch.cuda.empty_cache()

@@ -140,7 +140,8 @@ def main():
                       "mode": "module-wise", "estimate_seconds": secs,
                       "per_layer_paramgrad_response_over_eps": [r / eps for r in per_layer],
                       "spearman_layer_vs_response": spearman(list(range(L)), per_layer),
-                      "sqrt_bound_fit_c_over_eps": c / eps, "log_rms_residual": resid}))
+                      "sqrt_bound_fit_c": c, "log_rms_residual": resid,
+                      "fit": "response_l ~= c * sqrt(L / l) * eps"}))
 
 
 if __name__ == "__main__":
