@@ -44,16 +44,20 @@ def _check_vs_oracle(ref, cand, fmt="BF16"):
     return rep
 
 
-def test_empty_zero_d_and_ragged_tensors():
+def test_empty_single_and_ragged_tensors():
     import paper_2506_09280_b200 as td
     H = {"digest": "d", "mode": "cascade"}
     g = np.random.default_rng(0)
+    # 0-d payloads: np.ascontiguousarray makes them 1-d, so the reference's
+    # TraceRecord (tracestore.py:73-78) rejects them; the drop-in does too
+    with pytest.raises(td.ShapeMismatch):
+        _rec((), np.array(2.5, np.float32))
     ref = td.Trace(H, [_rec((0, 4), np.zeros((0, 4), np.float32), mb=0),
-                       _rec((), np.array(2.5, np.float32), mb=1),
+                       _rec((1,), np.array([2.5], np.float32), mb=1),
                        _rec((3, 7), g.standard_normal((3, 7)).astype(np.float32), mb=2),
                        _rec((5,), np.zeros(5, np.float32), mb=3)])
     cand = td.Trace(H, [_rec((0, 4), np.zeros((0, 4), np.float32), mb=0),
-                        _rec((), np.array(2.75, np.float32), mb=1),
+                        _rec((1,), np.array([2.75], np.float32), mb=1),
                         _rec((3, 7), ref.records[2].payload * np.float32(1.001), mb=2),
                         _rec((5,), np.array([0, 0, 1e-30, 0, 0], np.float32), mb=3)])
     rep = _check_vs_oracle(ref, cand)
