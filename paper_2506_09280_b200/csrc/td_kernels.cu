@@ -511,6 +511,18 @@ __device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t k) {
     return ((uint64_t)c1 << 32) | c0;
 }
 
+__device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
+    z = (z ^ (z >> 30)) * MIX1;
+    z = (z ^ (z >> 27)) * MIX2;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double signed_from_word(uint64_t w) {
+    const uint64_t m = w >> 11;
+    const double one_m = __longlong_as_double((long long)(0x3FF0000000000000ull | (m & 0xFFFFFFFFFFFFFull)));
+    return __dsub_rn(one_m, (m >> 52) ? 1.0 : 2.0);
+}
+
 // 2u - 1 with u = (w >> 11) * 2^-53 (generation.py:74-78, 166), without an
 // int->double conversion (XU pipe): t = 2u = m * 2^-52 for the 53-bit m is
 // exact as (1.m52 as a double) - (m < 2^52 ? 1 : 0); then t - 1 rounds once,
@@ -576,6 +588,24 @@ __device__ __forceinline__ void store_elem(void* base, int dt, int64_t idx, doub
     }
 }
 
+// Q_bf16(v) (tensor.py:64-77: RNE to 8 significant bits, unbounded exponent,
+// clamp to +-max_finite) straight to bf16 bits with 32-bit integer ops: the
+// round bit is f64 mantissa bit 44 (hi word bit 12), sticky = hi[11:0] | lo.
+// Exact for every f64 normal whose rounded value is a bf16 normal; anything
+// else (zero, bf16-subnormal range, inf/NaN) takes the exact slow path.
+__device__ __forceinline__ uint32_t bf16_q8_bits(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    const uint32_t hi = (uint32_t)(b >> 32), lo = (uint32_t)b;
+    const uint32_t sticky = (hi & 0xfffu) | lo;
+    const uint32_t up = ((hi >> 12) & 1u) & (((sticky != 0u) ? 1u : 0u) | ((hi >> 13) & 1u));
+    const uint32_t h = ((hi & 0x7fffffffu) >> 13) + up;      // exp(11) | mant(7), carry-safe
+    const uint32_t e = h >> 7;
+    const uint32_t sign = (hi >> 16) & 0x8000u;
+    if (e >= 897u && e <= 1150u) return sign | ((e - 896u) << 7) | (h & 0x7fu);
+    if (e > 1150u && e < 2047u) return sign | 0x7f7fu;              // clamp to bf16 max_finite
+    return (uint32_t)bf16_bits_q8(quantize_p(v, 8, 0x1.fep127));  // zero, tiny, inf/NaN
+}
+
 __device__ __forceinline__ double perturb_one(double xv, uint64_t seed, uint64_t k, double eps, int gen, int& bad) {
     const double u = signed_uniform(seed, k, gen);
     const double f = __dadd_rn(1.0, __dmul_rn(u, eps));   // 1.0 + u*eps
@@ -607,13 +637,25 @@ k_perturb_vec8(const char* x, char* y, int dt_in, int dt_out, int64_t rows, int6
             const uint32_t* iw = &in.x;
             uint4 out;
             uint32_t* ow = &out.x;
+            // splitmix64 state of word kb: seed + (kb+1)*gamma, then += gamma per element
+            uint64_t z = seed + (kb + 1) * GAMMA;
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
-                const double x0 = (double)__uint_as_float(iw[h] << 16);
-                const double x1 = (double)__uint_as_float(iw[h] & 0xffff0000u);
-                const double v0 = quantize_p(perturb_one(x0, seed, kb + 2 * h, eps, gen, bad), 8, 0x1.fep127);
-                const double v1 = quantize_p(perturb_one(x1, seed, kb + 2 * h + 1, eps, gen, bad), 8, 0x1.fep127);
-                ow[h] = (uint32_t)bf16_bits_q8(v0) | ((uint32_t)bf16_bits_q8(v1) << 16);
+                uint32_t pair = 0;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const uint32_t bits = half ? (iw[h] & 0xffff0000u) : (iw[h] << 16);
+                    const double xv = (double)__uint_as_float(bits);
+                    const uint64_t k = kb + 2 * h + half;
+                    const double u = gen == TD_GEN_PHILOX4x32 ? signed_uniform(seed, k, gen)
+                                                              : signed_from_word(splitmix_mix(z));
+                    z += GAMMA;
+                    const double f = __dadd_rn(1.0, __dmul_rn(u, eps));
+                    const double v = __dmul_rn(xv, f);
+                    bad |= !isfinite(v);
+                    pair |= bf16_q8_bits(v) << (16 * half);
+                }
+                ow[h] = pair;
             }
             *reinterpret_cast<uint4*>(y + idx * 2) = out;
         } else {

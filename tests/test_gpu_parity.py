@@ -371,3 +371,36 @@ def test_reports_are_byte_deterministic(cases, golden_trace_bytes):
     a = td.render_report(td.check(ref, cand, tol, fmt=td.FloatFormat.BF16), "json")
     b = td.render_report(td.check(ref, cand, tol, fmt=td.FloatFormat.BF16), "json")
     assert a == b
+
+
+def test_perturbation_full_exponent_range_bit_exact():
+    """bf16 in/out fast path (integer RNE on the fp64 bits) against the
+    oracle's quantize_array semantics over the whole bf16 exponent range,
+    zeros and values that round up into / clamp at bf16 max."""
+    rng = np.random.default_rng(5)
+    n = 1 << 16
+    mant = rng.integers(0, 128, n)
+    expo = rng.integers(-125, 128, n)
+    sign = rng.choice([-1.0, 1.0], n)
+    x = sign * (1 + mant / 128.0) * np.exp2(expo)
+    x[:64] = 0.0
+    x[64:128] = -0.0
+    x[128:192] = 1.9921875 * 2.0 ** 127
+    xb = torch.from_numpy(x).to(torch.bfloat16)
+    assert np.array_equal(xb.double().numpy(), x)       # all on the bf16 grid
+    ident = "iter=0|mb=0|kind=ActivationOut|mod=model.embedding"
+    for eps in (2.0 ** -8, 1e-3, 0.3):
+        spec = td.PerturbSpec(7, eps)
+        y = td.apply_perturbation(xb.cuda().reshape(256, 256), ident, spec, policy="bf16")
+        want = O.perturb(x.reshape(256, 256), "perturb|s=7|" + ident, eps, np.arange(256), 256, "BF16")
+        got = y.double().cpu().numpy()
+        normal = np.abs(want) >= 2.0 ** -126
+        assert np.array_equal(got[normal], want[normal]), eps
+        assert np.array_equal(np.signbit(got[want == 0]), np.signbit(want[want == 0]))
+    # philox stream on the same fast path
+    y = td.apply_perturbation(xb.cuda().reshape(256, 256), ident, td.PerturbSpec(1, 2.0 ** -8),
+                              policy="bf16", generator="philox")
+    want = O.perturb(x.reshape(256, 256), "perturb|s=1|" + ident, 2.0 ** -8, np.arange(256), 256, "BF16",
+                     generator="philox")
+    normal = np.abs(want) >= 2.0 ** -126
+    assert np.array_equal(y.double().cpu().numpy()[normal], want[normal])
