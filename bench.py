@@ -361,13 +361,18 @@ def main():
                    prep.part_ptr, 0, N.stream_handle(stream))
         if seg_events is not None:
             seg_events[1].record(stream)
-        N.call("td_reduce_slots", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups, prep.part_ptr,
-               prep.idsum_ptr, prep.gsum_ptr, N.stream_handle(stream))
         if world > 1:
+            # partial sums cross ranks between the reduction and the verdict
+            N.call("td_reduce_slots", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups, prep.part_ptr,
+                   prep.idsum_ptr, prep.gsum_ptr, N.stream_handle(stream))
             allreduce_partials(prep)
-        N.call("td_verdict", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups, prep.idsum_ptr,
-               prep.gsum_ptr, prep.kappa, prep.eps, prep.replica_eps, prep.idres_ptr, prep.gres_ptr,
-               prep.tie_ptr, N.stream_handle(stream))
+            N.call("td_verdict", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups, prep.idsum_ptr,
+                   prep.gsum_ptr, prep.kappa, prep.eps, prep.replica_eps, prep.idres_ptr, prep.gres_ptr,
+                   prep.tie_ptr, N.stream_handle(stream))
+        else:
+            N.call("td_finalize", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups, prep.part_ptr,
+                   prep.idsum_ptr, prep.gsum_ptr, prep.kappa, prep.eps, prep.replica_eps, prep.idres_ptr,
+                   prep.gres_ptr, prep.tie_ptr, N.stream_handle(stream))
 
     for _ in range(args.warmup):
         step()
@@ -397,7 +402,7 @@ def main():
     value = alg_bytes * world / (ms_step / 1e3) / 1e9
     seg_avg = sum(seg_ms) / len(seg_ms)
     achieved = alg_bytes / (seg_avg / 1e3) / 1e9
-    launches = prep.launches_per_run * args.steps
+    launches = (prep.launches_per_run + (1 if world > 1 else 0)) * args.steps
 
     e2e = None
     if not args.no_e2e:

@@ -9,7 +9,7 @@
  *                fused with merge()'s box copies      (pkg/src/traindiff/canonical.py:182-212)
  *                and check_replicas' per-copy rel_err  (pkg/src/traindiff/canonical.py:225-247)
  *                and TraceRecord.values() widening     (pkg/src/traindiff/tracestore.py:84-86)
- *   td_reduce_slots + td_verdict
+ *   td_reduce_slots + td_verdict (or fused: td_finalize)
  *                replace check()'s per-id loop         (pkg/src/traindiff/checker.py:312-365)
  *                and _merge_one's replica verdicts     (pkg/src/traindiff/checker.py:151-198)
  *   td_perturb   replaces Emulator._apply_perturbation (pkg/src/traindiff/engine.py:351-361)
@@ -178,6 +178,16 @@ int td_verdict(const td_id_desc* ids, int32_t n_ids,
                double kappa, double eps, double replica_eps,
                td_id_result* id_out, td_group_result* group_out,
                unsigned long long* near_ties, void* stream);
+
+/* single-GPU finalisation: td_reduce_slots + td_verdict in one launch (one CTA
+ * per id).  Multi-GPU callers keep the two steps apart and all-reduce the
+ * slot sums between them. */
+int td_finalize(const td_id_desc* ids, int32_t n_ids,
+                const td_group_desc* groups, int32_t n_groups,
+                const double* partials, double* id_sums, double* group_sums,
+                double kappa, double eps, double replica_eps,
+                td_id_result* id_out, td_group_result* group_out,
+                unsigned long long* near_ties, void* stream);
 
 /* ---- kernel 2: eps-scaled perturbation fused with the storage cast ----
  * y[i, j] = Q_fmt(x[i, j] * (1 + u_k * eps)),  k = pos(i) * full_cols + col0 + j,

@@ -67,6 +67,7 @@ SIGNATURES = {
     "td_segnorm": (ctypes.c_int, [_P, _P, _I32, _P, _I32, _P]),
     "td_reduce_slots": (ctypes.c_int, [_P, _I32, _P, _I32, _P, _P, _P, _P]),
     "td_verdict": (ctypes.c_int, [_P, _I32, _P, _I32, _P, _P, _D, _D, _D, _P, _P, _P, _P]),
+    "td_finalize": (ctypes.c_int, [_P, _I32, _P, _I32, _P, _P, _P, _D, _D, _D, _P, _P, _P, _P]),
     "td_perturb": (ctypes.c_int, [_P, _P, _I32, _I32, _I64, _I64, _I64, _I64, _P, _I64, _U64, _D,
                                   _I32, _I32, _P, _P]),
     "td_signed_uniforms": (ctypes.c_int, [_P, _I64, _U64, _I64, _I32, _P]),

@@ -423,45 +423,35 @@ __device__ __forceinline__ double rel_from_sums(double d2, double r2) {
     return __ddiv_rn(diff, ref);
 }
 
-__global__ void k_verdict(const td_id_desc* __restrict__ ids, int n_ids,
-                          const td_group_desc* __restrict__ groups,
-                          const double* __restrict__ id_sums, const double* __restrict__ group_sums,
-                          double kappa, double eps, double replica_eps,
-                          td_id_result* __restrict__ id_out, td_group_result* __restrict__ group_out,
-                          unsigned long long* __restrict__ near_ties) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_ids) return;
-    const td_id_desc D = ids[i];
-    int kinds[2] = {D.cand_host, D.ref_host};
-    const int gb[2] = {D.cgroup_begin, D.rgroup_begin};
-    const int ge[2] = {D.cgroup_end, D.rgroup_end};
-    for (int side = 0; side < 2; ++side) {
-        bool any = false;
-        for (int g = gb[side]; g < ge[side]; ++g) {
-            const double* s = group_sums + (int64_t)g * TD_SLOT_STRIDE;
-            const int nz = groups[g].nz;
-            double worst = 0.0;
-            int widx = -1;
-            for (int j = 0; j < nz && j < TD_MAX_Z; ++j) {
-                const double err = rel_from_sums(s[1 + j], s[0]);
-                if (err > worst) { worst = err; widx = j + 1; }  // NaN never wins
-            }
-            const int mm = worst > replica_eps;
-            group_out[g].worst = worst;
-            group_out[g].worst_index = widx;
-            group_out[g].mismatch = mm;
-            any |= (mm != 0);
-        }
-        // replica problems (declared-size or numeric) precede the merge problem
-        if (kinds[side] != TD_REPLICA && any) kinds[side] = TD_REPLICA;
+// group result of check_replicas (canonical.py:236-247) from reduced sums
+__device__ __forceinline__ int group_verdict(const double* s, int nz, double replica_eps,
+                                             td_group_result* out) {
+    double worst = 0.0;
+    int widx = -1;
+    for (int j = 0; j < nz && j < TD_MAX_Z; ++j) {
+        const double err = rel_from_sums(s[1 + j], s[0]);
+        if (err > worst) { worst = err; widx = j + 1; }   // NaN never wins
     }
-    // threshold = kappa * max(tol, eps) (checker.py:330-331)
-    const double m = (eps > D.tolerance) ? eps : D.tolerance;
+    const int mm = worst > replica_eps;
+    out->worst = worst;
+    out->worst_index = widx;
+    out->mismatch = mm;
+    return mm;
+}
+
+// check()'s verdict precedence (checker.py:328-354) for id i
+__device__ __forceinline__ void id_verdict(int i, const td_id_desc& D, const int any_rep[2], double d2, double x2,
+                                           double kappa, double eps, td_id_result* __restrict__ id_out,
+                                           unsigned long long* __restrict__ near_ties) {
+    int kinds[2] = {D.cand_host, D.ref_host};
+    for (int side = 0; side < 2; ++side)   // replica problems precede the merge problem
+        if (kinds[side] != TD_REPLICA && any_rep[side]) kinds[side] = TD_REPLICA;
+    const double m = (eps > D.tolerance) ? eps : D.tolerance;   // kappa * max(tol, eps)
     const double thr = __dmul_rn(kappa, m);
     double obs = __longlong_as_double(0x7ff8000000000000LL);
     int tie = 0;
     int verdict;
-    if (D.has_compare) obs = rel_from_sums(id_sums[2 * i + 0], id_sums[2 * i + 1]);
+    if (D.has_compare) obs = rel_from_sums(d2, x2);
     if (kinds[0]) verdict = kinds[0];
     else if (kinds[1]) verdict = kinds[1];
     else if (!D.has_compare) verdict = TD_MERGE;
@@ -478,6 +468,86 @@ __global__ void k_verdict(const td_id_desc* __restrict__ ids, int n_ids,
     id_out[i].cand_kind = kinds[0];
     id_out[i].ref_kind = kinds[1];
     id_out[i].near_tie = tie;
+}
+
+__global__ void k_verdict(const td_id_desc* __restrict__ ids, int n_ids,
+                          const td_group_desc* __restrict__ groups,
+                          const double* __restrict__ id_sums, const double* __restrict__ group_sums,
+                          double kappa, double eps, double replica_eps,
+                          td_id_result* __restrict__ id_out, td_group_result* __restrict__ group_out,
+                          unsigned long long* __restrict__ near_ties) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_ids) return;
+    const td_id_desc D = ids[i];
+    int any[2] = {0, 0};
+    const int gb[2] = {D.cgroup_begin, D.rgroup_begin};
+    const int ge[2] = {D.cgroup_end, D.rgroup_end};
+    for (int side = 0; side < 2; ++side)
+        for (int g = gb[side]; g < ge[side]; ++g)
+            any[side] |= group_verdict(group_sums + (int64_t)g * TD_SLOT_STRIDE, groups[g].nz, replica_eps,
+                                       group_out + g);
+    id_verdict(i, D, any, id_sums[2 * i + 0], id_sums[2 * i + 1], kappa, eps, id_out, near_ties);
+}
+
+// fixed-order CTA sum (warp butterfly, then warps 0..7 in order); all threads get it
+__device__ __forceinline__ double cta_sum(double v, double* red) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NWARP; ++w) s += red[w];
+    __syncthreads();
+    return s;
+}
+
+// Single-GPU finalisation: td_reduce_slots + td_verdict in ONE launch, one
+// CTA per id (threads stride the id's partial rows; fixed-order reduction).
+__global__ void __launch_bounds__(BLOCK)
+k_finalize(const td_id_desc* __restrict__ ids, const td_group_desc* __restrict__ groups,
+           const double* __restrict__ partials, double* __restrict__ id_sums, double* __restrict__ group_sums,
+           double kappa, double eps, double replica_eps, td_id_result* __restrict__ id_out,
+           td_group_result* __restrict__ group_out, unsigned long long* __restrict__ near_ties) {
+    __shared__ double red[NWARP];
+    const int i = blockIdx.x;
+    const td_id_desc D = ids[i];
+    double d2 = 0.0, x2 = 0.0;
+    for (int64_t r = D.tile_begin * TD_WARPS_PER_TILE + threadIdx.x; r < D.tile_end * TD_WARPS_PER_TILE;
+         r += BLOCK) {
+        d2 += partials[r * TD_PARTIAL_STRIDE + 0];
+        x2 += partials[r * TD_PARTIAL_STRIDE + 1];
+    }
+    d2 = cta_sum(d2, red);
+    x2 = cta_sum(x2, red);
+    int any[2] = {0, 0};
+    const int gb[2] = {D.cgroup_begin, D.rgroup_begin};
+    const int ge[2] = {D.cgroup_end, D.rgroup_end};
+    for (int side = 0; side < 2; ++side) {
+        for (int g = gb[side]; g < ge[side]; ++g) {
+            const td_group_desc G = groups[g];
+            double sums[TD_SLOT_STRIDE];
+#pragma unroll
+            for (int k = 0; k < TD_SLOT_STRIDE; ++k) sums[k] = 0.0;
+            for (int64_t r = G.tile_begin * TD_WARPS_PER_TILE + threadIdx.x; r < G.tile_end * TD_WARPS_PER_TILE;
+                 r += BLOCK) {
+#pragma unroll
+                for (int k = 0; k < TD_SLOT_STRIDE; ++k)
+                    if (k <= G.nz) sums[k] += partials[r * TD_PARTIAL_STRIDE + 2 + k];
+            }
+#pragma unroll
+            for (int k = 0; k < TD_SLOT_STRIDE; ++k) sums[k] = (k <= G.nz) ? cta_sum(sums[k], red) : 0.0;
+            if (threadIdx.x == 0) {
+#pragma unroll
+                for (int k = 0; k < TD_SLOT_STRIDE; ++k) group_sums[(int64_t)g * TD_SLOT_STRIDE + k] = sums[k];
+                any[side] |= group_verdict(sums, G.nz, replica_eps, group_out + g);
+            }
+        }
+    }
+    if (threadIdx.x == 0) {
+        id_sums[2 * i + 0] = d2;
+        id_sums[2 * i + 1] = x2;
+        id_verdict(i, D, any, d2, x2, kappa, eps, id_out, near_ties);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -973,6 +1043,21 @@ int td_verdict(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups
     k_verdict<<<(n_ids + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(
         ids, n_ids, groups, id_sums, group_sums, kappa, eps, replica_eps, id_out, group_out, near_ties);
     return check_launch("td_verdict");
+}
+
+int td_finalize(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups, int32_t n_groups,
+                const double* partials, double* id_sums, double* group_sums, double kappa, double eps,
+                double replica_eps, td_id_result* id_out, td_group_result* group_out,
+                unsigned long long* near_ties, void* stream) {
+    if (n_ids == 0) return 0;
+    if (n_ids < 0 || !ids || !partials || !id_sums || !id_out || !near_ties ||
+        (n_groups && (!groups || !group_sums || !group_out)))
+        return fail("td_finalize: invalid arguments");
+    if (cudaMemsetAsync(near_ties, 0, sizeof(unsigned long long), (cudaStream_t)stream) != cudaSuccess)
+        return fail("td_finalize: cannot reset the near-tie counter");
+    k_finalize<<<n_ids, BLOCK, 0, (cudaStream_t)stream>>>(ids, groups, partials, id_sums, group_sums, kappa, eps,
+                                                         replica_eps, id_out, group_out, near_ties);
+    return check_launch("td_finalize");
 }
 
 int td_perturb(const void* x, void* y, int32_t dtype_in, int32_t dtype_out, int64_t rows, int64_t cols,

@@ -533,7 +533,7 @@ class Prepared:
         for k, (vec, dt, nz, hx) in enumerate(plan.class_keys):
             self.classes[k] = (base + offsets[1 + k], len(plan.class_lists[k]), dt, nz, int(hx),
                                int(vec), mode, 0, atol, rtol)
-        self.launches_per_run = len(self.classes) + 2
+        self.launches_per_run = len(self.classes) + 1
         self._events = None
 
     def launch(self, timing: dict | None = None) -> None:
@@ -550,9 +550,7 @@ class Prepared:
                    len(self.classes), self.part_ptr, 0, sh)
         if ev:
             ev[1].record(self.stream)
-        N.call("td_reduce_slots", self.ids_ptr, self.n_ids, self.grp_ptr, self.n_groups,
-               self.part_ptr, self.idsum_ptr, self.gsum_ptr, sh)
-        N.call("td_verdict", self.ids_ptr, self.n_ids, self.grp_ptr, self.n_groups,
+        N.call("td_finalize", self.ids_ptr, self.n_ids, self.grp_ptr, self.n_groups, self.part_ptr,
                self.idsum_ptr, self.gsum_ptr, self.kappa, self.eps, self.replica_eps,
                self.idres_ptr, self.gres_ptr, self.tie_ptr, sh)
         if ev:
