@@ -77,8 +77,8 @@ def workload(name: str, rank: int = 0):
         g = int(parts[3]) if len(parts) > 3 else (4 if maps != "identity" else 1)
         ref, cand = synthetic.sweep_pair(mib << 20, maps=maps, g=g, seed=rank)
         desc = {"workload": f"config5 raw compare sweep: one id, {mib} MiB bf16 per tensor, "
-                            f"shape (N/4096, 4096), candidate {maps} x{g}", "model": "none",
-                "dtype": "bf16", "tensor_mib": mib, "maps": maps, "shards": g}
+                            f"shape (N/4096, 4096), candidate {maps} x{g}",
+                "storage_dtype": "bf16", "tensor_mib": mib, "maps": maps, "shards": g}
         fmt = FloatFormat.BF16
     else:
         if name == "cfg1":
@@ -101,10 +101,10 @@ def workload(name: str, rank: int = 0):
                     "iter=0|mb=0|kind=ActivationOut|mod=model.layers.7.attn": "partial",
                     "iter=0|mb=0|kind=ActivationOut|mod=model.embedding": "scale"}
         ref, cand = synthetic.build(model, pcfg, dtype=dtype, seed=rank, eps=fmt.eps, bugs=bugs)
-        desc = {"workload": label, "model": f"layers={model.layers} d={model.d_model} ff={model.d_ff} "
-                                           f"S={model.seq_len} V={model.vocab}",
+        desc = {"workload": label, "trace_shapes": f"layers={model.layers} d={model.d_model} "
+                                                  f"ff={model.d_ff} S={model.seq_len} V={model.vocab}",
                 "candidate_layout": f"tp={pcfg.tp} dp={pcfg.dp} cp={pcfg.cp} sp={pcfg.sp}",
-                "dtype": "bf16" if dtype == torch.bfloat16 else "f32"}
+                "storage_dtype": "bf16" if dtype == torch.bfloat16 else "f32"}
     eps = fmt.eps
     tol = ToleranceMap({r.id.encode(): 2 * eps for r in ref.records}, n_samples=1, eps_p=eps)
     return desc, ref, cand, tol, fmt
@@ -451,7 +451,8 @@ def main():
         line = {"metric": "traced-tensor compare GB/s vs HBM roofline; layer-checks/sec",
                 "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": desc.get("dtype", "bf16"),
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64",   # arithmetic type: fp64 accumulation of bf16/f32 payloads
                 "data": "synthetic (N(0,sigma) per id rounded to the storage dtype; candidate = "
                         "Q(ref*(1+2^-8 u)), counter-based stream)",
                 "config": dict(desc, inputs="8+ GB resident, larger than the 126 MB L2 (no flush)"
