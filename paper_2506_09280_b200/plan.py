@@ -557,6 +557,25 @@ class Prepared:
             ev[2].record(self.stream)
         self._events = ev
 
+    def capture(self):
+        """A CUDA graph of launch(): replaying it re-runs the whole check
+        (segnorm classes incl. their auxiliary-stream fork/join, finalize)
+        with one host call — for checks small enough that launch latency
+        dominates.  The graph reads whatever the bound payload buffers hold
+        at replay time."""
+        import torch
+        graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(self.stream)
+        keep, self.stream = self.stream, side
+        try:
+            with torch.cuda.graph(graph, stream=side):
+                self.launch()
+        finally:
+            self.stream = keep
+        self.stream.wait_stream(side)
+        return graph
+
     def read_timing(self, timing: dict) -> None:
         ev = self._events
         if ev:

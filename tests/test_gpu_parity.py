@@ -404,3 +404,28 @@ def test_perturbation_full_exponent_range_bit_exact():
                      generator="philox")
     normal = np.abs(want) >= 2.0 ** -126
     assert np.array_equal(y.double().cpu().numpy()[normal], want[normal])
+
+
+def test_graph_replay_matches_eager_launch(cases, golden_trace_bytes):
+    """A captured CUDA graph of the whole check replays to the same results
+    and follows payload updates made in place."""
+    from paper_2506_09280_b200.checker import CheckPlan
+    from paper_2506_09280_b200.device import resolve_operands
+    case = next(c for c in cases["checks"] if c["name"] == "bug_tp_row_allreduce_k3")
+    ref = trace_from_bytes(golden_trace_bytes(case["ref"]), device="cuda")
+    cand = trace_from_bytes(golden_trace_bytes(case["cand"]), device="cuda")
+    tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+    cp = CheckPlan(ref, cand, tol, fmt=td.FloatFormat.BF16)
+    ptrs, keep = resolve_operands(cp.plan.operands, cp.plan.operand_dtypes)
+    prep = cp.plan.prepare(ptrs, kappa=3.0, eps=td.FloatFormat.BF16.eps, replica_eps=td.FloatFormat.BF16.eps)
+    prep.launch()
+    eager = prep.fetch()
+    graph = prep.capture()
+    graph.replay()
+    replay = prep.fetch()
+    assert np.array_equal(eager[0], replay[0]) and np.array_equal(eager[1], replay[1])
+    keep[0].mul_(2.0)                       # operand 0 changes in place
+    graph.replay()
+    moved = prep.fetch()
+    prep.launch()
+    assert np.array_equal(moved[0], prep.fetch()[0])

@@ -47,11 +47,9 @@ def main():
                 N.call("td_segnorm", prep.seg_ptr, prep.classes.ctypes.data,
                        len(prep.classes), prep.part_ptr, 0, N.stream_handle())
                 ev[1].record()
-                N.call("td_reduce_slots", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups,
-                       prep.part_ptr, prep.idsum_ptr, prep.gsum_ptr, N.stream_handle())
-                N.call("td_verdict", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups,
-                       prep.idsum_ptr, prep.gsum_ptr, prep.kappa, prep.eps, prep.replica_eps,
-                       prep.idres_ptr, prep.gres_ptr, prep.tie_ptr, N.stream_handle())
+                N.call("td_finalize", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups,
+                       prep.part_ptr, prep.idsum_ptr, prep.gsum_ptr, prep.kappa, prep.eps,
+                       prep.replica_eps, prep.idres_ptr, prep.gres_ptr, prep.tie_ptr, N.stream_handle())
                 ev[2].record()
                 torch.cuda.synchronize()
                 if rep >= 3:
@@ -59,11 +57,25 @@ def main():
                     step_ms.append(ev[0].elapsed_time(ev[2]))
             seg = sorted(seg_ms)[len(seg_ms) // 2]
             step = sorted(step_ms)[len(step_ms) // 2]
+            # the same check as one CUDA-graph replay (launch latency folded)
+            graph = prep.capture()
+            gms = []
+            for rep in range(args.reps + 3):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                graph.replay()
+                e1.record()
+                torch.cuda.synchronize()
+                if rep >= 3:
+                    gms.append(e0.elapsed_time(e1))
+            gstep = sorted(gms)[len(gms) // 2]
             b = cp.algorithmic_bytes
             print(json.dumps({"mib": mib, "maps": maps, "shards": int(g), "bytes": b,
                               "segnorm_ms": seg, "segnorm_gbs": b / seg / 1e6, "frac": b / seg / 1e6 / peak,
                               "check_ms": step, "check_gbs": b / step / 1e6,
-                              "checks_per_s": 1e3 / step}), flush=True)
+                              "checks_per_s": 1e3 / step, "graph_check_ms": gstep,
+                              "graph_checks_per_s": 1e3 / gstep}), flush=True)
             del keep, prep, cp, ref, cand
             torch.cuda.empty_cache()
 
