@@ -356,23 +356,17 @@ def main():
     def step(seg_events=None):
         if seg_events is not None:
             seg_events[0].record(stream)
-        if len(prep.classes):
-            N.call("td_segnorm", prep.seg_ptr, prep.classes.ctypes.data, len(prep.classes),
-                   prep.part_ptr, 0, N.stream_handle(stream))
+        sh = N.stream_handle(stream)
+        prep.segnorm(sh)
         if seg_events is not None:
             seg_events[1].record(stream)
         if world > 1:
-            # partial sums cross ranks between the reduction and the verdict
-            N.call("td_reduce_slots", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups, prep.part_ptr,
-                   prep.idsum_ptr, prep.gsum_ptr, N.stream_handle(stream))
+            # slot sums cross ranks between the reduction and the verdict
+            prep.reduce(sh)
             allreduce_partials(prep)
-            N.call("td_verdict", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups, prep.idsum_ptr,
-                   prep.gsum_ptr, prep.kappa, prep.eps, prep.replica_eps, prep.idres_ptr, prep.gres_ptr,
-                   prep.tie_ptr, N.stream_handle(stream))
+            prep.verdict(sh)
         else:
-            N.call("td_finalize", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups, prep.part_ptr,
-                   prep.idsum_ptr, prep.gsum_ptr, prep.kappa, prep.eps, prep.replica_eps, prep.idres_ptr,
-                   prep.gres_ptr, prep.tie_ptr, N.stream_handle(stream))
+            prep.finalize(sh)
 
     for _ in range(args.warmup):
         step()

@@ -65,6 +65,9 @@ enum td_generator { TD_GEN_SPLITMIX64 = 0, TD_GEN_PHILOX4x32 = 1 };
 /* segment flags */
 #define TD_SEG_HAS_X 1u         /* x present: accumulate d2=sum (x-y)^2 and x2=sum x^2 */
 #define TD_SEG_VEC 2u           /* 16-byte vector path legal (alignment + cols%8 proven by host) */
+/* flags bits 8..12: log2 of the units per tile for this segment; 0 means
+   TD_TILE_UNITS.  Small plans use smaller tiles so every SM gets work. */
+#define TD_SEG_TILE_SHIFT_POS 8
 
 /*
  * A segment is a 2-D strided block read in lockstep from x (the reference
@@ -168,6 +171,25 @@ int td_reduce_slots(const td_id_desc* ids, int32_t n_ids,
                     const td_group_desc* groups, int32_t n_groups,
                     const double* partials,
                     double* id_sums, double* group_sums, void* stream);
+
+/* one chunk of a slot's partial rows for td_reduce_chunks */
+typedef struct td_chunk {
+    int64_t row_begin;          /* first partial row (tile * TD_WARPS_PER_TILE + warp) */
+    int64_t row_end;            /* one past the last */
+    int32_t k0;                 /* first partial column summed (0 for ids, 2 for groups) */
+    int32_t nk;                 /* columns summed: 2 for ids, 1 + nz for groups */
+} td_chunk;                     /* 24 bytes */
+
+/* first level of the slot reduction for slots with many partial rows:
+ * chunk c's sums go to row c * TD_WARPS_PER_TILE of `out` (columns
+ * k0..k0+nk-1, every other cell of its TD_WARPS_PER_TILE rows zeroed), so
+ * `out` is itself a partials array in which chunk c is "tile" c.  Id / group
+ * descriptors whose tile ranges name chunk ranges then run td_reduce_slots /
+ * td_finalize on `out` unchanged.  Fixed-order, deterministic.
+ * (Replaces no reference code: the reference sums a whole tensor in numpy,
+ * tensor.py:163-164.) */
+int td_reduce_chunks(const double* partials, const td_chunk* chunks, int64_t n_chunks,
+                     double* out, void* stream);
 
 /* ---- kernel 3: batched threshold compare -> per-id verdicts ----
  * eps = fmt.eps (threshold floor); replica_eps = fmt.eps for check_replicas.

@@ -27,6 +27,7 @@ TILE_UNITS = int(os.environ.get("TD_TILE_UNITS", "8192"))  # must match the libr
 SLOT_STRIDE = 8
 SEG_HAS_X = 1
 SEG_VEC = 2
+SEG_TILE_SHIFT_POS = 8
 
 SEGMENT = np.dtype([
     ("x", "<u8"), ("y", "<u8"), ("z", "<u8", (MAX_Z,)),
@@ -46,6 +47,8 @@ GROUP_DESC = np.dtype([("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")
 ID_RESULT = np.dtype([("observed", "<f8"), ("threshold", "<f8"), ("verdict", "<i4"),
                       ("cand_kind", "<i4"), ("ref_kind", "<i4"), ("near_tie", "<i4")])
 GROUP_RESULT = np.dtype([("worst", "<f8"), ("worst_index", "<i4"), ("mismatch", "<i4")])
+CHUNK = np.dtype([("row_begin", "<i8"), ("row_end", "<i8"), ("k0", "<i4"), ("nk", "<i4")])
+assert CHUNK.itemsize == 24
 CLASS = np.dtype([("tiles", "<u8"), ("n_tiles", "<i8"), ("dtype", "<i4"), ("nz", "<i4"),
                   ("has_x", "<i4"), ("vec", "<i4"), ("mode", "<i4"), ("pad", "<i4"),
                   ("atol", "<f8"), ("rtol", "<f8")])
@@ -67,6 +70,7 @@ SIGNATURES = {
     "td_segnorm": (ctypes.c_int, [_P, _P, _I32, _P, _I32, _P]),
     "td_reduce_slots": (ctypes.c_int, [_P, _I32, _P, _I32, _P, _P, _P, _P]),
     "td_verdict": (ctypes.c_int, [_P, _I32, _P, _I32, _P, _P, _D, _D, _D, _P, _P, _P, _P]),
+    "td_reduce_chunks": (ctypes.c_int, [_P, _P, _I64, _P, _P]),
     "td_finalize": (ctypes.c_int, [_P, _I32, _P, _I32, _P, _P, _P, _D, _D, _D, _P, _P, _P, _P]),
     "td_perturb": (ctypes.c_int, [_P, _P, _I32, _I32, _I64, _I64, _I64, _I64, _P, _I64, _U64, _D,
                                   _I32, _I32, _P, _P]),

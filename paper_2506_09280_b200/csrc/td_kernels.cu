@@ -159,6 +159,11 @@ __device__ __forceinline__ double warp_sum(double v) {
 __device__ __forceinline__ int entry_seg(int64_t e) { return (int)(e >> 32); }
 __device__ __forceinline__ int64_t entry_tile(int64_t e) { return e & 0xffffffffll; }
 
+__device__ __forceinline__ int64_t tile_units(const td_segment* g) {
+    const int sh = (__ldg(&g->flags) >> TD_SEG_TILE_SHIFT_POS) & 31;
+    return sh ? (int64_t)1 << sh : (int64_t)TD_TILE_UNITS;
+}
+
 __device__ __forceinline__ void load_desc(const td_segment* __restrict__ g, SegView& S, int nz_max) {
     S.x = reinterpret_cast<const char*>(__ldg(&g->x));
     S.y = reinterpret_cast<const char*>(__ldg(&g->y));
@@ -201,9 +206,10 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
         SegView S;
         load_desc(g, S, NZ);
         const uint32_t vpr = (uint32_t)(S.cols >> 3);
-        const int64_t first = (t - __ldg(&g->tile_begin)) * (int64_t)TD_TILE_UNITS;
+        const int64_t tu = tile_units(g);
+        const int64_t first = (t - __ldg(&g->tile_begin)) * tu;
         const uint32_t u0 = (uint32_t)first;
-        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, __ldg(&g->n_units));
+        const uint32_t u1 = (uint32_t)min(first + tu, __ldg(&g->n_units));
         Acc a;
         a.zero();
         for (uint32_t base = u0 + threadIdx.x; base < u1; base += BLOCK * U) {
@@ -274,9 +280,10 @@ k_segnorm_generic(const td_segment* __restrict__ segs, const int64_t* __restrict
         SegView S;
         load_desc(g, S, nz);
         const uint32_t cols = (uint32_t)S.cols;
-        const int64_t first = (t - __ldg(&g->tile_begin)) * (int64_t)TD_TILE_UNITS;
+        const int64_t tu = tile_units(g);
+        const int64_t first = (t - __ldg(&g->tile_begin)) * tu;
         const uint32_t u0 = (uint32_t)first;
-        const uint32_t u1 = (uint32_t)min(first + (int64_t)TD_TILE_UNITS, __ldg(&g->n_units));
+        const uint32_t u1 = (uint32_t)min(first + tu, __ldg(&g->n_units));
         Acc a;
         a.zero();
         for (uint32_t u = u0 + threadIdx.x; u < u1; u += BLOCK) {
@@ -320,6 +327,7 @@ static_assert(sizeof(td_group_desc) == 24, "td_group_desc layout");
 static_assert(sizeof(td_id_result) == 32, "td_id_result layout");
 static_assert(sizeof(td_group_result) == 16, "td_group_result layout");
 static_assert(sizeof(td_class) == 56, "td_class layout");
+static_assert(sizeof(td_chunk) == 24, "td_chunk layout");
 
 #ifndef TD_NZ7_U
 #define TD_NZ7_U 1
@@ -547,6 +555,44 @@ k_finalize(const td_id_desc* __restrict__ ids, const td_group_desc* __restrict__
         id_sums[2 * i + 0] = d2;
         id_sums[2 * i + 1] = x2;
         id_verdict(i, D, any, d2, x2, kappa, eps, id_out, near_ties);
+    }
+}
+
+// First level of the slot reduction (td_reduce_chunks): 320 threads = 10
+// warps, thread t owns partial column t % 10 and walks the chunk's rows as
+// one flat, fully coalesced double array (320 is a multiple of the row
+// stride, so a thread's column never changes).  Column sums are then taken
+// over the 32 owners of each column in thread order.
+constexpr int CHUNK_BLOCK = 32 * TD_PARTIAL_STRIDE;
+
+__global__ void __launch_bounds__(CHUNK_BLOCK)
+k_reduce_chunks(const double* __restrict__ partials, const td_chunk* __restrict__ chunks, int64_t n,
+                double* __restrict__ out) {
+    __shared__ double red[CHUNK_BLOCK];
+    const int t = threadIdx.x;
+    constexpr int ROW = TD_WARPS_PER_TILE * TD_PARTIAL_STRIDE;   // doubles per output "tile"
+    for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
+        const int64_t rb = __ldg(&chunks[c].row_begin), re = __ldg(&chunks[c].row_end);
+        const int k0 = __ldg(&chunks[c].k0), nk = __ldg(&chunks[c].nk);
+        const int64_t f1 = re * TD_PARTIAL_STRIDE;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int64_t f = rb * TD_PARTIAL_STRIDE + t;
+        for (; f + 3 * CHUNK_BLOCK < f1; f += 4 * CHUNK_BLOCK) {
+            s0 += __ldg(partials + f);
+            s1 += __ldg(partials + f + CHUNK_BLOCK);
+            s2 += __ldg(partials + f + 2 * CHUNK_BLOCK);
+            s3 += __ldg(partials + f + 3 * CHUNK_BLOCK);
+        }
+        for (; f < f1; f += CHUNK_BLOCK) s0 += __ldg(partials + f);
+        red[t] = (s0 + s1) + (s2 + s3);
+        __syncthreads();
+        if (t < ROW) {
+            double v = 0.0;
+            if (t >= k0 && t < k0 + nk && t < TD_PARTIAL_STRIDE)
+                for (int i = t; i < CHUNK_BLOCK; i += TD_PARTIAL_STRIDE) v += red[i];
+            out[c * ROW + t] = v;
+        }
+        __syncthreads();
     }
 }
 
@@ -1043,6 +1089,18 @@ int td_verdict(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups
     k_verdict<<<(n_ids + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(
         ids, n_ids, groups, id_sums, group_sums, kappa, eps, replica_eps, id_out, group_out, near_ties);
     return check_launch("td_verdict");
+}
+
+int td_reduce_chunks(const double* partials, const td_chunk* chunks, int64_t n_chunks, double* out,
+                     void* stream) {
+    if (n_chunks == 0) return 0;
+    if (n_chunks < 0 || !partials || !chunks || !out) return fail("td_reduce_chunks: invalid arguments");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t grid = std::min<int64_t>(n_chunks, (int64_t)sms * 6);
+    k_reduce_chunks<<<(unsigned)grid, CHUNK_BLOCK, 0, (cudaStream_t)stream>>>(partials, chunks, n_chunks, out);
+    return check_launch("td_reduce_chunks");
 }
 
 int td_finalize(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups, int32_t n_groups,

@@ -209,7 +209,7 @@ def allreduce_partials(prep, comm: Comm | None = None) -> None:
     """Sum the reduced slot vector of a Prepared plan across ranks, in place
     (NCCL enqueues on torch's current stream)."""
     import torch
-    slots = prep.work[prep.n_part:]
+    slots = prep.slot_sums
     if slots.numel() == 0:
         return
     if comm is None:
@@ -317,19 +317,14 @@ class DistributedCheckPlan:
         prep = self.plan.prepare(ptrs, kappa=self.kappa, eps=self.fmt.eps,
                                  replica_eps=self.fmt.eps)
         sh = N.stream_handle(prep.stream)
-        if len(prep.classes):
-            N.call("td_segnorm", prep.seg_ptr, prep.classes.ctypes.data,
-                   len(prep.classes), prep.part_ptr, 0, sh)
-        N.call("td_reduce_slots", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups,
-               prep.part_ptr, prep.idsum_ptr, prep.gsum_ptr, sh)
+        prep.segnorm(sh)
+        prep.reduce(sh)
         if extra:
-            gsum = prep.work[prep.n_part + 2 * prep.n_ids:].view(-1, N.SLOT_STRIDE)
+            gsum = prep.slot_sums[2 * prep.n_ids:].view(-1, N.SLOT_STRIDE)
             for slot, vals in extra.items():
                 gsum[slot] += torch.from_numpy(vals).to(gsum.device)
         allreduce_partials(prep, self.comm)
-        N.call("td_verdict", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups,
-               prep.idsum_ptr, prep.gsum_ptr, prep.kappa, prep.eps, prep.replica_eps,
-               prep.idres_ptr, prep.gres_ptr, prep.tie_ptr, sh)
+        prep.verdict(sh)
         out = prep.fetch()
         del keep
         return out

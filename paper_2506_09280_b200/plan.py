@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import functools
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -346,7 +347,87 @@ class Plan:
         self.ids = np.array(id_rows, dtype=N.ID_DESC) if id_rows else np.zeros(0, N.ID_DESC)
         self.groups = (np.array(group_rows, dtype=[("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")])
                        if group_rows else np.zeros(0, [("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")]))
+        self.tile_shift = self._retile()
         self._freeze_segments()
+        self._chunk_slots()
+
+    # tiles per SM worth aiming for before the default tile is shrunk
+    TARGET_TILES = 148 * 8
+    MIN_TILE_SHIFT = 8
+
+    def _retile(self) -> int:
+        """Shrink the tile below TD_TILE_UNITS when the plan is small.
+
+        A tile is one CTA's unit of work; at the default 8192 units (128 KB
+        per bf16 operand) a 1 MiB check has 8 tiles, so 8 SMs stream it
+        through a chain of dependent DRAM round trips.  The largest
+        2^k units (k >= 8, one unit per thread) that still yields about
+        TARGET_TILES tiles is used instead, carried to the kernels in the
+        segment flags.  Id / group tile ranges sit on segment boundaries, so
+        they are remapped boundary to boundary.  Returns the shift stored in
+        the flags (0 = the library default)."""
+        b = self.builder
+        self.tile_units = N.TILE_UNITS
+        default = N.TILE_UNITS.bit_length() - 1
+        if not b.seg_rows or (1 << default) != N.TILE_UNITS:
+            return 0
+        units = np.array([r[10] for r in b.seg_rows], np.int64)
+        shift = default
+        while shift > self.MIN_TILE_SHIFT and int((-(-units // (1 << shift))).sum()) < self.TARGET_TILES:
+            shift -= 1
+        if shift == default:
+            return 0
+        self.tile_units = 1 << shift
+        counts = -(-units // self.tile_units)
+        new_begin = np.concatenate([[0], np.cumsum(counts)])
+        old_begin = np.array([r[9] for r in b.seg_rows] + [b.n_tiles], np.int64)
+        b.seg_rows = [r[:9] + (int(new_begin[i]),) + r[10:] for i, r in enumerate(b.seg_rows)]
+        b.n_tiles = self.n_tiles = int(new_begin[-1])
+
+        def remap(v):
+            return new_begin[np.searchsorted(old_begin, v)]
+        for table in (self.ids, self.groups):
+            if len(table):
+                table["tile_begin"] = remap(table["tile_begin"])
+                table["tile_end"] = remap(table["tile_end"])
+        return shift
+
+    # partial rows per chunk of the two-level slot reduction, and the largest
+    # slot (in partial rows) below which one level is enough
+    CHUNK_ROWS = 2048
+    CHUNK_MIN_ROWS = int(os.environ.get("TD_CHUNK_MIN_ROWS", "8192"))
+
+    def _chunk_slots(self) -> None:
+        """Two-level slot reduction for plans with a big slot.
+
+        td_finalize gives each id one CTA, which walks all of that id's
+        partial rows: 8 per tile, so a 2 GB logits tensor is ~128 k rows on
+        one SM.  When some slot exceeds CHUNK_MIN_ROWS rows, every slot's row
+        range is cut into CHUNK_ROWS chunks (td_chunk table, reduced across
+        the whole GPU by td_reduce_chunks), and `ids_chunked` /
+        `groups_chunked` carry chunk ranges in place of tile ranges.  Sets
+        self.chunks = None when one level suffices."""
+        W = N.WARPS_PER_TILE
+        spans = [(int(tb) * W, int(te) * W, 0, 2) for tb, te in zip(self.ids["tile_begin"], self.ids["tile_end"])]
+        spans += [(int(tb) * W, int(te) * W, 2, 1 + int(nz)) for tb, te, nz in
+                  zip(self.groups["tile_begin"], self.groups["tile_end"], self.groups["nz"])]
+        self.chunks = None
+        if not spans or max(re - rb for rb, re, _, _ in spans) < self.CHUNK_MIN_ROWS:
+            return
+        rows, ranges = [], []
+        for rb, re, k0, nk in spans:
+            c0 = len(rows)
+            rows.extend((r, min(r + self.CHUNK_ROWS, re), k0, nk) for r in range(rb, re, self.CHUNK_ROWS))
+            ranges.append((c0, len(rows)))
+        self.chunks = np.array(rows, dtype=N.CHUNK) if rows else np.zeros(0, N.CHUNK)
+        ranges = np.array(ranges, np.int64).reshape(-1, 2)
+        n_ids = len(self.ids)
+        self.ids_chunked = self.ids.copy()
+        self.ids_chunked["tile_begin"], self.ids_chunked["tile_end"] = ranges[:n_ids, 0], ranges[:n_ids, 1]
+        self.groups_chunked = self.groups.copy()
+        if len(self.groups):
+            self.groups_chunked["tile_begin"] = ranges[n_ids:, 0]
+            self.groups_chunked["tile_end"] = ranges[n_ids:, 1]
 
     # -- geometry -------------------------------------------------------------
 
@@ -404,7 +485,8 @@ class Plan:
             s["tile_begin"], s["n_units"] = tb, nu
             s["x_dtype"] = x.dtype if x is not None else y.dtype
             s["y_dtype"], s["nz"] = y.dtype, len(zs)
-            s["flags"] = (N.SEG_HAS_X if x is not None else 0) | (N.SEG_VEC if vec else 0)
+            s["flags"] = ((N.SEG_HAS_X if x is not None else 0) | (N.SEG_VEC if vec else 0)
+                          | (self.tile_shift << N.SEG_TILE_SHIFT_POS))
             m, p = _magic(c // 8 if vec else c)
             s["div_m"], s["div_p"] = m, p
             if x is not None:
@@ -412,7 +494,7 @@ class Plan:
             self.seg_yslot[i], self.seg_yoff[i] = y.slot, yo * y.esize
             for j, z in enumerate(zs):
                 self.seg_zslot[i, j] = z.slot
-            nt = -(-nu // N.TILE_UNITS)
+            nt = -(-nu // self.tile_units)
             tile_seg[tb:tb + nt] = i
             key = (bool(vec), y.dtype, len(zs), x is not None)
             class_tiles.setdefault(key, []).append((tb, nt))
@@ -495,16 +577,20 @@ class Prepared:
             parts.append(raw)
             cursor += raw.size
 
+        chunked = plan.chunks is not None
+        groups = plan.groups_chunked if chunked else plan.groups
         gdesc = np.zeros(n_groups, N.GROUP_DESC)
         if n_groups:
-            gdesc["tile_begin"] = plan.groups["tile_begin"]
-            gdesc["tile_end"] = plan.groups["tile_end"]
-            gdesc["nz"] = plan.groups["nz"]
+            gdesc["tile_begin"] = groups["tile_begin"]
+            gdesc["tile_end"] = groups["tile_end"]
+            gdesc["nz"] = groups["nz"]
         put(segs)
         for lst in plan.class_lists:
             put(lst)
-        put(plan.ids)
+        put(plan.ids_chunked if chunked else plan.ids)
         put(gdesc)
+        if chunked:
+            put(plan.chunks)
         blob = np.concatenate(parts) if parts else np.zeros(16, np.uint8)
         host = torch.from_numpy(blob).pin_memory()
         self.tables = torch.empty(blob.size, dtype=torch.uint8, device=dev)
@@ -517,10 +603,18 @@ class Prepared:
         self.ids_ptr = base + offsets[1 + n_cls]
         self.grp_ptr = base + offsets[2 + n_cls]
         self.n_part = max(1, plan.n_tiles * N.WARPS_PER_TILE * N.PARTIAL_STRIDE)
-        self.work = torch.empty(self.n_part + 2 * n_ids + N.SLOT_STRIDE * n_groups,
+        # ids / groups tables hold chunk ranges when the plan is chunked, and
+        # the slot reduction then reads the chunk rows instead of the partials
+        self.n_chunks = len(plan.chunks) if chunked else 0
+        n_crow = self.n_chunks * N.WARPS_PER_TILE * N.PARTIAL_STRIDE
+        self.work = torch.empty(self.n_part + n_crow + 2 * n_ids + N.SLOT_STRIDE * n_groups,
                                 dtype=torch.float64, device=dev)
         self.part_ptr = self.work.data_ptr()
-        self.idsum_ptr = self.part_ptr + 8 * self.n_part
+        self.chunk_ptr = base + offsets[3 + n_cls] if chunked else 0
+        self.red_ptr = self.part_ptr + 8 * self.n_part if chunked else self.part_ptr
+        self.idsum_ptr = self.part_ptr + 8 * (self.n_part + n_crow)
+        # the slot-sum vector (id sums, then group sums): what crosses ranks
+        self.slot_sums = self.work[self.n_part + n_crow:]
         self.gsum_ptr = self.idsum_ptr + 8 * 2 * n_ids
         self.res_bytes = N.ID_RESULT.itemsize * n_ids + N.GROUP_RESULT.itemsize * n_groups + 8
         self.res = torch.zeros(self.res_bytes, dtype=torch.uint8, device=dev)
@@ -533,26 +627,52 @@ class Prepared:
         for k, (vec, dt, nz, hx) in enumerate(plan.class_keys):
             self.classes[k] = (base + offsets[1 + k], len(plan.class_lists[k]), dt, nz, int(hx),
                                int(vec), mode, 0, atol, rtol)
-        self.launches_per_run = len(self.classes) + 1
+        self.launches_per_run = len(self.classes) + 1 + (1 if chunked else 0)
         self._events = None
 
+    # -- the steps of one check (all stream-ordered, no host sync) ----------
+
+    def segnorm(self, sh) -> None:
+        if len(self.classes):
+            N.call("td_segnorm", self.seg_ptr, self.classes.ctypes.data,
+                   len(self.classes), self.part_ptr, 0, sh)
+
+    def _chunks(self, sh) -> None:
+        if self.n_chunks:
+            N.call("td_reduce_chunks", self.part_ptr, self.chunk_ptr, self.n_chunks, self.red_ptr, sh)
+
+    def reduce(self, sh) -> None:
+        """partials -> per-slot sums (multi-GPU: all-reduced before verdict)."""
+        self._chunks(sh)
+        N.call("td_reduce_slots", self.ids_ptr, self.n_ids, self.grp_ptr, self.n_groups,
+               self.red_ptr, self.idsum_ptr, self.gsum_ptr, sh)
+
+    def verdict(self, sh) -> None:
+        N.call("td_verdict", self.ids_ptr, self.n_ids, self.grp_ptr, self.n_groups,
+               self.idsum_ptr, self.gsum_ptr, self.kappa, self.eps, self.replica_eps,
+               self.idres_ptr, self.gres_ptr, self.tie_ptr, sh)
+
+    def finalize(self, sh) -> None:
+        """reduce + verdict, fused (single GPU)."""
+        self._chunks(sh)
+        N.call("td_finalize", self.ids_ptr, self.n_ids, self.grp_ptr, self.n_groups, self.red_ptr,
+               self.idsum_ptr, self.gsum_ptr, self.kappa, self.eps, self.replica_eps,
+               self.idres_ptr, self.gres_ptr, self.tie_ptr, sh)
+
     def launch(self, timing: dict | None = None) -> None:
-        """Enqueue td_segnorm (one launch per tile class), td_reduce_slots
-        and td_verdict on the plan's stream; no host synchronisation."""
+        """Enqueue td_segnorm (one launch per tile class) and td_finalize
+        (after td_reduce_chunks for a chunked plan) on the plan's stream; no
+        host synchronisation."""
         import torch
         sh = N.stream_handle(self.stream)
         ev = None
         if timing is not None:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
             ev[0].record(self.stream)
-        if len(self.classes):
-            N.call("td_segnorm", self.seg_ptr, self.classes.ctypes.data,
-                   len(self.classes), self.part_ptr, 0, sh)
+        self.segnorm(sh)
         if ev:
             ev[1].record(self.stream)
-        N.call("td_finalize", self.ids_ptr, self.n_ids, self.grp_ptr, self.n_groups, self.part_ptr,
-               self.idsum_ptr, self.gsum_ptr, self.kappa, self.eps, self.replica_eps,
-               self.idres_ptr, self.gres_ptr, self.tie_ptr, sh)
+        self.finalize(sh)
         if ev:
             ev[2].record(self.stream)
         self._events = ev

@@ -429,3 +429,30 @@ def test_graph_replay_matches_eager_launch(cases, golden_trace_bytes):
     moved = prep.fetch()
     prep.launch()
     assert np.array_equal(moved[0], prep.fetch()[0])
+
+
+@pytest.mark.parametrize("chunk_rows", [5, 64])
+def test_two_level_slot_reduction_matches_oracle(monkeypatch, cases, golden_trace_bytes, shardings, chunk_rows):
+    """Force td_reduce_chunks (plan.Plan._chunk_slots) on every plan, with
+    chunk sizes that do and do not align with tiles."""
+    from paper_2506_09280_b200.plan import Plan
+    monkeypatch.setattr(Plan, "CHUNK_MIN_ROWS", 0)
+    monkeypatch.setattr(Plan, "CHUNK_ROWS", chunk_rows)
+    for case in cases["checks"]:
+        ref = trace_from_bytes(golden_trace_bytes(case["ref"]))
+        cand = trace_from_bytes(golden_trace_bytes(case["cand"]))
+        tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+        rep = td.check(ref, cand, tol, case["kappa"], fmt=td.FloatFormat(case["fmt"]))
+        assert_reports_match(json.loads(td.render_report(rep, "json")), json.loads(case["report"]), case["name"])
+    rng = np.random.default_rng(5)
+    for i, case in enumerate(shardings[:60]):
+        ref, cand = _random_trace_pair(rng, case, "f32", ("none", "value", "replica")[i % 3])
+        rep = td.check(ref, cand, td.ToleranceMap({}, n_samples=1, eps_p=0.0), fmt=td.FloatFormat.BF16)
+        oref = [O.Rec(r.id.encode(), r.rank_meta.as_tuple(), r.mapping.local_shape,
+                      r.mapping.global_shape, [(l.bounds, g.bounds) for l, g in r.mapping.pairs],
+                      r.replica_group_size, np.asarray(r.values(), np.float32)) for r in ref.records]
+        ocand = [O.Rec(r.id.encode(), r.rank_meta.as_tuple(), r.mapping.local_shape,
+                       r.mapping.global_shape, [(l.bounds, g.bounds) for l, g in r.mapping.pairs],
+                       r.replica_group_size, np.asarray(r.values(), np.float32)) for r in cand.records]
+        want = O.check(oref, ocand, ref.header, cand.header, {}, 3.0, "BF16")
+        assert_reports_match(json.loads(td.render_report(rep, "json")), want, f"chunked case {i}")

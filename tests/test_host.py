@@ -129,3 +129,48 @@ def test_host_metadata_agrees_with_oracle(cases, golden_trace_bytes):
             assert (host or None) == (o["detail"] or None), (name, ident)
             if meta.merge_ok:
                 assert tuple(o["values"].shape) == meta.global_shape
+
+
+def test_retiled_and_chunked_plan_tables_are_consistent(monkeypatch, cases, golden_trace_bytes):
+    """Plan._retile / Plan._chunk_slots: every slot's tile range still
+    covers exactly its segments' tiles, and the chunk table partitions each
+    slot's partial rows in order."""
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200 import _native as N
+    from paper_2506_09280_b200.checker import CheckPlan
+    from paper_2506_09280_b200.plan import Plan
+    monkeypatch.setattr(Plan, "CHUNK_MIN_ROWS", 0)
+    monkeypatch.setattr(Plan, "CHUNK_ROWS", 7)
+    W = N.WARPS_PER_TILE
+    for case in cases["checks"]:
+        ref = trace_from_bytes(golden_trace_bytes(case["ref"]))
+        cand = trace_from_bytes(golden_trace_bytes(case["cand"]))
+        tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+        plan = CheckPlan(ref, cand, tol, case["kappa"], fmt=td.FloatFormat(case["fmt"])).plan
+        # golden traces are tiny: the tile shrinks to the minimum
+        assert plan.tile_units == 1 << Plan.MIN_TILE_SHIFT
+        segs = plan.segs
+        if len(segs):
+            assert ((segs["flags"] >> N.SEG_TILE_SHIFT_POS) & 31 == Plan.MIN_TILE_SHIFT).all()
+            n_t = -(-segs["n_units"] // plan.tile_units)
+            assert (segs["tile_begin"][1:] == np.cumsum(n_t)[:-1]).all() and n_t.sum() == plan.n_tiles
+            starts = set(segs["tile_begin"].tolist()) | {plan.n_tiles}
+            for table in (plan.ids, plan.groups):
+                for tb, te in zip(table["tile_begin"], table["tile_end"]):
+                    assert tb in starts and te in starts and tb <= te
+        ch = plan.chunks
+        spans = [(tb * W, te * W, 0, 2) for tb, te in zip(plan.ids["tile_begin"], plan.ids["tile_end"])]
+        spans += [(tb * W, te * W, 2, 1 + nz) for tb, te, nz in
+                  zip(plan.groups["tile_begin"], plan.groups["tile_end"], plan.groups["nz"])]
+        ranges = list(zip(plan.ids_chunked["tile_begin"], plan.ids_chunked["tile_end"]))
+        ranges += list(zip(plan.groups_chunked["tile_begin"], plan.groups_chunked["tile_end"]))
+        cursor = 0
+        for (rb, re, k0, nk), (c0, c1) in zip(spans, ranges):
+            assert c0 == cursor
+            rows = ch[c0:c1]
+            assert (rows["k0"] == k0).all() and (rows["nk"] == nk).all()
+            edges = [rb] + rows["row_end"].tolist()
+            assert rows["row_begin"].tolist() == edges[:-1] and edges[-1] == re
+            assert ((rows["row_end"] - rows["row_begin"]) <= 7).all()
+            cursor = c1
+        assert cursor == len(ch)

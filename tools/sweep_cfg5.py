@@ -44,12 +44,9 @@ def main():
                 flush.zero_()
                 ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
                 ev[0].record()
-                N.call("td_segnorm", prep.seg_ptr, prep.classes.ctypes.data,
-                       len(prep.classes), prep.part_ptr, 0, N.stream_handle())
+                prep.segnorm(N.stream_handle())
                 ev[1].record()
-                N.call("td_finalize", prep.ids_ptr, prep.n_ids, prep.grp_ptr, prep.n_groups,
-                       prep.part_ptr, prep.idsum_ptr, prep.gsum_ptr, prep.kappa, prep.eps,
-                       prep.replica_eps, prep.idres_ptr, prep.gres_ptr, prep.tie_ptr, N.stream_handle())
+                prep.finalize(N.stream_handle())
                 ev[2].record()
                 torch.cuda.synchronize()
                 if rep >= 3:
