@@ -113,6 +113,21 @@ __device__ __forceinline__ double load_elem(const char* base, int dt, int64_t id
     }
 }
 
+#ifndef TD_REPLICA_SKIP
+#define TD_REPLICA_SKIP 1
+#endif
+#ifndef TD_REPLICA_SKIP_MIN_NZ
+#define TD_REPLICA_SKIP_MIN_NZ 3
+#endif
+
+template <int Q>
+__device__ __forceinline__ bool same_bits(const uint4* a, const uint4* b) {
+    uint32_t d = 0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) d |= (a[q].x ^ b[q].x) | (a[q].y ^ b[q].y) | (a[q].z ^ b[q].z) | (a[q].w ^ b[q].w);
+    return d == 0;
+}
+
 struct Acc {
     double d2, x2, y2, z[TD_MAX_Z];
     __device__ __forceinline__ void zero() {
@@ -198,6 +213,9 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
     constexpr int Q = Vec<DT>::Q;
     constexpr int ES = (DT == TD_F32) ? 4 : 2;
     constexpr int USED = NZ > 0 ? 3 + NZ : 2;
+    // classes with >= 3 replicas (fewer: little XU work to save, more spills)
+    // (2-byte payloads; f32 vectors need twice the registers)
+    constexpr bool SKIP = TD_REPLICA_SKIP && NZ >= TD_REPLICA_SKIP_MIN_NZ && Q == 1;
     const int warp = threadIdx.x >> 5;
     for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
         const int64_t e = __ldg(tiles + i);
@@ -246,12 +264,29 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
                         a.d2 = fma(d, d, a.d2);
                         a.x2 = fma(xv, xv, a.x2);
                     }
-                    if (NZ > 0) {
-                        a.y2 = fma(yv, yv, a.y2);
+                    if (NZ > 0) a.y2 = fma(yv, yv, a.y2);
+                    if constexpr (!SKIP) {
 #pragma unroll
                         for (int j = 0; j < NZ; ++j) {
                             const double dz = yv - Vec<DT>::at(zr[j][k], e8);
                             a.z[j] = fma(dz, dz, a.z[j]);
+                        }
+                    }
+                }
+                if constexpr (SKIP) {
+                    // a replica vector bit-identical to copy 0 adds exactly +0
+                    // to its sum (or, for equal inf/NaN cells, turns a NaN
+                    // error into 0 — neither ever wins check_replicas' strict
+                    // max): skip its conversions, the bulk of the XU-pipe work
+                    // in replica classes
+#pragma unroll
+                    for (int j = 0; j < NZ; ++j) {
+                        if (!same_bits<Q>(zr[j][k], yr[k])) {
+#pragma unroll
+                            for (int e8 = 0; e8 < 8; ++e8) {
+                                const double dz = Vec<DT>::at(yr[k], e8) - Vec<DT>::at(zr[j][k], e8);
+                                a.z[j] = fma(dz, dz, a.z[j]);
+                            }
                         }
                     }
                 }
@@ -372,7 +407,7 @@ segnorm_fn pick_vec(int nz, bool hx) {
         case 1: return k_segnorm_vec<DT, 1, false, U4, 4>;
         case 2: return k_segnorm_vec<DT, 2, false, U2, 4>;
         case 3: return k_segnorm_vec<DT, 3, false, 1, 4>;
-        case 4: return k_segnorm_vec<DT, 4, false, 1, 4>;
+        case 4: return k_segnorm_vec<DT, 4, false, 1, 2>;
         case 5: return k_segnorm_vec<DT, 5, false, 1, 2>;
         case 6: return k_segnorm_vec<DT, 6, false, 1, 2>;
         case 7: return k_segnorm_vec<DT, 7, false, 1, 2>;
