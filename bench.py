@@ -63,48 +63,60 @@ def peaks():
     return 6650.0, "fallback"
 
 
-def workload(name: str, rank: int = 0):
-    """(model/config description, ref trace, cand trace, tolerance map, fmt)."""
-    import torch
+def describe(name: str):
+    """(config description for the JSON line, build spec) — metadata only, so
+    both arms print the same `config`."""
     from paper_2506_09280_b200 import layout as L
-    from paper_2506_09280_b200 import synthetic
-    from paper_2506_09280_b200.checker import ToleranceMap
     from paper_2506_09280_b200.tensor import FloatFormat
     if name.startswith("cfg5"):
         parts = name.split(":")
         mib = int(parts[1]) if len(parts) > 1 else 1024
         maps = parts[2] if len(parts) > 2 else "identity"
         g = int(parts[3]) if len(parts) > 3 else (4 if maps != "identity" else 1)
-        ref, cand = synthetic.sweep_pair(mib << 20, maps=maps, g=g, seed=rank)
         desc = {"workload": f"config5 raw compare sweep: one id, {mib} MiB bf16 per tensor, "
                             f"shape (N/4096, 4096), candidate {maps} x{g}",
                 "storage_dtype": "bf16", "tensor_mib": mib, "maps": maps, "shards": g}
-        fmt = FloatFormat.BF16
+        return desc, {"sweep": (mib, maps, g), "fmt": FloatFormat.BF16}
+    if name == "cfg1":
+        model, pcfg, dtype, fmt = L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), "f32", FloatFormat.FP32
+        label = "config1 GPT-2-small-shape L=2 fp32 traces, TP=2 candidate vs single-device reference"
+    elif name == "cfg3":
+        model = L.LLAMA3_1B
+        pcfg, dtype, fmt = L.ParallelConfig(tp=8), "bf16", FloatFormat.BF16
+        label = ("config3 Llama-3-1B-shape bf16 traces (L=16 d=2048 GQA 32/8 ff=8192 SwiGLU S=8192 "
+                 "V=128256), TP=8 candidate vs single-device reference, injected bugs: wrong shard "
+                 "order (lm_head logits), missing row-parallel allreduce (layers.7.attn output), "
+                 "scale error (embedding output)")
     else:
-        if name == "cfg1":
-            model, pcfg, dtype, fmt = L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), torch.float32, FloatFormat.FP32
-            label = "config1 GPT-2-small-shape L=2 fp32 traces, TP=2 candidate vs single-device reference"
-        elif name == "cfg3":
-            model = L.LLAMA3_1B
-            pcfg, dtype, fmt = L.ParallelConfig(tp=8), torch.bfloat16, FloatFormat.BF16
-            label = ("config3 Llama-3-1B-shape bf16 traces (L=16 d=2048 GQA 32/8 ff=8192 SwiGLU S=8192 "
-                     "V=128256), TP=8 candidate vs single-device reference, injected bugs: wrong shard "
-                     "order (lm_head logits), missing row-parallel allreduce (layers.7.attn output), "
-                     "scale error (embedding output)")
-        else:
-            model, pcfg, dtype, fmt = L.GPT2_MEDIUM, L.ParallelConfig(tp=4), torch.bfloat16, FloatFormat.BF16
-            label = ("config2 GPT-2-medium-shape bf16 traces (L=24 d=1024 ff=4096 S=1024 V=50304), TP=4 "
-                     "candidate vs single-device reference, activations+grads+MainGrad+Param")
-        bugs = None
-        if name == "cfg3":
-            bugs = {"iter=0|mb=0|kind=ActivationOut|mod=model.lm_head": "order",
-                    "iter=0|mb=0|kind=ActivationOut|mod=model.layers.7.attn": "partial",
-                    "iter=0|mb=0|kind=ActivationOut|mod=model.embedding": "scale"}
-        ref, cand = synthetic.build(model, pcfg, dtype=dtype, seed=rank, eps=fmt.eps, bugs=bugs)
-        desc = {"workload": label, "trace_shapes": f"layers={model.layers} d={model.d_model} "
-                                                  f"ff={model.d_ff} S={model.seq_len} V={model.vocab}",
-                "candidate_layout": f"tp={pcfg.tp} dp={pcfg.dp} cp={pcfg.cp} sp={pcfg.sp}",
-                "storage_dtype": "bf16" if dtype == torch.bfloat16 else "f32"}
+        model, pcfg, dtype, fmt = L.GPT2_MEDIUM, L.ParallelConfig(tp=4), "bf16", FloatFormat.BF16
+        label = ("config2 GPT-2-medium-shape bf16 traces (L=24 d=1024 ff=4096 S=1024 V=50304), TP=4 "
+                 "candidate vs single-device reference, activations+grads+MainGrad+Param")
+    bugs = None
+    if name == "cfg3":
+        bugs = {"iter=0|mb=0|kind=ActivationOut|mod=model.lm_head": "order",
+                "iter=0|mb=0|kind=ActivationOut|mod=model.layers.7.attn": "partial",
+                "iter=0|mb=0|kind=ActivationOut|mod=model.embedding": "scale"}
+    desc = {"workload": label, "trace_shapes": f"layers={model.layers} d={model.d_model} "
+                                              f"ff={model.d_ff} S={model.seq_len} V={model.vocab}",
+            "candidate_layout": f"tp={pcfg.tp} dp={pcfg.dp} cp={pcfg.cp} sp={pcfg.sp}",
+            "storage_dtype": dtype}
+    return desc, {"model": model, "pcfg": pcfg, "dtype": dtype, "fmt": fmt, "bugs": bugs}
+
+
+def workload(name: str, rank: int = 0):
+    """(config description, ref trace, cand trace, tolerance map, fmt), built in HBM."""
+    import torch
+    from paper_2506_09280_b200 import synthetic
+    from paper_2506_09280_b200.checker import ToleranceMap
+    desc, spec = describe(name)
+    fmt = spec["fmt"]
+    if "sweep" in spec:
+        mib, maps, g = spec["sweep"]
+        ref, cand = synthetic.sweep_pair(mib << 20, maps=maps, g=g, seed=rank)
+    else:
+        dtype = torch.bfloat16 if spec["dtype"] == "bf16" else torch.float32
+        ref, cand = synthetic.build(spec["model"], spec["pcfg"], dtype=dtype, seed=rank, eps=fmt.eps,
+                                    bugs=spec["bugs"])
     eps = fmt.eps
     tol = ToleranceMap({r.id.encode(): 2 * eps for r in ref.records}, n_samples=1, eps_p=eps)
     return desc, ref, cand, tol, fmt
@@ -306,9 +318,10 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (host numpy, same shapes/layout as the GPU arm)",
-            "config": {"workload": f"{args.config} (see the GPU arm's line)", "sampled_ids": n_sample},
+            "config": describe(args.config)[0],
             "layer_checks_per_s": n_sample / t,
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
+                             "sampled_ids": n_sample,
                              "sample": f"every {stride}th id of the workload ({n_sample} ids, "
                                        f"{nbytes / 1e9:.3f} GB at 2 B/elem), merge+rel_err per id on "
                                        f"{cores} processes"},

@@ -30,4 +30,4 @@ def test_reference_arm_json_line():
 
 def test_reference_arm_samples_the_layout_workload():
     d = _run("--impl", "reference", "--steps", "1", "--warmup", "0", "--config", "cfg1")
-    assert d["config"]["sampled_ids"] >= 3 and d["layer_checks_per_s"] > 0
+    assert d["cpu_baseline"]["sampled_ids"] >= 3 and d["layer_checks_per_s"] > 0
