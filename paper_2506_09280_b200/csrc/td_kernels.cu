@@ -668,12 +668,6 @@ __device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ double signed_from_word(uint64_t w) {
-    const uint64_t m = w >> 11;
-    const double one_m = __longlong_as_double((long long)(0x3FF0000000000000ull | (m & 0xFFFFFFFFFFFFFull)));
-    return __dsub_rn(one_m, (m >> 52) ? 1.0 : 2.0);
-}
-
 // 2u - 1 with u = (w >> 11) * 2^-53 (generation.py:74-78, 166), without an
 // int->double conversion (XU pipe): t = 2u = m * 2^-52 for the 53-bit m is
 // exact as (1.m52 as a double) - (m < 2^52 ? 1 : 0); then t - 1 rounds once,
@@ -767,7 +761,6 @@ __device__ __forceinline__ double perturb_one(double xv, uint64_t seed, uint64_t
 
 // One thread per group of 8 consecutive elements of a row (cols % 8 == 0,
 // 16-byte aligned rows): 16-byte loads/stores for bf16, one division per group.
-template <bool BF16_Q8>
 __global__ void __launch_bounds__(256)
 k_perturb_vec8(const char* x, char* y, int dt_in, int dt_out, int64_t rows, int64_t cols,
                int64_t full_cols, int64_t col0, const int64_t* __restrict__ row_pos, int64_t row0,
@@ -783,39 +776,84 @@ k_perturb_vec8(const char* x, char* y, int dt_in, int dt_out, int64_t rows, int6
         const int64_t pos = row_pos ? __ldg(row_pos + r) : row0 + r;
         const uint64_t kb = (uint64_t)(pos * full_cols + col0 + c);
         const int64_t idx = r * cols + c;
-        if (BF16_Q8) {
-            const uint4 in = *reinterpret_cast<const uint4*>(x + idx * 2);
-            const uint32_t* iw = &in.x;
-            uint4 out;
-            uint32_t* ow = &out.x;
-            // splitmix64 state of word kb: seed + (kb+1)*gamma, then += gamma per element
-            uint64_t z = seed + (kb + 1) * GAMMA;
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                uint32_t pair = 0;
+        for (int h = 0; h < 8; ++h) {
+            const double v = perturb_one(load_elem(x, dt_in, idx + h), seed, kb + h, eps, gen, bad);
+            store_elem(y, dt_out, idx + h, apply_format(v, fmt));
+        }
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(nonfinite, 1ull);
+}
+
+// bf16 -> bf16 with the bf16 policy, 16-B aligned rows, cols % 8 == 0: the
+// common case (block inputs / embedding outputs of a bf16 model).  One thread
+// per 8-element group; the generator is a template parameter so the loop has
+// no stream switch, and the per-element work is branch-free:
+//   * splitmix64 word kb+j = mix(z0 + j*gamma) (z0 = seed + (kb+1)*gamma);
+//   * 2u-1 from the word's top 53 bits by exponent splice (no I2F);
+//   * v = x * (1 + u*eps) in fp64, each op rounded (numpy's order);
+//   * Q_bf16(v) as one 64-bit add of the RNE bias (2^44 - 1 + lsb) on |v|'s
+//     bits, giving the bf16 pattern pre-shifted into the top half-word, and
+//     a range test on the rounded exponent (bf16 normal range, finite).
+// A group with any element outside that range (zero, bf16-subnormal range,
+// overflow clamp, inf/NaN) is recomputed element by element with the exact
+// general path (rare; zeros only cost a redo of their own group).
+// The kernel is integer-issue bound (ncu: ALU pipe 80%, fmaheavy 44%).
+// Moving the 64-bit right shifts to the FMA pipe as multiply-highs by
+// 2^(32-s) (IMAD.HI + IMAD.WIDE instead of two SHF) was measured per shift
+// site: every mix of sites lost 2-31% (fmaheavy saturates first; each
+// IMAD.HI/WIDE costs ~2.6x the SHF it replaces), so the shifts stay on ALU.
+template <int GEN>
+__global__ void __launch_bounds__(256)
+k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows, uint32_t gpr,
+               int64_t full_cols, int64_t col0, const int64_t* __restrict__ row_pos, int64_t row0,
+               uint64_t seed, double eps, uint32_t div_m, int div_p,
+               unsigned long long* __restrict__ nonfinite) {
+    const int64_t groups = rows * (int64_t)gpr;
+    int bad = 0;
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = groups < (1ll << 31) ? (int64_t)udiv((uint32_t)g, div_m, div_p) : g / gpr;
+        const int64_t c = (g - r * gpr) * 8;
+        const int64_t pos = row_pos ? __ldg(row_pos + r) : row0 + r;
+        const uint64_t kb = (uint64_t)(pos * full_cols + col0 + c);
+        const uint4 in = __ldcs(x + g);
+        const uint32_t iw[4] = {in.x, in.y, in.z, in.w};
+        uint32_t ow[4];
+        uint32_t out_of_range = 0;
+        const uint64_t z0 = seed + (kb + 1) * GAMMA;
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    const uint32_t bits = half ? (iw[h] & 0xffff0000u) : (iw[h] << 16);
-                    const double xv = (double)__uint_as_float(bits);
-                    const uint64_t k = kb + 2 * h + half;
-                    const double u = gen == TD_GEN_PHILOX4x32 ? signed_uniform(seed, k, gen)
-                                                              : signed_from_word(splitmix_mix(z));
-                    z += GAMMA;
-                    const double f = __dadd_rn(1.0, __dmul_rn(u, eps));
-                    const double v = __dmul_rn(xv, f);
-                    bad |= !isfinite(v);
-                    pair |= bf16_q8_bits(v) << (16 * half);
-                }
-                ow[h] = pair;
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t xb = (j & 1) ? (iw[j >> 1] & 0xffff0000u) : (iw[j >> 1] << 16);
+            const double xv = (double)__uint_as_float(xb);
+            double u;
+            if (GEN == TD_GEN_PHILOX4x32) {
+                u = signed_uniform(seed, kb + j, GEN);
+            } else {
+                const uint64_t m = splitmix_mix(z0 + (uint64_t)j * GAMMA) >> 11;
+                const double one_m = __longlong_as_double((long long)(0x3FF0000000000000ull | (m & 0xFFFFFFFFFFFFFull)));
+                u = __dsub_rn(one_m, (m >> 52) ? 1.0 : 2.0);
             }
-            *reinterpret_cast<uint4*>(y + idx * 2) = out;
-        } else {
+            const double v = __dmul_rn(xv, __dadd_rn(1.0, __dmul_rn(u, eps)));
+            const uint64_t b = (uint64_t)__double_as_longlong(v);
+            const uint32_t hi = (uint32_t)(b >> 32);
+            const uint64_t rb = (b & 0x7fffffffffffffffull) + 0xfffffffffffull + ((hi >> 13) & 1u);
+            const uint32_t rh = (uint32_t)(rb >> 32);      // rounded |v|: exp(11) at 30..20, mant7 at 19..13
+            out_of_range |= (rh - (897u << 20)) < (254u << 20) ? 0u : 1u;
+            const uint32_t t = (((rh << 3) - (896u << 23)) & 0x7fff0000u) | (hi & 0x80000000u);
+            if (j & 1) ow[j >> 1] = __byte_perm(ow[j >> 1], t, 0x7632);
+            else ow[j >> 1] = t;
+        }
+        if (out_of_range) {
 #pragma unroll
-            for (int h = 0; h < 8; ++h) {
-                const double v = perturb_one(load_elem(x, dt_in, idx + h), seed, kb + h, eps, gen, bad);
-                store_elem(y, dt_out, idx + h, apply_format(v, fmt));
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t xb = (j & 1) ? (iw[j >> 1] & 0xffff0000u) : (iw[j >> 1] << 16);
+                const double v = perturb_one((double)__uint_as_float(xb), seed, kb + j, eps, GEN, bad);
+                const uint32_t q = bf16_q8_bits(v);
+                ow[j >> 1] = (j & 1) ? ((ow[j >> 1] & 0xffffu) | (q << 16)) : ((ow[j >> 1] & 0xffff0000u) | q);
             }
         }
+        __stcs(y + g, make_uint4(ow[0], ow[1], ow[2], ow[3]));
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicAdd(nonfinite, 1ull);
 }
@@ -1173,12 +1211,16 @@ int td_perturb(const void* x, void* y, int32_t dtype_in, int32_t dtype_out, int6
         const uint32_t m = (uint32_t)(((1ull << p) + gpr - 1) / gpr);
         const int grid = grid_for(groups, threads, 148 * 8);
         const bool q8 = dtype_in == TD_BF16 && dtype_out == TD_BF16 && fmt == TD_FMT_BF16;
-        if (q8)
-            k_perturb_vec8<true><<<grid, threads, 0, (cudaStream_t)stream>>>(
-                static_cast<const char*>(x), static_cast<char*>(y), dtype_in, dtype_out, rows, cols, full_cols,
-                col0, row_pos, row0, seed, eps, fmt, generator, m, p, nonfinite);
+        if (q8 && generator == TD_GEN_PHILOX4x32)
+            k_perturb_bf16<TD_GEN_PHILOX4x32><<<grid, threads, 0, (cudaStream_t)stream>>>(
+                static_cast<const uint4*>(x), static_cast<uint4*>(y), rows, gpr, full_cols, col0, row_pos, row0,
+                seed, eps, m, p, nonfinite);
+        else if (q8)
+            k_perturb_bf16<TD_GEN_SPLITMIX64><<<grid, threads, 0, (cudaStream_t)stream>>>(
+                static_cast<const uint4*>(x), static_cast<uint4*>(y), rows, gpr, full_cols, col0, row_pos, row0,
+                seed, eps, m, p, nonfinite);
         else
-            k_perturb_vec8<false><<<grid, threads, 0, (cudaStream_t)stream>>>(
+            k_perturb_vec8<<<grid, threads, 0, (cudaStream_t)stream>>>(
                 static_cast<const char*>(x), static_cast<char*>(y), dtype_in, dtype_out, rows, cols, full_cols,
                 col0, row_pos, row0, seed, eps, fmt, generator, m, p, nonfinite);
     } else {
