@@ -56,11 +56,14 @@ def splitmix_words(seed: int, k0: int, n: int) -> np.ndarray:
 
 
 def philox_words(seed: int, k0: int, n: int) -> np.ndarray:
-    """Philox4x32-10 keyed by the seed, counter = k; the opt-in generator
+    """Philox4x32-10 keyed by the seed; block b = Philox(counter = b) gives
+    word 2b = (out1:out0) and word 2b+1 = (out3:out2).  The opt-in generator
     (not in the reference; restated here so the device stream is checked)."""
     k = np.arange(k0, k0 + n, dtype=np.uint64)
-    c0 = (k & np.uint64(0xFFFFFFFF)).astype(np.uint64)
-    c1 = (k >> np.uint64(32)).astype(np.uint64)
+    lane = k & np.uint64(1)
+    blk = k >> np.uint64(1)
+    c0 = (blk & np.uint64(0xFFFFFFFF)).astype(np.uint64)
+    c1 = (blk >> np.uint64(32)).astype(np.uint64)
     c2 = np.zeros_like(c0)
     c3 = np.zeros_like(c0)
     k0_ = np.uint64(seed & 0xFFFFFFFF)
@@ -74,7 +77,7 @@ def philox_words(seed: int, k0: int, n: int) -> np.ndarray:
         c0, c1, c2, c3 = (hi1 ^ c1 ^ k0_) & m32, lo1, (hi0 ^ c3 ^ k1_) & m32, lo0
         k0_ = (k0_ + np.uint64(0x9E3779B9)) & m32
         k1_ = (k1_ + np.uint64(0xBB67AE85)) & m32
-    return (c1 << np.uint64(32)) | c0
+    return np.where(lane == 0, (c1 << np.uint64(32)) | c0, (c3 << np.uint64(32)) | c2)
 
 
 def signed_uniforms(seed: int, n: int, k0: int = 0, generator: str = "splitmix64") -> np.ndarray:

@@ -284,6 +284,15 @@ def _layout_key(trace) -> tuple:
                   tuple(r.shape), r.replica_group_size) for r in trace.records)
 
 
+def _forget_payloads(view, plan: Plan, keep_ids) -> None:
+    """Drop a sample trace's record references from a cached view / plan
+    (the cached path re-binds operands by position and reads only metadata)."""
+    for meta in view.values():
+        for g in meta.groups:
+            g.records = [None] * len(g.records)
+    plan.operands[:] = [o if id(o) in keep_ids else None for o in plan.operands]
+
+
 def estimate_tolerance(runner: Runner, *, n_samples: int = 5, eps_p: float,
                        aggregation: str = "max") -> ToleranceMap:
     """Per-id response to an eps_p input nudge (checker.py:102-138).
@@ -342,6 +351,11 @@ def estimate_tolerance(runner: Runner, *, n_samples: int = 5, eps_p: float,
                 raise ShapeMismatch(f"rel_err: {meta.global_shape} vs {moved.global_shape}")
             resp = float(idres[k]["observed"])
             samples[ident].append(resp if math.isfinite(resp) else 0.0)
+        # hold no payload of this sample while the next one runs: only one
+        # perturbed trace is alive at a time (with the base), so a run whose
+        # traces are a third of HBM still fits
+        _forget_payloads(pert, plan, base_pos)
+        del trace, ptrs
     responses = {}
     for ident, resp in samples.items():
         if not resp:

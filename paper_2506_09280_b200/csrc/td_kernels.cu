@@ -646,9 +646,10 @@ __device__ __forceinline__ uint64_t splitmix_word(uint64_t seed, uint64_t k) {
     return z ^ (z >> 31);
 }
 
-// Philox4x32-10 keyed by the seed, counter = k; the 64-bit word is (out1:out0)
-__device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t k) {
-    uint32_t c0 = (uint32_t)k, c1 = (uint32_t)(k >> 32), c2 = 0, c3 = 0;
+// Philox4x32-10 keyed by the seed: block b = Philox(counter = b) yields two
+// 64-bit words, word 2b = (out1:out0) and word 2b+1 = (out3:out2)
+__device__ __forceinline__ uint4 philox_block(uint64_t seed, uint64_t blk) {
+    uint32_t c0 = (uint32_t)blk, c1 = (uint32_t)(blk >> 32), c2 = 0, c3 = 0;
     uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
@@ -659,7 +660,16 @@ __device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t k) {
         k0 += 0x9E3779B9u;
         k1 += 0xBB67AE85u;
     }
-    return ((uint64_t)c1 << 32) | c0;
+    return make_uint4(c0, c1, c2, c3);
+}
+
+__device__ __forceinline__ uint64_t philox_lane(const uint4& o, uint64_t k) {
+    return (k & 1) ? (((uint64_t)o.w << 32) | o.z) : (((uint64_t)o.y << 32) | o.x);
+}
+
+// word k of the Philox stream
+__device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t k) {
+    return philox_lane(philox_block(seed, k >> 1), k);
 }
 
 __device__ __forceinline__ uint64_t splitmix_mix(uint64_t z) {
@@ -822,15 +832,22 @@ k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows,
         uint32_t ow[4];
         uint32_t out_of_range = 0;
         const uint64_t z0 = seed + (kb + 1) * GAMMA;
+        uint4 blk;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const uint32_t xb = (j & 1) ? (iw[j >> 1] & 0xffff0000u) : (iw[j >> 1] << 16);
             const double xv = (double)__uint_as_float(xb);
             double u;
-            if (GEN == TD_GEN_PHILOX4x32) {
-                u = signed_uniform(seed, kb + j, GEN);
-            } else {
-                const uint64_t m = splitmix_mix(z0 + (uint64_t)j * GAMMA) >> 11;
+            {
+                uint64_t w;
+                if (GEN == TD_GEN_PHILOX4x32) {
+                    // one Philox block per two words: recompute at even words (and word 0)
+                    if (j == 0 || ((kb + j) & 1) == 0) blk = philox_block(seed, (kb + j) >> 1);
+                    w = philox_lane(blk, kb + j);
+                } else {
+                    w = splitmix_mix(z0 + (uint64_t)j * GAMMA);
+                }
+                const uint64_t m = w >> 11;
                 const double one_m = __longlong_as_double((long long)(0x3FF0000000000000ull | (m & 0xFFFFFFFFFFFFFull)));
                 u = __dsub_rn(one_m, (m >> 52) ? 1.0 : 2.0);
             }

@@ -406,6 +406,26 @@ def test_perturbation_full_exponent_range_bit_exact():
     assert np.array_equal(y.double().cpu().numpy()[normal], want[normal])
 
 
+@pytest.mark.parametrize("generator", ["splitmix64", "philox"])
+def test_perturbation_column_shards_compose(generator):
+    """A TP column shard perturbed with its column offset (odd offsets and an
+    odd full width, so words start mid Philox block) equals the same columns
+    of the whole-tensor perturbation, on the bf16 fast path."""
+    full_cols, rows = 8 * 37 + 3, 64
+    x = torch.randn(rows, full_cols, dtype=torch.float64).to(torch.bfloat16)
+    ident = "iter=0|mb=0|kind=ActivationIn|mod=model.layers.3.mlp"
+    spec = td.PerturbSpec(2, 2.0 ** -8)
+    whole = td.apply_perturbation(x.cuda(), ident, spec, policy="bf16", generator=generator)
+    want = O.perturb(x.double().numpy(), f"perturb|s=2|{ident}", 2.0 ** -8, np.arange(rows), full_cols,
+                     "BF16", generator=generator)
+    assert np.array_equal(whole.double().cpu().numpy(), want)
+    for col0 in (1, 3, 8, 131):
+        part = x[:, col0:col0 + 64].contiguous().cuda()
+        got = td.apply_perturbation(part, ident, spec, policy="bf16", full_cols=full_cols, col0=col0,
+                                    generator=generator)
+        assert torch.equal(got, whole[:, col0:col0 + 64]), col0
+
+
 def test_graph_replay_matches_eager_launch(cases, golden_trace_bytes):
     """A captured CUDA graph of the whole check replays to the same results
     and follows payload updates made in place."""

@@ -9,6 +9,7 @@ Prints one JSON line: per-layer responses, Spearman(l, response), and the
 least-squares c of the sqrt(L/l) fit with its log-rms residual.
 
     python tools/depth_sweep.py [--layers 16] [--d 256] [--seq 256] [--samples 5]
+    python tools/depth_sweep.py --llama3-8b [--seq 8192]     # config 4's shape
 """
 
 import argparse
@@ -22,7 +23,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def build(layers, d, seq, vocab, kv):
+def build(layers, d, seq, vocab, kv, heads=8, ff=None):
     import torch
 
     class RMS(torch.nn.Module):
@@ -37,7 +38,7 @@ def build(layers, d, seq, vocab, kv):
         def __init__(self):
             super().__init__()
             self.norm = RMS(d)
-            self.h, self.kv, self.hd = 8, kv, d // 8
+            self.h, self.kv, self.hd = heads, kv, d // heads
             self.wq = torch.nn.Linear(d, d, bias=False)
             self.wk = torch.nn.Linear(d, kv * self.hd, bias=False)
             self.wv = torch.nn.Linear(d, kv * self.hd, bias=False)
@@ -46,18 +47,21 @@ def build(layers, d, seq, vocab, kv):
         def forward(self, x):
             a = self.norm(x)
             q = self.wq(a).view(seq, self.h, self.hd).transpose(0, 1)
+            # GQA by repeating the kv heads: keeps SDPA on its flash backend
+            # (enable_gqa falls back to the S x S math path)
             k = self.wk(a).view(seq, self.kv, self.hd).transpose(0, 1).repeat_interleave(self.h // self.kv, 0)
             v = self.wv(a).view(seq, self.kv, self.hd).transpose(0, 1).repeat_interleave(self.h // self.kv, 0)
-            o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+            o = torch.nn.functional.scaled_dot_product_attention(q[None], k[None], v[None], is_causal=True)[0]
             return x + self.wo(o.transpose(0, 1).reshape(seq, d))
 
     class Mlp(torch.nn.Module):
         def __init__(self):
             super().__init__()
             self.norm = RMS(d)
-            self.w1 = torch.nn.Linear(d, 4 * d, bias=False)
-            self.w3 = torch.nn.Linear(d, 4 * d, bias=False)
-            self.w2 = torch.nn.Linear(4 * d, d, bias=False)
+            f = ff or 4 * d
+            self.w1 = torch.nn.Linear(d, f, bias=False)
+            self.w3 = torch.nn.Linear(d, f, bias=False)
+            self.w2 = torch.nn.Linear(f, d, bias=False)
 
         def forward(self, x):
             a = self.norm(x)
@@ -103,16 +107,40 @@ def main():
     ap.add_argument("--d", type=int, default=256)
     ap.add_argument("--seq", type=int, default=256)
     ap.add_argument("--samples", type=int, default=5)
+    ap.add_argument("--heads", type=int, default=8)
+    ap.add_argument("--kv", type=int, default=2)
+    ap.add_argument("--ff", type=int, default=None)
+    ap.add_argument("--vocab", type=int, default=1024)
+    ap.add_argument("--rewrite-std", type=float, default=0.02,
+                    help="std of the regenerated block inputs (reference HIDDEN_REWRITE_STD = 0.02, "
+                         "engine.py:55); the 8B preset uses 1.0, see below")
+    ap.add_argument("--llama3-8b", action="store_true",
+                    help="Llama-3-8B shape: L=32 d=4096 32/8 heads ff=14336 V=128256 (seq from --seq)")
     args = ap.parse_args()
+    if args.llama3_8b:
+        args.layers, args.d, args.heads, args.kv, args.ff, args.vocab = 32, 4096, 32, 8, 14336, 128256
+        # at d=4096 a 0.02-std block input makes each RMSNorm's backward gain
+        # 1/0.02 = 50 and the module-wise gradient chain grows ~20x per block
+        # (bf16 overflow below layer ~16: non-finite responses, recorded as 0
+        # like the reference); unit-variance inputs, the scale of a real
+        # residual stream, keep every block's Jacobian contractive
+        args.rewrite_std = 1.0
     import torch
     import paper_2506_09280_b200 as td
     from paper_2506_09280_b200.runner import torch_runner
     from paper_2506_09280_b200.torchtap import TapConfig
     torch.manual_seed(0)
-    vocab = 1024
-    model = build(args.layers, args.d, args.seq, vocab, kv=2).cuda().bfloat16()
-    for p in model.parameters():
-        torch.nn.init.normal_(p, 0.0, 0.02) if p.dim() > 1 else None
+    vocab = args.vocab
+    torch.set_default_dtype(torch.bfloat16)       # built in place: no fp32 copy of 8B params
+    with torch.device("cuda"):
+        model = build(args.layers, args.d, args.seq, vocab, kv=args.kv, heads=args.heads, ff=args.ff)
+    torch.set_default_dtype(torch.float32)
+    # the reference's init (model.py:82-106): N(0, 0.02), residual-branch
+    # output projections (wo, w2) N(0, 0.02 / sqrt(2L)); norms at 1
+    residual_std = 0.02 / math.sqrt(2.0 * args.layers)
+    for name, p in model.named_parameters():
+        if p.dim() > 1:
+            torch.nn.init.normal_(p, 0.0, residual_std if name.endswith(("wo.weight", "w2.weight")) else 0.02)
     ids = torch.randint(0, vocab, (args.seq,), device="cuda")
     labels = torch.roll(ids, -1)
 
@@ -121,10 +149,20 @@ def main():
     blocks = tuple(f"layers.{i}" for i in range(2 * args.layers))
     runner = torch_runner(model, step, embedding="embedding",
                           tap=TapConfig(patterns=("layers.*",), precision="bf16"),
-                          module_inputs=blocks, rewrite=True)
+                          module_inputs=blocks, rewrite=True, rewrite_std=args.rewrite_std)
     eps = td.FloatFormat.BF16.eps
+    torch.cuda.synchronize()
+    t_run = time.perf_counter()
+    warm = runner(None)
+    torch.cuda.synchronize()
+    run_s = time.perf_counter() - t_run
+    warm_gb = sum(r.payload.numel() * r.payload.element_size() for r in warm.records) / 1e9
+    del warm
+    print(f"one trace: {warm_gb:.1f} GB; allocated after the warm-up run "
+          f"{torch.cuda.memory_allocated() / 1e9:.1f} GB", file=sys.stderr, flush=True)
     t0 = time.perf_counter()
     tol = td.estimate_tolerance(runner, n_samples=args.samples, eps_p=eps)
+    torch.cuda.synchronize()
     secs = time.perf_counter() - t0
     per_layer = []
     for l in range(args.layers):
@@ -136,8 +174,16 @@ def main():
     basis = [math.sqrt(L / (l + 1)) * eps for l in range(L)]
     c = sum(b * r for b, r in zip(basis, per_layer)) / sum(b * b for b in basis)
     resid = math.sqrt(sum(math.log(max(r, 1e-30) / (c * b)) ** 2 for b, r in zip(basis, per_layer)) / L)
+    n_params = sum(p.numel() for p in model.parameters())
     print(json.dumps({"layers": L, "d_model": args.d, "seq": args.seq, "samples": args.samples,
-                      "mode": "module-wise", "estimate_seconds": secs,
+                      "heads": args.heads, "kv_heads": args.kv, "d_ff": args.ff or 4 * args.d,
+                      "vocab": vocab, "params": n_params, "dtype": "bf16",
+                      "mode": "module-wise", "estimate_seconds": secs, "one_traced_run_seconds": run_s,
+                      "ids": len(tol.responses), "trace_gb_per_run": warm_gb,
+                      "rewrite_std": args.rewrite_std,
+                      "zero_or_nonfinite_paramgrad_responses": sum(
+                          1 for k, v in tol.responses.items() if "kind=ParamGrad" in k and v == 0.0),
+                      "peak_hbm_gb": torch.cuda.max_memory_allocated() / 1e9,
                       "per_layer_paramgrad_response_over_eps": [r / eps for r in per_layer],
                       "spearman_layer_vs_response": spearman(list(range(L)), per_layer),
                       "sqrt_bound_fit_c": c, "log_rms_residual": resid,
