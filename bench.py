@@ -1,7 +1,7 @@
 """Benchmark of the B200 tensor-comparison hot path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg2|cfg1|cfg3|cfg5:<MiB>[:columns|stripes][:G]]
+                    [--config cfg2|cfg1|cfg3|cfg4|cfg5:<MiB>[:columns|stripes][:G]]
 
 Metric (BASELINE.json): traced-tensor compare GB/s vs the HBM roofline, plus
 layer-checks/s.  A *step* is one `check` of the candidate trace against the
@@ -77,6 +77,17 @@ def describe(name: str):
                             f"shape (N/4096, 4096), candidate {maps} x{g}",
                 "storage_dtype": "bf16", "tensor_mib": mib, "maps": maps, "shards": g}
         return desc, {"sweep": (mib, maps, g), "fmt": FloatFormat.BF16}
+    if name == "cfg4":
+        model, pcfg = L.LLAMA3_8B, L.ParallelConfig(tp=2, dp=4, microbatches=4)
+        desc = {"workload": "config4 Llama-3-8B-shape bf16 full-step traces (L=32 d=4096 GQA 32/8 ff=14336 "
+                            "S=8192 V=128256), TP=2 x DP=4 candidate, M=4: this GPU's share of the "
+                            "8-GPU check (rank r of 8: its candidate records, the reference slices of "
+                            "the compares it runs, digests of its copies of cross-GPU replica groups)",
+                "trace_shapes": f"layers={model.layers} d={model.d_model} ff={model.d_ff} "
+                                f"S={model.seq_len} V={model.vocab}",
+                "candidate_layout": "tp=2 dp=4 cp=1 sp=False microbatches=4", "storage_dtype": "bf16",
+                "job_gpus": 8}
+        return desc, {"model": model, "pcfg": pcfg, "dtype": "bf16", "fmt": FloatFormat.BF16, "share": 8}
     if name == "cfg1":
         model, pcfg, dtype, fmt = L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), "f32", FloatFormat.FP32
         label = "config1 GPT-2-small-shape L=2 fp32 traces, TP=2 candidate vs single-device reference"
@@ -284,6 +295,126 @@ def host_sample(name: str, stride: int):
     return rr, cr, fmt, len(sample)
 
 
+def run_share(args, world: int, rank: int, local: int):
+    """Config 4: this GPU's share of the 8-GPU TP=2 x DP=4 check.  Rank r
+    (< world <= 8) holds virtual rank r's records (synthetic.ShareLayout) and
+    plans with every rank's metadata (StaticComm), so the same plan runs
+    whether the other 7 shares are live GPUs or absent.  A step = digests of
+    the local copies of cross-GPU replica groups (td_fingerprint, one launch)
+    + their table all_reduce + td_segnorm + slot reduction + the partial-sum
+    all_reduce + verdicts.  Weak scaling: N GPUs process N shares."""
+    import torch
+    import torch.distributed as dist
+    from paper_2506_09280_b200 import _native as N
+    from paper_2506_09280_b200 import synthetic
+    from paper_2506_09280_b200.checker import ToleranceMap
+    from paper_2506_09280_b200.device import resolve_operands
+    from paper_2506_09280_b200.distributed import (DistributedCheckPlan, StaticComm, TorchComm,
+                                                   allreduce_partials)
+    hbm, peak_kind = peaks()
+    desc, spec = describe("cfg4")
+    fmt, share = spec["fmt"], spec["share"]
+    if world > share:
+        raise SystemExit(f"config 4 is an {share}-GPU job: run it on at most {share} GPUs")
+    t0 = time.perf_counter()
+    lay = synthetic.ShareLayout(spec["model"], spec["pcfg"], share)
+    ref, cand = lay.build(rank, seed=0, eps=fmt.eps)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    ref_metas, cand_metas = lay.metas()
+    comm = StaticComm(rank, share, [ref_metas, cand_metas], inner=TorchComm() if world > 1 else None)
+    tol = ToleranceMap({i: 2 * fmt.eps for i in lay.ids}, n_samples=1, eps_p=fmt.eps)
+    t0 = time.perf_counter()
+    dcp = DistributedCheckPlan(ref, cand, tol, 3.0, fmt=fmt, comm=comm)
+    plan_s = time.perf_counter() - t0
+    ptrs, keep = resolve_operands(dcp.plan.operands, dcp.plan.operand_dtypes)
+    prep = dcp.plan.prepare(ptrs, kappa=3.0, eps=fmt.eps, replica_eps=fmt.eps)
+    fps, where = dcp.digests()
+    n_remote = len(dcp.plan.remote_groups)
+    table = torch.zeros((max(n_remote, 1), N.MAX_Z + 1, 2), dtype=torch.int64, device="cuda")
+    rows = torch.tensor([k for k, _ in where], dtype=torch.int64, device="cuda")
+    cols = torch.tensor([c for _, c in where], dtype=torch.int64, device="cuda")
+    stream = prep.stream
+    alg_bytes = dcp.plan.algorithmic_bytes + fps.nbytes
+
+    def step(seg_events=None):
+        sh = N.stream_handle(stream)
+        with torch.cuda.stream(stream):
+            if seg_events is not None:
+                seg_events[0].record(stream)
+            fps.run(stream)
+            if seg_events is not None:
+                seg_events[1].record(stream)
+            if where:
+                table[rows, cols] = fps.out[:fps.n]
+            if world > 1:
+                dist.all_reduce(table)
+            if seg_events is not None:
+                seg_events[2].record(stream)
+            prep.segnorm(sh)
+            if seg_events is not None:
+                seg_events[3].record(stream)
+            prep.reduce(sh)
+            if world > 1:
+                allreduce_partials(prep)
+            prep.verdict(sh)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for k in range(args.steps):
+            step(ev[k])
+        end.record(stream)
+        torch.cuda.synchronize()
+    idres, gres, ties = prep.fetch()
+    t_local = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_step = float(t_local.item()) / args.steps
+    fp_ms = statistics.mean(a.elapsed_time(b) for a, b, _, _ in ev)
+    seg_ms = statistics.mean(c.elapsed_time(d) for _, _, c, d in ev)
+    seg_bytes = dcp.plan.algorithmic_bytes
+    n_ids = len(dcp.common)
+    if rank == 0:
+        line = {"metric": "traced-tensor compare GB/s vs HBM roofline; layer-checks/sec",
+                "value": alg_bytes * world / (ms_step / 1e3) / 1e9, "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (N(0,sigma) per id rounded to bf16; candidate = Q(ref*(1+2^-8 u)))",
+                "config": dict(desc, inputs=f"{(ref.nbytes + cand.nbytes) / 1e9:.1f} GB resident on this GPU "
+                                            "(>> 126 MB L2, no flush)",
+                               algorithmic_bytes_per_step=alg_bytes, ids=n_ids,
+                               parallelism=f"{world} of the job's {share} GPUs live"),
+                "layer_checks_per_s": n_ids * world / (ms_step / 1e3),
+                "build_seconds": build_s, "plan_seconds": plan_s,
+                "share": {"candidate_gb": cand.nbytes / 1e9, "reference_gb": ref.nbytes / 1e9,
+                          "digested_gb": fps.nbytes / 1e9, "compare_gb": seg_bytes / 1e9,
+                          "remote_replica_groups": n_remote, "digest_ms": fp_ms,
+                          "digest_gbs": fps.nbytes / (fp_ms / 1e3) / 1e9},
+                "verdict_counts_partial": {k: int((idres["verdict"] == v).sum()) for k, v in
+                                           (("pass", 0), ("flag", 1), ("replica-mismatch", 2),
+                                            ("merge-error", 3))},
+                "near_ties": ties,
+                "roofline": {"bound": "hbm", "achieved": seg_bytes / (seg_ms / 1e3) / 1e9, "peak": hbm,
+                             "unit": "GB/s", "frac": seg_bytes / (seg_ms / 1e3) / 1e9 / hbm, "traffic": None,
+                             "kernel": "td_segnorm (k_segnorm_vec / k_segnorm_generic)", "kernel_ms": seg_ms,
+                             "peak_source": peak_kind},
+                "cpu_baseline": None, "e2e": None,
+                "gpu_launches": (prep.launches_per_run + 2) * args.steps,
+                "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+    del keep
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm on the CPU (the oracle port;
     the reference is pure Python and /root/reference does not travel to the
@@ -353,6 +484,8 @@ def main():
     from paper_2506_09280_b200.checker import CheckPlan, check
     from paper_2506_09280_b200.device import resolve_operands
     from paper_2506_09280_b200.distributed import allreduce_partials
+    if args.config == "cfg4":
+        return run_share(args, world, rank, local)
     hbm, peak_kind = peaks()
 
     desc, ref, cand, tol, fmt = workload(args.config, rank)

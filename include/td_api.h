@@ -232,10 +232,19 @@ int td_signed_uniforms(double* out, int64_t n, uint64_t seed, int64_t k0,
 int td_quantize(const double* x, void* y, int32_t dtype_out, int64_t n, int32_t fmt,
                 unsigned long long* nonfinite, void* stream);
 
-/* ---- replica digests for multi-GPU replica groups ----
- * out[0..1] += order-independent 128-bit digest of n elements (bit patterns). */
-int td_fingerprint(const void* x, int32_t dtype, int64_t n,
-                   unsigned long long* out, void* stream);
+/* ---- replica digests for multi-GPU replica groups (SURVEY 8(e)) ----
+ * One launch for n_items byte ranges: out[2i], out[2i+1] = order-independent
+ * 128-bit digest of item i's bytes (8-byte words keyed by their index, tail
+ * zero-padded); out is cleared by the call.  chunk_begin (device, n_items+1
+ * int64) is the prefix sum of ceil(nbytes / TD_FP_CHUNK) per item and
+ * n_chunks its last entry.  items and chunk_begin live in device memory. */
+#define TD_FP_CHUNK (1 << 18)
+typedef struct {
+    const void* ptr;
+    int64_t nbytes;
+} td_fp_item;
+int td_fingerprint(const td_fp_item* items, const int64_t* chunk_begin, int32_t n_items,
+                   int64_t n_chunks, unsigned long long* out, void* stream);
 
 /* ---- merge() materialisation: copy a strided box of src into dst (f64) ----
  * boxes: n_boxes rows of {src_off, dst_off, rows, cols, src_stride, dst_stride} int64 */

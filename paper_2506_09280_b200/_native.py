@@ -28,6 +28,8 @@ SLOT_STRIDE = 8
 SEG_HAS_X = 1
 SEG_VEC = 2
 SEG_TILE_SHIFT_POS = 8
+FP_CHUNK = 1 << 18          # bytes per td_fingerprint work chunk (TD_FP_CHUNK)
+FP_ITEM = np.dtype([("ptr", "<u8"), ("nbytes", "<i8")])
 
 SEGMENT = np.dtype([
     ("x", "<u8"), ("y", "<u8"), ("z", "<u8", (MAX_Z,)),
@@ -76,7 +78,7 @@ SIGNATURES = {
                                   _I32, _I32, _P, _P]),
     "td_signed_uniforms": (ctypes.c_int, [_P, _I64, _U64, _I64, _I32, _P]),
     "td_quantize": (ctypes.c_int, [_P, _P, _I32, _I64, _I32, _P, _P]),
-    "td_fingerprint": (ctypes.c_int, [_P, _I32, _I64, _P, _P]),
+    "td_fingerprint": (ctypes.c_int, [_P, _P, _I32, _I64, _P, _P]),
     "td_box_gather": (ctypes.c_int, [_P, _I32, _P, _P, _I32, _P]),
     "td_gather_bytes": (ctypes.c_int, [_P, _P, _P, _I64, _P]),
     "td_generate": (ctypes.c_int, [_P, _I64, _U64, _I32, _D, _D, _I64, _P, _I32, _P, _P, _I32, _P]),

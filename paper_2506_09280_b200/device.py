@@ -49,6 +49,45 @@ def to_device(x, stream=None):
 _TORCH_DTYPES = None
 
 
+class Fingerprints:
+    """128-bit digests of many device tensors in ONE td_fingerprint launch
+    (replica groups whose copies live on different GPUs).
+
+    The item and chunk tables are staged once; run() can be replayed while
+    the tensors stay where they are (the bench times it inside the step).
+    `out` is an (n, 2) int64 CUDA tensor, written on the launching stream."""
+
+    def __init__(self, tensors):
+        import torch
+        self.tensors = [t if t.is_contiguous() else t.contiguous() for t in tensors]
+        for t in self.tensors:
+            if t.device.type != "cuda":
+                raise N.NativeError("Fingerprints: tensors must be CUDA tensors")
+        n = len(self.tensors)
+        items = np.zeros(n, N.FP_ITEM)
+        items["ptr"] = [t.data_ptr() for t in self.tensors]
+        items["nbytes"] = [t.numel() * t.element_size() for t in self.tensors]
+        chunks = -(-items["nbytes"] // N.FP_CHUNK)
+        begin = np.zeros(n + 1, np.int64)
+        np.cumsum(chunks, out=begin[1:])
+        self.n, self.n_chunks = n, int(begin[-1])
+        self.nbytes = int(items["nbytes"].sum())
+        self._items = torch.from_numpy(items.view(np.uint8)).to("cuda")
+        self._begin = torch.from_numpy(begin).to("cuda")
+        self.out = torch.zeros((max(n, 1), 2), dtype=torch.int64, device="cuda")
+
+    def run(self, stream=None):
+        if self.n:
+            N.call("td_fingerprint", self._items.data_ptr(), self._begin.data_ptr(), self.n,
+                   self.n_chunks, self.out.data_ptr(), N.stream_handle(stream))
+        return self.out[:self.n]
+
+
+def fingerprints(tensors):
+    """(n, 2) int64 CUDA tensor of the tensors' byte digests (one launch)."""
+    return Fingerprints(tensors).run()
+
+
 def stage_host_payloads(traces, stream=None) -> dict:
     """Start the H2D copies of every host-resident payload of `traces` and
     return {id(record): CUDA tensor}.  Copies are asynchronous on the current

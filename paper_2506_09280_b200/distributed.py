@@ -10,11 +10,14 @@ SURVEY §8(e).  A canonical id's compare is a sum over disjoint boxes, so:
    reference slice must be local), replica sums fused when a group's copies
    are all on that rank;
 3. replica groups whose copies live on several ranks are decided by 128-bit
-   order-independent fingerprints (td_fingerprint, one int64 all_reduce of
-   a small table): equal fingerprints = identical copies = rel_err 0, so the
-   group's slot stays zero; on a mismatch (the bug path only) the differing
-   copies are sent point-to-point to copy 0's rank, which computes the exact
-   rel_err sums;
+   order-independent digests (td_fingerprint: every local copy in one
+   launch; one int64 all_reduce of a small table): equal digests = identical
+   copies = rel_err 0, so the group's slot stays zero, and the group's
+   compare may read any copy — plan.compare_copies spreads those compares
+   over the holders to balance bytes per GPU; on a mismatch (the bug path
+   only) the differing copies are sent point-to-point to copy 0's rank,
+   which computes the exact rel_err sums, and a compare that read another
+   copy is handed copy 0 instead;
 4. ONE all_reduce(sum, f64) of the per-id / per-group slot vector crosses
    NVLink, then every rank runs td_verdict on identical sums and can render
    the report.
@@ -136,6 +139,34 @@ class ThreadComm(Comm):
         self._sync()
 
 
+class StaticComm(Comm):
+    """A rank of a job whose record metadata is known in advance
+    (synthetic.ShareLayout): all_gather_object answers from the precomputed
+    per-rank lists (one list of lists per call, in call order), reductions
+    and exchanges go to `inner` (the ranks actually running; None = this
+    process alone).  Lets one GPU plan and time its share of an 8-GPU job."""
+
+    def __init__(self, rank: int, world: int, gathers: list, inner: Comm | None = None):
+        self.rank, self.world = rank, world
+        self._gathers = list(gathers)
+        self.inner = inner
+
+    def all_gather_object(self, obj) -> list:
+        out = list(self._gathers.pop(0))
+        out[self.rank] = obj
+        return out
+
+    def all_reduce_sum_(self, tensor) -> None:
+        if self.inner is not None:
+            self.inner.all_reduce_sum_(tensor)
+
+    def exchange(self, sends, recvs) -> None:
+        if self.inner is not None:
+            self.inner.exchange(sends, recvs)
+        elif sends or recvs:
+            raise N.NativeError("StaticComm: point-to-point traffic with ranks that are not running")
+
+
 # ---------------------------------------------------------------------------
 # record metadata that crosses ranks
 
@@ -221,21 +252,13 @@ def allreduce_partials(prep, comm: Comm | None = None) -> None:
         comm.all_reduce_sum_(slots)
 
 
-def _fingerprint(tensor) -> tuple:
-    import torch
-    out = torch.zeros(2, dtype=torch.int64, device=tensor.device)
-    N.call("td_fingerprint", tensor.data_ptr(), N.dtype_code(tensor), tensor.numel(),
-           out.data_ptr(), N.stream_handle())
-    return out
-
-
 class DistributedCheckPlan:
     """check() across ranks; construct and run collectively on every rank."""
 
     def __init__(self, ref, cand, tol, kappa: float = 3.0, *, fmt, comm: Comm, order_key=None):
         from .checker import CheckPlan, _require_same_setup
         from .errors import ConfigInvalid
-        from .plan import Plan, PlanEntry, merge_view
+        from .plan import Plan, PlanEntry, compare_copies, merge_view
         if kappa <= 0:
             raise ConfigInvalid("kappa must be positive")
         _require_same_setup(ref, cand)
@@ -248,7 +271,9 @@ class DistributedCheckPlan:
         self.common = [i for i in self.cand_view if i in self.ref_view]
         self.plan = Plan([PlanEntry(i, x=self.ref_view[i], y=self.cand_view[i], x_rep=True,
                                     y_rep=True, tolerance=tol.get(i)) for i in self.common],
-                         owner=lambda m: m.owner, me=comm.rank)
+                         owner=lambda m: m.owner, me=comm.rank,
+                         compare_copy=compare_copies(self.cand_view, lambda m: m.owner))
+        self._digest = None
         self.mode = str(cand.header.get("mode", ""))
         self._report = CheckPlan.report
 
@@ -258,24 +283,50 @@ class DistributedCheckPlan:
         meta = e.y if side == 0 else e.x
         return meta.groups[gi].records
 
+    def digests(self):
+        """(Fingerprints over this rank's copies of cross-rank replica groups,
+        [(row k of the remote table, copy index)]) — staged once, replayable."""
+        if self._digest is None:
+            from .device import Fingerprints
+            where, tensors = [], []
+            for k, entry in enumerate(self.plan.remote_groups):
+                for c, m in enumerate(self._remote_group_records(entry)):
+                    if m.owner == self.comm.rank:
+                        where.append((k, c))
+                        tensors.append(m.device_payload().reshape(-1))
+            self._digest = (Fingerprints(tensors), where)
+        return self._digest
+
     def _resolve_remote(self):
-        """Fingerprint the locally held copies of cross-rank replica groups,
-        exchange the table, and compute exact sums for mismatching groups on
-        copy 0's rank.  Returns {group slot: 8 sums} for this rank to add."""
+        """Digest the locally held copies of cross-rank replica groups (one
+        td_fingerprint launch), exchange the digest table (one all_reduce),
+        and on a mismatch (bug path only):
+          * copy 0's rank receives the other copies and computes the exact
+            replica sums — returned as {group slot: 8 sums} to add;
+          * when the compare of that group reads a copy other than copy 0
+            (compare_copies) and that copy differs from copy 0, its rank
+            receives copy 0 and the compare reads it instead — returned as
+            {id(record): tensor} operand overrides.
+        Messages are issued in remote-group order on every rank, so each
+        (source, destination) pair sees sends and receives in the same order."""
         import torch
         from .device import _Raw, _one_group, resolve_operands
         from .plan import Plan, PlanEntry
         remote = self.plan.remote_groups
         if not remote:
-            return {}
+            return {}, {}
+        fps, where = self.digests()
         table = torch.zeros((len(remote), N.MAX_Z + 1, 2), dtype=torch.int64, device="cuda")
-        for k, entry in enumerate(remote):
-            for c, m in enumerate(self._remote_group_records(entry)):
-                if m.owner == self.comm.rank:
-                    table[k, c] = _fingerprint(m.device_payload().reshape(-1))
+        if where:
+            got = fps.run()
+            rows = torch.tensor([k for k, _ in where], device="cuda")
+            cols = torch.tensor([c for _, c in where], device="cuda")
+            table[rows, cols] = got
         self.comm.all_reduce_sum_(table)
         fp = table.cpu().numpy()
-        extra = {}
+        compare_copy = {(ei, gi): c for ei, gi, c in self.plan.compare_reads}
+        me = self.comm.rank
+        extra, overrides = {}, {}
         sends, recvs, pending = [], [], []
         for k, entry in enumerate(remote):
             recs = self._remote_group_records(entry)
@@ -283,10 +334,10 @@ class DistributedCheckPlan:
             if not differs:
                 continue
             y0 = recs[0]
-            if y0.owner == self.comm.rank:
+            if y0.owner == me:
                 bufs = []
                 for c, m in enumerate(recs[1:], start=1):
-                    if m.owner == self.comm.rank:
+                    if m.owner == me:
                         bufs.append(m.device_payload().reshape(-1))
                     else:
                         buf = torch.empty(int(np.prod(m.shape)), dtype=_torch_dtype(m.dtype_code),
@@ -296,8 +347,20 @@ class DistributedCheckPlan:
                 pending.append((entry[0], y0, bufs))
             else:
                 for m in recs[1:]:
-                    if m.owner == self.comm.rank:
+                    if m.owner == me:
                         sends.append((y0.owner, m.device_payload().reshape(-1)))
+            _, ei, side, gi = entry
+            cc = compare_copy.get((ei, gi), 0) if side == 0 else 0
+            if cc and cc in differs:
+                holder = recs[cc]
+                if holder.owner == me and y0.owner == me:
+                    overrides[id(holder)] = y0.device_payload()
+                elif holder.owner == me:
+                    buf = torch.empty(tuple(y0.shape), dtype=_torch_dtype(y0.dtype_code), device="cuda")
+                    recvs.append((y0.owner, buf.view(-1)))
+                    overrides[id(holder)] = buf
+                elif y0.owner == me:
+                    sends.append((holder.owner, y0.device_payload().reshape(-1)))
         self.comm.exchange(sends, recvs)
         for slot, y0, bufs in pending:
             raws = [_Raw(y0.device_payload().reshape(-1))] + [_Raw(b) for b in bufs]
@@ -307,13 +370,13 @@ class DistributedCheckPlan:
             sums: dict = {}
             mini.run(ptrs, sums=sums)
             extra[slot] = sums["group"][0]
-        return extra
+        return extra, overrides
 
     def execute(self, timing: dict | None = None):
         import torch
         from .device import resolve_operands
-        extra = self._resolve_remote()
-        ptrs, keep = resolve_operands(self.plan.operands, self.plan.operand_dtypes)
+        extra, overrides = self._resolve_remote()
+        ptrs, keep = resolve_operands(self.plan.operands, self.plan.operand_dtypes, overrides)
         prep = self.plan.prepare(ptrs, kappa=self.kappa, eps=self.fmt.eps,
                                  replica_eps=self.fmt.eps)
         sh = N.stream_handle(prep.stream)
@@ -351,19 +414,21 @@ def check_distributed(ref, cand, tol, kappa: float = 3.0, *, fmt, comm: Comm | N
 
 def split_reference(ref, cand_global, world: int):
     """Per-rank reference traces: each rank gets the reference slices that
-    cover the global boxes of the candidate copy-0 shards it holds (the
-    compare runs there), cut from the reference records it was given.
+    cover the global boxes of the candidate shards whose compare it runs
+    (copy 0, or the copy plan.compare_copies picks for a cross-rank replica
+    group), cut from the reference records it was given.
 
     cand_global: the candidate's global metadata trace (global_trace()), so
     owners are known.  Ids the candidate cannot merge, ids whose hulls
     differ, and reference-only ids keep their records whole on rank 0 (no
     compare runs for them)."""
     from .canonical import ShardMapping, SliceBox
-    from .plan import merge_view
+    from .plan import compare_copies, merge_view
     from .tracestore import RankMeta, Trace, TraceRecord
     out = [Trace(header=ref.header, raw_header=ref.raw_header) for _ in range(world)]
     cview = merge_view(cand_global)
     rview = merge_view(ref)
+    choice = compare_copies(cview, lambda m: m.owner)
     for ident, rmeta in rview.items():
         cmeta = cview.get(ident)
         records = [rec for g in rmeta.groups for rec in g.records]
@@ -372,8 +437,8 @@ def split_reference(ref, cand_global, world: int):
             out[0].records.extend(records)
             continue
         k = 0
-        for g in cmeta.groups:
-            y0 = g.records[0]
+        for gi, g in enumerate(cmeta.groups):
+            y0 = g.records[choice.get((ident, gi), 0)]
             for _, gbox in y0.mapping.pairs:
                 for rg in rmeta.groups:
                     x0 = rg.records[0]

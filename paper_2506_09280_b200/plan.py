@@ -239,6 +239,45 @@ class PlanBuilder:
 # ---------------------------------------------------------------------------
 # plans
 
+def compare_copies(view: dict, owner) -> dict:
+    """Which copy of each cross-rank replica group the representative compare
+    reads (multi-GPU): {(ident, group index): copy index}.
+
+    The reference compares copy 0 of every shard group (checker.py:184-191).
+    When the copies of a replica-checked group live on several ranks they are
+    all digested (td_fingerprint) where they live, and equal digests mean
+    every copy IS copy 0 — so the compare may read whichever copy is least
+    loaded instead of always copy 0's rank (which, for DP-replicated
+    parameters and TP-replicated activations, would pile every compare on the
+    dp=0 / tp=0 GPUs: 1.6x the mean on config 4).  Greedy, largest group
+    first, onto the holder with the fewest bytes to read so far; ties keep
+    the lower copy index.  Deterministic from the global view, so every rank
+    and split_reference agree.  On a digest mismatch (bug path) the compare
+    holder is handed copy 0 (distributed.py) so the result stays exact."""
+    load: dict = {}
+    remote = []
+    for ident, meta in view.items():
+        if meta.rank_problem:
+            continue
+        for gi, g in enumerate(meta.groups):
+            recs = g.records
+            nb = math.prod(recs[0].shape) * N.DTYPE_SIZE[recs[0].dtype_code]
+            owners = [owner(r) for r in recs]
+            for o in owners:
+                load[o] = load.get(o, 0) + nb          # digest / fused replica read
+            if g.numeric and len(set(owners)) > 1:
+                remote.append((nb, ident, gi, owners))
+            else:
+                load[owners[0]] = load.get(owners[0], 0) + nb   # the reference slice
+    remote.sort(key=lambda t: -t[0])
+    out = {}
+    for nb, ident, gi, owners in remote:
+        best = min(range(len(owners)), key=lambda c: (load[owners[c]], c))
+        out[(ident, gi)] = best
+        load[owners[best]] += 2 * nb                   # copy re-read + reference slice
+    return out
+
+
 @dataclass
 class PlanEntry:
     ident: str
@@ -253,7 +292,7 @@ class Plan:
     """Frozen layout of one comparison; `run()` executes it on the GPU."""
 
     def __init__(self, entries: list[PlanEntry], static: tuple[float, float] | None = None,
-                 owner=None, me: int = 0):
+                 owner=None, me: int = 0, compare_copy: dict | None = None):
         """static=(atol, rtol) builds compare_static's plan: the elementwise
         failure count replaces d2 (generic walker, no replica checks).
 
@@ -264,7 +303,10 @@ class Plan:
         candidate's copy 0 (the reference slice must be there too), fused
         replica sums when every copy of the group is on that rank.  Groups
         whose copies span ranks are listed in `remote_groups` and resolved
-        by fingerprints (zero sums = identical copies)."""
+        by fingerprints (zero sums = identical copies).  compare_copy
+        (compare_copies()) picks which copy of such a group the compare
+        reads; `compare_reads` lists (entry, group index, copy index) for
+        the groups where it is not copy 0."""
         self.entries = entries
         self.static = static
         owner = owner if owner is not None else (lambda rec: me)
@@ -274,6 +316,8 @@ class Plan:
         group_rows = []
         self.group_owner = []     # (entry index, side, group index)
         self.remote_groups = []   # (group slot, entry index, side, group index)
+        self.compare_reads = []   # (entry index, group index, copy index != 0)
+        compare_copy = compare_copy or {}
         for ei, e in enumerate(entries):
             t0 = b.tile_cursor
             has_compare = (e.x is not None and e.y is not None and e.x.merge_ok and e.y.merge_ok
@@ -287,10 +331,15 @@ class Plan:
                             f"{e.ident}: replica groups of more than {N.MAX_Z + 1} copies")
                     s0 = b.tile_cursor
                     y0 = g.records[0]
-                    mine = is_local(y0)
-                    together = rep and all(is_local(r) for r in g.records) if mine else False
-                    if rep and len({owner(r) for r in g.records}) > 1:
+                    spans = rep and len({owner(r) for r in g.records}) > 1
+                    if spans:
                         self.remote_groups.append((len(group_rows), ei, 0, gi))
+                        c = compare_copy.get((e.ident, gi), 0)
+                        if c:
+                            y0 = g.records[c]
+                            self.compare_reads.append((ei, gi, c))
+                    mine = is_local(y0)
+                    together = rep and not spans and mine
                     if mine:
                         gdt = _group_dtype(g.records) if together else y0.dtype_code
                         yop = b.operand(y0, gdt)

@@ -142,61 +142,126 @@ def sweep_pair(n_bytes: int, *, maps: str = "identity", g: int = 1, dtype=None, 
     return ref, cand
 
 
+class ShareLayout:
+    """Every GPU's share of a multi-GPU job, as metadata (no payloads).
+
+    Candidate record r lives on owner(r) (default: (dp, tp) -> dp*tp_size +
+    tp, cp ranks after, mod world).  The compare of each candidate shard group
+    runs where the copy plan.compare_copies picks lives (copy 0, or the
+    least-loaded holder of a cross-rank replica group), and that rank also
+    holds the reference slices covering the group's global boxes — what
+    distributed.split_reference hands it.  `records(rank)` is the ordered
+    content of one rank's (reference, candidate) traces, `metas()` the
+    RecordMeta lists every rank would publish, so one process can build the
+    global plan of a job whose other ranks are not present (bench config 4)."""
+
+    def __init__(self, model: ModelShape, pcfg: ParallelConfig, world: int, owner=None,
+                 dtype_code: int = 1):
+        from .canonical import ShardMapping, SliceBox
+        from .distributed import RecordMeta, _MetaTrace
+        from .plan import compare_copies, merge_view
+        self.model, self.pcfg, self.world = model, pcfg, world
+        self.owner = owner or (lambda s: (s.rank[0] * pcfg.tp + s.rank[1] + pcfg.tp * pcfg.dp * s.rank[4]) % world)
+        self.ref_specs = {s.ident: s for s in emit_records(model, ParallelConfig(microbatches=pcfg.microbatches))}
+        self.cand_specs = emit_records(model, pcfg)
+        self.ids: dict = {}                      # ident -> generation index
+        for spec in self.cand_specs:
+            self.ids.setdefault(spec.ident, len(self.ids))
+        # candidate: each rank's records in emission order
+        self.cand = [[] for _ in range(world)]   # [(ident, spec)]
+        metas = []
+        for spec in self.cand_specs:
+            o = self.owner(spec)
+            pos = len(self.cand[o])
+            self.cand[o].append((spec.ident, spec))
+            metas.append(RecordMeta(parse_canonical(spec.ident), RankMeta(*spec.rank), spec.mapping,
+                                    spec.replica, tuple(spec.mapping.local_shape), dtype_code,
+                                    spec.module_class, o, (o, pos)))
+        metas.sort(key=lambda m: m.order)
+        view = merge_view(_MetaTrace({}, metas))
+        choice = compare_copies(view, lambda m: m.owner)
+        # reference slices: for every compared group, its global boxes on the
+        # compare holder, numbered per id across all ranks (distinct rank
+        # metadata per piece, as split_reference does)
+        self.ref = [[] for _ in range(world)]    # [(ident, piece k, ShardMapping, module class)]
+        for ident, meta in view.items():
+            rspec = self.ref_specs.get(ident)
+            if rspec is None or not meta.merge_ok or meta.global_shape != rspec.mapping.global_shape:
+                continue
+            shape = rspec.mapping.global_shape
+            k = 0
+            for gi, g in enumerate(meta.groups):
+                holder = g.records[choice.get((ident, gi), 0)]
+                for _, gbox in holder.mapping.pairs:
+                    ext = gbox.extents
+                    local = SliceBox(tuple((0, e) for e in ext))
+                    self.ref[holder.owner].append(
+                        (ident, k, ShardMapping(ext, shape, ((local, gbox),)), rspec.module_class))
+                    k += 1
+
+    def metas(self, dtype_code: int = 1) -> tuple[list, list]:
+        """(reference metas per rank, candidate metas per rank): what each
+        rank's global_trace() publishes, in its local record order."""
+        from .distributed import RecordMeta
+        ref = [[RecordMeta(parse_canonical(i), RankMeta(0, k, 0, 0, 0, 0), m, 1, tuple(m.local_shape),
+                           dtype_code, mc, r, (r, pos)) for pos, (i, k, m, mc) in enumerate(self.ref[r])]
+               for r in range(self.world)]
+        cand = [[RecordMeta(parse_canonical(i), RankMeta(*s.rank), s.mapping, s.replica,
+                            tuple(s.mapping.local_shape), dtype_code, s.module_class, r, (r, pos))
+                 for pos, (i, s) in enumerate(self.cand[r])] for r in range(self.world)]
+        return ref, cand
+
+    def build(self, rank: int, *, dtype=None, seed: int = 0, eps: float = 2.0 ** -8,
+              header: dict | None = None):
+        """(reference trace, candidate trace) of `rank`, payloads in HBM.
+        Values: as build() — every rank draws an id's logical tensors from
+        the same seed, so shards on different ranks fit together."""
+        import torch
+        dtype = dtype or torch.bfloat16
+        hdr = header or {"digest": f"synthetic-{self.model}-{seed}", "mode": "cascade"}
+        policy = "bf16" if dtype == torch.bfloat16 else "fp32"
+        ref, cand = Trace(header=dict(hdr)), Trace(header=dict(hdr))
+        need = {i for i, _ in self.cand[rank]} | {i for i, *_ in self.ref[rank]}
+        cand_by_id: dict = {}
+        for pos, (ident, spec) in enumerate(self.cand[rank]):
+            cand_by_id.setdefault(ident, []).append(pos)
+        ref_by_id: dict = {}
+        for pos, entry in enumerate(self.ref[rank]):
+            ref_by_id.setdefault(entry[0], []).append(pos)
+        cand_recs = [None] * len(self.cand[rank])
+        ref_recs = [None] * len(self.ref[rank])
+        gen = torch.Generator(device="cuda")
+        for ident in sorted(need, key=self.ids.__getitem__):
+            gen.manual_seed(seed * 1000003 + self.ids[ident])
+            rspec = self.ref_specs.get(ident)
+            shape = rspec.mapping.global_shape if rspec else \
+                self.cand[rank][cand_by_id[ident][0]][1].mapping.global_shape
+            kind = ident.split("|")[2][5:]
+            x = _fill(shape, kind, self.model.vocab, gen, dtype)
+            if ident in cand_by_id:
+                y = x if x.dim() == 0 else apply_perturbation(
+                    x.reshape(-1, shape[-1]) if x.dim() > 1 else x.reshape(1, -1),
+                    "cand|" + ident, PerturbSpec(0, eps), policy=policy).reshape(shape)
+                for pos in cand_by_id[ident]:
+                    s = self.cand[rank][pos][1]
+                    cand_recs[pos] = TraceRecord(parse_canonical(ident), RankMeta(*s.rank), s.mapping,
+                                                 s.replica, _shard(y, s.mapping), s.module_class)
+                del y
+            for pos in ref_by_id.get(ident, ()):
+                _, k, m, mc = self.ref[rank][pos]
+                gbox = m.pairs[0][1]
+                ref_recs[pos] = TraceRecord(parse_canonical(ident), RankMeta(0, k, 0, 0, 0, 0), m, 1,
+                                            x[gbox.as_slices()].contiguous(), mc)
+            del x
+        ref.records, cand.records = ref_recs, cand_recs
+        return ref, cand
+
+
 def build_rank_share(model: ModelShape, pcfg: ParallelConfig, world: int, rank: int, *,
                      owner=None, dtype=None, seed: int = 0, eps: float = 2.0 ** -8,
                      header: dict | None = None):
     """One GPU's share of a multi-GPU job, built without materialising the
-    others': the candidate records `owner(spec) == rank` (default: candidate
-    rank (dp, tp) -> dp*tp_size + tp, mod world) and, from the same logical
-    tensors, the reference slices covering the global boxes of the copy-0
-    shards this rank compares (what distributed.split_reference hands it).
-
-    Returns (ref_local, cand_local, all candidate RecordSpecs, owner function)
-    so a caller can build the global plan (plan.Plan(owner=..., me=rank))."""
-    import torch
-    from .canonical import ShardMapping, SliceBox
-    dtype = dtype or torch.bfloat16
-    owner = owner or (lambda s: (s.rank[0] * pcfg.tp + s.rank[1] + pcfg.tp * pcfg.dp * s.rank[4]) % world)
-    hdr = header or {"digest": f"synthetic-{model}-{seed}", "mode": "cascade"}
-    ref_specs = {s.ident: s for s in emit_records(model, ParallelConfig(microbatches=pcfg.microbatches))}
-    cand_specs = emit_records(model, pcfg)
-    by_id: dict = {}
-    for s in cand_specs:
-        by_id.setdefault(s.ident, []).append(s)
-    policy = "bf16" if dtype == torch.bfloat16 else "fp32"
-    ref, cand = Trace(header=dict(hdr)), Trace(header=dict(hdr))
-    gen = torch.Generator(device="cuda")
-    for n, (ident, specs) in enumerate(by_id.items()):
-        mine = [s for s in specs if owner(s) == rank]
-        # copy 0 of each shard layout = first record with that (local shape, pairs)
-        seen, copy0 = set(), []
-        for s in specs:
-            key = (s.mapping.local_shape, tuple((l.bounds, g.bounds) for l, g in s.mapping.pairs))
-            if key not in seen:
-                seen.add(key)
-                copy0.append(s)
-        compares = [s for s in copy0 if owner(s) == rank]
-        if not mine:
-            continue
-        gen.manual_seed(seed * 1000003 + n)
-        rspec = ref_specs.get(ident)
-        shape = rspec.mapping.global_shape if rspec else specs[0].mapping.global_shape
-        kind = ident.split("|")[2][5:]
-        x = _fill(shape, kind, model.vocab, gen, dtype)
-        y = x if x.dim() == 0 else apply_perturbation(
-            x.reshape(-1, shape[-1]) if x.dim() > 1 else x.reshape(1, -1),
-            "cand|" + ident, PerturbSpec(0, eps), policy=policy).reshape(shape)
-        for s in mine:
-            cand.records.append(TraceRecord(parse_canonical(ident), RankMeta(*s.rank), s.mapping,
-                                            s.replica, _shard(y, s.mapping), s.module_class))
-        if rspec is None:
-            continue
-        for k, s in enumerate(compares):
-            for _, gbox in s.mapping.pairs:
-                ext = gbox.extents
-                local = SliceBox(tuple((0, e) for e in ext))
-                m = ShardMapping(ext, shape, ((local, gbox),))
-                ref.records.append(TraceRecord(parse_canonical(ident), RankMeta(0, len(ref.records), 0, 0, 0, 0),
-                                               m, 1, x[gbox.as_slices()].contiguous(), rspec.module_class))
-        del x, y
-    return ref, cand, cand_specs, owner
+    others' (see ShareLayout).  Returns (ref_local, cand_local, layout)."""
+    layout = ShareLayout(model, pcfg, world, owner)
+    ref, cand = layout.build(rank, dtype=dtype, seed=seed, eps=eps, header=header)
+    return ref, cand, layout

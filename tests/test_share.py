@@ -1,0 +1,163 @@
+"""Per-GPU shares of a multi-GPU check (synthetic.ShareLayout, StaticComm,
+plan.compare_copies) and the batched replica digests (td_fingerprint).
+
+CPU: every rank plans the same global job from metadata alone, the compares
+of cross-GPU replica groups are spread over their holders, and each compare
+holder has its reference slices.  GPU: all shares run as threads on one GPU
+(the whole distributed algorithm, real kernels) and reproduce a single-GPU
+check of the union of the shares — clean, and with a replica corrupted on a
+GPU whose copy a compare reads (digest mismatch -> copy 0 handed over)."""
+
+import json
+import math
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2506_09280_b200 import layout as L
+from paper_2506_09280_b200 import synthetic
+from paper_2506_09280_b200.checker import ToleranceMap
+from paper_2506_09280_b200.distributed import DistributedCheckPlan, StaticComm, ThreadComm, _MetaTrace
+from paper_2506_09280_b200.tensor import FloatFormat
+from paper_2506_09280_b200.tracestore import Trace
+
+SMALL = L.ModelShape(layers=2, d_model=64, n_heads=4, d_ff=128, seq_len=32, vocab=256)
+PCFG = L.ParallelConfig(tp=2, dp=2, microbatches=2)
+WORLD = 4
+
+
+def _tol(layout):
+    return ToleranceMap({i: 2 * FloatFormat.BF16.eps for i in layout.ids}, n_samples=1,
+                        eps_p=FloatFormat.BF16.eps)
+
+
+def test_share_plans_agree_and_balance():
+    lay = synthetic.ShareLayout(SMALL, PCFG, WORLD)
+    ref_metas, cand_metas = lay.metas()
+    plans = []
+    for r in range(WORLD):
+        comm = StaticComm(r, WORLD, [ref_metas, cand_metas])
+        hdr = {"digest": "x", "mode": "cascade"}
+        plans.append(DistributedCheckPlan(_MetaTrace(hdr, ref_metas[r]), _MetaTrace(hdr, cand_metas[r]),
+                                          _tol(lay), fmt=FloatFormat.BF16, comm=comm))
+    first = plans[0]
+    for p in plans[1:]:
+        assert p.common == first.common
+        assert len(p.plan.groups) == len(first.plan.groups)
+        assert p.plan.remote_groups == first.plan.remote_groups
+        assert p.plan.compare_reads == first.plan.compare_reads
+    assert first.plan.remote_groups, "TP/DP replicas must span GPUs in this layout"
+    assert first.plan.compare_reads, "some compares must read a copy other than copy 0"
+    reads = [p.plan.algorithmic_bytes + sum(math.prod(m.shape) * 2 for m in cand_metas[r]
+                                            if any(m is x for e in p.plan.remote_groups
+                                                   for x in p._remote_group_records(e)))
+             for r, p in enumerate(plans)]
+    assert max(reads) / (sum(reads) / len(reads)) < 1.25, reads
+
+
+def test_compare_copies_is_copy0_on_one_rank():
+    from paper_2506_09280_b200.plan import compare_copies, merge_view
+    lay = synthetic.ShareLayout(SMALL, PCFG, WORLD)
+    _, cand_metas = lay.metas()
+    allm = sorted([m for ms in cand_metas for m in ms], key=lambda m: m.order)
+    view = merge_view(_MetaTrace({}, allm))
+    assert compare_copies(view, lambda m: 0) == {}
+    choice = compare_copies(view, lambda m: m.owner)
+    assert choice and any(c > 0 for c in choice.values())
+    for (ident, gi), c in choice.items():
+        assert 0 <= c < len(view[ident].groups[gi].records)
+
+
+def _run_threads(world, body):
+    hub = ThreadComm.hub(world)
+    out, errors = [None] * world, []
+
+    def worker(rank):
+        try:
+            out[rank] = body(rank, ThreadComm(hub, rank))
+        except Exception as exc:  # pragma: no cover - surfaced below
+            import traceback
+            errors.append(traceback.format_exc())
+            hub.barrier.abort()
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not errors, errors[0]
+    return out
+
+
+def _union(shares, header):
+    ref, cand = Trace(header=dict(header)), Trace(header=dict(header))
+    for r, c in shares:
+        ref.records.extend(r.records)
+        cand.records.extend(c.records)
+    return ref, cand
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("corrupt", [False, True])
+def test_shares_as_threads_match_single_gpu_check(corrupt):
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200.checker import check
+    lay = synthetic.ShareLayout(SMALL, PCFG, WORLD)
+    shares = [lay.build(r) for r in range(WORLD)]
+    tol = _tol(lay)
+    ref_metas, cand_metas = lay.metas()
+    if corrupt:
+        # a replica copy that some compare reads instead of copy 0
+        comm = StaticComm(0, WORLD, [ref_metas, cand_metas])
+        probe = DistributedCheckPlan(_MetaTrace({"digest": "x", "mode": "cascade"}, ref_metas[0]),
+                                     _MetaTrace({"digest": "x", "mode": "cascade"}, cand_metas[0]),
+                                     tol, fmt=FloatFormat.BF16, comm=comm)
+        ei, gi, c = probe.plan.compare_reads[0]
+        meta = probe.plan.entries[ei].y.groups[gi].records[c]
+        pos = meta.order[1]
+        rec = shares[meta.owner][1].records[pos]
+        assert rec.id.encode() == meta.id.encode()
+        rec.payload.mul_(2)
+
+    def body(rank, comm):
+        ref, cand = shares[rank]
+        plan = DistributedCheckPlan(ref, cand, tol, fmt=FloatFormat.BF16, comm=comm)
+        return json.loads(td.render_report(plan.run(), "json"))
+    reports = _run_threads(WORLD, body)
+    ref_all, cand_all = _union(shares, shares[0][0].header)
+    want = json.loads(td.render_report(check(ref_all, cand_all, tol, fmt=FloatFormat.BF16), "json"))
+    from tests.test_gpu_parity import assert_reports_match
+    for rep in reports:
+        assert_reports_match(rep, want, f"corrupt={corrupt}")
+    if corrupt:
+        assert want["summary"]["replica-mismatch"] == 1
+    else:
+        assert want["summary"]["pass"] == len(want["entries"])
+
+
+@pytest.mark.gpu
+def test_fingerprint_digests():
+    from paper_2506_09280_b200.device import Fingerprints, fingerprints
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randn(1 << 20, device="cuda", generator=g).to(torch.bfloat16)
+    b = a.clone()
+    c = a.clone()
+    c.view(torch.int16)[12345] ^= 1                      # one bit
+    d = torch.cat([a[1 << 19:], a[:1 << 19]])            # halves swapped (same multiset)
+    e = a.view(torch.uint8)[3:3 + 1000003]               # unaligned, odd length
+    f = e.clone()
+    z = a[:0]
+    out = fingerprints([a, b, c, d, e, f, z]).cpu().numpy()
+    assert np.array_equal(out[0], out[1])
+    assert not np.array_equal(out[0], out[2])
+    assert not np.array_equal(out[0], out[3])
+    assert np.array_equal(out[4], out[5])                # aligned copy == unaligned view
+    assert np.array_equal(out[6], [0, 0])
+    # one launch over many items == item by item; replays are deterministic
+    parts = [a[k * 1000:(k + 1) * 1000 + 7] for k in range(50)]
+    fp = Fingerprints(parts)
+    many = fp.run().cpu().numpy()
+    again = fp.run().cpu().numpy()
+    one = np.stack([fingerprints([p]).cpu().numpy()[0] for p in parts])
+    assert np.array_equal(many, one) and np.array_equal(many, again)
