@@ -327,33 +327,35 @@ def run_share(args, world: int, rank: int, local: int):
     t0 = time.perf_counter()
     dcp = DistributedCheckPlan(ref, cand, tol, 3.0, fmt=fmt, comm=comm)
     plan_s = time.perf_counter() - t0
+    digests, fps, where, n_fused = dcp.digests()
     ptrs, keep = resolve_operands(dcp.plan.operands, dcp.plan.operand_dtypes)
-    prep = dcp.plan.prepare(ptrs, kappa=3.0, eps=fmt.eps, replica_eps=fmt.eps)
-    fps, where = dcp.digests()
+    prep = dcp.plan.prepare(ptrs, kappa=3.0, eps=fmt.eps, replica_eps=fmt.eps, digests=digests.data_ptr())
     n_remote = len(dcp.plan.remote_groups)
     table = torch.zeros((max(n_remote, 1), N.MAX_Z + 1, 2), dtype=torch.int64, device="cuda")
     rows = torch.tensor([k for k, _ in where], dtype=torch.int64, device="cuda")
     cols = torch.tensor([c for _, c in where], dtype=torch.int64, device="cuda")
     stream = prep.stream
-    alg_bytes = dcp.plan.algorithmic_bytes + fps.nbytes
+    # every byte this GPU holds, read once: its candidate
+    # records (digested or compared) and the reference slices it compares
+    alg_bytes = ref.nbytes + cand.nbytes
 
     def step(seg_events=None):
         sh = N.stream_handle(stream)
         with torch.cuda.stream(stream):
             if seg_events is not None:
                 seg_events[0].record(stream)
+            digests.zero_()
             fps.run(stream)
             if seg_events is not None:
                 seg_events[1].record(stream)
-            if where:
-                table[rows, cols] = fps.out[:fps.n]
-            if world > 1:
-                dist.all_reduce(table)
-            if seg_events is not None:
                 seg_events[2].record(stream)
-            prep.segnorm(sh)
+            prep.segnorm(sh)              # compares; fills the fused digest slots
             if seg_events is not None:
                 seg_events[3].record(stream)
+            if where:
+                table[rows, cols] = digests[:len(where)]
+            if world > 1:
+                dist.all_reduce(table)
             prep.reduce(sh)
             if world > 1:
                 allreduce_partials(prep)
@@ -396,7 +398,9 @@ def run_share(args, world: int, rank: int, local: int):
                 "build_seconds": build_s, "plan_seconds": plan_s,
                 "share": {"candidate_gb": cand.nbytes / 1e9, "reference_gb": ref.nbytes / 1e9,
                           "digested_gb": fps.nbytes / 1e9, "compare_gb": seg_bytes / 1e9,
-                          "remote_replica_groups": n_remote, "digest_ms": fp_ms,
+                          "bytes_read_gb": (fps.nbytes + seg_bytes) / 1e9,
+                          "remote_replica_groups": n_remote, "digests_fused_in_compare": n_fused,
+                          "digest_ms": fp_ms,
                           "digest_gbs": fps.nbytes / (fp_ms / 1e3) / 1e9},
                 "verdict_counts_partial": {k: int((idres["verdict"] == v).sum()) for k, v in
                                            (("pass", 0), ("flag", 1), ("replica-mismatch", 2),
@@ -407,7 +411,7 @@ def run_share(args, world: int, rank: int, local: int):
                              "kernel": "td_segnorm (k_segnorm_vec / k_segnorm_generic)", "kernel_ms": seg_ms,
                              "peak_source": peak_kind},
                 "cpu_baseline": None, "e2e": None,
-                "gpu_launches": (prep.launches_per_run + 2) * args.steps,
+                "gpu_launches": (prep.launches_per_run + 3) * args.steps,
                 "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
     del keep

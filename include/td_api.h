@@ -93,7 +93,10 @@ typedef struct td_segment {
     uint32_t flags;
     uint32_t div_m;             /* magic divisor for units-per-row: q = (n*div_m) >> div_p */
     int32_t  div_p;
-} td_segment;
+    int64_t  y_word0;           /* 8-byte word index of y's first element in its record (digests) */
+    int32_t  digest_slot;       /* >= 0: also digest y's bytes into digests[2*slot..] (td_class.digests) */
+    int32_t  pad;
+} td_segment;                   /* 160 bytes */
 
 /* per canonical id: where its partial sums live and what the host already knows */
 typedef struct td_id_desc {
@@ -149,10 +152,13 @@ typedef struct td_class {
     int32_t has_x;
     int32_t vec;
     int32_t mode;               /* TD_MODE_NORMS, or TD_MODE_STATIC (generic walker only) */
-    int32_t pad;
+    int32_t digest;             /* vector classes: segments carry digest slots (same hash as
+                                   td_fingerprint, so a record covered exactly once by its
+                                   segments gets the digest td_fingerprint would give it) */
     double  atol;               /* static mode: count |y - x| > atol + rtol*|x| into d2 */
     double  rtol;
-} td_class;                     /* 56 bytes */
+    unsigned long long* digests; /* device, 2 u64 per digest slot, accumulated (caller zeroes) */
+} td_class;                     /* 64 bytes */
 
 #define TD_MODE_NORMS 0
 #define TD_MODE_STATIC 1        /* compare_static's elementwise test (checker.py:403-443) */
@@ -233,9 +239,9 @@ int td_quantize(const double* x, void* y, int32_t dtype_out, int64_t n, int32_t 
                 unsigned long long* nonfinite, void* stream);
 
 /* ---- replica digests for multi-GPU replica groups ----
- * One launch for n_items byte ranges: out[2i], out[2i+1] = order-independent
+ * One launch for n_items byte ranges: out[2i], out[2i+1] += order-independent
  * 128-bit digest of item i's bytes (8-byte words keyed by their index, tail
- * zero-padded); out is cleared by the call.  chunk_begin (device, n_items+1
+ * zero-padded); the caller zeroes out first.  chunk_begin (device, n_items+1
  * int64) is the prefix sum of ceil(nbytes / TD_FP_CHUNK) per item and
  * n_chunks its last entry.  items and chunk_begin live in device memory. */
 #define TD_FP_CHUNK (1 << 18)

@@ -37,6 +37,7 @@ SEGMENT = np.dtype([
     ("tile_begin", "<i8"), ("n_units", "<i8"),
     ("x_dtype", "<i4"), ("y_dtype", "<i4"), ("nz", "<i4"), ("flags", "<u4"),
     ("div_m", "<u4"), ("div_p", "<i4"),
+    ("y_word0", "<i8"), ("digest_slot", "<i4"), ("pad", "<i4"),
 ])
 ID_DESC = np.dtype([
     ("tile_begin", "<i8"), ("tile_end", "<i8"),
@@ -52,12 +53,12 @@ GROUP_RESULT = np.dtype([("worst", "<f8"), ("worst_index", "<i4"), ("mismatch", 
 CHUNK = np.dtype([("row_begin", "<i8"), ("row_end", "<i8"), ("k0", "<i4"), ("nk", "<i4")])
 assert CHUNK.itemsize == 24
 CLASS = np.dtype([("tiles", "<u8"), ("n_tiles", "<i8"), ("dtype", "<i4"), ("nz", "<i4"),
-                  ("has_x", "<i4"), ("vec", "<i4"), ("mode", "<i4"), ("pad", "<i4"),
-                  ("atol", "<f8"), ("rtol", "<f8")])
+                  ("has_x", "<i4"), ("vec", "<i4"), ("mode", "<i4"), ("digest", "<i4"),
+                  ("atol", "<f8"), ("rtol", "<f8"), ("digests", "<u8")])
 MODE_NORMS, MODE_STATIC = 0, 1
 
-assert SEGMENT.itemsize == 144 and ID_DESC.itemsize == 56 and GROUP_DESC.itemsize == 24
-assert ID_RESULT.itemsize == 32 and GROUP_RESULT.itemsize == 16 and CLASS.itemsize == 56
+assert SEGMENT.itemsize == 160 and ID_DESC.itemsize == 56 and GROUP_DESC.itemsize == 24
+assert ID_RESULT.itemsize == 32 and GROUP_RESULT.itemsize == 16 and CLASS.itemsize == 64
 
 # every function the header declares, with its ctypes signature
 _P = ctypes.c_void_p

@@ -113,6 +113,21 @@ __device__ __forceinline__ double load_elem(const char* base, int dt, int64_t id
     }
 }
 
+constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t MIX1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t MIX2 = 0x94D049BB133111EBull;
+
+// one 8-byte word w at word index j into a 128-bit digest (see k_fingerprint)
+__device__ __forceinline__ void fp_word(uint64_t w, uint64_t j, uint64_t& h0, uint64_t& h1) {
+    uint64_t z = w ^ ((j + 1) * GAMMA);
+    z *= MIX1;
+    z ^= z >> 32;
+    z *= MIX2;
+    z ^= z >> 32;
+    h0 += z;
+    h1 += z * z;
+}
+
 #ifndef TD_REPLICA_SKIP
 #define TD_REPLICA_SKIP 1
 #endif
@@ -206,10 +221,14 @@ __device__ __forceinline__ void write_warp_partial(const Acc& a, int used, doubl
 }
 
 // vector class: every operand has dtype DT, rows 16-byte aligned, cols % 8 == 0
-template <int DT, int NZ, bool HX, int U, int MINB>
+// DG: also digest y's bytes into digests[slot] (multi-GPU: the compare copy
+// of a cross-GPU replica group is digested in the pass that compares it, so
+// it is read once; the planner guarantees such a record's segments cover it
+// exactly once, so the sum equals td_fingerprint's digest of the record).
+template <int DT, int NZ, bool HX, int U, int MINB, bool DG = false>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ tiles, int64_t n,
-              double* __restrict__ partials) {
+              double* __restrict__ partials, unsigned long long* __restrict__ digests) {
     constexpr int Q = Vec<DT>::Q;
     constexpr int ES = (DT == TD_F32) ? 4 : 2;
     constexpr int USED = NZ > 0 ? 3 + NZ : 2;
@@ -230,6 +249,8 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
         const uint32_t u1 = (uint32_t)min(first + tu, __ldg(&g->n_units));
         Acc a;
         a.zero();
+        uint64_t h0 = 0, h1 = 0;
+        const int64_t w0 = DG ? __ldg(&g->y_word0) : 0;
         for (uint32_t base = u0 + threadIdx.x; base < u1; base += BLOCK * U) {
             uint4 xr[U][Q];
             uint4 yr[U][Q];
@@ -249,6 +270,21 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
                         yr[k][q] = ld_stream(S.y + yo + 16 * q);
 #pragma unroll
                         for (int j = 0; j < NZ; ++j) zr[j][k][q] = ld_stream(S.z[j] + yo + 16 * q);
+                    }
+                }
+            }
+            if constexpr (DG) {
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    if (!ok[k]) continue;
+                    const uint32_t u = base + k * BLOCK;
+                    const uint32_t row = udiv(u, S.div_m, S.div_p);
+                    const uint32_t cv = u - row * vpr;
+                    const uint64_t j = (uint64_t)(w0 + (((int64_t)row * S.ys + (int64_t)cv * 8) * ES >> 3));
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        fp_word(((uint64_t)yr[k][q].y << 32) | yr[k][q].x, j + 2 * q, h0, h1);
+                        fp_word(((uint64_t)yr[k][q].w << 32) | yr[k][q].z, j + 2 * q + 1, h0, h1);
                     }
                 }
             }
@@ -293,6 +329,18 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
             }
         }
         write_warp_partial(a, USED, partials + (t * TD_WARPS_PER_TILE + warp) * TD_PARTIAL_STRIDE);
+        if constexpr (DG) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                h0 += __shfl_xor_sync(0xffffffffu, h0, o);
+                h1 += __shfl_xor_sync(0xffffffffu, h1, o);
+            }
+            const int slot = __ldg(&g->digest_slot);
+            if ((threadIdx.x & 31) == 0 && slot >= 0) {
+                atomicAdd(digests + 2 * slot, (unsigned long long)h0);
+                atomicAdd(digests + 2 * slot + 1, (unsigned long long)h1);
+            }
+        }
     }
 }
 
@@ -353,15 +401,15 @@ k_segnorm_generic(const td_segment* __restrict__ segs, const int64_t* __restrict
     }
 }
 
-typedef void (*segnorm_fn)(const td_segment*, const int64_t*, int64_t, double*);
+typedef void (*segnorm_fn)(const td_segment*, const int64_t*, int64_t, double*, unsigned long long*);
 
-static_assert(sizeof(td_segment) == 144, "td_segment layout");
+static_assert(sizeof(td_segment) == 160, "td_segment layout");
 static_assert(BLOCK / 32 == TD_WARPS_PER_TILE, "one partial row per warp of a tile");
 static_assert(sizeof(td_id_desc) == 56, "td_id_desc layout");
 static_assert(sizeof(td_group_desc) == 24, "td_group_desc layout");
 static_assert(sizeof(td_id_result) == 32, "td_id_result layout");
 static_assert(sizeof(td_group_result) == 16, "td_group_result layout");
-static_assert(sizeof(td_class) == 56, "td_class layout");
+static_assert(sizeof(td_class) == 64, "td_class layout");
 static_assert(sizeof(td_chunk) == 24, "td_chunk layout");
 
 #ifndef TD_NZ7_U
@@ -385,11 +433,21 @@ static_assert(sizeof(td_chunk) == 24, "td_chunk layout");
 
 // U keeps ~4-8 16-byte loads in flight per thread; wide replica classes trade
 // occupancy (2 CTAs/SM, 128 registers) for no spills.
+#ifndef TD_DG_U
+#define TD_DG_U 2
+#endif
+#ifndef TD_DG_MINB
+#define TD_DG_MINB 4
+#endif
 template <int DT>
-segnorm_fn pick_vec(int nz, bool hx) {
+segnorm_fn pick_vec(int nz, bool hx, bool dg) {
     constexpr int Q = Vec<DT>::Q;
     constexpr int U4 = 4 / Q > 0 ? 4 / Q : 1;
     constexpr int U2 = 2 / Q > 0 ? 2 / Q : 1;
+    if (dg)   // compares of cross-GPU replica groups: copy 0 alone (nz = 0)
+        return (hx && nz == 0)
+                   ? k_segnorm_vec<DT, 0, true, (TD_DG_U / Q > 0 ? TD_DG_U / Q : 1), TD_DG_MINB, true>
+                   : nullptr;
     if (hx) {
         switch (nz) {
             case 0: return k_segnorm_vec<DT, 0, true, (TD_NZ0_U / Q > 0 ? TD_NZ0_U / Q : 1), TD_NZ0_MINB>;
@@ -634,9 +692,6 @@ k_reduce_chunks(const double* __restrict__ partials, const td_chunk* __restrict_
 // ---------------------------------------------------------------------------
 // RNG streams
 
-constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ull;
-constexpr uint64_t MIX1 = 0xBF58476D1CE4E5B9ull;
-constexpr uint64_t MIX2 = 0x94D049BB133111EBull;
 
 // word k (0-based) of the splitmix64 stream: mix(seed + (k+1)*gamma)  (generation.py:67-78)
 __device__ __forceinline__ uint64_t splitmix_word(uint64_t seed, uint64_t k) {
@@ -923,15 +978,6 @@ __global__ void k_quantize(const double* __restrict__ x, char* __restrict__ y, i
 // 4 vectors in flight per thread; warp sums are added atomically (wrapping
 // u64 adds commute: the digest does not depend on the order).  ~8 ALU ops per
 // 8 bytes: HBM-bound, unlike the per-element mix of the first version.
-__device__ __forceinline__ void fp_word(uint64_t w, uint64_t j, uint64_t& h0, uint64_t& h1) {
-    uint64_t z = w ^ ((j + 1) * GAMMA);
-    z *= MIX1;
-    z ^= z >> 32;
-    z *= MIX2;
-    z ^= z >> 32;
-    h0 += z;
-    h1 += z * z;
-}
 
 __global__ void __launch_bounds__(BLOCK)
 k_fingerprint(const td_fp_item* __restrict__ items, const int64_t* __restrict__ chunk_begin, int n_items,
@@ -1174,6 +1220,7 @@ int td_segnorm(const td_segment* segs, const td_class* classes, int32_t n_classe
         int64_t grid = (int64_t)sms * per_sm;
         if (grid > C.n_tiles) grid = C.n_tiles;
         if (!C.vec || C.mode != TD_MODE_NORMS) {
+            if (C.digest) return fail("td_segnorm: digests need a vector class (class %d)", c);
             k_segnorm_generic<<<(unsigned)grid, BLOCK, 0, st>>>(
                 segs, C.tiles, C.n_tiles, partials, C.mode, C.atol, C.rtol);
             if (int rc = check_launch("td_segnorm")) return rc;
@@ -1183,15 +1230,16 @@ int td_segnorm(const td_segment* segs, const td_class* classes, int32_t n_classe
         segnorm_fn fn = nullptr;
         {
             switch (C.dtype) {
-                case TD_BF16: fn = pick_vec<TD_BF16>(C.nz, C.has_x != 0); break;
-                case TD_F16: fn = pick_vec<TD_F16>(C.nz, C.has_x != 0); break;
-                case TD_F32: fn = pick_vec<TD_F32>(C.nz, C.has_x != 0); break;
+                case TD_BF16: fn = pick_vec<TD_BF16>(C.nz, C.has_x != 0, C.digest != 0); break;
+                case TD_F16: fn = pick_vec<TD_F16>(C.nz, C.has_x != 0, C.digest != 0); break;
+                case TD_F32: fn = pick_vec<TD_F32>(C.nz, C.has_x != 0, C.digest != 0); break;
                 default: break;
             }
-            if (!fn) return fail("td_segnorm: no vector walker for class %d (dtype=%d nz=%d has_x=%d)", c,
-                                 C.dtype, C.nz, C.has_x);
+            if (!fn) return fail("td_segnorm: no vector walker for class %d (dtype=%d nz=%d has_x=%d digest=%d)",
+                                 c, C.dtype, C.nz, C.has_x, C.digest);
         }
-        fn<<<(unsigned)grid, BLOCK, 0, st>>>(segs, C.tiles, C.n_tiles, partials);
+        if (C.digest && !C.digests) return fail("td_segnorm: digest class %d without a digest table", c);
+        fn<<<(unsigned)grid, BLOCK, 0, st>>>(segs, C.tiles, C.n_tiles, partials, C.digests);
         if (int rc = check_launch("td_segnorm")) return rc;
         if (st != main_stream) join_aux(aux, k - 1, main_stream);
     }

@@ -57,7 +57,7 @@ class Fingerprints:
     the tensors stay where they are (the bench times it inside the step).
     `out` is an (n, 2) int64 CUDA tensor, written on the launching stream."""
 
-    def __init__(self, tensors):
+    def __init__(self, tensors, out=None):
         import torch
         self.tensors = [t if t.is_contiguous() else t.contiguous() for t in tensors]
         for t in self.tensors:
@@ -74,10 +74,18 @@ class Fingerprints:
         self.nbytes = int(items["nbytes"].sum())
         self._items = torch.from_numpy(items.view(np.uint8)).to("cuda")
         self._begin = torch.from_numpy(begin).to("cuda")
-        self.out = torch.zeros((max(n, 1), 2), dtype=torch.int64, device="cuda")
+        # out: (n, 2) int64 digests, accumulated — run() zeroes its own table,
+        # a caller-provided one (a slice of a larger digest table) is zeroed
+        # by the caller
+        self._own = out is None
+        self.out = torch.zeros((max(n, 1), 2), dtype=torch.int64, device="cuda") if out is None else out
 
     def run(self, stream=None):
+        import torch
         if self.n:
+            if self._own:
+                with torch.cuda.stream(stream or torch.cuda.current_stream()):
+                    self.out.zero_()
             N.call("td_fingerprint", self._items.data_ptr(), self._begin.data_ptr(), self.n,
                    self.n_chunks, self.out.data_ptr(), N.stream_handle(stream))
         return self.out[:self.n]

@@ -272,7 +272,7 @@ class DistributedCheckPlan:
         self.plan = Plan([PlanEntry(i, x=self.ref_view[i], y=self.cand_view[i], x_rep=True,
                                     y_rep=True, tolerance=tol.get(i)) for i in self.common],
                          owner=lambda m: m.owner, me=comm.rank,
-                         compare_copy=compare_copies(self.cand_view, lambda m: m.owner))
+                         compare_copy=compare_copies(self.cand_view, lambda m: m.owner), digest=True)
         self._digest = None
         self.mode = str(cand.header.get("mode", ""))
         self._report = CheckPlan.report
@@ -284,29 +284,37 @@ class DistributedCheckPlan:
         return meta.groups[gi].records
 
     def digests(self):
-        """(Fingerprints over this rank's copies of cross-rank replica groups,
-        [(row k of the remote table, copy index)]) — staged once, replayable."""
+        """(table, Fingerprints, where, F): the digest table of this rank's
+        copies of cross-rank replica groups.  Rows [0, F) are the digest
+        slots td_segnorm fills while comparing (plan.fused_digests), rows
+        [F, ...) the other local copies, digested by one td_fingerprint
+        launch; where[row] = (remote group index, copy index).  Staged once;
+        zero the table before each run."""
         if self._digest is None:
+            import torch
             from .device import Fingerprints
-            where, tensors = [], []
+            fused = list(self.plan.fused_digests)
+            done = set(fused)
+            where, tensors = list(fused), []
             for k, entry in enumerate(self.plan.remote_groups):
                 for c, m in enumerate(self._remote_group_records(entry)):
-                    if m.owner == self.comm.rank:
+                    if m.owner == self.comm.rank and (k, c) not in done:
                         where.append((k, c))
                         tensors.append(m.device_payload().reshape(-1))
-            self._digest = (Fingerprints(tensors), where)
+            table = torch.zeros((max(len(where), 1), 2), dtype=torch.int64, device="cuda")
+            fps = Fingerprints(tensors, out=table[len(fused):])
+            self._digest = (table, fps, where, len(fused))
         return self._digest
 
-    def _resolve_remote(self):
-        """Digest the locally held copies of cross-rank replica groups (one
-        td_fingerprint launch), exchange the digest table (one all_reduce),
-        and on a mismatch (bug path only):
+    def _resolve_remote(self, table, where):
+        """Exchange the digests (one all_reduce of a small table) and, on a
+        mismatch (bug path only):
           * copy 0's rank receives the other copies and computes the exact
             replica sums — returned as {group slot: 8 sums} to add;
           * when the compare of that group reads a copy other than copy 0
             (compare_copies) and that copy differs from copy 0, its rank
-            receives copy 0 and the compare reads it instead — returned as
-            {id(record): tensor} operand overrides.
+            receives copy 0 and the compare must be re-run reading it —
+            returned as {id(record): tensor} operand overrides.
         Messages are issued in remote-group order on every rank, so each
         (source, destination) pair sees sends and receives in the same order."""
         import torch
@@ -315,15 +323,13 @@ class DistributedCheckPlan:
         remote = self.plan.remote_groups
         if not remote:
             return {}, {}
-        fps, where = self.digests()
-        table = torch.zeros((len(remote), N.MAX_Z + 1, 2), dtype=torch.int64, device="cuda")
+        full = torch.zeros((len(remote), N.MAX_Z + 1, 2), dtype=torch.int64, device="cuda")
         if where:
-            got = fps.run()
             rows = torch.tensor([k for k, _ in where], device="cuda")
             cols = torch.tensor([c for _, c in where], device="cuda")
-            table[rows, cols] = got
-        self.comm.all_reduce_sum_(table)
-        fp = table.cpu().numpy()
+            full[rows, cols] = table[:len(where)]
+        self.comm.all_reduce_sum_(full)
+        fp = full.cpu().numpy()
         compare_copy = {(ei, gi): c for ei, gi, c in self.plan.compare_reads}
         me = self.comm.rank
         extra, overrides = {}, {}
@@ -373,14 +379,29 @@ class DistributedCheckPlan:
         return extra, overrides
 
     def execute(self, timing: dict | None = None):
+        """Digests of the local copies of cross-rank groups (td_fingerprint +
+        the digest slots of the compare pass), td_segnorm, the digest
+        exchange, then — only when a compare read a copy that differs from
+        copy 0 — the compare pass again reading copy 0, slot reduction, the
+        partial-sum all_reduce and the verdicts."""
         import torch
         from .device import resolve_operands
-        extra, overrides = self._resolve_remote()
-        ptrs, keep = resolve_operands(self.plan.operands, self.plan.operand_dtypes, overrides)
+        table, fps, where, _ = self.digests()
+        ptrs, keep = resolve_operands(self.plan.operands, self.plan.operand_dtypes)
         prep = self.plan.prepare(ptrs, kappa=self.kappa, eps=self.fmt.eps,
-                                 replica_eps=self.fmt.eps)
+                                 replica_eps=self.fmt.eps, digests=table.data_ptr())
         sh = N.stream_handle(prep.stream)
+        with torch.cuda.stream(prep.stream):
+            table.zero_()
+        fps.run(prep.stream)
         prep.segnorm(sh)
+        extra, overrides = self._resolve_remote(table, where)
+        if overrides:
+            ptrs, keep2 = resolve_operands(self.plan.operands, self.plan.operand_dtypes, overrides)
+            prep = self.plan.prepare(ptrs, kappa=self.kappa, eps=self.fmt.eps,
+                                     replica_eps=self.fmt.eps, digests=table.data_ptr())
+            sh = N.stream_handle(prep.stream)
+            prep.segnorm(sh)
         prep.reduce(sh)
         if extra:
             gsum = prep.slot_sums[2 * prep.n_ids:].view(-1, N.SLOT_STRIDE)

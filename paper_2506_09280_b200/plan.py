@@ -176,8 +176,10 @@ class PlanBuilder:
         self.operands: list = []          # payload owners (records or raw tensors)
         self.operand_dtypes: list = []    # dtype each operand is read as
         self._operand_index: dict = {}
-        self.seg_rows: list = []          # (xs, xoff, ys, yoff, zs, rows, cols, rx, ry, tile_begin, n_units, vec_ok)
+        self.seg_rows: list = []          # (xs, xoff, ys, yoff, zs, rows, cols, rx, ry, tile_begin, n_units, vec_ok,
+        #                                    digest slot or -1)
         self.n_tiles = 0
+        self.digest_slot = -1             # stamped on segments emitted while >= 0
         self.classes: dict = {}           # class key -> list of (tile_begin, n_tiles)
 
     def operand(self, owner, dtype: int) -> _Operand:
@@ -228,7 +230,7 @@ class PlanBuilder:
         n_units = rows * cols // unit
         n_tiles = -(-n_units // N.TILE_UNITS)
         self.seg_rows.append((x, x_off, y, y_off, list(zs), rows, cols, rx, ry,
-                              self.n_tiles, n_units, vec))
+                              self.n_tiles, n_units, vec, self.digest_slot))
         self.n_tiles += n_tiles
 
     @property
@@ -292,7 +294,7 @@ class Plan:
     """Frozen layout of one comparison; `run()` executes it on the GPU."""
 
     def __init__(self, entries: list[PlanEntry], static: tuple[float, float] | None = None,
-                 owner=None, me: int = 0, compare_copy: dict | None = None):
+                 owner=None, me: int = 0, compare_copy: dict | None = None, digest: bool = False):
         """static=(atol, rtol) builds compare_static's plan: the elementwise
         failure count replaces d2 (generic walker, no replica checks).
 
@@ -306,7 +308,11 @@ class Plan:
         by fingerprints (zero sums = identical copies).  compare_copy
         (compare_copies()) picks which copy of such a group the compare
         reads; `compare_reads` lists (entry, group index, copy index) for
-        the groups where it is not copy 0."""
+        the groups where it is not copy 0.  digest=True digests the copy a
+        local compare of a cross-rank group reads inside that compare
+        (td_segnorm digest classes) when its segments cover the record
+        exactly once; `fused_digests` lists (remote group index, copy index)
+        per digest slot, the other local copies still need td_fingerprint."""
         self.entries = entries
         self.static = static
         owner = owner if owner is not None else (lambda rec: me)
@@ -317,6 +323,7 @@ class Plan:
         self.group_owner = []     # (entry index, side, group index)
         self.remote_groups = []   # (group slot, entry index, side, group index)
         self.compare_reads = []   # (entry index, group index, copy index != 0)
+        self.fused_digests = []   # digest slot -> (remote group index, copy index)
         compare_copy = compare_copy or {}
         for ei, e in enumerate(entries):
             t0 = b.tile_cursor
@@ -332,6 +339,7 @@ class Plan:
                     s0 = b.tile_cursor
                     y0 = g.records[0]
                     spans = rep and len({owner(r) for r in g.records}) > 1
+                    c = 0
                     if spans:
                         self.remote_groups.append((len(group_rows), ei, 0, gi))
                         c = compare_copy.get((e.ident, gi), 0)
@@ -345,7 +353,14 @@ class Plan:
                         yop = b.operand(y0, gdt)
                         zops = [b.operand(r, gdt) for r in g.records[1:]] if together else []
                         if has_compare:
+                            fuse = digest and spans and static is None
+                            first_seg = len(b.seg_rows)
+                            if fuse:
+                                b.digest_slot = len(self.fused_digests)
                             self._compare_runs(b, e.x, y0, yop, zops, is_local)
+                            b.digest_slot = -1
+                            if fuse:
+                                self._settle_digest(b, first_seg, y0, yop, len(self.remote_groups) - 1, c)
                             if zops:
                                 self._replica_remainder(b, y0, yop, zops)
                         elif zops:
@@ -496,6 +511,21 @@ class Plan:
                 for xo, yo, rows, cols, rx, ry in blocks:
                     b.add(xop, xo, yop, yo, zops, rows, cols, rx, ry)
 
+    def _settle_digest(self, b: PlanBuilder, first: int, y0, yop, remote_k: int, copy: int) -> None:
+        """Keep the digest slot on a compare's segments only when they are all
+        vector segments reading y0's payload and cover it exactly once (the
+        reference boxes partition the candidate box); otherwise unstamp them
+        (that copy is then digested by td_fingerprint)."""
+        rows = b.seg_rows[first:]
+        cells = sum(r[5] * r[6] for r in rows)
+        ok = (rows and all(r[11] and r[2] is yop for r in rows)
+              and cells == math.prod(y0.shape)
+              and sum(loc.volume for loc, _ in y0.mapping.pairs) == math.prod(y0.shape))
+        if ok:
+            self.fused_digests.append((remote_k, copy))
+        else:
+            b.seg_rows[first:] = [r[:12] + (-1,) for r in rows]
+
     @staticmethod
     def _replica_remainder(b: PlanBuilder, y0, yop, zops) -> None:
         """Replica sums over payload cells no local box covers (usually none)."""
@@ -528,7 +558,7 @@ class Plan:
         self.seg_zslot = np.full((n, N.MAX_Z), -1, np.int64)
         tile_seg = np.zeros(self.n_tiles, np.int32)
         class_tiles: dict = {}
-        for i, (x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec) in enumerate(rows):
+        for i, (x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec, ds) in enumerate(rows):
             s = segs[i]
             s["x_stride"], s["y_stride"], s["rows"], s["cols"] = rx, ry, r, c
             s["tile_begin"], s["n_units"] = tb, nu
@@ -538,6 +568,7 @@ class Plan:
                           | (self.tile_shift << N.SEG_TILE_SHIFT_POS))
             m, p = _magic(c // 8 if vec else c)
             s["div_m"], s["div_p"] = m, p
+            s["y_word0"], s["digest_slot"] = (yo * y.esize) // 8, ds
             if x is not None:
                 self.seg_xslot[i], self.seg_xoff[i] = x.slot, xo * x.esize
             self.seg_yslot[i], self.seg_yoff[i] = y.slot, yo * y.esize
@@ -545,7 +576,7 @@ class Plan:
                 self.seg_zslot[i, j] = z.slot
             nt = -(-nu // self.tile_units)
             tile_seg[tb:tb + nt] = i
-            key = (bool(vec), y.dtype, len(zs), x is not None)
+            key = (bool(vec), y.dtype, len(zs), x is not None, ds >= 0)
             class_tiles.setdefault(key, []).append((tb, nt))
         self.segs = segs
         self.tile_seg = tile_seg
@@ -577,16 +608,18 @@ class Plan:
         return out
 
     def prepare(self, pointers: np.ndarray, *, kappa: float = 3.0, eps: float = 0.0,
-                replica_eps: float = 0.0, stream=None) -> "Prepared":
+                replica_eps: float = 0.0, stream=None, digests: int | None = None) -> "Prepared":
         """Patch live addresses into the segment table and stage every
-        device-side table and workspace; the result can be launched repeatedly."""
-        return Prepared(self, pointers, kappa, eps, replica_eps, stream)
+        device-side table and workspace; the result can be launched repeatedly.
+        digests: device address of the (len(fused_digests), 2) u64 table the
+        digest classes accumulate into (the caller zeroes it per run)."""
+        return Prepared(self, pointers, kappa, eps, replica_eps, stream, digests)
 
 
 class Prepared:
     """A plan bound to payload addresses, with its tables resident in HBM."""
 
-    def __init__(self, plan: Plan, pointers, kappa, eps, replica_eps, stream):
+    def __init__(self, plan: Plan, pointers, kappa, eps, replica_eps, stream, digests=None):
         import torch
         self.plan = plan
         self.kappa, self.eps, self.replica_eps = float(kappa), float(eps), float(replica_eps)
@@ -673,9 +706,14 @@ class Prepared:
         mode = N.MODE_STATIC if plan.static else N.MODE_NORMS
         atol, rtol = plan.static if plan.static else (0.0, 0.0)
         self.classes = np.zeros(len(plan.class_keys), N.CLASS)
-        for k, (vec, dt, nz, hx) in enumerate(plan.class_keys):
+        self.n_digests = len(plan.fused_digests)
+        if self.n_digests and digests is None:
+            self.digest_table = torch.zeros((self.n_digests, 2), dtype=torch.int64, device=dev)
+            digests = self.digest_table.data_ptr()
+        self.digest_ptr = digests or 0
+        for k, (vec, dt, nz, hx, dg) in enumerate(plan.class_keys):
             self.classes[k] = (base + offsets[1 + k], len(plan.class_lists[k]), dt, nz, int(hx),
-                               int(vec), mode, 0, atol, rtol)
+                               int(vec), mode, int(dg), atol, rtol, self.digest_ptr if dg else 0)
         self.launches_per_run = len(self.classes) + 1 + (1 if chunked else 0)
         self._events = None
 

@@ -59,10 +59,30 @@ def test_last_error_reports_bad_arguments():
     assert b"td_verdict" in lib.td_last_error()
 
 
-def test_struct_layouts_match_header():
-    assert N.SEGMENT.itemsize == 144
-    assert N.ID_DESC.itemsize == 56
-    assert N.GROUP_DESC.itemsize == 24
-    assert N.ID_RESULT.itemsize == 32
-    assert N.GROUP_RESULT.itemsize == 16
-    assert N.CLASS.itemsize == 56
+def test_struct_layouts_match_header(tmp_path):
+    """The numpy mirrors of the ABI structs have the sizes and field offsets
+    the C compiler gives include/td_api.h."""
+    import shutil
+    import subprocess
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    structs = {"td_segment": N.SEGMENT, "td_id_desc": N.ID_DESC, "td_group_desc": N.GROUP_DESC,
+               "td_id_result": N.ID_RESULT, "td_group_result": N.GROUP_RESULT, "td_class": N.CLASS,
+               "td_chunk": N.CHUNK, "td_fp_item": N.FP_ITEM}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "td_api.h"', "int main(void) {"]
+    for name, dt in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for field in dt.names:
+            lines.append(f'printf("{name}.{field} %zu\\n", offsetof({name}, {field}));')
+    lines += ["return 0;", "}"]
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run([cc, "-I", build.INCLUDE, "-o", str(exe), str(src)], check=True)
+    got = dict(line.split() for line in subprocess.run([str(exe)], capture_output=True, text=True,
+                                                        check=True).stdout.splitlines())
+    for name, dt in structs.items():
+        assert int(got[name]) == dt.itemsize, name
+        for field in dt.names:
+            assert int(got[f"{name}.{field}"]) == dt.fields[field][1], f"{name}.{field}"

@@ -161,3 +161,31 @@ def test_fingerprint_digests():
     again = fp.run().cpu().numpy()
     one = np.stack([fingerprints([p]).cpu().numpy()[0] for p in parts])
     assert np.array_equal(many, one) and np.array_equal(many, again)
+
+
+@pytest.mark.gpu
+def test_digests_fused_in_compare_equal_fingerprints():
+    """The digest slots td_segnorm fills while comparing a cross-GPU replica
+    group's copy equal td_fingerprint's digest of that copy."""
+    from paper_2506_09280_b200 import _native as N
+    from paper_2506_09280_b200.device import fingerprints, resolve_operands
+    lay = synthetic.ShareLayout(SMALL, PCFG, WORLD)
+    ref_metas, cand_metas = lay.metas()
+    fused_total = 0
+    for r in range(WORLD):
+        ref, cand = lay.build(r)
+        dcp = DistributedCheckPlan(ref, cand, _tol(lay), fmt=FloatFormat.BF16,
+                                   comm=StaticComm(r, WORLD, [ref_metas, cand_metas]))
+        table, fps, where, nf = dcp.digests()
+        ptrs, keep = resolve_operands(dcp.plan.operands, dcp.plan.operand_dtypes)
+        prep = dcp.plan.prepare(ptrs, eps=FloatFormat.BF16.eps, digests=table.data_ptr())
+        table.zero_()
+        fps.run()
+        prep.segnorm(N.stream_handle(prep.stream))
+        torch.cuda.synchronize()
+        recs = [dcp._remote_group_records(dcp.plan.remote_groups[k])[c].device_payload().reshape(-1)
+                for k, c in where]
+        want = fingerprints(recs).cpu().numpy()
+        assert np.array_equal(table[:len(where)].cpu().numpy(), want), r
+        fused_total += nf
+    assert fused_total > 0
