@@ -117,15 +117,29 @@ constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ull;
 constexpr uint64_t MIX1 = 0xBF58476D1CE4E5B9ull;
 constexpr uint64_t MIX2 = 0x94D049BB133111EBull;
 
-// one 8-byte word w at word index j into a 128-bit digest (see k_fingerprint)
-__device__ __forceinline__ void fp_word(uint64_t w, uint64_t j, uint64_t& h0, uint64_t& h1) {
-    uint64_t z = w ^ ((j + 1) * GAMMA);
-    z *= MIX1;
-    z ^= z >> 32;
-    z *= MIX2;
+// One 8-byte word w with position key k = (j+1)*gamma (j = word index) into
+// a 128-bit digest: z = fold((w ^ k) * MIX1) — for a fixed key a bijection of
+// w, so a changed word always changes z — then h0 += z and h1 += hi32(z) *
+// lo32(z) (a non-linear second lane).  One 64-bit multiply and one 32x32
+// wide multiply per word: ncu showed the fmaheavy pipe (IMAD / IMAD.WIDE)
+// binding at 80% with the first, two-round version (5.6 TB/s).  Keys of
+// consecutive words differ by gamma, so callers step them with adds.
+__device__ __forceinline__ void fp_key_word(uint64_t w, uint64_t key, uint64_t& h0, uint64_t& h1) {
+    uint64_t z = (w ^ key) * MIX1;
     z ^= z >> 32;
     h0 += z;
-    h1 += z * z;
+    h1 += (uint64_t)(uint32_t)(z >> 32) * (uint32_t)z;
+}
+
+__device__ __forceinline__ void fp_word(uint64_t w, uint64_t j, uint64_t& h0, uint64_t& h1) {
+    fp_key_word(w, (j + 1) * GAMMA, h0, h1);
+}
+
+// a 16-byte vector at word index j (words j, j+1)
+__device__ __forceinline__ void fp_vec(const uint4& v, uint64_t j, uint64_t& h0, uint64_t& h1) {
+    const uint64_t k0 = (j + 1) * GAMMA;
+    fp_key_word(((uint64_t)v.y << 32) | v.x, k0, h0, h1);
+    fp_key_word(((uint64_t)v.w << 32) | v.z, k0 + GAMMA, h0, h1);
 }
 
 #ifndef TD_REPLICA_SKIP
@@ -282,10 +296,7 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
                     const uint32_t cv = u - row * vpr;
                     const uint64_t j = (uint64_t)(w0 + (((int64_t)row * S.ys + (int64_t)cv * 8) * ES >> 3));
 #pragma unroll
-                    for (int q = 0; q < Q; ++q) {
-                        fp_word(((uint64_t)yr[k][q].y << 32) | yr[k][q].x, j + 2 * q, h0, h1);
-                        fp_word(((uint64_t)yr[k][q].w << 32) | yr[k][q].z, j + 2 * q + 1, h0, h1);
-                    }
+                    for (int q = 0; q < Q; ++q) fp_vec(yr[k][q], j + 2 * q, h0, h1);
                 }
             }
 #pragma unroll
@@ -969,15 +980,13 @@ __global__ void k_quantize(const double* __restrict__ x, char* __restrict__ y, i
 
 // ---------------------------------------------------------------------------
 // Replica digests (multi-GPU replica groups): for each item, an
-// order-independent 128-bit digest of its bytes, (sum z_j, sum z_j^2) mod 2^64
-// over 8-byte words w_j (tail zero-padded) with z_j = f(w_j ^ (j+1)*gamma),
-// f = two multiply / xor-fold rounds (each step a bijection, so a changed
-// word always changes its z).  Position-keyed, so permuted shards differ.
+// order-independent 128-bit digest of its bytes, sum over 8-byte words w_j
+// (tail zero-padded) of fp_key_word(w_j, (j+1)*gamma) mod 2^64 (see there).
+// Position-keyed, so permuted shards differ.
 // One launch covers every item: a flat list of 256 KB chunks (prefix sums of
 // per-item chunk counts, binary-searched per chunk), 16-byte streaming loads,
 // 4 vectors in flight per thread; warp sums are added atomically (wrapping
-// u64 adds commute: the digest does not depend on the order).  ~8 ALU ops per
-// 8 bytes: HBM-bound, unlike the per-element mix of the first version.
+// u64 adds commute: the digest does not depend on the order).
 
 __global__ void __launch_bounds__(BLOCK)
 k_fingerprint(const td_fp_item* __restrict__ items, const int64_t* __restrict__ chunk_begin, int n_items,
@@ -999,6 +1008,7 @@ k_fingerprint(const td_fp_item* __restrict__ items, const int64_t* __restrict__ 
         if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
             const int64_t vend = off1 & ~(int64_t)15;
             for (int64_t base = off0 + 16 * threadIdx.x; base < vend; base += 16 * BLOCK * U) {
+                const uint64_t kbase = (uint64_t)((base >> 3) + 1) * GAMMA;
                 uint4 v[U];
 #pragma unroll
                 for (int k = 0; k < U; ++k) {
@@ -1009,8 +1019,10 @@ k_fingerprint(const td_fp_item* __restrict__ items, const int64_t* __restrict__ 
                 for (int k = 0; k < U; ++k) {
                     const int64_t o = base + 16 * BLOCK * k;
                     if (o < vend) {
-                        fp_word(((uint64_t)v[k].y << 32) | v[k].x, (uint64_t)(o >> 3), h0, h1);
-                        fp_word(((uint64_t)v[k].w << 32) | v[k].z, (uint64_t)(o >> 3) + 1, h0, h1);
+                        // key of word o/8: base key + k * (2 * BLOCK) * gamma (adds only)
+                        const uint64_t key = kbase + (uint64_t)k * (2ull * BLOCK * GAMMA);
+                        fp_key_word(((uint64_t)v[k].y << 32) | v[k].x, key, h0, h1);
+                        fp_key_word(((uint64_t)v[k].w << 32) | v[k].z, key + GAMMA, h0, h1);
                     }
                 }
             }

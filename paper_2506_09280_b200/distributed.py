@@ -393,8 +393,13 @@ class DistributedCheckPlan:
         sh = N.stream_handle(prep.stream)
         with torch.cuda.stream(prep.stream):
             table.zero_()
-        fps.run(prep.stream)
+        # copies no local compare reads are digested beside the compare pass
+        # (both stream HBM; each fills the other's tail)
+        side = torch.cuda.Stream()
+        side.wait_stream(prep.stream)
+        fps.run(side)
         prep.segnorm(sh)
+        prep.stream.wait_stream(side)
         extra, overrides = self._resolve_remote(table, where)
         if overrides:
             ptrs, keep2 = resolve_operands(self.plan.operands, self.plan.operand_dtypes, overrides)
