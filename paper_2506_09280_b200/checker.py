@@ -197,10 +197,16 @@ class CheckPlan:
         return self.plan.algorithmic_bytes
 
     def execute(self, timing: dict | None = None, staged: dict | None = None):
-        """Device part only: resolve payloads, launch, fetch raw results."""
+        """Device part only: resolve payloads, launch, fetch raw results.
+        The host-side half of the report is built between the launch and the
+        fetch, i.e. while host payloads are still crossing PCIe."""
         ptrs, keep = resolve_operands(self.plan.operands, self.plan.operand_dtypes, staged)
-        out = self.plan.run(ptrs, kappa=self.kappa, eps=self.fmt.eps, replica_eps=self.fmt.eps,
-                            timing=timing)
+        prep = self.plan.prepare(ptrs, kappa=self.kappa, eps=self.fmt.eps, replica_eps=self.fmt.eps)
+        prep.launch(timing=timing)
+        self._report_rows()
+        out = prep.fetch()
+        if timing is not None:
+            prep.read_timing(timing)
         del keep
         return out
 
@@ -208,43 +214,61 @@ class CheckPlan:
         idres, gres, ties = self.execute(timing, staged)
         return self.report(idres, gres, ties)
 
-    def report(self, idres, gres, ties) -> CheckReport:
-        per_entry: dict = {}
-        for row, (ei, side, gi) in zip(gres, self.plan.group_owner):
-            per_entry.setdefault((ei, side), {})[gi] = row
+    def _report_rows(self) -> list:
+        """Everything of the report that does not depend on device results:
+        per entry (ident, compare index or -1, tolerance, threshold, has
+        compare, static detail), in report order (checker.py:328-365)."""
+        rows = getattr(self, "_rows", None)
+        if rows is not None:
+            return rows
         kappa, eps = self.kappa, self.fmt.eps
         index = {ident: k for k, ident in enumerate(self.common)}
-        entries = []
+        has = self.plan.ids["has_compare"].tolist() if len(self.plan.ids) else []
+        rows = []
         for ident, got in self.cand_view.items():
             tolerance = self.tol.get(ident)
             threshold = kappa * max(tolerance, eps)
             k = index.get(ident)
             if k is None:
-                entries.append(CheckEntry(ident, VERDICT_MISSING, None, tolerance, threshold,
-                                          "only in candidate trace"))
+                rows.append((ident, -1, tolerance, threshold, False, "only in candidate trace"))
                 continue
-            r = idres[k]
+            has_compare = bool(has[k])
             want = self.ref_view[ident]
-            has_compare = bool(self.plan.ids[k]["has_compare"])
-            observed = float(r["observed"]) if has_compare else None
-            verdict = _NAME[int(r["verdict"])]
-            if int(r["cand_kind"]):
-                detail = _side_detail(got, per_entry.get((k, 0), {}))
-            elif int(r["ref_kind"]):
-                detail = "reference side: " + _side_detail(want, per_entry.get((k, 1), {}))
-            elif not has_compare:
-                detail = (f"merged shapes differ: reference {want.global_shape} vs "
-                          f"candidate {got.global_shape}")
-            else:
-                detail = ""
-            entries.append(CheckEntry(ident, verdict, observed, tolerance, threshold, detail))
+            detail = "" if has_compare else (f"merged shapes differ: reference {want.global_shape} vs "
+                                             f"candidate {got.global_shape}")
+            rows.append((ident, k, tolerance, threshold, has_compare, detail))
         for ident in self.ref_view:
             if ident in self.cand_view:
                 continue
             tolerance = self.tol.get(ident)
-            entries.append(CheckEntry(ident, VERDICT_MISSING, None, tolerance,
-                                      kappa * max(tolerance, eps), "only in reference trace"))
-        return CheckReport(entries=tuple(entries), mode=self.mode, kappa=kappa, fmt=self.fmt,
+            rows.append((ident, -1, tolerance, kappa * max(tolerance, eps), False, "only in reference trace"))
+        self._rows = rows
+        return rows
+
+    def report(self, idres, gres, ties) -> CheckReport:
+        rows = self._report_rows()
+        observed = idres["observed"].tolist()
+        verdict = idres["verdict"].tolist()
+        cand_kind = idres["cand_kind"].tolist()
+        ref_kind = idres["ref_kind"].tolist()
+        per_entry: dict | None = None
+        entries = []
+        for ident, k, tolerance, threshold, has_compare, detail in rows:
+            if k < 0:
+                entries.append(CheckEntry(ident, VERDICT_MISSING, None, tolerance, threshold, detail))
+                continue
+            if cand_kind[k] or ref_kind[k]:
+                if per_entry is None:
+                    per_entry = {}
+                    for row, (ei, side, gi) in zip(gres, self.plan.group_owner):
+                        per_entry.setdefault((ei, side), {})[gi] = row
+                if cand_kind[k]:
+                    detail = _side_detail(self.cand_view[ident], per_entry.get((k, 0), {}))
+                else:
+                    detail = "reference side: " + _side_detail(self.ref_view[ident], per_entry.get((k, 1), {}))
+            entries.append(CheckEntry(ident, _NAME[verdict[k]], observed[k] if has_compare else None,
+                                      tolerance, threshold, detail))
+        return CheckReport(entries=tuple(entries), mode=self.mode, kappa=self.kappa, fmt=self.fmt,
                            near_ties=ties)
 
 

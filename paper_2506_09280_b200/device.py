@@ -115,13 +115,18 @@ def stage_host_payloads(traces, stream=None) -> dict:
                     continue
                 if p.is_pinned():
                     st = p.untyped_storage()
-                    arenas.setdefault(st.data_ptr(), (st, []))[1].append(rec)
+                    entry = arenas.get(st.data_ptr())
+                    if entry is None:
+                        # a new arena: its DMA starts now, before the rest of
+                        # the records are even looked at
+                        host = torch.empty(0, dtype=torch.uint8).set_(st)
+                        dev = torch.empty(host.numel(), dtype=torch.uint8, device="cuda")
+                        dev.copy_(host, non_blocking=True)
+                        entry = arenas[st.data_ptr()] = (dev, [])
+                    entry[1].append(rec)
                     continue
             staged[id(rec)] = to_device(p)
-    for st, recs in arenas.values():
-        host = torch.empty(0, dtype=torch.uint8).set_(st)
-        dev = torch.empty(host.numel(), dtype=torch.uint8, device="cuda")
-        dev.copy_(host, non_blocking=True)
+    for dev, recs in arenas.values():
         dst = dev.untyped_storage()
         for rec in recs:
             p = rec.payload

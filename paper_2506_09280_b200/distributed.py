@@ -276,6 +276,7 @@ class DistributedCheckPlan:
         self._digest = None
         self.mode = str(cand.header.get("mode", ""))
         self._report = CheckPlan.report
+        self._report_rows = lambda: CheckPlan._report_rows(self)
 
     def _remote_group_records(self, slot_entry):
         _, ei, side, gi = slot_entry
