@@ -239,6 +239,9 @@ __device__ __forceinline__ void write_warp_partial(const Acc& a, int used, doubl
 // of a cross-GPU replica group is digested in the pass that compares it, so
 // it is read once; the planner guarantees such a record's segments cover it
 // exactly once, so the sum equals td_fingerprint's digest of the record).
+// Hashing in the loads' registers needs U=2 to stay at 64 registers; a second
+// pass over the warp's tile slice from L2 instead (U=4 compare loop) measured
+// 18% slower on the config-4 share, U=4 at 3 CTAs/SM 5% slower.
 template <int DT, int NZ, bool HX, int U, int MINB, bool DG = false>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ tiles, int64_t n,
