@@ -1,0 +1,70 @@
+"""Config 3 at its full BASELINE size (Llama-3-1B shape, S=8192, TP=8, 69 GB
+of bf16 traces in HBM) with the three injected bugs.  Too big for the CPU
+oracle, so the checks are size-independent: the verdicts are exactly the
+injections, and the observed rel_err of the bug ids and of a sample of clean
+ids equals an independent torch fp64 computation over the materialised
+merges (copy 0 of every shard group, reference semantics) within 1e-12."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+BUGS = {"iter=0|mb=0|kind=ActivationOut|mod=model.lm_head": "order",
+        "iter=0|mb=0|kind=ActivationOut|mod=model.layers.7.attn": "partial",
+        "iter=0|mb=0|kind=ActivationOut|mod=model.embedding": "scale"}
+
+
+def _merged_f64(trace, ident):
+    """merge() of copy 0 of each shard group, in fp64, with torch indexing."""
+    recs = [r for r in trace.records if r.id.encode() == ident]
+    seen, out = set(), None
+    for r in recs:
+        key = (tuple(r.mapping.local_shape), tuple((l.bounds, g.bounds) for l, g in r.mapping.pairs))
+        if key in seen:
+            continue
+        seen.add(key)
+        if out is None:
+            out = torch.zeros(r.mapping.global_shape, dtype=torch.float64, device="cuda")
+        for loc, glob in r.mapping.pairs:
+            out[glob.as_slices()] = r.payload[loc.as_slices()].double()
+    return out
+
+
+def _rel_err_fp64(a, b):
+    d = torch.linalg.vector_norm((a - b).reshape(-1), dtype=torch.float64)
+    r = torch.linalg.vector_norm(a.reshape(-1), dtype=torch.float64)
+    return float(d / r)
+
+
+def test_config3_full_size_injections_and_fp64_norms():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if torch.cuda.get_device_properties(0).total_memory < 150e9:
+        pytest.skip("needs a 180 GB B200")
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200 import layout as L, synthetic
+    ref, cand = synthetic.build(L.LLAMA3_1B, L.ParallelConfig(tp=8), bugs=BUGS, seed=0)
+    eps = td.FloatFormat.BF16.eps
+    tol = td.ToleranceMap({r.id.encode(): 2 * eps for r in ref.records}, n_samples=1, eps_p=eps)
+    rep = td.check(ref, cand, tol, fmt=td.FloatFormat.BF16)
+    verdicts = {e.ident: e for e in rep.entries}
+    assert rep.counts["flag"] == 2 and rep.counts["replica-mismatch"] == 1
+    assert rep.counts["pass"] == len(rep.entries) - 3 and rep.near_ties == 0
+    assert verdicts[[k for k, v in BUGS.items() if v == "order"][0]].verdict == "flag"
+    assert verdicts[[k for k, v in BUGS.items() if v == "scale"][0]].verdict == "flag"
+    partial = verdicts[[k for k, v in BUGS.items() if v == "partial"][0]]
+    assert partial.verdict == "replica-mismatch" and partial.detail.startswith("replicas diverge")
+    sample = list(BUGS) + ["iter=0|mb=0|kind=ActivationIn|mod=model.layers.15.mlp",
+                           "iter=0|mb=0|kind=ParamGrad|mod=model.layers.3.mlp.w1",
+                           "iter=0|mb=0|kind=ActivationOut|mod=model.layers.0.attn"]
+    for ident in sample:
+        if ident not in verdicts:
+            continue
+        want = _rel_err_fp64(_merged_f64(ref, ident), _merged_f64(cand, ident))
+        got = verdicts[ident].observed
+        assert abs(got - want) <= 1e-12 * want, (ident, got, want)
+        torch.cuda.empty_cache()
+    # the scale bug multiplies by tp = 8 exactly: rel_err of 8x vs x is 7 up
+    # to the simulated round-off
+    assert abs(verdicts[[k for k, v in BUGS.items() if v == "scale"][0]].observed - 7.0) < 0.1
