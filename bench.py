@@ -571,7 +571,22 @@ def main():
         # through the public check() and moves all of it over PCIe again
         from paper_2506_09280_b200.tracestore import pack_pinned
         del keep, prep
-        href, hcand = pack_pinned(ref), pack_pinned(cand)
+        # pinned host arenas: 16 GB per rank for config 2; if a rank cannot
+        # pin them, every rank skips e2e together (no rank left in a collective)
+        try:
+            href, hcand = pack_pinned(ref), pack_pinned(cand)
+            ok = 1
+        except (RuntimeError, MemoryError) as exc:
+            href = hcand = None
+            ok, why = 0, str(exc).splitlines()[0][:200]
+        if world > 1:
+            flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            ok = int(flag.item())
+    if not args.no_e2e and not ok:
+        e2e = {"value": None, "unit": "GB/s", "error": f"pinned host arenas unavailable on some rank: "
+                                                      f"{why if href is None else 'another rank failed'}"}
+    elif not args.no_e2e:
         h2d = href.nbytes + hcand.nbytes
         d2h = n_ids * N.ID_RESULT.itemsize
         del ref, cand
@@ -597,7 +612,7 @@ def main():
                "verdicts": rep.counts}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        if e2e is not None:
+        if e2e is not None and e2e.get("value") is not None:
             cpu = cpu_baseline(href, hcand, tol, fmt, args.cpu_stride)
         else:
             cpu = cpu_baseline(ref, cand, tol, fmt, args.cpu_stride)

@@ -626,11 +626,25 @@ k_finalize(const td_id_desc* __restrict__ ids, const td_group_desc* __restrict__
     __shared__ double red[NWARP];
     const int i = blockIdx.x;
     const td_id_desc D = ids[i];
+    // FIN_U rows per thread in flight (independent loads, summed in a fixed
+    // order): one CTA walks up to ~8 k rows, so a load-add chain per row was
+    // pure L2 latency (6 us for a 1 MiB check, as long as its td_segnorm)
+    constexpr int FIN_U = 8;
     double d2 = 0.0, x2 = 0.0;
-    for (int64_t r = D.tile_begin * TD_WARPS_PER_TILE + threadIdx.x; r < D.tile_end * TD_WARPS_PER_TILE;
-         r += BLOCK) {
-        d2 += partials[r * TD_PARTIAL_STRIDE + 0];
-        x2 += partials[r * TD_PARTIAL_STRIDE + 1];
+    const int64_t r1 = D.tile_end * TD_WARPS_PER_TILE;
+    for (int64_t r0 = D.tile_begin * TD_WARPS_PER_TILE + threadIdx.x; r0 < r1; r0 += BLOCK * FIN_U) {
+        double a[FIN_U], b[FIN_U];
+#pragma unroll
+        for (int k = 0; k < FIN_U; ++k) {
+            const int64_t r = r0 + (int64_t)k * BLOCK;
+            a[k] = r < r1 ? __ldg(partials + r * TD_PARTIAL_STRIDE + 0) : 0.0;
+            b[k] = r < r1 ? __ldg(partials + r * TD_PARTIAL_STRIDE + 1) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < FIN_U; ++k) {
+            d2 += a[k];
+            x2 += b[k];
+        }
     }
     d2 = cta_sum(d2, red);
     x2 = cta_sum(x2, red);
@@ -643,11 +657,20 @@ k_finalize(const td_id_desc* __restrict__ ids, const td_group_desc* __restrict__
             double sums[TD_SLOT_STRIDE];
 #pragma unroll
             for (int k = 0; k < TD_SLOT_STRIDE; ++k) sums[k] = 0.0;
-            for (int64_t r = G.tile_begin * TD_WARPS_PER_TILE + threadIdx.x; r < G.tile_end * TD_WARPS_PER_TILE;
-                 r += BLOCK) {
+            const int64_t g1 = G.tile_end * TD_WARPS_PER_TILE;
+            for (int64_t r0 = G.tile_begin * TD_WARPS_PER_TILE + threadIdx.x; r0 < g1; r0 += BLOCK * 2) {
+                double v[2][TD_SLOT_STRIDE];
 #pragma unroll
-                for (int k = 0; k < TD_SLOT_STRIDE; ++k)
-                    if (k <= G.nz) sums[k] += partials[r * TD_PARTIAL_STRIDE + 2 + k];
+                for (int u = 0; u < 2; ++u) {
+                    const int64_t r = r0 + (int64_t)u * BLOCK;
+#pragma unroll
+                    for (int k = 0; k < TD_SLOT_STRIDE; ++k)
+                        v[u][k] = (r < g1 && k <= G.nz) ? __ldg(partials + r * TD_PARTIAL_STRIDE + 2 + k) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int k = 0; k < TD_SLOT_STRIDE; ++k) sums[k] += v[u][k];
             }
 #pragma unroll
             for (int k = 0; k < TD_SLOT_STRIDE; ++k) sums[k] = (k <= G.nz) ? cta_sum(sums[k], red) : 0.0;
