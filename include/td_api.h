@@ -199,7 +199,9 @@ int td_reduce_chunks(const double* partials, const td_chunk* chunks, int64_t n_c
 
 /* ---- kernel 3: batched threshold compare -> per-id verdicts ----
  * eps = fmt.eps (threshold floor); replica_eps = fmt.eps for check_replicas.
- * near_ties: one device uint64 counter, reset and then counted. */
+ * near_ties: optional device uint64 counter, reset and then counted (NULL: per-id
+ * near_tie flags only; callers that sum them keep the verdict kernel free to
+ * launch programmatically behind its producer, PDL). */
 int td_verdict(const td_id_desc* ids, int32_t n_ids,
                const td_group_desc* groups, int32_t n_groups,
                const double* id_sums, const double* group_sums,

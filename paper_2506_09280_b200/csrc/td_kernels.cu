@@ -180,6 +180,15 @@ __device__ __forceinline__ uint32_t udiv(uint32_t n, uint32_t m, int p) {
     return (uint32_t)(((uint64_t)n * (uint64_t)m) >> p);
 }
 
+// Programmatic dependent launch (sm_90+): the slot reduction / verdict
+// kernels are launched with programmatic stream serialisation and wait for
+// their producer at entry, so their launch (and CTA rasterisation) overlaps
+// the producer's tail instead of following its completion; the segnorm
+// walkers signal once a CTA has written its last partial row.  Without the
+// launch attribute (TD_PDL=0, or a non-kernel predecessor) both are no-ops.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // ---------------------------------------------------------------------------
 // tile walkers.  Every (dtype, nz, has_x) class is its own __global__ so ptxas
 // allocates registers for exactly one loop; the host launches one persistent
@@ -356,6 +365,7 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
             }
         }
     }
+    griddep_launch_dependents();
 }
 
 // generic class: per element, runtime dtypes, any alignment, any nz (<= 7).
@@ -413,6 +423,7 @@ k_segnorm_generic(const td_segment* __restrict__ segs, const int64_t* __restrict
         write_warp_partial(a, nz > 0 ? 3 + nz : 2,
                            partials + (t * TD_WARPS_PER_TILE + warp) * TD_PARTIAL_STRIDE);
     }
+    griddep_launch_dependents();
 }
 
 typedef void (*segnorm_fn)(const td_segment*, const int64_t*, int64_t, double*, unsigned long long*);
@@ -494,6 +505,7 @@ __global__ void k_reduce_slots(const td_id_desc* __restrict__ ids, int n_ids,
                                const td_group_desc* __restrict__ groups, int n_groups,
                                const double* __restrict__ partials,
                                double* __restrict__ id_sums, double* __restrict__ group_sums) {
+    griddep_wait();
     const int lane = threadIdx.x & 31;
     const int64_t slot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (slot >= (int64_t)n_ids + n_groups) return;
@@ -574,7 +586,7 @@ __device__ __forceinline__ void id_verdict(int i, const td_id_desc& D, const int
         verdict = (obs > thr) ? TD_FLAG : TD_PASS;   // NaN -> pass (reference quirk)
         if (fabs(obs - thr) <= 1e-12 * thr) {
             tie = 1;
-            atomicAdd(near_ties, 1ull);
+            if (near_ties) atomicAdd(near_ties, 1ull);
         }
     }
     id_out[i].observed = obs;
@@ -591,6 +603,7 @@ __global__ void k_verdict(const td_id_desc* __restrict__ ids, int n_ids,
                           double kappa, double eps, double replica_eps,
                           td_id_result* __restrict__ id_out, td_group_result* __restrict__ group_out,
                           unsigned long long* __restrict__ near_ties) {
+    griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_ids) return;
     const td_id_desc D = ids[i];
@@ -624,6 +637,7 @@ k_finalize(const td_id_desc* __restrict__ ids, const td_group_desc* __restrict__
            double kappa, double eps, double replica_eps, td_id_result* __restrict__ id_out,
            td_group_result* __restrict__ group_out, unsigned long long* __restrict__ near_ties) {
     __shared__ double red[NWARP];
+    griddep_wait();
     const int i = blockIdx.x;
     const td_id_desc D = ids[i];
     // FIN_U rows per thread in flight (independent loads, summed in a fixed
@@ -699,6 +713,7 @@ __global__ void __launch_bounds__(CHUNK_BLOCK)
 k_reduce_chunks(const double* __restrict__ partials, const td_chunk* __restrict__ chunks, int64_t n,
                 double* __restrict__ out) {
     __shared__ double red[CHUNK_BLOCK];
+    griddep_wait();
     const int t = threadIdx.x;
     constexpr int ROW = TD_WARPS_PER_TILE * TD_PARTIAL_STRIDE;   // doubles per output "tile"
     for (int64_t c = blockIdx.x; c < n; c += gridDim.x) {
@@ -724,6 +739,7 @@ k_reduce_chunks(const double* __restrict__ partials, const td_chunk* __restrict_
         }
         __syncthreads();
     }
+    griddep_launch_dependents();
 }
 
 // ---------------------------------------------------------------------------
@@ -1205,6 +1221,31 @@ int grid_for(int64_t n, int per_block, int cap) {
     return (int)g;
 }
 
+// launch a consumer kernel with programmatic stream serialisation (PDL; see
+// griddep_wait).  TD_PDL=0 disables it (A/B and debugging).
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("TD_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_dependent(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1292,8 +1333,9 @@ int td_reduce_slots(const td_id_desc* ids, int32_t n_ids, const td_group_desc* g
         return fail("td_reduce_slots: invalid arguments");
     const int threads = 256;
     const int64_t blocks = (slots * 32 + threads - 1) / threads;
-    k_reduce_slots<<<(unsigned)blocks, threads, 0, (cudaStream_t)stream>>>(ids, n_ids, groups, n_groups,
-                                                                          partials, id_sums, group_sums);
+    if (launch_dependent(k_reduce_slots, dim3((unsigned)blocks), dim3(threads), (cudaStream_t)stream, ids, n_ids,
+                         groups, n_groups, partials, id_sums, group_sums) != cudaSuccess)
+        return check_launch("td_reduce_slots");
     return check_launch("td_reduce_slots");
 }
 
@@ -1302,13 +1344,14 @@ int td_verdict(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups
                double replica_eps, td_id_result* id_out, td_group_result* group_out,
                unsigned long long* near_ties, void* stream) {
     if (n_ids == 0) return 0;
-    if (n_ids < 0 || !ids || !id_sums || !id_out || !near_ties || (n_groups && (!groups || !group_sums || !group_out)))
+    if (n_ids < 0 || !ids || !id_sums || !id_out || (n_groups && (!groups || !group_sums || !group_out)))
         return fail("td_verdict: invalid arguments");
     const int threads = 128;
-    if (cudaMemsetAsync(near_ties, 0, sizeof(unsigned long long), (cudaStream_t)stream) != cudaSuccess)
+    if (near_ties && cudaMemsetAsync(near_ties, 0, sizeof(unsigned long long), (cudaStream_t)stream) != cudaSuccess)
         return fail("td_verdict: cannot reset the near-tie counter");
-    k_verdict<<<(n_ids + threads - 1) / threads, threads, 0, (cudaStream_t)stream>>>(
-        ids, n_ids, groups, id_sums, group_sums, kappa, eps, replica_eps, id_out, group_out, near_ties);
+    launch_dependent(k_verdict, dim3((unsigned)((n_ids + threads - 1) / threads)), dim3(threads),
+                     (cudaStream_t)stream, ids, n_ids, groups, id_sums, group_sums, kappa, eps, replica_eps,
+                     id_out, group_out, near_ties);
     return check_launch("td_verdict");
 }
 
@@ -1320,7 +1363,8 @@ int td_reduce_chunks(const double* partials, const td_chunk* chunks, int64_t n_c
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t grid = std::min<int64_t>(n_chunks, (int64_t)sms * 6);
-    k_reduce_chunks<<<(unsigned)grid, CHUNK_BLOCK, 0, (cudaStream_t)stream>>>(partials, chunks, n_chunks, out);
+    launch_dependent(k_reduce_chunks, dim3((unsigned)grid), dim3(CHUNK_BLOCK), (cudaStream_t)stream, partials,
+                     chunks, n_chunks, out);
     return check_launch("td_reduce_chunks");
 }
 
@@ -1329,13 +1373,13 @@ int td_finalize(const td_id_desc* ids, int32_t n_ids, const td_group_desc* group
                 double replica_eps, td_id_result* id_out, td_group_result* group_out,
                 unsigned long long* near_ties, void* stream) {
     if (n_ids == 0) return 0;
-    if (n_ids < 0 || !ids || !partials || !id_sums || !id_out || !near_ties ||
+    if (n_ids < 0 || !ids || !partials || !id_sums || !id_out ||
         (n_groups && (!groups || !group_sums || !group_out)))
         return fail("td_finalize: invalid arguments");
-    if (cudaMemsetAsync(near_ties, 0, sizeof(unsigned long long), (cudaStream_t)stream) != cudaSuccess)
+    if (near_ties && cudaMemsetAsync(near_ties, 0, sizeof(unsigned long long), (cudaStream_t)stream) != cudaSuccess)
         return fail("td_finalize: cannot reset the near-tie counter");
-    k_finalize<<<n_ids, BLOCK, 0, (cudaStream_t)stream>>>(ids, groups, partials, id_sums, group_sums, kappa, eps,
-                                                         replica_eps, id_out, group_out, near_ties);
+    launch_dependent(k_finalize, dim3((unsigned)n_ids), dim3(BLOCK), (cudaStream_t)stream, ids, groups, partials,
+                     id_sums, group_sums, kappa, eps, replica_eps, id_out, group_out, near_ties);
     return check_launch("td_finalize");
 }
 

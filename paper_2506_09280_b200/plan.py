@@ -702,7 +702,10 @@ class Prepared:
         self.res = torch.zeros(self.res_bytes, dtype=torch.uint8, device=dev)
         self.idres_ptr = self.res.data_ptr()
         self.gres_ptr = self.idres_ptr + N.ID_RESULT.itemsize * n_ids
-        self.tie_ptr = self.gres_ptr + N.GROUP_RESULT.itemsize * n_groups
+        # near ties are counted on the host from the per-id flags: no counter
+        # reset between td_segnorm and the verdict kernel, which would keep
+        # the verdict kernel from launching programmatically (PDL)
+        self.tie_ptr = 0
         mode = N.MODE_STATIC if plan.static else N.MODE_NORMS
         atol, rtol = plan.static if plan.static else (0.0, 0.0)
         self.classes = np.zeros(len(plan.class_keys), N.CLASS)
@@ -799,7 +802,7 @@ class Prepared:
         idres = raw[:N.ID_RESULT.itemsize * n_ids].view(N.ID_RESULT)
         lo = N.ID_RESULT.itemsize * n_ids
         gres = raw[lo:lo + N.GROUP_RESULT.itemsize * n_groups].view(N.GROUP_RESULT)
-        ties = int(raw[-8:].view(np.uint64)[0])
+        ties = int(idres["near_tie"].sum()) if n_ids else 0
         return idres, gres, ties
 
     def sums(self) -> dict:
