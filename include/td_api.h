@@ -197,6 +197,18 @@ typedef struct td_chunk {
 int td_reduce_chunks(const double* partials, const td_chunk* chunks, int64_t n_chunks,
                      double* out, void* stream);
 
+/* ---- rel_err_arrays for one pair, one launch ----
+ * out[0] = sum (a-b)^2, out[1] = sum a^2, out[2] = rel_err with the
+ * reference's conventions (0/0 -> 0, x/0 -> +inf; tensor.py:158-167), for two
+ * contiguous device arrays of n elements of one dtype (16-byte-aligned bf16 /
+ * f16 / f32 stream as vectors).  work: TD_REL_ERR_WORK_BYTES of device memory,
+ * zeroed once before first use (its ticket is reset by every call); calls
+ * sharing a work buffer must be stream-ordered. */
+#define TD_REL_ERR_MAX_CTAS 1024
+#define TD_REL_ERR_WORK_BYTES (16 * TD_REL_ERR_MAX_CTAS + 16)
+int td_rel_err(const void* a, const void* b, int32_t dtype, int64_t n, void* work, double* out,
+               void* stream);
+
 /* ---- kernel 3: batched threshold compare -> per-id verdicts ----
  * eps = fmt.eps (threshold floor); replica_eps = fmt.eps for check_replicas.
  * near_ties: optional device uint64 counter, reset and then counted (NULL: per-id

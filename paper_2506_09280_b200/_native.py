@@ -28,6 +28,7 @@ SLOT_STRIDE = 8
 SEG_HAS_X = 1
 SEG_VEC = 2
 SEG_TILE_SHIFT_POS = 8
+REL_ERR_WORK_BYTES = 16 * 1024 + 16   # TD_REL_ERR_WORK_BYTES
 FP_CHUNK = 1 << 18          # bytes per td_fingerprint work chunk (TD_FP_CHUNK)
 FP_ITEM = np.dtype([("ptr", "<u8"), ("nbytes", "<i8")])
 
@@ -80,6 +81,7 @@ SIGNATURES = {
     "td_signed_uniforms": (ctypes.c_int, [_P, _I64, _U64, _I64, _I32, _P]),
     "td_quantize": (ctypes.c_int, [_P, _P, _I32, _I64, _I32, _P, _P]),
     "td_fingerprint": (ctypes.c_int, [_P, _P, _I32, _I64, _P, _P]),
+    "td_rel_err": (ctypes.c_int, [_P, _P, _I32, _I64, _P, _P, _P]),
     "td_box_gather": (ctypes.c_int, [_P, _I32, _P, _P, _I32, _P]),
     "td_gather_bytes": (ctypes.c_int, [_P, _P, _P, _I64, _P]),
     "td_generate": (ctypes.c_int, [_P, _I64, _U64, _I32, _D, _D, _I64, _P, _I32, _P, _P, _I32, _P]),

@@ -702,6 +702,85 @@ k_finalize(const td_id_desc* __restrict__ ids, const td_group_desc* __restrict__
     }
 }
 
+// rel_err_arrays(a, b) of two contiguous arrays in ONE launch (tensor.py:
+// 158-167, the reference's basic compare): a grid-stride stream of 16-byte
+// vectors (U=4 per operand in flight), fp64 d2 / a2 per thread, CTA sums to
+// per-CTA partials, and the last CTA to finish (atomic ticket) reduces the
+// partials in CTA order and applies the reference's zero conventions.  No
+// planner, no second launch: the public API's latency for one pair is one
+// kernel + one 24-byte D2H.  Deterministic for a given (n, grid).
+template <int DT>
+__global__ void __launch_bounds__(BLOCK, 4)
+k_rel_err(const char* __restrict__ a, const char* __restrict__ b, int64_t n, double* __restrict__ part,
+          unsigned int* __restrict__ ticket, double* __restrict__ out) {
+    __shared__ double red[NWARP];
+    __shared__ bool last;
+    constexpr int Q = DT == TD_F64 ? 1 : Vec<DT == TD_F64 ? TD_F32 : DT>::Q;
+    constexpr int ES = DT == TD_F32 ? 4 : (DT == TD_F64 ? 8 : 2);
+    constexpr int U = 4 / Q;
+    double d2 = 0.0, a2 = 0.0;
+    const bool vec = DT != TD_F64 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+    const int64_t nv = vec ? n / 8 : 0;
+    if constexpr (DT != TD_F64) {
+        const int64_t stride = (int64_t)gridDim.x * BLOCK;
+        for (int64_t v0 = (int64_t)blockIdx.x * BLOCK + threadIdx.x; v0 < nv; v0 += stride * U) {
+            uint4 xr[U][Q], yr[U][Q];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int64_t v = v0 + k * stride;
+                if (v < nv) {
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) {
+                        xr[k][q] = ld_stream(a + (v * 8) * ES + 16 * q);
+                        yr[k][q] = ld_stream(b + (v * 8) * ES + 16 * q);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                if (v0 + k * stride >= nv) continue;
+#pragma unroll
+                for (int e8 = 0; e8 < 8; ++e8) {
+                    const double xv = Vec<DT>::at(xr[k], e8);
+                    const double d = xv - Vec<DT>::at(yr[k], e8);
+                    d2 = fma(d, d, d2);
+                    a2 = fma(xv, xv, a2);
+                }
+            }
+        }
+    }
+    for (int64_t i = nv * 8 + (int64_t)blockIdx.x * BLOCK + threadIdx.x; i < n; i += (int64_t)gridDim.x * BLOCK) {
+        const double xv = load_elem(a, DT, i);
+        const double d = xv - load_elem(b, DT, i);
+        d2 = fma(d, d, d2);
+        a2 = fma(xv, xv, a2);
+    }
+    d2 = cta_sum(d2, red);
+    a2 = cta_sum(a2, red);
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = d2;
+        part[2 * blockIdx.x + 1] = a2;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double s0 = 0.0, s1 = 0.0;
+    for (int c = threadIdx.x; c < (int)gridDim.x; c += BLOCK) {
+        s0 += __ldcg(part + 2 * c);
+        s1 += __ldcg(part + 2 * c + 1);
+    }
+    s0 = cta_sum(s0, red);
+    s1 = cta_sum(s1, red);
+    if (threadIdx.x == 0) {
+        out[0] = s0;
+        out[1] = s1;
+        out[2] = rel_from_sums(s0, s1);
+        *ticket = 0u;                     // ready for the next call
+    }
+}
+
 // First level of the slot reduction (td_reduce_chunks): 320 threads = 10
 // warps, thread t owns partial column t % 10 and walks the chunk's rows as
 // one flat, fully coalesced double array (320 is a multiple of the row
@@ -1353,6 +1432,28 @@ int td_verdict(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups
                      (cudaStream_t)stream, ids, n_ids, groups, id_sums, group_sums, kappa, eps, replica_eps,
                      id_out, group_out, near_ties);
     return check_launch("td_verdict");
+}
+
+int td_rel_err(const void* a, const void* b, int32_t dtype, int64_t n, void* work, double* out, void* stream) {
+    if (!a || !b || !work || !out || n < 0 || dtype < 0 || dtype > 3) return fail("td_rel_err: invalid arguments");
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t per = dtype == TD_F64 ? 1 : 8;            // elements per work item
+    int64_t grid = (n / per + BLOCK - 1) / BLOCK;
+    grid = std::max<int64_t>(1, std::min<int64_t>(grid, std::min<int64_t>((int64_t)sms * 4, TD_REL_ERR_MAX_CTAS)));
+    double* part = static_cast<double*>(work);
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(part + 2 * TD_REL_ERR_MAX_CTAS);
+    const char* pa = static_cast<const char*>(a);
+    const char* pb = static_cast<const char*>(b);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (dtype) {
+        case TD_BF16: k_rel_err<TD_BF16><<<(unsigned)grid, BLOCK, 0, st>>>(pa, pb, n, part, ticket, out); break;
+        case TD_F16: k_rel_err<TD_F16><<<(unsigned)grid, BLOCK, 0, st>>>(pa, pb, n, part, ticket, out); break;
+        case TD_F32: k_rel_err<TD_F32><<<(unsigned)grid, BLOCK, 0, st>>>(pa, pb, n, part, ticket, out); break;
+        default: k_rel_err<TD_F64><<<(unsigned)grid, BLOCK, 0, st>>>(pa, pb, n, part, ticket, out); break;
+    }
+    return check_launch("td_rel_err");
 }
 
 int td_reduce_chunks(const double* partials, const td_chunk* chunks, int64_t n_chunks, double* out,

@@ -189,11 +189,35 @@ def _one_group(ident, records, numeric):
     return meta
 
 
+_REL_ERR_WORK: dict = {}
+
+
+def pair_sums(ta, tb) -> tuple[float, float, float]:
+    """(sum (a-b)^2, sum a^2, rel_err) of two contiguous same-dtype CUDA
+    tensors: td_rel_err, one launch and one 24-byte D2H."""
+    import torch
+    dev = ta.device
+    work = _REL_ERR_WORK.get(dev)
+    if work is None:
+        work = _REL_ERR_WORK[dev] = (torch.zeros(N.REL_ERR_WORK_BYTES, dtype=torch.uint8, device=dev),
+                                     torch.zeros(3, dtype=torch.float64, device=dev))
+    N.call("td_rel_err", ta.data_ptr(), tb.data_ptr(), N.dtype_code(ta), ta.numel(),
+           work[0].data_ptr(), work[1].data_ptr(), N.stream_handle())
+    d2, a2, rel = work[1].tolist()
+    return d2, a2, rel
+
+
 def rel_err_pair(a, b) -> float:
     """rel_err_arrays(a, b) on the GPU: ||a - b|| / ||a|| with the reference's
-    zero conventions (tensor.py:158-167).  Shapes must already agree."""
+    zero conventions (tensor.py:158-167).  Shapes must already agree.
+
+    Same-dtype operands take td_rel_err (one launch, one 24-byte D2H);
+    mixed dtypes go through a one-id plan (widening in the compare pass)."""
     from .plan import Plan, PlanEntry
-    ra, rb = _Raw(to_device(a).reshape(-1)), _Raw(to_device(b).reshape(-1))
+    ta, tb = to_device(a).reshape(-1), to_device(b).reshape(-1)
+    if ta.dtype == tb.dtype:
+        return pair_sums(ta, tb)[2]
+    ra, rb = _Raw(ta), _Raw(tb)
     plan = Plan([PlanEntry("pair", x=_one_group("pair", [ra], False),
                            y=_one_group("pair", [rb], False), x_rep=False, y_rep=False)])
     ptrs, keep = resolve_operands(plan.operands, plan.operand_dtypes)

@@ -91,16 +91,10 @@ def rel_err(a: Tensor, b: Tensor) -> float:
 
 def frobenius_norm(a: Tensor) -> float:
     """sqrt(sum a^2) (tensor.py:144-145): the reference-norm sum of a
-    self-compare plan (x = y = a), reduced on the GPU."""
-    from .device import _Raw, _one_group, resolve_operands, to_device
-    from .plan import Plan, PlanEntry
-    ra = _Raw(to_device(a.data).reshape(-1))
-    plan = Plan([PlanEntry("norm", x=_one_group("norm", [ra], False),
-                           y=_one_group("norm", [ra], False), x_rep=False, y_rep=False)])
-    ptrs, keep = resolve_operands(plan.operands, plan.operand_dtypes)
-    sums = {}
-    plan.run(ptrs, sums=sums)
-    return float(np.sqrt(sums["id"][0, 1]))
+    self-compare (td_rel_err with b = a), reduced on the GPU."""
+    from .device import pair_sums, to_device
+    ta = to_device(a.data).reshape(-1)
+    return float(np.sqrt(pair_sums(ta, ta)[1]))
 
 
 def quantize_array(x, fmt: FloatFormat) -> np.ndarray:

@@ -476,3 +476,30 @@ def test_two_level_slot_reduction_matches_oracle(monkeypatch, cases, golden_trac
                        r.replica_group_size, np.asarray(r.values(), np.float32)) for r in cand.records]
         want = O.check(oref, ocand, ref.header, cand.header, {}, 3.0, "BF16")
         assert_reports_match(json.loads(td.render_report(rep, "json")), want, f"chunked case {i}")
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16, torch.float32, torch.float64])
+def test_rel_err_one_launch_vs_fp64(dtype):
+    """td_rel_err (the same-dtype fast path of rel_err_arrays): aligned and
+    misaligned views, lengths that are not a multiple of the vector, sizes
+    from 1 element to beyond one grid stride, against a torch fp64 reduction;
+    repeated calls are bit-identical."""
+    g = torch.Generator(device="cuda").manual_seed(11)
+    for n in (1, 7, 8, 1000, 4096 + 3, (1 << 20) + 5, (1 << 24) + 9):
+        base = torch.randn(n + 1, device="cuda", generator=g, dtype=torch.float64)
+        a = base.to(dtype)
+        b = (base * (1 + 0.01 * torch.randn(n + 1, device="cuda", generator=g, dtype=torch.float64))).to(dtype)
+        for off in (0, 1):
+            x, y = a[off:off + n], b[off:off + n]
+            want = float(torch.linalg.vector_norm(x.double() - y.double()) / torch.linalg.vector_norm(x.double()))
+            got = td.rel_err_arrays(x, y)
+            assert abs(got - want) <= 1e-12 * want, (dtype, n, off, got, want)
+            assert td.rel_err_arrays(x, y) == got
+    z = torch.zeros(100, device="cuda", dtype=dtype)
+    o = torch.ones(100, device="cuda", dtype=dtype)
+    assert td.rel_err_arrays(z, z) == 0.0
+    assert td.rel_err_arrays(z, o) == math.inf
+    assert td.rel_err_arrays(o, z) == 1.0
+    nan = o.clone()
+    nan[3] = float("nan")
+    assert math.isnan(td.rel_err_arrays(o, nan))
