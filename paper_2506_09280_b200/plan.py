@@ -80,8 +80,7 @@ def id_meta(ident: str, entries: list, replica_check: bool = True) -> IdMeta:
     meta.global_shape = hull
     buckets: dict[tuple, list] = {}
     for _, rec in entries:
-        key = (rec.mapping.local_shape,
-               tuple((loc.bounds, glob.bounds) for loc, glob in rec.mapping.pairs))
+        key = (rec.mapping.local_shape, rec.mapping.pairs_bounds)
         buckets.setdefault(key, []).append(rec)
     for recs in buckets.values():
         detail = None
@@ -558,26 +557,32 @@ class Plan:
         self.seg_zslot = np.full((n, N.MAX_Z), -1, np.int64)
         tile_seg = np.zeros(self.n_tiles, np.int32)
         class_tiles: dict = {}
+        cols = {k: [0] * n for k in ("x_stride", "y_stride", "rows", "cols", "tile_begin", "n_units", "x_dtype",
+                                     "y_dtype", "nz", "flags", "div_m", "div_p", "y_word0", "digest_slot")}
+        xslot, xoff, yslot, yoff = [-1] * n, [0] * n, [0] * n, [0] * n
+        shift_bits = self.tile_shift << N.SEG_TILE_SHIFT_POS
         for i, (x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec, ds) in enumerate(rows):
-            s = segs[i]
-            s["x_stride"], s["y_stride"], s["rows"], s["cols"] = rx, ry, r, c
-            s["tile_begin"], s["n_units"] = tb, nu
-            s["x_dtype"] = x.dtype if x is not None else y.dtype
-            s["y_dtype"], s["nz"] = y.dtype, len(zs)
-            s["flags"] = ((N.SEG_HAS_X if x is not None else 0) | (N.SEG_VEC if vec else 0)
-                          | (self.tile_shift << N.SEG_TILE_SHIFT_POS))
-            m, p = _magic(c // 8 if vec else c)
-            s["div_m"], s["div_p"] = m, p
-            s["y_word0"], s["digest_slot"] = (yo * y.esize) // 8, ds
+            cols["x_stride"][i], cols["y_stride"][i], cols["rows"][i], cols["cols"][i] = rx, ry, r, c
+            cols["tile_begin"][i], cols["n_units"][i] = tb, nu
+            cols["x_dtype"][i] = x.dtype if x is not None else y.dtype
+            cols["y_dtype"][i], cols["nz"][i] = y.dtype, len(zs)
+            cols["flags"][i] = ((N.SEG_HAS_X if x is not None else 0) | (N.SEG_VEC if vec else 0) | shift_bits)
+            cols["div_m"][i], cols["div_p"][i] = _magic(c // 8 if vec else c)
+            cols["y_word0"][i], cols["digest_slot"][i] = (yo * y.esize) // 8, ds
             if x is not None:
-                self.seg_xslot[i], self.seg_xoff[i] = x.slot, xo * x.esize
-            self.seg_yslot[i], self.seg_yoff[i] = y.slot, yo * y.esize
+                xslot[i], xoff[i] = x.slot, xo * x.esize
+            yslot[i], yoff[i] = y.slot, yo * y.esize
             for j, z in enumerate(zs):
                 self.seg_zslot[i, j] = z.slot
             nt = -(-nu // self.tile_units)
             tile_seg[tb:tb + nt] = i
             key = (bool(vec), y.dtype, len(zs), x is not None, ds >= 0)
             class_tiles.setdefault(key, []).append((tb, nt))
+        if n:
+            for k, v in cols.items():
+                segs[k] = v
+            self.seg_xslot[:], self.seg_xoff[:] = xslot, xoff
+            self.seg_yslot[:], self.seg_yoff[:] = yslot, yoff
         self.segs = segs
         self.tile_seg = tile_seg
         self.class_keys = sorted(class_tiles)
