@@ -30,6 +30,12 @@ def to_device(x, stream=None):
     """A contiguous, 16-byte-aligned CUDA tensor holding x's values in x's
     own dtype (numpy arrays keep their dtype; f64 stays f64)."""
     import torch
+    if is_torch(x) and x.device.type == "cuda":
+        # already resident (the common case, called per operand per check):
+        # no availability probe
+        if not x.is_contiguous():
+            x = x.contiguous()
+        return x if x.data_ptr() % 16 == 0 else x.clone()
     if not torch.cuda.is_available():
         raise N.NativeError("no CUDA device: the B200 compare path cannot run here")
     if not is_torch(x):

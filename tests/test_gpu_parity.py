@@ -503,3 +503,29 @@ def test_rel_err_one_launch_vs_fp64(dtype):
     nan = o.clone()
     nan[3] = float("nan")
     assert math.isnan(td.rel_err_arrays(o, nan))
+
+
+def test_check_plan_cache_same_layout(cases, golden_trace_bytes):
+    """check() reuses the plan of an earlier check of the same layout and
+    binds the new payloads by position: the report equals a fresh plan's;
+    a different tolerance map or kappa is a different plan."""
+    from paper_2506_09280_b200 import checker
+    case = next(c for c in cases["checks"] if c["name"] == "bug_tp_row_allreduce_k3")
+    ref = trace_from_bytes(golden_trace_bytes(case["ref"]), device="cuda")
+    cand = trace_from_bytes(golden_trace_bytes(case["cand"]), device="cuda")
+    tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+    fmt = td.FloatFormat(case["fmt"])
+    checker._PLAN_CACHE.clear()
+    first = td.render_report(td.check(ref, cand, tol, case["kappa"], fmt=fmt), "json")
+    assert len(checker._PLAN_CACHE) == 1
+    # same layout, other values: every candidate payload scaled
+    cand2 = Trace(header=cand.header, raw_header=cand.raw_header)
+    cand2.records = [TraceRecord(r.id, r.rank_meta, r.mapping, r.replica_group_size, r.payload * 1.5,
+                                 r.module_class) for r in cand.records]
+    hit = td.render_report(td.check(ref, cand2, tol, case["kappa"], fmt=fmt), "json")
+    assert len(checker._PLAN_CACHE) == 1
+    checker._PLAN_CACHE.clear()
+    fresh = td.render_report(td.check(ref, cand2, tol, case["kappa"], fmt=fmt), "json")
+    assert hit == fresh and hit != first
+    td.check(ref, cand, tol, case["kappa"] * 2, fmt=fmt)
+    assert len(checker._PLAN_CACHE) == 2
