@@ -609,7 +609,9 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "seconds_per_step": float(t_e2e.item()),
                "layer_checks_per_s": n_ids * world / float(t_e2e.item()),
-               "verdicts": rep.counts}
+               "verdicts": rep.counts,
+               "plan": "check()'s layout-keyed plan cache: planned by the warm-up call, reused by the "
+                       "timed calls (same layout every step; the payloads cross PCIe every step)"}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         if e2e is not None and e2e.get("value") is not None:
