@@ -43,7 +43,7 @@ sys.path.insert(0, ROOT)
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg2")
@@ -150,10 +150,13 @@ class ClockSampler:
 
     def _run(self):
         nv, h = self._nvml
+        try:
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception:
+            mx = None
         while True:
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
                 try:
                     reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except AttributeError:
@@ -185,7 +188,8 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
         reasons = sorted({name for _, _, r in self.samples for bit, name in self.REASONS.items() if r & bit})
         return {"sm_mhz": statistics.median(s[0] for s in self.samples),
-                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "sm_max_mhz": max((s[1] for s in self.samples if s[1] is not None), default=None),
+                "reasons": reasons,
                 "samples": len(self.samples)}
 
 
