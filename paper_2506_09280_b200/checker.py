@@ -330,7 +330,7 @@ _PLAN_CACHE_SIZE = 4
 
 def _check_key(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float, fmt: FloatFormat) -> tuple:
     return (_layout_key(ref), _layout_key(cand), ref.header.get("mode"), cand.header.get("mode"),
-            hash(frozenset(tol.responses.items())), len(tol.responses), float(kappa), fmt)
+            frozenset(tol.responses.items()), float(kappa), fmt)
 
 
 def _strict_problem(view, plan: Plan, gres, side_of_entry: dict) -> str | None:
