@@ -1,4 +1,5 @@
-"""Config 3 at its full BASELINE size (Llama-3-1B shape, S=8192, TP=8, 69 GB
+"""BASELINE configs at full size.  Configs 1 and 2 (2.8 GB, 8.2 GB) run the CPU
+oracle on the whole trace: identical reports.  Config 3 (Llama-3-1B shape, S=8192, TP=8, 69 GB
 of bf16 traces in HBM) with the three injected bugs.  Too big for the CPU
 oracle, so the checks are size-independent: the verdicts are exactly the
 injections, and the observed rel_err of the bug ids and of a sample of clean
@@ -68,3 +69,52 @@ def test_config3_full_size_injections_and_fp64_norms():
     # the scale bug multiplies by tp = 8 exactly: rel_err of 8x vs x is 7 up
     # to the simulated round-off
     assert abs(verdicts[[k for k, v in BUGS.items() if v == "scale"][0]].observed - 7.0) < 0.1
+
+
+def test_config1_full_size_against_cpu_oracle():
+    """Config 1 at its full size (GPT-2-small shape, L=2, S=1024, V=50304,
+    fp32, TP=2 candidate: 123 ids, 2.8 GB) — small enough for the CPU
+    oracle on the whole trace: identical report (verdicts, details,
+    thresholds; observed within 1e-12)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+
+    import paper_2506_09280_b200 as td
+    from oracle import traindiff_oracle as O
+    from paper_2506_09280_b200 import layout as L, synthetic
+    from tests.test_configs_gpu import _oracle_recs
+    from tests.test_gpu_parity import assert_reports_match
+    eps = td.FloatFormat.FP32.eps
+    ref, cand = synthetic.build(L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), dtype=torch.float32, eps=eps, seed=1)
+    tol = td.ToleranceMap({r.id.encode(): 2 * eps for r in ref.records}, n_samples=1, eps_p=eps)
+    rep = td.check(ref, cand, tol, fmt=td.FloatFormat.FP32)
+    assert len(rep.entries) == 123
+    want = O.check(_oracle_recs(ref), _oracle_recs(cand), ref.header, cand.header, tol.responses, 3.0, "FP32")
+    assert_reports_match(json.loads(td.render_report(rep, "json")), want, "config1 full size")
+
+
+def test_config2_full_size_against_cpu_oracle():
+    """Config 2, the bench workload, at its full size (GPT-2-medium shape,
+    bf16, TP=4 candidate: 1179 ids, 8.2 GB) against the CPU oracle on the
+    whole trace (~40 s of numpy): identical report."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+
+    import paper_2506_09280_b200 as td
+    from oracle import traindiff_oracle as O
+    from paper_2506_09280_b200 import layout as L, synthetic
+    from tests.test_configs_gpu import _oracle_recs
+    from tests.test_gpu_parity import assert_reports_match
+    eps = td.FloatFormat.BF16.eps
+    ref, cand = synthetic.build(L.GPT2_MEDIUM, L.ParallelConfig(tp=4), eps=eps, seed=2)
+    tol = td.ToleranceMap({r.id.encode(): 2 * eps for r in ref.records}, n_samples=1, eps_p=eps)
+    rep = td.check(ref, cand, tol, fmt=td.FloatFormat.BF16)
+    assert len(rep.entries) == 1179 and rep.near_ties == 0
+    got = json.loads(td.render_report(rep, "json"))
+    rrecs, crecs, rh, ch = _oracle_recs(ref), _oracle_recs(cand), ref.header, cand.header
+    del ref, cand
+    torch.cuda.empty_cache()
+    want = O.check(rrecs, crecs, rh, ch, tol.responses, 3.0, "BF16")
+    assert_reports_match(got, want, "config2 full size")
