@@ -54,6 +54,11 @@ def parse_args():
     return ap.parse_args()
 
 
+# measured pure-read HBM stream (tools/hbm_probe.cu read_xor, 2 x 4 GiB,
+# 16-B ld.global.nc.L1::no_allocate; profiles/r1_summary.md): 7246-7273 GB/s
+READ_CEILING_GBS = 7246.0
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -652,7 +657,11 @@ def main():
                              "frac": achieved / hbm, "traffic": traffic,
                              "kernel": "td_segnorm (k_segnorm_vec / k_segnorm_generic)",
                              "kernel_ms": seg_avg, "peak_source": peak_kind,
-                             "frac_of_8TBps_spec": achieved / 8000.0},
+                             "frac_of_8TBps_spec": achieved / 8000.0,
+                             # a read-only stream beats the copy peak (no write turnaround):
+                             # tools/hbm_probe.cu's 16-B read ceiling on this pool's B200s
+                             "read_ceiling_gbs": READ_CEILING_GBS,
+                             "frac_of_read_ceiling": achieved / READ_CEILING_GBS},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
