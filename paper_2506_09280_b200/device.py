@@ -111,14 +111,15 @@ def stage_host_payloads(traces, stream=None) -> dict:
     import torch
     staged: dict = {}
     arenas: dict = {}
+    tensor = torch.Tensor
     for trace in traces:
         for rec in trace.records:
             p = rec.payload
+            if isinstance(p, tensor) and p.is_cuda:
+                continue                      # resident: nothing to stage
             if id(rec) in staged:
                 continue
             if is_torch(p):
-                if p.device.type == "cuda":
-                    continue
                 if p.is_pinned():
                     st = p.untyped_storage()
                     entry = arenas.get(st.data_ptr())
@@ -153,6 +154,9 @@ def resolve_operands(operands, dtypes=None, staged: dict | None = None) -> tuple
     if _TORCH_DTYPES is None:
         _TORCH_DTYPES = {N.F32: torch.float32, N.BF16: torch.bfloat16,
                          N.F16: torch.float16, N.F64: torch.float64}
+    fast = _resolve_resident(operands, dtypes, staged)
+    if fast is not None:
+        return fast
     keep = []
     ptrs = np.zeros(len(operands), np.uint64)
     memo: dict = {}
@@ -169,6 +173,29 @@ def resolve_operands(operands, dtypes=None, staged: dict | None = None) -> tuple
         keep.append(t)
         ptrs[k] = t.data_ptr()
     return ptrs, keep
+
+
+def _resolve_resident(operands, dtypes, staged):
+    """resolve_operands when every operand is a record whose payload is
+    already a contiguous CUDA tensor of the wanted dtype (device-resident
+    traces: torchtap captures, read_trace(device="cuda")): pointers in one
+    pass, alignment checked in bulk.  None when any operand needs the general
+    path (host payload, staged copy, widening, misalignment)."""
+    import torch
+    if staged or dtypes is None:
+        return None
+    try:
+        payloads = [o.payload for o in operands]
+    except AttributeError:
+        return None
+    want = [_TORCH_DTYPES[d] for d in dtypes]
+    for t, w in zip(payloads, want):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype is w and t.is_contiguous()):
+            return None
+    ptrs = np.fromiter((t.data_ptr() for t in payloads), dtype=np.uint64, count=len(payloads))
+    if len(ptrs) and (ptrs % 16).any():
+        return None
+    return ptrs, payloads
 
 
 class _Raw:

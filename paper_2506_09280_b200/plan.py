@@ -679,10 +679,22 @@ class Prepared:
         if chunked:
             put(plan.chunks)
         blob = np.concatenate(parts) if parts else np.zeros(16, np.uint8)
-        host = torch.from_numpy(blob).pin_memory()
+        # one pinned staging buffer per plan, reused by every binding of it
+        # (cudaHostAlloc per check cost ~ms); the previous copy out of it must
+        # have completed before it is overwritten
+        staging, done = getattr(plan, "_staging", (None, None))
+        if staging is None or staging.numel() < blob.size:
+            staging = torch.empty(blob.size, dtype=torch.uint8).pin_memory()
+        elif done is not None:
+            done.synchronize()
+        host = staging[:blob.size]
+        host.numpy()[:] = blob
         self.tables = torch.empty(blob.size, dtype=torch.uint8, device=dev)
         with torch.cuda.stream(self.stream):
             self.tables.copy_(host, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(self.stream)
+        plan._staging = (staging, done)
         self._host_blob = host                    # keep the pinned source alive
         base = self.tables.data_ptr()
         self.seg_ptr = base + offsets[0]
