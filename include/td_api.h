@@ -158,7 +158,10 @@ typedef struct td_class {
     double  atol;               /* static mode: count |y - x| > atol + rtol*|x| into d2 */
     double  rtol;
     unsigned long long* digests; /* device, 2 u64 per digest slot, accumulated (caller zeroes) */
-} td_class;                     /* 64 bytes */
+    const struct td_segment* host_seg; /* HOST copy of the class's only segment (its tiles are
+                                   that segment's, in order), or NULL: passed to the kernel by
+                                   value, so no tile list / descriptor load precedes the data */
+} td_class;                     /* 72 bytes */
 
 #define TD_MODE_NORMS 0
 #define TD_MODE_STATIC 1        /* compare_static's elementwise test (checker.py:403-443) */

@@ -55,11 +55,11 @@ CHUNK = np.dtype([("row_begin", "<i8"), ("row_end", "<i8"), ("k0", "<i4"), ("nk"
 assert CHUNK.itemsize == 24
 CLASS = np.dtype([("tiles", "<u8"), ("n_tiles", "<i8"), ("dtype", "<i4"), ("nz", "<i4"),
                   ("has_x", "<i4"), ("vec", "<i4"), ("mode", "<i4"), ("digest", "<i4"),
-                  ("atol", "<f8"), ("rtol", "<f8"), ("digests", "<u8")])
+                  ("atol", "<f8"), ("rtol", "<f8"), ("digests", "<u8"), ("host_seg", "<u8")])
 MODE_NORMS, MODE_STATIC = 0, 1
 
 assert SEGMENT.itemsize == 160 and ID_DESC.itemsize == 56 and GROUP_DESC.itemsize == 24
-assert ID_RESULT.itemsize == 32 and GROUP_RESULT.itemsize == 16 and CLASS.itemsize == 64
+assert ID_RESULT.itemsize == 32 and GROUP_RESULT.itemsize == 16 and CLASS.itemsize == 72
 
 # every function the header declares, with its ctypes signature
 _P = ctypes.c_void_p

@@ -212,22 +212,34 @@ __device__ __forceinline__ double warp_sum(double v) {
 __device__ __forceinline__ int entry_seg(int64_t e) { return (int)(e >> 32); }
 __device__ __forceinline__ int64_t entry_tile(int64_t e) { return e & 0xffffffffll; }
 
+// a segment-descriptor field: from the global table (read-only path), or —
+// PARAM, a single-segment class — from the kernel's __grid_constant__
+// parameter copy, so the first tile starts without two dependent DRAM round
+// trips (tile list, then descriptor)
+template <bool PARAM, typename T>
+__device__ __forceinline__ T rd(const T* p) {
+    if constexpr (PARAM) return *p;
+    else return __ldg(p);
+}
+
+template <bool PARAM = false>
 __device__ __forceinline__ int64_t tile_units(const td_segment* g) {
-    const int sh = (__ldg(&g->flags) >> TD_SEG_TILE_SHIFT_POS) & 31;
+    const int sh = (rd<PARAM>(&g->flags) >> TD_SEG_TILE_SHIFT_POS) & 31;
     return sh ? (int64_t)1 << sh : (int64_t)TD_TILE_UNITS;
 }
 
+template <bool PARAM = false>
 __device__ __forceinline__ void load_desc(const td_segment* __restrict__ g, SegView& S, int nz_max) {
-    S.x = reinterpret_cast<const char*>(__ldg(&g->x));
-    S.y = reinterpret_cast<const char*>(__ldg(&g->y));
+    S.x = reinterpret_cast<const char*>(rd<PARAM>(&g->x));
+    S.y = reinterpret_cast<const char*>(rd<PARAM>(&g->y));
 #pragma unroll
     for (int j = 0; j < TD_MAX_Z; ++j)
-        S.z[j] = j < nz_max ? reinterpret_cast<const char*>(__ldg(&g->z[j])) : nullptr;
-    S.xs = __ldg(&g->x_stride);
-    S.ys = __ldg(&g->y_stride);
-    S.cols = __ldg(&g->cols);
-    S.div_m = __ldg(&g->div_m);
-    S.div_p = __ldg(&g->div_p);
+        S.z[j] = j < nz_max ? reinterpret_cast<const char*>(rd<PARAM>(&g->z[j])) : nullptr;
+    S.xs = rd<PARAM>(&g->x_stride);
+    S.ys = rd<PARAM>(&g->y_stride);
+    S.cols = rd<PARAM>(&g->cols);
+    S.div_m = rd<PARAM>(&g->div_m);
+    S.div_p = rd<PARAM>(&g->div_p);
 }
 
 // warp-level partial: lane 0 writes the first `used` fixed-order sums
@@ -251,10 +263,13 @@ __device__ __forceinline__ void write_warp_partial(const Acc& a, int used, doubl
 // Hashing in the loads' registers needs U=2 to stay at 64 registers; a second
 // pass over the warp's tile slice from L2 instead (U=4 compare loop) measured
 // 18% slower on the config-4 share, U=4 at 3 CTAs/SM 5% slower.
-template <int DT, int NZ, bool HX, int U, int MINB, bool DG = false>
+// ONE: the class is one segment, passed by value (seg1) — tile i of the
+// class is global tile seg1.tile_begin + i, no tile list, no descriptor load.
+template <int DT, int NZ, bool HX, int U, int MINB, bool DG = false, bool ONE = false>
 __global__ void __launch_bounds__(BLOCK, MINB)
 k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ tiles, int64_t n,
-              double* __restrict__ partials, unsigned long long* __restrict__ digests) {
+              double* __restrict__ partials, unsigned long long* __restrict__ digests,
+              const __grid_constant__ td_segment seg1) {
     constexpr int Q = Vec<DT>::Q;
     constexpr int ES = (DT == TD_F32) ? 4 : 2;
     constexpr int USED = NZ > 0 ? 3 + NZ : 2;
@@ -263,20 +278,27 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
     constexpr bool SKIP = TD_REPLICA_SKIP && NZ >= TD_REPLICA_SKIP_MIN_NZ && Q == 1;
     const int warp = threadIdx.x >> 5;
     for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const int64_t e = __ldg(tiles + i);
-        const int64_t t = entry_tile(e);
-        const td_segment* g = segs + entry_seg(e);
+        int64_t t;
+        const td_segment* g;
+        if constexpr (ONE) {
+            g = &seg1;
+            t = seg1.tile_begin + i;
+        } else {
+            const int64_t e = __ldg(tiles + i);
+            t = entry_tile(e);
+            g = segs + entry_seg(e);
+        }
         SegView S;
-        load_desc(g, S, NZ);
+        load_desc<ONE>(g, S, NZ);
         const uint32_t vpr = (uint32_t)(S.cols >> 3);
-        const int64_t tu = tile_units(g);
-        const int64_t first = (t - __ldg(&g->tile_begin)) * tu;
+        const int64_t tu = tile_units<ONE>(g);
+        const int64_t first = (t - rd<ONE>(&g->tile_begin)) * tu;
         const uint32_t u0 = (uint32_t)first;
-        const uint32_t u1 = (uint32_t)min(first + tu, __ldg(&g->n_units));
+        const uint32_t u1 = (uint32_t)min(first + tu, rd<ONE>(&g->n_units));
         Acc a;
         a.zero();
         uint64_t h0 = 0, h1 = 0;
-        const int64_t w0 = DG ? __ldg(&g->y_word0) : 0;
+        const int64_t w0 = DG ? rd<ONE>(&g->y_word0) : 0;
         for (uint32_t base = u0 + threadIdx.x; base < u1; base += BLOCK * U) {
             uint4 xr[U][Q];
             uint4 yr[U][Q];
@@ -358,7 +380,7 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
                 h0 += __shfl_xor_sync(0xffffffffu, h0, o);
                 h1 += __shfl_xor_sync(0xffffffffu, h1, o);
             }
-            const int slot = __ldg(&g->digest_slot);
+            const int slot = rd<ONE>(&g->digest_slot);
             if ((threadIdx.x & 31) == 0 && slot >= 0) {
                 atomicAdd(digests + 2 * slot, (unsigned long long)h0);
                 atomicAdd(digests + 2 * slot + 1, (unsigned long long)h1);
@@ -426,7 +448,7 @@ k_segnorm_generic(const td_segment* __restrict__ segs, const int64_t* __restrict
     griddep_launch_dependents();
 }
 
-typedef void (*segnorm_fn)(const td_segment*, const int64_t*, int64_t, double*, unsigned long long*);
+typedef void (*segnorm_fn)(const td_segment*, const int64_t*, int64_t, double*, unsigned long long*, td_segment);
 
 static_assert(sizeof(td_segment) == 160, "td_segment layout");
 static_assert(BLOCK / 32 == TD_WARPS_PER_TILE, "one partial row per warp of a tile");
@@ -434,7 +456,7 @@ static_assert(sizeof(td_id_desc) == 56, "td_id_desc layout");
 static_assert(sizeof(td_group_desc) == 24, "td_group_desc layout");
 static_assert(sizeof(td_id_result) == 32, "td_id_result layout");
 static_assert(sizeof(td_group_result) == 16, "td_group_result layout");
-static_assert(sizeof(td_class) == 64, "td_class layout");
+static_assert(sizeof(td_class) == 72, "td_class layout");
 static_assert(sizeof(td_chunk) == 24, "td_chunk layout");
 
 #ifndef TD_NZ7_U
@@ -465,10 +487,14 @@ static_assert(sizeof(td_chunk) == 24, "td_chunk layout");
 #define TD_DG_MINB 4
 #endif
 template <int DT>
-segnorm_fn pick_vec(int nz, bool hx, bool dg) {
+segnorm_fn pick_vec(int nz, bool hx, bool dg, bool one = false) {
     constexpr int Q = Vec<DT>::Q;
     constexpr int U4 = 4 / Q > 0 ? 4 / Q : 1;
     constexpr int U2 = 2 / Q > 0 ? 2 / Q : 1;
+    if (one)   // single-segment compare classes (one tensor per side)
+        return (hx && nz == 0 && !dg)
+                   ? k_segnorm_vec<DT, 0, true, (TD_NZ0_U / Q > 0 ? TD_NZ0_U / Q : 1), TD_NZ0_MINB, false, true>
+                   : nullptr;
     if (dg)   // compares of cross-GPU replica groups: copy 0 alone (nz = 0)
         return (hx && nz == 0)
                    ? k_segnorm_vec<DT, 0, true, (TD_DG_U / Q > 0 ? TD_DG_U / Q : 1), TD_DG_MINB, true>
@@ -1387,17 +1413,21 @@ int td_segnorm(const td_segment* segs, const td_class* classes, int32_t n_classe
         }
         segnorm_fn fn = nullptr;
         {
+            const bool one = C.host_seg != nullptr && C.nz == 0 && C.has_x && !C.digest;
             switch (C.dtype) {
-                case TD_BF16: fn = pick_vec<TD_BF16>(C.nz, C.has_x != 0, C.digest != 0); break;
-                case TD_F16: fn = pick_vec<TD_F16>(C.nz, C.has_x != 0, C.digest != 0); break;
-                case TD_F32: fn = pick_vec<TD_F32>(C.nz, C.has_x != 0, C.digest != 0); break;
+                case TD_BF16: fn = pick_vec<TD_BF16>(C.nz, C.has_x != 0, C.digest != 0, one); break;
+                case TD_F16: fn = pick_vec<TD_F16>(C.nz, C.has_x != 0, C.digest != 0, one); break;
+                case TD_F32: fn = pick_vec<TD_F32>(C.nz, C.has_x != 0, C.digest != 0, one); break;
                 default: break;
             }
             if (!fn) return fail("td_segnorm: no vector walker for class %d (dtype=%d nz=%d has_x=%d digest=%d)",
                                  c, C.dtype, C.nz, C.has_x, C.digest);
         }
         if (C.digest && !C.digests) return fail("td_segnorm: digest class %d without a digest table", c);
-        fn<<<(unsigned)grid, BLOCK, 0, st>>>(segs, C.tiles, C.n_tiles, partials, C.digests);
+        td_segment seg1;
+        if (C.host_seg) seg1 = *C.host_seg;
+        else memset(&seg1, 0, sizeof(seg1));
+        fn<<<(unsigned)grid, BLOCK, 0, st>>>(segs, C.tiles, C.n_tiles, partials, C.digests, seg1);
         if (int rc = check_launch("td_segnorm")) return rc;
         if (st != main_stream) join_aux(aux, k - 1, main_stream);
     }

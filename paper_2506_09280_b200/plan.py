@@ -586,6 +586,7 @@ class Plan:
         self.segs = segs
         self.tile_seg = tile_seg
         self.class_keys = sorted(class_tiles)
+        self.class_segs = [[int(tile_seg[tb]) for tb, _ in class_tiles[k]] for k in self.class_keys]
         # packed (segment << 32 | tile) entries, grid-stride walked by the kernels
         self.class_lists = [np.concatenate([(np.int64(tile_seg[tb]) << 32) + np.arange(tb, tb + nt, dtype=np.int64)
                                             for tb, nt in class_tiles[k]]) for k in self.class_keys]
@@ -619,6 +620,9 @@ class Plan:
         digests: device address of the (len(fused_digests), 2) u64 table the
         digest classes accumulate into (the caller zeroes it per run)."""
         return Prepared(self, pointers, kappa, eps, replica_eps, stream, digests)
+
+
+_ONE_SEG = os.environ.get("TD_ONE_SEG", "1") != "0"      # A/B switch for by-value single segments
 
 
 class Prepared:
@@ -731,9 +735,17 @@ class Prepared:
             self.digest_table = torch.zeros((self.n_digests, 2), dtype=torch.int64, device=dev)
             digests = self.digest_table.data_ptr()
         self.digest_ptr = digests or 0
+        # single-segment classes hand their (patched) descriptor to the kernel
+        # by value: host copies kept alive with this binding
+        self._one_segs = []
         for k, (vec, dt, nz, hx, dg) in enumerate(plan.class_keys):
+            host_seg = 0
+            if len(plan.class_segs[k]) == 1 and vec and mode == N.MODE_NORMS and _ONE_SEG:
+                one = segs[plan.class_segs[k][0]:plan.class_segs[k][0] + 1].copy()
+                self._one_segs.append(one)
+                host_seg = one.ctypes.data
             self.classes[k] = (base + offsets[1 + k], len(plan.class_lists[k]), dt, nz, int(hx),
-                               int(vec), mode, int(dg), atol, rtol, self.digest_ptr if dg else 0)
+                               int(vec), mode, int(dg), atol, rtol, self.digest_ptr if dg else 0, host_seg)
         self.launches_per_run = len(self.classes) + 1 + (1 if chunked else 0)
         self._events = None
 
