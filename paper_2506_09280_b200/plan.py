@@ -200,6 +200,13 @@ class PlanBuilder:
         same = [y.dtype] + [z.dtype for z in zs] + ([x.dtype] if x is not None else [])
         vec_dtype = (not self.force_generic and same[0] in _VEC_DTYPES
                      and all(d == same[0] for d in same))
+        if rows == 1 and vec_dtype and cols > 8 and cols % 8:
+            # a flat run whose length is not a multiple of the vector (an odd
+            # vocabulary, say): vector head, element-wise tail of < 8 cells
+            head = cols - cols % 8
+            self.add(x, x_off, y, y_off, zs, 1, head, rx, ry)
+            self.add(x, x_off + head, y, y_off + head, zs, 1, cols - head, rx, ry)
+            return
         esize = y.esize
         # row-stride alignment is a property of the layout; base alignment is
         # re-checked against live addresses at run time

@@ -529,3 +529,28 @@ def test_check_plan_cache_same_layout(cases, golden_trace_bytes):
     assert hit == fresh and hit != first
     td.check(ref, cand, tol, case["kappa"] * 2, fmt=fmt)
     assert len(checker._PLAN_CACHE) == 2
+
+
+def test_odd_length_flat_runs_take_the_vector_walker():
+    """A tensor whose element count is not a multiple of 8 (GPT-2's 50257
+    vocabulary) streams through the vector walker with a < 8-cell generic
+    tail; the result equals a torch fp64 reduction."""
+    from paper_2506_09280_b200 import _native as N
+    from paper_2506_09280_b200.checker import CheckPlan
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = torch.randn(1023, 50257, device="cuda", generator=g).to(torch.bfloat16)
+    y = (x.double() * (1 + 2.0 ** -6 * torch.randn(x.shape, device="cuda", generator=g,
+                                                   dtype=torch.float64))).to(torch.bfloat16)
+    ident = CanonicalId(0, 0, TensorKind.ACTIVATION_OUT, "model.lm_head")
+    ref = Trace(header={"digest": "d", "mode": "cascade"})
+    cand = Trace(header={"digest": "d", "mode": "cascade"})
+    ref.records.append(TraceRecord(ident, RankMeta(), identity_mapping(tuple(x.shape)), 1, x, "Linear"))
+    cand.records.append(TraceRecord(ident, RankMeta(), identity_mapping(tuple(y.shape)), 1, y, "Linear"))
+    tol = td.ToleranceMap({ident.encode(): 1.0}, n_samples=1, eps_p=2.0 ** -8)
+    cp = CheckPlan(ref, cand, tol, fmt=td.FloatFormat.BF16)
+    vec = (cp.plan.segs["flags"] & N.SEG_VEC) != 0
+    cells = cp.plan.segs["rows"] * cp.plan.segs["cols"]
+    assert cells[vec].sum() >= x.numel() - 7 and cells[~vec].sum() <= 7
+    rep = td.check(ref, cand, tol, fmt=td.FloatFormat.BF16)
+    want = float(torch.linalg.vector_norm(x.double() - y.double()) / torch.linalg.vector_norm(x.double()))
+    assert abs(rep.entries[0].observed - want) <= 1e-12 * want
