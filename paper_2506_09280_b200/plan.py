@@ -93,15 +93,26 @@ def id_meta(ident: str, entries: list, replica_check: bool = True) -> IdMeta:
             else:
                 numeric = len(recs) > 1
         meta.groups.append(GroupMeta(records=recs, declared_detail=detail, numeric=numeric))
-    meta.merge_detail = _merge_detail(tuple(g.records[0].mapping for g in meta.groups), hull,
-                                      tuple(tuple(g.records[0].shape) for g in meta.groups))
+    maps = tuple(g.records[0].mapping for g in meta.groups)
+    shapes = tuple(tuple(g.records[0].shape) for g in meta.groups)
+    key = (tuple(m.signature() for m in maps), hull, shapes)
+    detail = _MERGE_DETAIL.get(key, _MISSING)
+    if detail is _MISSING:
+        if len(_MERGE_DETAIL) > 65536:
+            _MERGE_DETAIL.clear()
+        detail = _MERGE_DETAIL[key] = _merge_detail(maps, hull, shapes)
+    meta.merge_detail = detail
     return meta
 
 
-@functools.lru_cache(maxsize=65536)
+_MERGE_DETAIL: dict = {}
+_MISSING = object()
+
+
 def _merge_detail(mappings: tuple, hull: tuple, shapes: tuple) -> str | None:
-    """merge()'s verdict for these shard layouts, memoised: every id of one
-    layout (all hidden activations, say) shares one validation."""
+    """merge()'s verdict for these shard layouts, memoised by the layouts'
+    signatures (id_meta): every id of one layout (all hidden activations,
+    say) shares one validation."""
     normed = [ShardMapping(m.local_shape, hull, m.pairs) for m in mappings]
     err = merge_problem(normed, hull, list(shapes))
     return None if err is None else str(err)
@@ -851,7 +862,21 @@ class Prepared:
 
 @functools.lru_cache(maxsize=65536)
 def _run_blocks(ymap: ShardMapping, xmap: ShardMapping) -> tuple:
-    """2-D blocks of (candidate pair x reference pair) box intersections."""
+    """2-D blocks of (candidate pair x reference pair) box intersections
+    (memoised on the two maps' signatures: every id of one layout shares them)."""
+    key = (ymap.signature(), xmap.signature())
+    out = _RUN_BLOCKS.get(key)
+    if out is None:
+        if len(_RUN_BLOCKS) > 65536:
+            _RUN_BLOCKS.clear()
+        out = _RUN_BLOCKS[key] = _run_blocks_uncached(ymap, xmap)
+    return out
+
+
+_RUN_BLOCKS: dict = {}
+
+
+def _run_blocks_uncached(ymap: ShardMapping, xmap: ShardMapping) -> tuple:
     out = []
     for yl, yg in ymap.pairs:
         for xl, xg in xmap.pairs:
