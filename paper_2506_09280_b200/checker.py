@@ -436,6 +436,82 @@ def estimate_tolerance(runner: Runner, *, n_samples: int = 5, eps_p: float,
                         aggregation=aggregation)
 
 
+def estimate_tolerance_streaming(runner, *, n_samples: int = 5, eps_p: float,
+                                 aggregation: str = "max") -> ToleranceMap:
+    """estimate_tolerance (checker.py:102-138) without materialising the
+    perturbed traces: a B200 extension for single-GPU traced runs.
+
+    runner(None) returns the base Trace (device-resident, one identity-mapped
+    record per id, e.g. runner.torch_runner); runner(spec, sink=f) replays
+    the perturbed step and hands every capture to f instead of keeping it.
+    Each capture is compared with its base record the moment it is produced
+    — td_rel_err enqueued on the capturing stream, its sums written to a
+    per-(sample, id) slot in HBM, no host sync — so the compare overlaps the
+    model's own compute and only the base trace stays resident (config 4 at
+    S=8192: ~75 GB of traces instead of ~150).  Same semantics as
+    estimate_tolerance: rel_err(base, perturbed) per id, non-finite -> 0.0,
+    ids absent from a sample skipped, max / mean aggregation."""
+    import torch
+    from .canonical import identity_mapping
+    from .device import pair_sums, to_device
+    if n_samples < 1:
+        raise ConfigInvalid("n_samples must be >= 1")
+    if aggregation not in ("max", "mean"):
+        raise ConfigInvalid(f"unknown aggregation {aggregation!r}")
+    base_trace = runner(None)
+    base: dict = {}
+    for rec in base_trace.records:
+        ident = rec.id.encode()
+        if ident in base:
+            raise ConfigInvalid(f"{ident}: streaming estimation needs one record per id (single GPU)")
+        if rec.replica_group_size != 1 or \
+                rec.mapping.signature() != identity_mapping(tuple(rec.mapping.global_shape)).signature():
+            raise ConfigInvalid(f"{ident}: streaming estimation needs identity-mapped records")
+        base[ident] = to_device(rec.payload).reshape(-1)
+    ids = list(base)
+    index = {ident: k for k, ident in enumerate(ids)}
+    sums = torch.zeros((n_samples, max(len(ids), 1), 3), dtype=torch.float64, device="cuda")
+    work = torch.zeros(N.REL_ERR_WORK_BYTES, dtype=torch.uint8, device="cuda")
+    present = []
+    for s in range(n_samples):
+        got: dict = {}
+
+        def sink(ident, tensor, module_class, _s=s, _got=got):
+            x = base.get(ident)
+            if x is None:
+                return                                  # not in the base trace: ignored
+            y = tensor.reshape(-1)
+            if y.numel() != x.numel():
+                raise ShapeMismatch(f"rel_err: {ident} has {y.numel()} elements vs {x.numel()}")
+            k = index[ident]
+            if y.dtype == x.dtype:
+                N.call("td_rel_err", x.data_ptr(), y.data_ptr(), N.dtype_code(x), x.numel(),
+                       work.data_ptr(), sums[_s, k].data_ptr(), N.stream_handle())
+                _got[ident] = None
+            else:                                       # mixed dtypes: widening path, synchronous
+                _got[ident] = pair_sums(x.double(), y.double())[2]
+        runner(PerturbSpec(sample=s, eps=eps_p), sink=sink)
+        present.append(got)
+    rel = sums[:, :, 2].cpu().numpy()
+    responses = {}
+    for ident in ids:
+        k = index[ident]
+        resp = []
+        for s in range(n_samples):
+            if ident not in present[s]:
+                continue
+            v = present[s][ident]
+            v = float(rel[s, k]) if v is None else v
+            resp.append(v if math.isfinite(v) else 0.0)
+        if not resp:
+            responses[ident] = 0.0
+        elif aggregation == "max":
+            responses[ident] = max(resp)
+        else:
+            responses[ident] = sum(resp) / len(resp)
+    return ToleranceMap(responses=responses, n_samples=n_samples, eps_p=eps_p, aggregation=aggregation)
+
+
 # ---------------------------------------------------------------------------
 # static-threshold ablation and rendering
 

@@ -39,7 +39,9 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
     emb = model.get_submodule(embedding)
     emb_id = encode_id(tap.iteration, tap.microbatch, "ActivationOut", tap.canonical_name(embedding))
 
-    def runner(spec: PerturbSpec | None):
+    def runner(spec: PerturbSpec | None, sink=None):
+        """One traced step.  With sink, captures stream to sink(ident,
+        tensor, module_class) and nothing is kept (returns None)."""
         hooks = []
         if rewrite:
             for name in module_inputs:
@@ -69,7 +71,7 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
                     return (apply_perturbation(args[0], _ident, spec, policy=policy,
                                                generator=generator),) + tuple(args[1:])
                 hooks.append(model.get_submodule(name).register_forward_pre_hook(pre_hook, prepend=True))
-        handle = attach(model, tap)
+        handle = attach(model, tap, sink=sink)
         try:
             model.zero_grad(set_to_none=True)
             step(model)
@@ -77,6 +79,8 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
             detach(handle)
             for h in hooks:
                 h.remove()
+        if sink is not None:
+            return None
         hdr = header if header is not None else dict(handle.header(), mode="module-wise" if module_inputs else "cascade")
         return handle.trace(hdr)
     return runner

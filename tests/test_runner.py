@@ -150,3 +150,26 @@ def test_rewrite_mode_regenerates_inputs_and_localises_a_bug(setup):
     flagged_fwd = {e.ident for e in rep.entries if e.verdict == "flag" and "kind=Activation" in e.ident
                    and "Grad" not in e.ident}
     assert flagged_fwd == {"iter=0|mb=0|kind=ActivationOut|mod=model.layers.2"}
+
+
+@pytest.mark.parametrize("module_wise", [False, True])
+def test_streaming_estimate_equals_materialised(setup, module_wise):
+    """estimate_tolerance_streaming (captures compared as they are produced,
+    nothing kept) gives the responses estimate_tolerance gives on the
+    materialised traces."""
+    import paper_2506_09280_b200 as td
+    model, step = setup
+    kw = {}
+    if module_wise:
+        kw = dict(module_inputs=tuple(f"layers.{i}" for i in range(8)), rewrite=True)
+    runner = _runner(model, step, **kw)
+    eps = td.FloatFormat.BF16.eps
+    want = td.estimate_tolerance(runner, n_samples=3, eps_p=eps)
+    got = td.estimate_tolerance_streaming(runner, n_samples=3, eps_p=eps)
+    assert sorted(got.responses) == sorted(want.responses)
+    assert any(v > 0 for v in want.responses.values())
+    for k, v in want.responses.items():
+        g = got.responses[k]
+        assert (g == v) or abs(g - v) <= 1e-12 * max(abs(v), abs(g)), (k, g, v)
+    mean = td.estimate_tolerance_streaming(runner, n_samples=2, eps_p=eps, aggregation="mean")
+    assert mean.aggregation == "mean" and len(mean.responses) == len(want.responses)

@@ -114,6 +114,8 @@ def main():
     ap.add_argument("--rewrite-std", type=float, default=0.02,
                     help="std of the regenerated block inputs (reference HIDDEN_REWRITE_STD = 0.02, "
                          "engine.py:55); the 8B preset uses 1.0, see below")
+    ap.add_argument("--stream", action="store_true",
+                    help="estimate_tolerance_streaming: perturbed captures compared as produced, not kept")
     ap.add_argument("--llama3-8b", action="store_true",
                     help="Llama-3-8B shape: L=32 d=4096 32/8 heads ff=14336 V=128256 (seq from --seq)")
     args = ap.parse_args()
@@ -161,7 +163,9 @@ def main():
     print(f"one trace: {warm_gb:.1f} GB; allocated after the warm-up run "
           f"{torch.cuda.memory_allocated() / 1e9:.1f} GB", file=sys.stderr, flush=True)
     t0 = time.perf_counter()
-    tol = td.estimate_tolerance(runner, n_samples=args.samples, eps_p=eps)
+    estimate = td.estimate_tolerance_streaming if args.stream else td.estimate_tolerance
+    torch.cuda.reset_peak_memory_stats()
+    tol = estimate(runner, n_samples=args.samples, eps_p=eps)
     torch.cuda.synchronize()
     secs = time.perf_counter() - t0
     per_layer = []
@@ -178,7 +182,8 @@ def main():
     print(json.dumps({"layers": L, "d_model": args.d, "seq": args.seq, "samples": args.samples,
                       "heads": args.heads, "kv_heads": args.kv, "d_ff": args.ff or 4 * args.d,
                       "vocab": vocab, "params": n_params, "dtype": "bf16",
-                      "mode": "module-wise", "estimate_seconds": secs, "one_traced_run_seconds": run_s,
+                      "mode": "module-wise", "estimator": "streaming" if args.stream else "materialised",
+                      "estimate_seconds": secs, "one_traced_run_seconds": run_s,
                       "ids": len(tol.responses), "trace_gb_per_run": warm_gb,
                       "rewrite_std": args.rewrite_std,
                       "zero_or_nonfinite_paramgrad_responses": sum(
