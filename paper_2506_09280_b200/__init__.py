@@ -12,7 +12,8 @@ from .canonical import (CanonicalId, ReplicaGroup, ShardMapping, SliceBox, Tenso
                         canonical_layer_index, check_replicas, identity_mapping, locate_layer,
                         merge, parse_canonical, validate_mapping, whole_box)
 from .checker import (CheckEntry, CheckPlan, CheckReport, StaticReport, ToleranceMap, check,
-                      compare_static, estimate_tolerance, estimate_tolerance_streaming, render_report)
+                      check_streaming, compare_static, estimate_tolerance, estimate_tolerance_streaming,
+                      render_report)
 from .errors import (ConfigInvalid, DigestMismatch, FormatError, MappingInvalid, MergeConflict,
                      NonFinite, ReplicaMismatch, ShapeMismatch, TraindiffError, UnknownBugId)
 from .generation import (GenSpec, Normal, SplitMix64, TokenIds, Uniform, extract_shard, fnv1a_64,

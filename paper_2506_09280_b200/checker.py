@@ -452,22 +452,12 @@ def estimate_tolerance_streaming(runner, *, n_samples: int = 5, eps_p: float,
     estimate_tolerance: rel_err(base, perturbed) per id, non-finite -> 0.0,
     ids absent from a sample skipped, max / mean aggregation."""
     import torch
-    from .canonical import identity_mapping
-    from .device import pair_sums, to_device
+    from .device import pair_sums
     if n_samples < 1:
         raise ConfigInvalid("n_samples must be >= 1")
     if aggregation not in ("max", "mean"):
         raise ConfigInvalid(f"unknown aggregation {aggregation!r}")
-    base_trace = runner(None)
-    base: dict = {}
-    for rec in base_trace.records:
-        ident = rec.id.encode()
-        if ident in base:
-            raise ConfigInvalid(f"{ident}: streaming estimation needs one record per id (single GPU)")
-        if rec.replica_group_size != 1 or \
-                rec.mapping.signature() != identity_mapping(tuple(rec.mapping.global_shape)).signature():
-            raise ConfigInvalid(f"{ident}: streaming estimation needs identity-mapped records")
-        base[ident] = to_device(rec.payload).reshape(-1)
+    base = {ident: x for ident, (_, x) in _identity_records(runner(None), "streaming estimation").items()}
     ids = list(base)
     index = {ident: k for k, ident in enumerate(ids)}
     sums = torch.zeros((n_samples, max(len(ids), 1), 3), dtype=torch.float64, device="cuda")
@@ -510,6 +500,94 @@ def estimate_tolerance_streaming(runner, *, n_samples: int = 5, eps_p: float,
         else:
             responses[ident] = sum(resp) / len(resp)
     return ToleranceMap(responses=responses, n_samples=n_samples, eps_p=eps_p, aggregation=aggregation)
+
+
+def _identity_records(trace: Trace, what: str) -> dict:
+    """{id: (record, flat device payload)} of a single-GPU trace (one
+    identity-mapped record per id) — what the streaming entry points need."""
+    from .canonical import identity_mapping
+    from .device import to_device
+    out: dict = {}
+    for rec in trace.records:
+        ident = rec.id.encode()
+        if ident in out:
+            raise ConfigInvalid(f"{ident}: {what} needs one record per id (single GPU)")
+        if rec.replica_group_size != 1 or \
+                rec.mapping.signature() != identity_mapping(tuple(rec.mapping.global_shape)).signature():
+            raise ConfigInvalid(f"{ident}: {what} needs identity-mapped records")
+        out[ident] = (rec, to_device(rec.payload).reshape(-1))
+    return out
+
+
+def check_streaming(ref: Trace, run: Callable, tol: ToleranceMap, kappa: float = 3.0, *,
+                    fmt: FloatFormat) -> CheckReport:
+    """check() (checker.py:312-365) of a LIVE candidate step against a
+    resident single-GPU reference trace, without materialising the candidate
+    trace: a B200 extension.
+
+    run(sink) executes the candidate's traced step, handing every capture to
+    sink(ident, tensor, module_class) — e.g. `lambda sink: runner(None,
+    sink=sink)` with runner.torch_runner.  Each capture is compared with its
+    reference record as it is produced (td_rel_err on the capturing stream,
+    sums to a per-id HBM slot, no host sync).  The report is check()'s:
+    candidate execution order, then reference-only ids; threshold kappa *
+    max(tol, fmt.eps); NaN passes, +inf flags; differing shapes are merge
+    errors; ids on one side only are missing."""
+    import torch
+    from .device import pair_sums
+    if kappa <= 0:
+        raise ConfigInvalid("kappa must be positive")
+    base = _identity_records(ref, "check_streaming")
+    index = {ident: k for k, ident in enumerate(base)}
+    sums = torch.zeros((max(len(base), 1), 3), dtype=torch.float64, device="cuda")
+    work = torch.zeros(N.REL_ERR_WORK_BYTES, dtype=torch.uint8, device="cuda")
+    order: list = []
+    shapes: dict = {}
+    direct: dict = {}
+
+    def sink(ident, tensor, module_class):
+        order.append(ident)
+        entry = base.get(ident)
+        if entry is None:
+            return
+        rec, x = entry
+        if tuple(tensor.shape) != tuple(rec.mapping.global_shape):
+            shapes[ident] = tuple(tensor.shape)
+            return
+        y = tensor.reshape(-1)
+        if y.dtype == x.dtype:
+            N.call("td_rel_err", x.data_ptr(), y.data_ptr(), N.dtype_code(x), x.numel(),
+                   work.data_ptr(), sums[index[ident]].data_ptr(), N.stream_handle())
+        else:                                           # mixed dtypes: widening path, synchronous
+            direct[ident] = pair_sums(x.double(), y.double())[2]
+    run(sink)
+    rel = sums[:, 2].tolist()
+    eps = fmt.eps
+    entries, ties = [], 0
+    for ident in order:
+        tolerance = tol.get(ident)
+        threshold = kappa * max(tolerance, eps)
+        entry = base.get(ident)
+        if entry is None:
+            entries.append(CheckEntry(ident, VERDICT_MISSING, None, tolerance, threshold,
+                                      "only in candidate trace"))
+        elif ident in shapes:
+            entries.append(CheckEntry(ident, VERDICT_MERGE, None, tolerance, threshold,
+                                      f"merged shapes differ: reference {tuple(entry[0].mapping.global_shape)} "
+                                      f"vs candidate {shapes[ident]}"))
+        else:
+            observed = direct.get(ident, rel[index[ident]])
+            verdict = VERDICT_FLAG if observed > threshold else VERDICT_PASS   # NaN -> pass
+            ties += abs(observed - threshold) <= 1e-12 * threshold
+            entries.append(CheckEntry(ident, verdict, observed, tolerance, threshold, ""))
+    seen = set(order)
+    for ident in base:
+        if ident not in seen:
+            tolerance = tol.get(ident)
+            entries.append(CheckEntry(ident, VERDICT_MISSING, None, tolerance, kappa * max(tolerance, eps),
+                                      "only in reference trace"))
+    return CheckReport(entries=tuple(entries), mode=str(ref.header.get("mode", "")), kappa=kappa, fmt=fmt,
+                       near_ties=int(ties))
 
 
 # ---------------------------------------------------------------------------

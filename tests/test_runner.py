@@ -173,3 +173,29 @@ def test_streaming_estimate_equals_materialised(setup, module_wise):
         assert (g == v) or abs(g - v) <= 1e-12 * max(abs(v), abs(g)), (k, g, v)
     mean = td.estimate_tolerance_streaming(runner, n_samples=2, eps_p=eps, aggregation="mean")
     assert mean.aggregation == "mean" and len(mean.responses) == len(want.responses)
+
+
+def test_check_streaming_equals_check_of_the_materialised_trace(setup):
+    """check_streaming (a live candidate step compared against the resident
+    reference as its captures are produced) reports exactly what check()
+    reports for the materialised candidate trace — with a silent bug in the
+    candidate (one MLP's output scaled by 1.25) so flags appear."""
+    import json
+
+    import paper_2506_09280_b200 as td
+    model, step = setup
+    runner = _runner(model, step)
+    ref = runner(None)
+    eps = td.FloatFormat.BF16.eps
+    tol = td.estimate_tolerance(runner, n_samples=2, eps_p=eps)
+    bug = model.layers[3].register_forward_hook(lambda m, a, out: out * 1.25)
+    try:
+        cand = runner(None)
+        want = td.check(ref, cand, tol, fmt=td.FloatFormat.BF16)
+        got = td.check_streaming(ref, lambda sink: runner(None, sink=sink), tol, fmt=td.FloatFormat.BF16)
+    finally:
+        bug.remove()
+    w, g = json.loads(td.render_report(want, "json")), json.loads(td.render_report(got, "json"))
+    assert w["summary"]["flag"] > 0
+    from tests.test_gpu_parity import assert_reports_match
+    assert_reports_match(g, w, "check_streaming")
