@@ -1465,7 +1465,8 @@ int td_verdict(const td_id_desc* ids, int32_t n_ids, const td_group_desc* groups
 }
 
 int td_rel_err(const void* a, const void* b, int32_t dtype, int64_t n, void* work, double* out, void* stream) {
-    if (!a || !b || !work || !out || n < 0 || dtype < 0 || dtype > 3) return fail("td_rel_err: invalid arguments");
+    if ((n > 0 && (!a || !b)) || !work || !out || n < 0 || dtype < 0 || dtype > 3)
+        return fail("td_rel_err: invalid arguments");
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -554,3 +554,11 @@ def test_odd_length_flat_runs_take_the_vector_walker():
     rep = td.check(ref, cand, tol, fmt=td.FloatFormat.BF16)
     want = float(torch.linalg.vector_norm(x.double() - y.double()) / torch.linalg.vector_norm(x.double()))
     assert abs(rep.entries[0].observed - want) <= 1e-12 * want
+
+
+def test_rel_err_empty_and_scalar():
+    """0/0 -> 0 for empty arrays (tensor.py:163-167), 0-d arrays compare."""
+    e = torch.zeros(0, device="cuda", dtype=torch.bfloat16)
+    assert td.rel_err_arrays(e, e) == 0.0
+    assert td.rel_err_arrays(np.zeros(0), np.zeros(0)) == 0.0
+    assert td.rel_err_arrays(np.array(2.0), np.array(3.0)) == 0.5
