@@ -271,6 +271,9 @@ def host_sample(name: str, stride: int):
         model, pcfg, fmt = L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), "FP32"
     elif name == "cfg3":
         model, pcfg, fmt = L.LLAMA3_1B, L.ParallelConfig(tp=8), "BF16"
+    elif name == "cfg4":
+        # the whole 8-GPU job's layout (the CPU reference has no GPU shares)
+        model, pcfg, fmt = L.LLAMA3_8B, L.ParallelConfig(tp=2, dp=4, microbatches=4), "BF16"
     else:
         model, pcfg, fmt = L.GPT2_MEDIUM, L.ParallelConfig(tp=4), "BF16"
     eps = 2.0 ** -24 if fmt == "FP32" else 2.0 ** -8
