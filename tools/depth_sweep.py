@@ -114,6 +114,8 @@ def main():
     ap.add_argument("--rewrite-std", type=float, default=0.02,
                     help="std of the regenerated block inputs (reference HIDDEN_REWRITE_STD = 0.02, "
                          "engine.py:55); the 8B preset uses 1.0, see below")
+    ap.add_argument("--cascade", action="store_true",
+                    help="cascade mode: only the embedding output is perturbed (no block-input rewrite)")
     ap.add_argument("--stream", action="store_true",
                     help="estimate_tolerance_streaming: perturbed captures compared as produced, not kept")
     ap.add_argument("--llama3-8b", action="store_true",
@@ -151,7 +153,8 @@ def main():
     blocks = tuple(f"layers.{i}" for i in range(2 * args.layers))
     runner = torch_runner(model, step, embedding="embedding",
                           tap=TapConfig(patterns=("layers.*",), precision="bf16"),
-                          module_inputs=blocks, rewrite=True, rewrite_std=args.rewrite_std)
+                          module_inputs=() if args.cascade else blocks, rewrite=not args.cascade,
+                          rewrite_std=args.rewrite_std)
     eps = td.FloatFormat.BF16.eps
     torch.cuda.synchronize()
     t_run = time.perf_counter()
@@ -182,7 +185,7 @@ def main():
     print(json.dumps({"layers": L, "d_model": args.d, "seq": args.seq, "samples": args.samples,
                       "heads": args.heads, "kv_heads": args.kv, "d_ff": args.ff or 4 * args.d,
                       "vocab": vocab, "params": n_params, "dtype": "bf16",
-                      "mode": "module-wise", "estimator": "streaming" if args.stream else "materialised",
+                      "mode": "cascade" if args.cascade else "module-wise", "estimator": "streaming" if args.stream else "materialised",
                       "estimate_seconds": secs, "one_traced_run_seconds": run_s,
                       "ids": len(tol.responses), "trace_gb_per_run": warm_gb,
                       "rewrite_std": args.rewrite_std,
