@@ -67,3 +67,28 @@ def test_gradient_response_decreases_with_layer(streaming):
         per_layer.append(sum(vals) / len(vals))
     assert all(0.02 * eps <= r <= 100 * eps for r in per_layer), [r / eps for r in per_layer]
     assert _spearman(per_layer) <= -0.5, [r / eps for r in per_layer]
+
+
+def test_static_thresholds_fail_where_calibrated_check_holds(cases, golden_trace_bytes):
+    """The reference's Table-4 ablation criterion (test_acceptance.py:281-294)
+    on the golden traces, with the B200 kernels: a tight fixed threshold
+    cries wolf on a correct run, a loose one sleeps through a real bug
+    (MC_SP_NORM_GRAD), the calibrated check does neither."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200.tracestore import trace_from_bytes
+
+    def load(name):
+        case = next(c for c in cases["checks"] if c["name"] == name)
+        ref = trace_from_bytes(golden_trace_bytes(case["ref"]), device="cuda")
+        cand = trace_from_bytes(golden_trace_bytes(case["cand"]), device="cuda")
+        tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+        return ref, cand, td.check(ref, cand, tol, case["kappa"], fmt=td.FloatFormat(case["fmt"]))
+    ref, clean, clean_report = load("clean_tp2_cp2_k3")
+    _, buggy, bug_report = load("bug_sp_norm_grad_k3")
+    tight = td.compare_static(ref, clean, atol=0.0, rtol=1e-5)
+    loose = td.compare_static(ref, buggy, atol=1e-2, rtol=1e-1)
+    assert tight.counts["flag"] > 0
+    assert loose.counts["flag"] == 0
+    assert clean_report.exit_code() == 0 and bug_report.exit_code() != 0
