@@ -92,3 +92,27 @@ def test_static_thresholds_fail_where_calibrated_check_holds(cases, golden_trace
     assert tight.counts["flag"] > 0
     assert loose.counts["flag"] == 0
     assert clean_report.exit_code() == 0 and bug_report.exit_code() != 0
+
+
+def test_every_bug_flagged_with_separation_margin(cases, golden_trace_bytes):
+    """The reference's criteria (test_acceptance.py:208-236) over the golden
+    catalog runs, with the B200 kernels: every injected bug gates the check
+    (exit code != 0), and the earliest divergence's observed rel_err is at
+    least 10x its tolerance."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200.tracestore import trace_from_bytes
+    bugs = [c for c in cases["checks"] if c["name"].startswith("bug_") and c["name"].endswith("_k3")]
+    assert len(bugs) == 9
+    ratios = {}
+    for case in bugs:
+        ref = trace_from_bytes(golden_trace_bytes(case["ref"]), device="cuda")
+        cand = trace_from_bytes(golden_trace_bytes(case["cand"]), device="cuda")
+        tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+        fmt = td.FloatFormat(case["fmt"])
+        rep = td.check(ref, cand, tol, case["kappa"], fmt=fmt)
+        assert rep.exit_code() != 0, case["name"]
+        entry = next(e for e in rep.entries if e.ident == rep.earliest_divergence)
+        ratios[case["name"]] = entry.observed / max(entry.tolerance, fmt.eps)
+    assert all(r >= 10.0 for r in ratios.values()), ratios
