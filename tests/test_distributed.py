@@ -150,3 +150,49 @@ def test_distributed_check_threads_match_reference(world, cases, golden_trace_by
         want = json.loads(case["report"])
         for rep in reports:
             assert_reports_match(rep, want, f"{name} world={world}")
+
+
+def _nccl_world1(q):
+    try:
+        import paper_2506_09280_b200 as td
+        from paper_2506_09280_b200.checker import ToleranceMap
+        torch.cuda.set_device(0)
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29631")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        import gzip
+        with gzip.open(os.path.join(ROOT, "tests", "golden", "cases.json.gz"), "rt") as fh:
+            cases = json.load(fh)
+        case = next(c for c in cases["checks"] if c["name"] == "bug_tp_row_allreduce_k3")
+
+        def load(n):
+            with gzip.open(os.path.join(ROOT, "tests", "golden", "traces", n + ".ttrc.gz"), "rb") as fh:
+                return trace_from_bytes(fh.read(), device="cuda")
+        ref, cand = load(case["ref"]), load(case["cand"])
+        tol = ToleranceMap.from_json(cases["tols"][case["tol"]])
+        plan = DistributedCheckPlan(ref, cand, tol, case["kappa"], fmt=td.FloatFormat(case["fmt"]),
+                                    comm=TorchComm())
+        got = json.loads(td.render_report(plan.run(), "json"))
+        dist.destroy_process_group()
+        q.put(("ok", got, json.loads(case["report"])))
+    except Exception:  # surfaced in the parent
+        import traceback
+        q.put(("error", traceback.format_exc(), None))
+
+
+@pytest.mark.gpu
+def test_distributed_check_over_nccl_world1():
+    """The distributed check through torch.distributed's NCCL backend (the
+    production transport; one GPU here, so world size 1): metadata
+    all_gather_object, the digest and partial-sum all_reduces, verdicts —
+    the reference's report."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_world1, args=(q,))
+    p.start()
+    status, got, want = q.get(timeout=600)
+    p.join(timeout=60)
+    assert status == "ok", got
+    from tests.test_gpu_parity import assert_reports_match
+    assert_reports_match(got, want, "nccl world 1")
