@@ -14,6 +14,9 @@ from __future__ import annotations
 
 from typing import Callable
 
+import torch
+
+from .errors import NonFinite
 from .perturb import PerturbSpec, apply_perturbation
 from .torchtap import TapConfig, attach, detach
 from .torchtap.writer import encode_id
@@ -43,6 +46,9 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
         """One traced step.  With sink, captures stream to sink(ident,
         tensor, module_class) and nothing is kept (returns None)."""
         hooks = []
+        # one device counter of non-finite perturbed values per step, read
+        # once after it (no host sync inside the forward pass)
+        nonfinite = torch.zeros(1, dtype=torch.int64, device="cuda")
         if rewrite:
             for name in module_inputs:
                 ident = encode_id(tap.iteration, tap.microbatch, "ActivationIn", tap.canonical_name(name))
@@ -53,14 +59,16 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
                     x = args[0]
                     value = _regenerate(_ident, tuple(x.shape), rewrite_std, policy).to(x.dtype)
                     if spec is not None and spec.eps != 0.0:
-                        value = apply_perturbation(value, _ident, spec, policy=policy, generator=generator)
+                        value = apply_perturbation(value, _ident, spec, policy=policy, generator=generator,
+                                                   check=False, nonfinite=nonfinite)
                     # the module reads `value`; its input gradient still flows
                     # back to the chain unchanged (engine.py:383-385)
                     return (_replace(x, value),) + tuple(args[1:])
                 hooks.append(model.get_submodule(name).register_forward_pre_hook(regen, prepend=True))
         if spec is not None and spec.eps != 0.0:
             def out_hook(module, args, output):
-                return apply_perturbation(output, emb_id, spec, policy=policy, generator=generator)
+                return apply_perturbation(output, emb_id, spec, policy=policy, generator=generator,
+                                          check=False, nonfinite=nonfinite)
             hooks.append(emb.register_forward_hook(out_hook, prepend=True))
             for name in (() if rewrite else module_inputs):
                 ident = encode_id(tap.iteration, tap.microbatch, "ActivationIn", tap.canonical_name(name))
@@ -68,8 +76,8 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
                 def pre_hook(module, args, _ident=ident):
                     if not args:
                         return None
-                    return (apply_perturbation(args[0], _ident, spec, policy=policy,
-                                               generator=generator),) + tuple(args[1:])
+                    return (apply_perturbation(args[0], _ident, spec, policy=policy, generator=generator,
+                                               check=False, nonfinite=nonfinite),) + tuple(args[1:])
                 hooks.append(model.get_submodule(name).register_forward_pre_hook(pre_hook, prepend=True))
         handle = attach(model, tap, sink=sink)
         try:
@@ -79,6 +87,8 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
             detach(handle)
             for h in hooks:
                 h.remove()
+        if spec is not None and spec.eps != 0.0 and int(nonfinite.item()):
+            raise NonFinite("non-finite values in a perturbed input")
         if sink is not None:
             return None
         hdr = header if header is not None else dict(handle.header(), mode="module-wise" if module_inputs else "cascade")
