@@ -562,3 +562,21 @@ def test_rel_err_empty_and_scalar():
     assert td.rel_err_arrays(e, e) == 0.0
     assert td.rel_err_arrays(np.zeros(0), np.zeros(0)) == 0.0
     assert td.rel_err_arrays(np.array(2.0), np.array(3.0)) == 0.5
+
+
+def test_check_plan_cache_with_pinned_host_payloads(cases, golden_trace_bytes):
+    """The e2e path: traces in pinned host arenas, the plan cached by the
+    first check and reused with the next check's staged copies."""
+    from paper_2506_09280_b200 import checker
+    from paper_2506_09280_b200.tracestore import pack_pinned
+    case = next(c for c in cases["checks"] if c["name"] == "bug_stale_input_k3")
+    ref = pack_pinned(trace_from_bytes(golden_trace_bytes(case["ref"])))
+    cand = pack_pinned(trace_from_bytes(golden_trace_bytes(case["cand"])))
+    tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+    fmt = td.FloatFormat(case["fmt"])
+    checker._PLAN_CACHE.clear()
+    reports = [json.loads(td.render_report(td.check(ref, cand, tol, case["kappa"], fmt=fmt), "json"))
+               for _ in range(3)]
+    assert len(checker._PLAN_CACHE) == 1
+    for rep in reports:
+        assert_reports_match(rep, json.loads(case["report"]), "pinned + cached plan")

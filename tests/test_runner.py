@@ -199,3 +199,51 @@ def test_check_streaming_equals_check_of_the_materialised_trace(setup):
     assert w["summary"]["flag"] > 0
     from tests.test_gpu_parity import assert_reports_match
     assert_reports_match(g, w, "check_streaming")
+
+
+def test_check_streaming_missing_extra_and_shape_mismatch():
+    """Ids on one side only are 'missing' (candidate order, then reference
+    only), a capture whose shape differs from its reference record is a
+    merge error with the reference's detail, NaN passes, +inf flags — the
+    same report check() gives for the materialised candidate trace."""
+    import json
+
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200.canonical import identity_mapping, parse_canonical
+    from paper_2506_09280_b200.tracestore import RankMeta, Trace, TraceRecord
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    g = torch.Generator(device="cuda").manual_seed(9)
+    hdr = {"digest": "d", "mode": "cascade"}
+
+    def ident(name):
+        return f"iter=0|mb=0|kind=ActivationOut|mod=model.{name}"
+    base = {n: torch.randn(shape, device="cuda", generator=g).to(torch.bfloat16)
+            for n, shape in (("a", (64, 32)), ("b", (16,)), ("c", (8, 8)), ("only_ref", (4,)), ("nan", (5,)),
+                             ("inf", (6,)))}
+    base["inf"][0] = 0.0
+    ref = Trace(header=dict(hdr))
+    for n, t in base.items():
+        ref.records.append(TraceRecord(parse_canonical(ident(n)), RankMeta(), identity_mapping(tuple(t.shape)), 1,
+                                       t, "Linear"))
+    cand_t = {"a": base["a"] * 1.001, "only_cand": torch.ones(3, device="cuda", dtype=torch.bfloat16),
+              "b": base["b"] * 2, "c": torch.zeros(4, 16, device="cuda", dtype=torch.bfloat16),
+              "nan": base["nan"].clone(), "inf": base["inf"].clone()}
+    cand_t["nan"][1] = float("nan")
+    cand_t["inf"][0] = float("inf")
+    cand = Trace(header=dict(hdr))
+    for n, t in cand_t.items():
+        cand.records.append(TraceRecord(parse_canonical(ident(n)), RankMeta(), identity_mapping(tuple(t.shape)), 1,
+                                        t, "Linear"))
+    tol = td.ToleranceMap({ident("a"): 0.01}, n_samples=1, eps_p=2.0 ** -8)
+
+    def run(sink):
+        for n, t in cand_t.items():
+            sink(ident(n), t, "Linear")
+    got = json.loads(td.render_report(td.check_streaming(ref, run, tol, fmt=td.FloatFormat.BF16), "json"))
+    want = json.loads(td.render_report(td.check(ref, cand, tol, fmt=td.FloatFormat.BF16), "json"))
+    from tests.test_gpu_parity import assert_reports_match
+    assert_reports_match(got, want, "streaming edge cases")
+    verdicts = {e["id"].split("mod=model.")[1]: e["verdict"] for e in got["entries"]}
+    assert verdicts == {"a": "pass", "only_cand": "missing", "b": "flag", "c": "merge-error", "nan": "pass",
+                        "inf": "flag", "only_ref": "missing"}
