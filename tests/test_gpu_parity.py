@@ -210,8 +210,10 @@ def _random_trace_pair(rng, case, dtype, corrupt):
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
 def test_randomized_shardings_match_oracle(shardings, dtype):
+    # all 1000 randomized shardings of the reference's acceptance test
+    # (test_acceptance.py:90-112) x {none, value, replica} corruptions
     rng = np.random.default_rng(11)
-    for i, case in enumerate(shardings[:300]):
+    for i, case in enumerate(shardings):
         corrupt = ("none", "value", "replica")[i % 3]
         ref, cand = _random_trace_pair(rng, case, dtype, corrupt)
         if dtype == "bf16":
