@@ -86,3 +86,24 @@ def test_config4_shape_tp2_dp2_sp_cp_layout():
     tol = td.ToleranceMap({r.id.encode(): 2 * eps for r in ref.records}, n_samples=1, eps_p=eps)
     rep = _compare(ref, cand, tol, td.FloatFormat.BF16)
     assert rep.exit_code() == 0
+
+
+def test_fuzzed_layouts_and_bugs_match_oracle():
+    """A slice of tools/fuzz_parity.py: random small models x random valid
+    parallel layouts (tp/dp/pp/vp/cp/sp/microbatches) x random storage dtype,
+    kappa and injected bugs — device check == CPU oracle on every case."""
+    import random
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_parity
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200 import synthetic
+    rnd = random.Random(1234)
+    for k in range(40):
+        m, p, bugs = fuzz_parity.random_case(rnd)
+        dtype = rnd.choice([torch.bfloat16, torch.float32])
+        fmt = td.FloatFormat.BF16 if dtype == torch.bfloat16 else td.FloatFormat.FP32
+        ref, cand = synthetic.build(m, p, dtype=dtype, seed=k, eps=fmt.eps, bugs=bugs)
+        tol = td.ToleranceMap({r.id.encode(): 2 * fmt.eps for r in ref.records}, n_samples=1, eps_p=fmt.eps)
+        _compare(ref, cand, tol, fmt)
