@@ -189,3 +189,18 @@ def test_digests_fused_in_compare_equal_fingerprints():
         assert np.array_equal(table[:len(where)].cpu().numpy(), want), r
         fused_total += nf
     assert fused_total > 0
+
+
+@pytest.mark.gpu
+def test_fuzzed_shares_match_single_gpu_check():
+    """A slice of tools/fuzz_distributed.py: random layouts split into 2-4
+    shares run as threads (digests, balanced compares, copy-0 handover), with
+    random corruptions — every rank's report == check() of the union."""
+    import os
+    import random
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_distributed
+    rnd = random.Random(77)
+    for k in range(12):
+        fuzz_distributed.run_case(rnd, k)
