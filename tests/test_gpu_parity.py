@@ -582,3 +582,17 @@ def test_check_plan_cache_with_pinned_host_payloads(cases, golden_trace_bytes):
     assert len(checker._PLAN_CACHE) == 1
     for rep in reports:
         assert_reports_match(rep, json.loads(case["report"]), "pinned + cached plan")
+
+
+def test_fuzzed_perturbations_bit_exact():
+    """A slice of tools/fuzz_perturb.py: random shapes, column shards with
+    odd offsets, row subsets, eps, policies, in/out dtypes and generators —
+    td_perturb bit-identical to the oracle."""
+    import os
+    import random
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_perturb
+    rnd = random.Random(5)
+    for k in range(100):
+        fuzz_perturb.run_case(rnd, k)
