@@ -212,6 +212,15 @@ int td_reduce_chunks(const double* partials, const td_chunk* chunks, int64_t n_c
 int td_rel_err(const void* a, const void* b, int32_t dtype, int64_t n, void* work, double* out,
                void* stream);
 
+/* ---- the cross-GPU exchange without torch.distributed ----
+ * In-place sum over the ranks of an NCCL communicator (an ncclComm_t passed
+ * as void*), enqueued on `stream`: the per-id / per-group slot sums between
+ * td_reduce_slots and td_verdict (n doubles), and the replica digest table
+ * (n int64, wrapping).  NCCL is loaded at first use (dlopen "libnccl.so.2");
+ * without it these return non-zero with td_last_error() set. */
+int td_allreduce_partials(void* nccl_comm, double* slots, int64_t n, void* stream);
+int td_allreduce_digests(void* nccl_comm, long long* table, int64_t n, void* stream);
+
 /* ---- kernel 3: batched threshold compare -> per-id verdicts ----
  * eps = fmt.eps (threshold floor); replica_eps = fmt.eps for check_replicas.
  * near_ties: optional device uint64 counter, reset and then counted (NULL: per-id

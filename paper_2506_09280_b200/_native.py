@@ -82,6 +82,8 @@ SIGNATURES = {
     "td_quantize": (ctypes.c_int, [_P, _P, _I32, _I64, _I32, _P, _P]),
     "td_fingerprint": (ctypes.c_int, [_P, _P, _I32, _I64, _P, _P]),
     "td_rel_err": (ctypes.c_int, [_P, _P, _I32, _I64, _P, _P, _P]),
+    "td_allreduce_partials": (ctypes.c_int, [_P, _P, _I64, _P]),
+    "td_allreduce_digests": (ctypes.c_int, [_P, _P, _I64, _P]),
     "td_box_gather": (ctypes.c_int, [_P, _I32, _P, _P, _I32, _P]),
     "td_gather_bytes": (ctypes.c_int, [_P, _P, _P, _I64, _P]),
     "td_generate": (ctypes.c_int, [_P, _I64, _U64, _I32, _D, _D, _I64, _P, _I32, _P, _P, _I32, _P]),

@@ -27,6 +27,8 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
+#include <dlfcn.h>
+
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -1613,6 +1615,44 @@ int td_gather_bytes(const void* src, void* dst, const int64_t* ranges, int64_t n
     k_gather_bytes<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<const unsigned char*>(src),
                                                            static_cast<unsigned char*>(dst), ranges, n);
     return check_launch("td_gather_bytes");
+}
+
+}  // extern "C"
+
+// ---- the cross-GPU exchange for hosts without torch.distributed ----
+// NCCL is resolved at first use with dlopen (no link-time dependency: the
+// library loads on hosts without NCCL, and inside a torch process it binds
+// the libnccl.so.2 torch already loaded).  Enum values as in nccl.h.
+namespace {
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+nccl_allreduce_fn nccl_allreduce() {
+    static nccl_allreduce_fn fn = [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        return h ? reinterpret_cast<nccl_allreduce_fn>(dlsym(h, "ncclAllReduce")) : nullptr;
+    }();
+    return fn;
+}
+constexpr int NCCL_INT64 = 4, NCCL_FLOAT64 = 8, NCCL_SUM = 0;
+
+int allreduce_sum(void* comm, void* buf, int64_t n, int dtype, void* stream, const char* what) {
+    if (n == 0) return 0;
+    if (!comm || !buf || n < 0) return fail("%s: invalid arguments", what);
+    nccl_allreduce_fn fn = nccl_allreduce();
+    if (!fn) return fail("%s: libnccl.so.2 not found", what);
+    const int rc = fn(buf, buf, (size_t)n, dtype, NCCL_SUM, comm, (cudaStream_t)stream);
+    return rc ? fail("%s: ncclAllReduce returned %d", what, rc) : 0;
+}
+}  // namespace
+
+extern "C" {
+
+int td_allreduce_partials(void* nccl_comm, double* slots, int64_t n, void* stream) {
+    return allreduce_sum(nccl_comm, slots, n, NCCL_FLOAT64, stream, "td_allreduce_partials");
+}
+
+int td_allreduce_digests(void* nccl_comm, long long* table, int64_t n, void* stream) {
+    return allreduce_sum(nccl_comm, table, n, NCCL_INT64, stream, "td_allreduce_digests");
 }
 
 }  // extern "C"

@@ -4,6 +4,7 @@
  * perturbation of a bf16 tensor (td_perturb) and replica digests
  * (td_fingerprint), checked against host arithmetic.  Exit 0 = pass. */
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -96,11 +97,42 @@ int main(void) {
         fprintf(stderr, "digests disagree\n");
         return 6;
     }
+    /* the cross-GPU exchange on a one-rank NCCL communicator: the sums come
+     * back unchanged (NCCL resolved by dlopen here as in the library) */
+    void* nccl = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (nccl) {
+        typedef struct { char internal[128]; } nccl_id;
+        int (*get_id)(nccl_id*) = (int (*)(nccl_id*))dlsym(nccl, "ncclGetUniqueId");
+        int (*init_rank)(void**, int, nccl_id, int) = (int (*)(void**, int, nccl_id, int))dlsym(nccl, "ncclCommInitRank");
+        int (*destroy)(void*) = (int (*)(void*))dlsym(nccl, "ncclCommDestroy");
+        nccl_id uid;
+        void* comm = NULL;
+        if (!get_id || !init_rank || get_id(&uid) != 0 || init_rank(&comm, 1, uid, 0) != 0) {
+            fprintf(stderr, "cannot create a one-rank NCCL communicator\n");
+            return 8;
+        }
+        double sl[3] = {1.5, -2.0, 3.25}, back[3];
+        double* dsl;
+        CK(cudaMalloc((void**)&dsl, sizeof(sl)));
+        CK(cudaMemcpy(dsl, sl, sizeof(sl), cudaMemcpyHostToDevice));
+        TD(td_allreduce_partials(comm, dsl, 3, NULL));
+        TD(td_allreduce_digests(comm, (long long*)ddig, 6, NULL));
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(back, dsl, sizeof(back), cudaMemcpyDeviceToHost));
+        unsigned long long dig2[6];
+        CK(cudaMemcpy(dig2, ddig, sizeof(dig2), cudaMemcpyDeviceToHost));
+        if (memcmp(back, sl, sizeof(sl)) != 0 || memcmp(dig, dig2, sizeof(dig)) != 0) {
+            fprintf(stderr, "one-rank all-reduce changed the values\n");
+            return 9;
+        }
+        destroy(comm);
+    }
     /* errors come back as status codes with a message, not exceptions */
     if (td_rel_err(NULL, db, TD_BF16, n, work, dout, NULL) == 0 || !strstr(td_last_error(), "td_rel_err")) {
         fprintf(stderr, "invalid arguments not reported\n");
         return 7;
     }
-    printf("c abi ok: td_version %d, rel_err %.17g (host %.17g)\n", td_version(), got, want);
+    printf("c abi ok: td_version %d, rel_err %.17g (host %.17g), nccl exchange %s\n", td_version(), got, want,
+           nccl ? "checked" : "skipped (no libnccl.so.2)");
     return 0;
 }

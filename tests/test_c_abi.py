@@ -26,7 +26,7 @@ def _compile(tmp_path):
     exe = tmp_path / "abi_smoke"
     subprocess.run([cc, "-std=c99", "-Wall", "-Werror", "-I", build.INCLUDE, "-I", os.path.join(CUDA, "include"),
                     "-o", str(exe), SRC, "-L", lib_dir, "-l:libtdb200.so", "-L", os.path.join(CUDA, "lib64"),
-                    "-lcudart", "-lm", f"-Wl,-rpath,{lib_dir}:{os.path.join(CUDA, 'lib64')}"], check=True)
+                    "-lcudart", "-lm", "-ldl", f"-Wl,-rpath,{lib_dir}:{os.path.join(CUDA, 'lib64')}"], check=True)
     return exe
 
 
@@ -42,4 +42,4 @@ def test_c_host_runs_on_the_gpu(tmp_path):
     exe = _compile(tmp_path)
     proc = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert proc.returncode == 0, proc.stderr
-    assert "c abi ok" in proc.stdout
+    assert "c abi ok" in proc.stdout and "nccl exchange checked" in proc.stdout, proc.stdout
