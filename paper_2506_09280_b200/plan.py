@@ -493,12 +493,18 @@ class Plan:
         spans += [(int(tb) * W, int(te) * W, 2, 1 + int(nz)) for tb, te, nz in
                   zip(self.groups["tile_begin"], self.groups["tile_end"], self.groups["nz"])]
         self.chunks = None
-        if not spans or max(re - rb for rb, re, _, _ in spans) < self.CHUNK_MIN_ROWS:
+        longest = max((re - rb for rb, re, _, _ in spans), default=0)
+        if longest < self.CHUNK_MIN_ROWS:
             return
+        # chunks of CHUNK_ROWS for big slots; for mid-size plans (a few k rows,
+        # e.g. a 4 MiB single-tensor check) chunks short enough that the
+        # longest slot spreads over ~32 CTAs instead of one
+        step = self.CHUNK_ROWS if longest >= 32 * self.CHUNK_ROWS else \
+            min(self.CHUNK_ROWS, max(256, 1 << max(0, (longest // 32 - 1).bit_length())))
         rows, ranges = [], []
         for rb, re, k0, nk in spans:
             c0 = len(rows)
-            rows.extend((r, min(r + self.CHUNK_ROWS, re), k0, nk) for r in range(rb, re, self.CHUNK_ROWS))
+            rows.extend((r, min(r + step, re), k0, nk) for r in range(rb, re, step))
             ranges.append((c0, len(rows)))
         self.chunks = np.array(rows, dtype=N.CHUNK) if rows else np.zeros(0, N.CHUNK)
         ranges = np.array(ranges, np.int64).reshape(-1, 2)
