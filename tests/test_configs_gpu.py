@@ -102,8 +102,9 @@ def test_fuzzed_layouts_and_bugs_match_oracle():
     rnd = random.Random(1234)
     for k in range(40):
         m, p, bugs = fuzz_parity.random_case(rnd)
-        dtype = rnd.choice([torch.bfloat16, torch.float32])
-        fmt = td.FloatFormat.BF16 if dtype == torch.bfloat16 else td.FloatFormat.FP32
+        dtype = rnd.choice([torch.bfloat16, torch.float32, torch.float16])
+        fmt = td.FloatFormat.BF16 if dtype != torch.float32 else td.FloatFormat.FP32
         ref, cand = synthetic.build(m, p, dtype=dtype, seed=k, eps=fmt.eps, bugs=bugs)
+        fuzz_parity.scramble_dtypes(rnd, ref, cand)
         tol = td.ToleranceMap({r.id.encode(): 2 * fmt.eps for r in ref.records}, n_samples=1, eps_p=fmt.eps)
         _compare(ref, cand, tol, fmt)

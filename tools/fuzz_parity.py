@@ -50,6 +50,18 @@ def random_case(rnd):
         return m, p, bugs
 
 
+def scramble_dtypes(rnd, *traces, p=0.15):
+    """Widen a random subset of payloads exactly (bf16/f16 -> f32, f32 -> f64):
+    mixed-dtype operands and replica groups exercise the widening paths
+    (generic walker, per-group common dtype) with unchanged values."""
+    import torch
+    for trace in traces:
+        for rec in trace.records:
+            if rnd.random() < p and rec.payload.dtype != torch.float64:
+                wider = torch.float64 if rec.payload.dtype == torch.float32 else torch.float32
+                rec.payload = rec.payload.to(wider)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", type=int, default=200)
@@ -66,9 +78,10 @@ def main():
     stats = {"cases": 0, "ids": 0, "flag": 0, "replica-mismatch": 0, "merge-error": 0, "layouts": set()}
     for k in range(args.cases):
         m, p, bugs = random_case(rnd)
-        dtype = rnd.choice([torch.bfloat16, torch.float32])
-        fmt = td.FloatFormat.BF16 if dtype == torch.bfloat16 else td.FloatFormat.FP32
+        dtype = rnd.choice([torch.bfloat16, torch.float32, torch.float16])
+        fmt = td.FloatFormat.BF16 if dtype != torch.float32 else td.FloatFormat.FP32
         ref, cand = synthetic.build(m, p, dtype=dtype, seed=k, eps=fmt.eps, bugs=bugs)
+        scramble_dtypes(rnd, ref, cand)
         tol = td.ToleranceMap({r.id.encode(): 2 * fmt.eps for r in ref.records}, n_samples=1, eps_p=fmt.eps)
         kappa = rnd.choice([0.5, 3.0, 10.0])
         rep = td.check(ref, cand, tol, kappa, fmt=fmt)
