@@ -86,3 +86,17 @@ def test_struct_layouts_match_header(tmp_path):
         assert int(got[name]) == dt.itemsize, name
         for field in dt.names:
             assert int(got[f"{name}.{field}"]) == dt.fields[field][1], f"{name}.{field}"
+
+
+def test_integration_stub_matches_the_abi():
+    """The ctypes stub a maintainer would paste declares
+    the same argument types the library is loaded with (_native.SIGNATURES)."""
+    import ctypes
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    text = open(os.path.join(root, "INTEGRATION.md")).read()
+    kinds = {"_P": ctypes.c_void_p, "_I32": ctypes.c_int32, "_I64": ctypes.c_int64,
+             "_U64": ctypes.c_uint64, "_D": ctypes.c_double}
+    found = re.findall(r"_lib\.(td_\w+)\.argtypes\s*=\s*\[([^\]]*)\]", text)
+    assert len(found) >= 6
+    for name, args in found:
+        assert [kinds[a.strip()] for a in args.split(",") if a.strip()] == N.SIGNATURES[name][1], name
