@@ -147,6 +147,9 @@ __device__ __forceinline__ void fp_vec(const uint4& v, uint64_t j, uint64_t& h0,
 #ifndef TD_REPLICA_SKIP
 #define TD_REPLICA_SKIP 1
 #endif
+#ifndef TD_FP_U
+#define TD_FP_U 8
+#endif
 #ifndef TD_REPLICA_SKIP_MIN_NZ
 #define TD_REPLICA_SKIP_MIN_NZ 3
 #endif
@@ -1134,13 +1137,14 @@ __global__ void k_quantize(const double* __restrict__ x, char* __restrict__ y, i
 // Position-keyed, so permuted shards differ.
 // One launch covers every item: a flat list of 256 KB chunks (prefix sums of
 // per-item chunk counts, binary-searched per chunk), 16-byte streaming loads,
-// 4 vectors in flight per thread; warp sums are added atomically (wrapping
+// TD_FP_U = 8 vectors in flight per thread (4: 5.8 TB/s, 8: 6.7, 16: 6.4 —
+// tools/bench_digest.py); warp sums are added atomically (wrapping
 // u64 adds commute: the digest does not depend on the order).
 
 __global__ void __launch_bounds__(BLOCK)
 k_fingerprint(const td_fp_item* __restrict__ items, const int64_t* __restrict__ chunk_begin, int n_items,
               int64_t n_chunks, unsigned long long* __restrict__ out) {
-    constexpr int U = 4;
+    constexpr int U = TD_FP_U;
     for (int64_t c = blockIdx.x; c < n_chunks; c += gridDim.x) {
         int lo = 0, hi = n_items - 1;            // last item with chunk_begin[i] <= c
         while (lo < hi) {
