@@ -740,15 +740,23 @@ k_finalize(const td_id_desc* __restrict__ ids, const td_group_desc* __restrict__
 // partials in CTA order and applies the reference's zero conventions.  No
 // planner, no second launch: the public API's latency for one pair is one
 // kernel + one 24-byte D2H.  Deterministic for a given (n, grid).
+// U = 4 vectors per operand at 4 CTAs/SM; 8 at 2 or 3 CTAs/SM measured 7-15%
+// slower on a 1 GiB pair (tools/bench_relerr.py)
+#ifndef TD_RELERR_U
+#define TD_RELERR_U 4
+#endif
+#ifndef TD_RELERR_MINB
+#define TD_RELERR_MINB 4
+#endif
 template <int DT>
-__global__ void __launch_bounds__(BLOCK, 4)
+__global__ void __launch_bounds__(BLOCK, TD_RELERR_MINB)
 k_rel_err(const char* __restrict__ a, const char* __restrict__ b, int64_t n, double* __restrict__ part,
           unsigned int* __restrict__ ticket, double* __restrict__ out) {
     __shared__ double red[NWARP];
     __shared__ bool last;
     constexpr int Q = DT == TD_F64 ? 1 : Vec<DT == TD_F64 ? TD_F32 : DT>::Q;
     constexpr int ES = DT == TD_F32 ? 4 : (DT == TD_F64 ? 8 : 2);
-    constexpr int U = 4 / Q;
+    constexpr int U = TD_RELERR_U / Q;
     double d2 = 0.0, a2 = 0.0;
     const bool vec = DT != TD_F64 && ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
     const int64_t nv = vec ? n / 8 : 0;
