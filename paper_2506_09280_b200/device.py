@@ -11,6 +11,8 @@ from __future__ import annotations
 
 import numpy as np
 
+import os
+
 from . import _native as N
 
 
@@ -111,6 +113,7 @@ def stage_host_payloads(traces, stream=None) -> dict:
     import torch
     staged: dict = {}
     arenas: dict = {}
+    pageable: list = []
     tensor = torch.Tensor
     for trace in traces:
         for rec in trace.records:
@@ -132,7 +135,9 @@ def stage_host_payloads(traces, stream=None) -> dict:
                         entry = arenas[st.data_ptr()] = (dev, [])
                     entry[1].append(rec)
                     continue
-            staged[id(rec)] = to_device(p)
+            pageable.append(rec)
+    if pageable:
+        staged.update(_stage_pageable(pageable))
     for dev, recs in arenas.values():
         dst = dev.untyped_storage()
         for rec in recs:
@@ -141,6 +146,102 @@ def stage_host_payloads(traces, stream=None) -> dict:
                                                                      p.shape, p.stride())
             staged[id(rec)] = view if view.data_ptr() % 16 == 0 else view.clone()
     return staged
+
+
+# pageable host payloads (numpy traces, e.g. read_trace() on the host, as a
+# reference user has them) cross PCIe through a ring of pinned staging
+# buffers: host threads fill buffer k+1 (parallel memcpy, the GIL released
+# inside numpy's copy) while buffer k's DMA runs on a copy stream; every
+# payload lands 256-byte aligned in one device arena.  Small totals go per
+# record (to_device).
+_STAGE_CHUNK = 64 << 20
+_STAGE_RING = 4
+_STAGE_MIN = 64 << 20
+_STAGING = None
+
+
+def _stage_pageable(records) -> dict:
+    import concurrent.futures
+    import torch
+    global _STAGING
+    flat, kinds = [], []                      # raw bytes per payload, (torch dtype, shape)
+    for rec in records:
+        p = rec.payload
+        if is_torch(p):
+            t = p.detach().contiguous()
+            flat.append(t.reshape(-1).view(torch.uint8).numpy() if t.numel() else np.zeros(0, np.uint8))
+            kinds.append((t.dtype, tuple(t.shape)))
+        else:
+            a = np.ascontiguousarray(p)
+            dt = _TORCH_DTYPE_OF_NP.get(a.dtype.str)
+            if dt is None:
+                a = a.astype(np.float64)
+                dt = "float64"
+            flat.append(a.reshape(-1).view(np.uint8))
+            kinds.append((getattr(torch, dt), a.shape))
+    total = 0
+    offsets = []
+    for a in flat:
+        total = -(-total // 256) * 256
+        offsets.append(total)
+        total += a.nbytes
+    if total < _STAGE_MIN:
+        return {id(rec): to_device(rec.payload) for rec in records}
+    if _STAGING is None:
+        bufs = [torch.empty(_STAGE_CHUNK, dtype=torch.uint8).pin_memory() for _ in range(_STAGE_RING)]
+        pool = concurrent.futures.ThreadPoolExecutor(
+            max_workers=int(os.environ.get("TD_STAGE_THREADS", min(8, os.cpu_count() or 1))))
+        _STAGING = (bufs, [None] * _STAGE_RING, pool, torch.cuda.Stream())
+    bufs, events, pool, copy_stream = _STAGING
+    arena = torch.empty(max(total, 16), dtype=torch.uint8, device="cuda")
+    copy_stream.wait_stream(torch.cuda.current_stream())
+    item, inner, k = 0, 0, 0
+    while item < len(flat):
+        slot = k % _STAGE_RING
+        if events[slot] is not None:
+            events[slot].synchronize()           # its previous DMA has drained
+        host = bufs[slot].numpy()
+        pieces, fill = [], 0                     # (src array slice, staging offset, arena offset)
+        dst0 = offsets[item] + inner
+        while item < len(flat) and fill < _STAGE_CHUNK:
+            src = flat[item]
+            start = offsets[item] + inner
+            if start != dst0 + fill:             # alignment gap: flush this buffer here
+                break
+            n = min(src.nbytes - inner, _STAGE_CHUNK - fill)
+            pieces.append((src[inner:inner + n], fill))
+            fill += n
+            inner += n
+            if inner == src.nbytes:
+                item, inner = item + 1, 0
+        if fill == 0:                            # gap before the next payload: restart the buffer there
+            dst0 = offsets[item] + inner
+            continue
+        list(pool.map(lambda pc: np.copyto(host[pc[1]:pc[1] + pc[0].nbytes], pc[0]),
+                      _split_pieces(pieces, 8 << 20)))
+        with torch.cuda.stream(copy_stream):
+            arena[dst0:dst0 + fill].copy_(bufs[slot][:fill], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy_stream)
+        events[slot] = ev
+        k += 1
+    torch.cuda.current_stream().wait_stream(copy_stream)
+    staged = {}
+    for rec, a, (dt, shape), off in zip(records, flat, kinds, offsets):
+        staged[id(rec)] = arena[off:off + a.nbytes].view(dt).view(shape)
+    return staged
+
+
+_TORCH_DTYPE_OF_NP = {"<f4": "float32", "<f8": "float64", "<f2": "float16"}
+
+
+def _split_pieces(pieces, size):
+    """Cut (array, staging offset) copy pieces into <= size parts for the pool."""
+    out = []
+    for arr, off in pieces:
+        for s in range(0, arr.nbytes, size):
+            out.append((arr[s:s + size], off + s))
+    return out
 
 
 def resolve_operands(operands, dtypes=None, staged: dict | None = None) -> tuple[np.ndarray, list]:

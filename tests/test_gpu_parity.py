@@ -596,3 +596,36 @@ def test_fuzzed_perturbations_bit_exact():
     rnd = random.Random(5)
     for k in range(100):
         fuzz_perturb.run_case(rnd, k)
+
+
+def test_pageable_host_payloads_through_the_staging_ring():
+    """numpy (and pageable torch CPU) payloads above the staging threshold
+    cross PCIe through the pinned ring: odd sizes, payloads straddling
+    staging buffers, mixed f32 / bf16 / f64 — the report equals the one for
+    device-resident copies of the same traces."""
+    from paper_2506_09280_b200 import device
+    g = np.random.default_rng(21)
+    hdr = {"digest": "d", "mode": "cascade"}
+    ref, cand, ref_d, cand_d = (Trace(header=dict(hdr)) for _ in range(4))
+    shapes = [(4099, 1531), (7,), (3, 5, 7), (1 << 21,), (65537, 33), (12345, 1)]
+    for k, shape in enumerate(shapes):
+        ident = CanonicalId(0, 0, TensorKind.ACTIVATION_OUT, f"model.m{k}")
+        x = g.standard_normal(shape).astype(np.float32)
+        y = (x * (1 + 1e-3 * g.standard_normal(shape))).astype(np.float32)
+        if k % 3 == 1:
+            y_host = torch.from_numpy(y).to(torch.bfloat16)          # pageable torch CPU bf16
+        elif k % 3 == 2:
+            y_host = y.astype(np.float64)
+        else:
+            y_host = y
+        m = identity_mapping(shape)
+        ref.records.append(TraceRecord(ident, RankMeta(), m, 1, x, "Linear"))
+        cand.records.append(TraceRecord(ident, RankMeta(), m, 1, y_host, "Linear"))
+        ref_d.records.append(TraceRecord(ident, RankMeta(), m, 1, torch.from_numpy(x).cuda(), "Linear"))
+        yd = y_host if isinstance(y_host, torch.Tensor) else torch.from_numpy(np.asarray(y_host, np.float32))
+        cand_d.records.append(TraceRecord(ident, RankMeta(), m, 1, yd.cuda(), "Linear"))
+    assert sum(r.nbytes for r in ref.records) + sum(r.nbytes for r in cand.records) > device._STAGE_MIN
+    tol = td.ToleranceMap({}, n_samples=1, eps_p=0.0)
+    got = json.loads(td.render_report(td.check(ref, cand, tol, fmt=td.FloatFormat.FP32), "json"))
+    want = json.loads(td.render_report(td.check(ref_d, cand_d, tol, fmt=td.FloatFormat.FP32), "json"))
+    assert_reports_match(got, want, "staging ring")
