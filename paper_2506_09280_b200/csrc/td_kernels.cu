@@ -1276,22 +1276,45 @@ __global__ void k_generate(double* __restrict__ out, int64_t n, uint64_t seed, i
 
 // one CTA per range (grid-strided); bytes move 4 at a time when source and
 // destination agree mod 4, else one at a time (file payloads are unaligned)
-__global__ void k_gather_bytes(const unsigned char* __restrict__ src, unsigned char* __restrict__ dst,
-                               const int64_t* __restrict__ ranges, int64_t n) {
-    for (int64_t r = blockIdx.x; r < n; r += gridDim.x) {
+// Ranges are cut into TD_GATHER_PIECE-byte pieces dealt round-robin over the
+// grid (every CTA walks the range table, ~6k rows for a large trace), so one
+// 200 MB record spreads over every SM instead of serialising on one CTA.
+// Destinations are 16-byte aligned (the caller's arena); sources keep the
+// file's 4-byte alignment, so a thread loads four u32 and stores one uint4
+// unless the source happens to be 16-byte aligned too.
+#define TD_GATHER_PIECE (64 << 10)
+__global__ void __launch_bounds__(256) k_gather_bytes(const unsigned char* __restrict__ src,
+                                                      unsigned char* __restrict__ dst,
+                                                      const int64_t* __restrict__ ranges, int64_t n) {
+    const int64_t grid = gridDim.x;
+    int64_t base = 0;                                  // global index of range r's first piece
+    for (int64_t r = 0; r < n; ++r) {
         const int64_t so = ranges[3 * r], dof = ranges[3 * r + 1], nb = ranges[3 * r + 2];
-        const unsigned char* s = src + so;
-        unsigned char* d = dst + dof;
-        const int64_t head = (4 - (dof & 3)) & 3;
-        if (((so - dof) & 3) == 0 && nb > head) {
-            for (int64_t i = threadIdx.x; i < head; i += blockDim.x) d[i] = s[i];
-            const int64_t words = (nb - head) >> 2;
-            const uint32_t* s4 = reinterpret_cast<const uint32_t*>(s + head);
-            uint32_t* d4 = reinterpret_cast<uint32_t*>(d + head);
-            for (int64_t i = threadIdx.x; i < words; i += blockDim.x) d4[i] = s4[i];
-            for (int64_t i = head + 4 * words + threadIdx.x; i < nb; i += blockDim.x) d[i] = s[i];
-        } else {
-            for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) d[i] = s[i];
+        const int64_t pieces = (nb + TD_GATHER_PIECE - 1) / TD_GATHER_PIECE;
+        int64_t k = ((int64_t)blockIdx.x - base % grid + grid) % grid;
+        base += pieces;
+        const bool vec_ok = ((dof & 15) == 0) && ((so & 3) == 0);
+        const bool src16 = (so & 15) == 0;
+        for (; k < pieces; k += grid) {
+            const int64_t lo = k * TD_GATHER_PIECE;
+            const int64_t len = nb - lo < TD_GATHER_PIECE ? nb - lo : TD_GATHER_PIECE;
+            const unsigned char* s = src + so + lo;
+            unsigned char* d = dst + dof + lo;
+            if (vec_ok) {
+                const int64_t v = len >> 4;
+                uint4* d16 = reinterpret_cast<uint4*>(d);
+                if (src16) {
+                    const uint4* s16 = reinterpret_cast<const uint4*>(s);
+                    for (int64_t i = threadIdx.x; i < v; i += blockDim.x) d16[i] = s16[i];
+                } else {
+                    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(s);
+                    for (int64_t i = threadIdx.x; i < v; i += blockDim.x)
+                        d16[i] = make_uint4(s4[4 * i], s4[4 * i + 1], s4[4 * i + 2], s4[4 * i + 3]);
+                }
+                for (int64_t i = 16 * v + threadIdx.x; i < len; i += blockDim.x) d[i] = s[i];
+            } else {
+                for (int64_t i = threadIdx.x; i < len; i += blockDim.x) d[i] = s[i];
+            }
         }
     }
 }
@@ -1623,7 +1646,7 @@ int td_generate(double* out, int64_t n, uint64_t seed, int32_t dist, double a, d
 int td_gather_bytes(const void* src, void* dst, const int64_t* ranges, int64_t n, void* stream) {
     if (n == 0) return 0;
     if (!src || !dst || !ranges || n < 0) return fail("td_gather_bytes: invalid arguments");
-    const int grid = (int)(n < 148 * 32 ? n : 148 * 32);
+    const int grid = 148 * 8;
     k_gather_bytes<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<const unsigned char*>(src),
                                                            static_cast<unsigned char*>(dst), ranges, n);
     return check_launch("td_gather_bytes");

@@ -137,7 +137,21 @@ def stage_host_payloads(traces, stream=None) -> dict:
                     continue
             pageable.append(rec)
     if pageable:
-        staged.update(_stage_pageable(pageable))
+        images: dict = {}
+        rest = []
+        for rec in pageable:
+            p = rec.payload
+            hit = _image_of(p) if (not is_torch(p) and p.dtype == np.float32
+                                   and p.flags.c_contiguous) else None
+            if hit is None:
+                rest.append(rec)
+            else:
+                image, off = hit
+                images.setdefault(id(image), (image, []))[1].append((rec, off, p.nbytes))
+        if images:
+            staged.update(_stage_images(images))
+        if rest:
+            staged.update(_stage_pageable(rest))
     for dev, recs in arenas.values():
         dst = dev.untyped_storage()
         for rec in recs:
@@ -145,6 +159,63 @@ def stage_host_payloads(traces, stream=None) -> dict:
             view = torch.empty(0, dtype=p.dtype, device="cuda").set_(dst, p.storage_offset(),
                                                                      p.shape, p.stride())
             staged[id(rec)] = view if view.data_ptr() % 16 == 0 else view.clone()
+    return staged
+
+
+# pinned file images that host traces' numpy payloads view (read_trace on
+# the host): check() moves an image with one DMA and unpacks the payloads on
+# the GPU (td_gather_bytes) — no host copy at all.  Weak: an image lives as
+# long as its trace's payloads do.
+_PINNED_IMAGES = None
+
+
+def register_pinned_image(buf) -> None:
+    """buf: the uint8 numpy array over a pinned host allocation that trace
+    payloads view (np.frombuffer keeps it alive as their base, so a weak
+    reference to it lives exactly as long as the payloads)."""
+    global _PINNED_IMAGES
+    import weakref
+    if _PINNED_IMAGES is None:
+        _PINNED_IMAGES = weakref.WeakValueDictionary()
+    _PINNED_IMAGES[buf.__array_interface__["data"][0]] = buf
+
+
+def _image_of(arr):
+    """(image array, byte offset) when the numpy array views a registered
+    pinned image, else None."""
+    if not _PINNED_IMAGES:
+        return None
+    addr = arr.__array_interface__["data"][0]
+    for base, image in list(_PINNED_IMAGES.items()):
+        if base <= addr and addr + arr.nbytes <= base + image.nbytes:
+            return image, addr - base
+    return None
+
+
+def _stage_images(groups) -> dict:
+    """One DMA per pinned image, then one td_gather_bytes unpacking every
+    payload into a 256-byte-aligned device arena."""
+    import torch
+    staged, plans = {}, []
+    for image, items in groups.values():
+        table, cursor = [], 0
+        for rec, off, nbytes in items:
+            cursor = -(-cursor // 256) * 256
+            table.append((off, cursor, nbytes))
+            cursor += nbytes
+        # range tables cross before any image: a pageable copy queued behind
+        # an image DMA would hold the host until the image had landed
+        plans.append((image, items, table, cursor, torch.tensor(table, dtype=torch.int64).to("cuda")))
+    for image, items, table, cursor, ranges in plans:
+        dev = torch.from_numpy(image).to("cuda", non_blocking=True)
+        arena = torch.empty(max(cursor, 16), dtype=torch.uint8, device="cuda")
+        N.call("td_gather_bytes", dev.data_ptr(), arena.data_ptr(), ranges.data_ptr(), len(table),
+               N.stream_handle())
+        for (rec, _, nbytes), (_, dst, _) in zip(items, table):
+            p = rec.payload
+            staged[id(rec)] = arena[dst:dst + nbytes].view(torch.float32).view(p.shape)
+        # the device image is freed once the gather has consumed it (stream order)
+        del dev
     return staged
 
 

@@ -629,3 +629,24 @@ def test_pageable_host_payloads_through_the_staging_ring():
     got = json.loads(td.render_report(td.check(ref, cand, tol, fmt=td.FloatFormat.FP32), "json"))
     want = json.loads(td.render_report(td.check(ref_d, cand_d, tol, fmt=td.FloatFormat.FP32), "json"))
     assert_reports_match(got, want, "staging ring")
+
+
+def test_read_trace_host_payloads_move_as_pinned_images(cases, golden_trace_bytes, tmp_path, monkeypatch):
+    """read_trace() on the host returns numpy payloads viewing a pinned file
+    image; check() moves each image with one DMA (no staging copies) and the
+    report equals the reference's."""
+    from paper_2506_09280_b200 import device
+    case = next(c for c in cases["checks"] if c["name"] == "bug_stale_input_k3")
+    paths = {}
+    for side in ("ref", "cand"):
+        paths[side] = tmp_path / f"{side}.ttrc"
+        paths[side].write_bytes(golden_trace_bytes(case[side]))
+    ref, cand = td.read_trace(paths["ref"]), td.read_trace(paths["cand"])
+    assert all(isinstance(r.payload, np.ndarray) for r in ref.records + cand.records)
+
+    def no_staging(records):
+        raise AssertionError("pinned-image payloads went through the staging ring")
+    monkeypatch.setattr(device, "_stage_pageable", no_staging)
+    tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+    rep = td.check(ref, cand, tol, case["kappa"], fmt=td.FloatFormat(case["fmt"]))
+    assert_reports_match(json.loads(td.render_report(rep, "json")), json.loads(case["report"]), "pinned image")

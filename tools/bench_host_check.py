@@ -15,12 +15,27 @@ def main():
     import torch
     import bench
     import paper_2506_09280_b200 as td
-    from paper_2506_09280_b200.tracestore import trace_from_bytes, trace_to_bytes
+    from paper_2506_09280_b200.tracestore import trace_from_bytes, trace_to_bytes, write_trace
     _, ref, cand, tol, fmt = bench.workload("cfg2")
-    rb, cb = trace_to_bytes(ref), trace_to_bytes(cand)
-    del ref, cand
-    torch.cuda.empty_cache()
-    href, hcand = trace_from_bytes(rb), trace_from_bytes(cb)
+    if "--file" in sys.argv:
+        # read_trace(path) on the host: payloads view a pinned file image
+        tmp = os.environ.get("TMPDIR", "/tmp")
+        paths = [os.path.join(tmp, f"bhc_{n}.ttrc") for n in ("ref", "cand")]
+        write_trace(ref, paths[0])
+        write_trace(cand, paths[1])
+        del ref, cand
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        href, hcand = td.read_trace(paths[0]), td.read_trace(paths[1])
+        read_s = time.perf_counter() - t0
+        for p in paths:
+            os.unlink(p)
+    else:
+        read_s = None
+        rb, cb = trace_to_bytes(ref), trace_to_bytes(cand)
+        del ref, cand
+        torch.cuda.empty_cache()
+        href, hcand = trace_from_bytes(rb), trace_from_bytes(cb)
     nbytes = sum(r.nbytes for r in href.records) + sum(r.nbytes for r in hcand.records)
     times = []
     for _ in range(4):
@@ -29,7 +44,8 @@ def main():
         rep = td.check(href, hcand, tol, fmt=fmt)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
-    print(json.dumps({"payload_bytes_f32": nbytes, "first_s": times[0], "cached_s": min(times[1:]),
+    print(json.dumps({"mode": "file" if read_s is not None else "bytes", "read_s": read_s,
+                      "payload_bytes_f32": nbytes, "first_s": times[0], "cached_s": min(times[1:]),
                       "cached_gbs": nbytes / min(times[1:]) / 1e9, "verdicts": rep.counts}))
 
 
