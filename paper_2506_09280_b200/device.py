@@ -148,6 +148,12 @@ def stage_host_payloads(traces, stream=None) -> dict:
             else:
                 image, off = hit
                 images.setdefault(id(image), (image, []))[1].append((rec, off, p.nbytes))
+        for key, (image, items) in list(images.items()):
+            # an image mostly not referenced by these traces (a subset of a
+            # big file) is cheaper through the staging ring than whole
+            if 2 * sum(nb for _, _, nb in items) < image.nbytes:
+                rest.extend(rec for rec, _, _ in items)
+                del images[key]
         if images:
             staged.update(_stage_images(images))
         if rest:

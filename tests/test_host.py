@@ -174,3 +174,21 @@ def test_retiled_and_chunked_plan_tables_are_consistent(monkeypatch, cases, gold
             assert ((rows["row_end"] - rows["row_begin"]) <= 7).all()
             cursor = c1
         assert cursor == len(ch)
+
+
+def test_parallel_file_read_fills_every_byte(tmp_path, monkeypatch):
+    """read_trace's pinned-image reader: 64 MiB preads over threads (here
+    shrunk to 4 KiB pieces, odd tail) land every byte where it belongs, and a
+    short file is an error, not silent zeros."""
+    from paper_2506_09280_b200 import tracestore
+    monkeypatch.setattr(tracestore, "_READ_PIECE", 4096)
+    data = np.random.default_rng(5).integers(0, 256, 10 * 4096 + 123, dtype=np.uint8).tobytes()
+    path = tmp_path / "blob"
+    path.write_bytes(data)
+    for threads in ("1", "4"):
+        monkeypatch.setenv("TD_READ_THREADS", threads)
+        buf = bytearray(len(data))
+        tracestore._read_parallel(str(path), memoryview(buf), len(data))
+        assert bytes(buf) == data
+    with pytest.raises(EOFError):
+        tracestore._read_parallel(str(path), memoryview(bytearray(len(data) + 10)), len(data) + 10)
