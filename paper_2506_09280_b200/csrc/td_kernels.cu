@@ -1279,9 +1279,14 @@ __global__ void k_generate(double* __restrict__ out, int64_t n, uint64_t seed, i
 // Ranges are cut into TD_GATHER_PIECE-byte pieces dealt round-robin over the
 // grid (every CTA walks the range table, ~6k rows for a large trace), so one
 // 200 MB record spreads over every SM instead of serialising on one CTA.
-// Destinations are 16-byte aligned (the caller's arena); sources keep the
-// file's 4-byte alignment, so a thread loads four u32 and stores one uint4
-// unless the source happens to be 16-byte aligned too.
+// Each piece stores aligned uint4s: a few head bytes bring the destination to
+// 16 B, then the source is read as uint4 (same alignment), as four u32
+// (4-byte aligned), or as five aligned u32 funnel-shifted into place (any
+// other offset: TTRC payload offsets are arbitrary, and the file writer
+// scatters a 4-byte-aligned f32 arena to them).  The shifted path reads
+// only aligned words holding at least one byte of the range (it stops 3
+// bytes short of the end; the tail goes bytewise), so it never crosses an
+// allocation boundary.
 #define TD_GATHER_PIECE (64 << 10)
 __global__ void __launch_bounds__(256) k_gather_bytes(const unsigned char* __restrict__ src,
                                                       unsigned char* __restrict__ dst,
@@ -1293,28 +1298,41 @@ __global__ void __launch_bounds__(256) k_gather_bytes(const unsigned char* __res
         const int64_t pieces = (nb + TD_GATHER_PIECE - 1) / TD_GATHER_PIECE;
         int64_t k = ((int64_t)blockIdx.x - base % grid + grid) % grid;
         base += pieces;
-        const bool vec_ok = ((dof & 15) == 0) && ((so & 3) == 0);
-        const bool src16 = (so & 15) == 0;
         for (; k < pieces; k += grid) {
             const int64_t lo = k * TD_GATHER_PIECE;
             const int64_t len = nb - lo < TD_GATHER_PIECE ? nb - lo : TD_GATHER_PIECE;
             const unsigned char* s = src + so + lo;
             unsigned char* d = dst + dof + lo;
-            if (vec_ok) {
-                const int64_t v = len >> 4;
-                uint4* d16 = reinterpret_cast<uint4*>(d);
-                if (src16) {
-                    const uint4* s16 = reinterpret_cast<const uint4*>(s);
-                    for (int64_t i = threadIdx.x; i < v; i += blockDim.x) d16[i] = s16[i];
-                } else {
-                    const uint32_t* s4 = reinterpret_cast<const uint32_t*>(s);
-                    for (int64_t i = threadIdx.x; i < v; i += blockDim.x)
-                        d16[i] = make_uint4(s4[4 * i], s4[4 * i + 1], s4[4 * i + 2], s4[4 * i + 3]);
-                }
-                for (int64_t i = 16 * v + threadIdx.x; i < len; i += blockDim.x) d[i] = s[i];
+            int64_t head = (16 - (int64_t)(reinterpret_cast<uintptr_t>(d) & 15)) & 15;
+            if (head > len) head = len;
+            for (int64_t i = threadIdx.x; i < head; i += blockDim.x) d[i] = s[i];
+            const unsigned char* s1 = s + head;
+            uint4* d16 = reinterpret_cast<uint4*>(d + head);
+            const int64_t rest = len - head;
+            const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(s1) & 15);
+            int64_t v;
+            if (mis == 0) {
+                v = rest >> 4;
+                const uint4* s16 = reinterpret_cast<const uint4*>(s1);
+                for (int64_t i = threadIdx.x; i < v; i += blockDim.x) d16[i] = s16[i];
+            } else if ((mis & 3) == 0) {
+                v = rest >> 4;
+                const uint32_t* s4 = reinterpret_cast<const uint32_t*>(s1);
+                for (int64_t i = threadIdx.x; i < v; i += blockDim.x)
+                    d16[i] = make_uint4(s4[4 * i], s4[4 * i + 1], s4[4 * i + 2], s4[4 * i + 3]);
             } else {
-                for (int64_t i = threadIdx.x; i < len; i += blockDim.x) d[i] = s[i];
+                const uint32_t sh = 8 * (mis & 3);
+                v = rest >= 3 ? (rest - 3) >> 4 : 0;
+                const uint32_t* sw = reinterpret_cast<const uint32_t*>(s1 - (mis & 3));
+                for (int64_t i = threadIdx.x; i < v; i += blockDim.x) {
+                    const uint32_t w0 = sw[4 * i], w1 = sw[4 * i + 1], w2 = sw[4 * i + 2],
+                                   w3 = sw[4 * i + 3], w4 = sw[4 * i + 4];
+                    d16[i] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh),
+                                        __funnelshift_r(w2, w3, sh), __funnelshift_r(w3, w4, sh));
+                }
             }
+            unsigned char* d1 = d + head;
+            for (int64_t i = 16 * v + threadIdx.x; i < rest; i += blockDim.x) d1[i] = s1[i];
         }
     }
 }

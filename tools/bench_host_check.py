@@ -21,8 +21,10 @@ def main():
         # read_trace(path) on the host: payloads view a pinned file image
         tmp = os.environ.get("TMPDIR", "/tmp")
         paths = [os.path.join(tmp, f"bhc_{n}.ttrc") for n in ("ref", "cand")]
+        t0 = time.perf_counter()
         write_trace(ref, paths[0])
         write_trace(cand, paths[1])
+        write_s = time.perf_counter() - t0
         del ref, cand
         torch.cuda.empty_cache()
         t0 = time.perf_counter()
@@ -31,7 +33,7 @@ def main():
         for p in paths:
             os.unlink(p)
     else:
-        read_s = None
+        read_s = write_s = None
         rb, cb = trace_to_bytes(ref), trace_to_bytes(cand)
         del ref, cand
         torch.cuda.empty_cache()
@@ -44,7 +46,7 @@ def main():
         rep = td.check(href, hcand, tol, fmt=fmt)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
-    print(json.dumps({"mode": "file" if read_s is not None else "bytes", "read_s": read_s,
+    print(json.dumps({"mode": "file" if read_s is not None else "bytes", "read_s": read_s, "write_s": write_s,
                       "payload_bytes_f32": nbytes, "first_s": times[0], "cached_s": min(times[1:]),
                       "cached_gbs": nbytes / min(times[1:]) / 1e9, "verdicts": rep.counts}))
 
