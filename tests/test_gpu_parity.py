@@ -632,16 +632,17 @@ def test_pageable_host_payloads_through_the_staging_ring():
 
 
 def test_read_trace_host_payloads_move_as_pinned_images(cases, golden_trace_bytes, tmp_path, monkeypatch):
-    """read_trace() on the host returns numpy payloads viewing a pinned file
-    image; check() moves each image with one DMA (no staging copies) and the
-    report equals the reference's."""
+    """read_trace(pin=True) on the host returns numpy payloads viewing a
+    page-locked file image; check() moves each image with one DMA (no
+    staging copies) and the report equals the reference's (and equals the
+    default, unpinned read's)."""
     from paper_2506_09280_b200 import device
     case = next(c for c in cases["checks"] if c["name"] == "bug_stale_input_k3")
     paths = {}
     for side in ("ref", "cand"):
         paths[side] = tmp_path / f"{side}.ttrc"
         paths[side].write_bytes(golden_trace_bytes(case[side]))
-    ref, cand = td.read_trace(paths["ref"]), td.read_trace(paths["cand"])
+    ref, cand = td.read_trace(paths["ref"], pin=True), td.read_trace(paths["cand"], pin=True)
     assert all(isinstance(r.payload, np.ndarray) for r in ref.records + cand.records)
 
     def no_staging(records):
@@ -650,6 +651,10 @@ def test_read_trace_host_payloads_move_as_pinned_images(cases, golden_trace_byte
     tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
     rep = td.check(ref, cand, tol, case["kappa"], fmt=td.FloatFormat(case["fmt"]))
     assert_reports_match(json.loads(td.render_report(rep, "json")), json.loads(case["report"]), "pinned image")
+    monkeypatch.undo()
+    plain = td.check(td.read_trace(paths["ref"]), td.read_trace(paths["cand"]), tol, case["kappa"],
+                     fmt=td.FloatFormat(case["fmt"]))
+    assert_reports_match(json.loads(td.render_report(plain, "json")), json.loads(case["report"]), "unpinned")
 
 
 def test_gather_bytes_any_offsets_against_numpy():

@@ -192,3 +192,28 @@ def test_parallel_file_read_fills_every_byte(tmp_path, monkeypatch):
         assert bytes(buf) == data
     with pytest.raises(EOFError):
         tracestore._read_parallel(str(path), memoryview(bytearray(len(data) + 10)), len(data) + 10)
+
+
+def test_header_parse_from_file_windows_matches_in_memory(tmp_path, cases, golden_trace_bytes):
+    """The device reader parses record headers through small preads
+    (_FileBytes; payloads skipped, never read): same rows as parsing the
+    whole image, and truncation is still a FormatError."""
+    from paper_2506_09280_b200 import tracestore as T
+    for name in cases["traces"][:6]:
+        raw = golden_trace_bytes(name)
+        path = tmp_path / (name + ".ttrc")
+        path.write_bytes(raw)
+        src = T._FileBytes(str(path), len(raw))
+        try:
+            got = T._parse(src)
+        finally:
+            src.close()
+        want = T._parse(memoryview(raw))
+        assert got[1] == want[1] and [r[6:] for r in got[2]] == [r[6:] for r in want[2]], name
+        assert [r[0].encode() for r in got[2]] == [r[0].encode() for r in want[2]]
+    cut = tmp_path / "cut.ttrc"
+    cut.write_bytes(raw[:-7])
+    src = T._FileBytes(str(cut), len(raw) - 7)
+    with pytest.raises(FormatError):
+        T._parse(src)
+    src.close()

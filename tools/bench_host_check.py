@@ -27,13 +27,22 @@ def main():
         write_s = time.perf_counter() - t0
         del ref, cand
         torch.cuda.empty_cache()
+        read_dev = []
+        for _ in range(2):                      # the CLI's reader: file -> HBM
+            t0 = time.perf_counter()
+            dref, dcand = td.read_trace(paths[0], device="cuda"), td.read_trace(paths[1], device="cuda")
+            torch.cuda.synchronize()
+            read_dev.append(time.perf_counter() - t0)
+            del dref, dcand
+            torch.cuda.empty_cache()
+        pin = "--pin" in sys.argv
         t0 = time.perf_counter()
-        href, hcand = td.read_trace(paths[0]), td.read_trace(paths[1])
+        href, hcand = td.read_trace(paths[0], pin=pin), td.read_trace(paths[1], pin=pin)
         read_s = time.perf_counter() - t0
         for p in paths:
             os.unlink(p)
     else:
-        read_s = write_s = None
+        read_s = write_s = read_dev = None
         rb, cb = trace_to_bytes(ref), trace_to_bytes(cand)
         del ref, cand
         torch.cuda.empty_cache()
@@ -46,7 +55,7 @@ def main():
         rep = td.check(href, hcand, tol, fmt=fmt)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
-    print(json.dumps({"mode": "file" if read_s is not None else "bytes", "read_s": read_s, "write_s": write_s,
+    print(json.dumps({"mode": ("file+pin" if "--pin" in sys.argv else "file") if read_s is not None else "bytes", "read_s": read_s, "write_s": write_s, "read_device_s": read_dev,
                       "payload_bytes_f32": nbytes, "first_s": times[0], "cached_s": min(times[1:]),
                       "cached_gbs": nbytes / min(times[1:]) / 1e9, "verdicts": rep.counts}))
 
