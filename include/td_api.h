@@ -296,8 +296,12 @@ int td_generate(double* out, int64_t n, uint64_t seed, int32_t dist, double a, d
                 int64_t vocab, const int64_t* skips, int32_t n_skips,
                 unsigned long long* zero_count, int64_t* zero_pos, int32_t zero_cap, void* stream);
 
-/* ---- device TTRC reader: byte ranges of a file image -> aligned arena ----
- * ranges: n rows of {src_off, dst_off, nbytes} int64 (device); any alignment. */
+/* ---- device TTRC reader / writer: byte-range scatter-gather in HBM ----
+ * ranges: n rows of {src_off, dst_off, nbytes} int64 (device), any alignment
+ * on either side, ranges must not overlap in dst.  Reader: file image ->
+ * 256-B-aligned f32 arena (tracestore.trace_from_bytes); writer: f32 arena
+ * and header blob -> file image (tracestore.write_trace).  Replaces the
+ * reference's per-record np.frombuffer / tobytes (tracestore.py:155-289). */
 int td_gather_bytes(const void* src, void* dst, const int64_t* ranges, int64_t n, void* stream);
 
 #ifdef __cplusplus
