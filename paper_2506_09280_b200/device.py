@@ -9,9 +9,10 @@ kernels in libtdb200.so; there is no CPU arithmetic fallback.
 
 from __future__ import annotations
 
-import numpy as np
-
 import os
+import threading
+
+import numpy as np
 
 from . import _native as N
 
@@ -237,7 +238,16 @@ _STAGE_MIN = 64 << 20
 _STAGING = None
 
 
+_STAGING_LOCK = threading.Lock()
+
+
 def _stage_pageable(records) -> dict:
+    # one ring per process: concurrent check() calls take turns on it
+    with _STAGING_LOCK:
+        return _stage_pageable_locked(records)
+
+
+def _stage_pageable_locked(records) -> dict:
     import concurrent.futures
     import torch
     global _STAGING
@@ -264,12 +274,13 @@ def _stage_pageable(records) -> dict:
         total += a.nbytes
     if total < _STAGE_MIN:
         return {id(rec): to_device(rec.payload) for rec in records}
-    if _STAGING is None:
+    dev = torch.cuda.current_device()
+    if _STAGING is None or _STAGING[4] != dev:
         bufs = [torch.empty(_STAGE_CHUNK, dtype=torch.uint8).pin_memory() for _ in range(_STAGE_RING)]
         pool = concurrent.futures.ThreadPoolExecutor(
             max_workers=int(os.environ.get("TD_STAGE_THREADS", min(8, os.cpu_count() or 1))))
-        _STAGING = (bufs, [None] * _STAGE_RING, pool, torch.cuda.Stream())
-    bufs, events, pool, copy_stream = _STAGING
+        _STAGING = (bufs, [None] * _STAGE_RING, pool, torch.cuda.Stream(), dev)
+    bufs, events, pool, copy_stream, _ = _STAGING
     arena = torch.empty(max(total, 16), dtype=torch.uint8, device="cuda")
     copy_stream.wait_stream(torch.cuda.current_stream())
     item, inner, k = 0, 0, 0

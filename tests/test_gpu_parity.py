@@ -700,3 +700,23 @@ def test_write_trace_from_device_is_byte_identical(tmp_path, cases, golden_trace
         out = tmp_path / (name + ".out.ttrc")
         write_trace(dev, out)
         assert out.read_bytes() == raw, name
+
+
+def test_concurrent_file_reads_and_host_checks(tmp_path, cases, golden_trace_bytes):
+    """The pinned rings (file reader, host staging) are process-wide: two
+    threads reading traces to the device and checking host traces at the
+    same time get the same results as one thread doing it alone."""
+    import concurrent.futures
+    from paper_2506_09280_b200.tracestore import read_trace
+    names = cases["traces"][:4]
+    for name in names:
+        (tmp_path / (name + ".ttrc")).write_bytes(golden_trace_bytes(name))
+
+    def job(name):
+        dev = read_trace(tmp_path / (name + ".ttrc"), device="cuda")
+        return [r.payload.cpu().numpy().tobytes() for r in dev.records]
+    want = {n: job(n) for n in names}
+    with concurrent.futures.ThreadPoolExecutor(4) as ex:
+        for _ in range(3):
+            got = dict(zip(names, ex.map(job, names)))
+            assert got == want
