@@ -169,10 +169,10 @@ def stage_host_payloads(traces, stream=None) -> dict:
     return staged
 
 
-# pinned file images that host traces' numpy payloads view (read_trace on
-# the host): check() moves an image with one DMA and unpacks the payloads on
-# the GPU (td_gather_bytes) — no host copy at all.  Weak: an image lives as
-# long as its trace's payloads do.
+# page-locked file images that host traces' numpy payloads view
+# (read_trace(path, pin=True)): check() moves an image with one DMA and
+# unpacks the payloads on the GPU (td_gather_bytes) — no host copy at all.
+# Weak: an image lives as long as its trace's payloads do.
 _PINNED_IMAGES = None
 
 
