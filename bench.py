@@ -30,6 +30,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import sys
@@ -46,12 +47,35 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg3")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-stride", type=int, default=8, help="cpu_baseline samples every k-th id")
     return ap.parse_args()
+
+
+# L2 of a B200 (126.5 MiB): workloads under 4x this are timed with the L2
+# flushed before every step; both arms state the same rule in `config`
+L2_BYTES = 132644864
+
+
+def host_cpu() -> dict:
+    """CPU model and the cores this process may use (both CPU arms)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"cpu_model": model or "unknown", "cpu_count": os.cpu_count() or 1, "cpu_usable": usable}
 
 
 # measured pure-read HBM stream (tools/hbm_probe.cu read_xor, 2 x 4 GiB,
@@ -80,8 +104,9 @@ def describe(name: str):
         g = int(parts[3]) if len(parts) > 3 else (4 if maps != "identity" else 1)
         desc = {"workload": f"config5 raw compare sweep: one id, {mib} MiB bf16 per tensor, "
                             f"shape (N/4096, 4096), candidate {maps} x{g}",
-                "storage_dtype": "bf16", "tensor_mib": mib, "maps": maps, "shards": g}
-        return desc, {"sweep": (mib, maps, g), "fmt": FloatFormat.BF16}
+                "storage_dtype": "bf16", "tensor_mib": mib, "maps": maps, "shards": g,
+                "inputs": l2_note(2 * (mib << 20))}
+        return desc, {"sweep": (mib, maps, g), "fmt": FloatFormat.BF16, "nbytes": 2 * (mib << 20)}
     if name == "cfg4":
         model, pcfg = L.LLAMA3_8B, L.ParallelConfig(tp=2, dp=4, microbatches=4)
         desc = {"workload": "config4 Llama-3-8B-shape bf16 full-step traces (L=32 d=4096 GQA 32/8 ff=14336 "
@@ -91,7 +116,8 @@ def describe(name: str):
                 "trace_shapes": f"layers={model.layers} d={model.d_model} ff={model.d_ff} "
                                 f"S={model.seq_len} V={model.vocab}",
                 "candidate_layout": "tp=2 dp=4 cp=1 sp=False microbatches=4", "storage_dtype": "bf16",
-                "job_gpus": 8}
+                "job_gpus": 8,
+                "inputs": "~74 GB of trace payload per GPU share, far larger than the 126.5 MiB L2: no flush"}
         return desc, {"model": model, "pcfg": pcfg, "dtype": "bf16", "fmt": FloatFormat.BF16, "share": 8}
     if name == "cfg1":
         model, pcfg, dtype, fmt = L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), "f32", FloatFormat.FP32
@@ -116,7 +142,20 @@ def describe(name: str):
                                               f"ff={model.d_ff} S={model.seq_len} V={model.vocab}",
             "candidate_layout": f"tp={pcfg.tp} dp={pcfg.dp} cp={pcfg.cp} sp={pcfg.sp}",
             "storage_dtype": dtype}
-    return desc, {"model": model, "pcfg": pcfg, "dtype": dtype, "fmt": fmt, "bugs": bugs}
+    esize = 4 if dtype == "f32" else 2
+    nbytes = sum(math.prod(s.mapping.local_shape) * esize
+                 for s in L.emit_records(model, L.ParallelConfig(microbatches=pcfg.microbatches)))
+    nbytes += sum(math.prod(s.mapping.local_shape) * esize for s in L.emit_records(model, pcfg))
+    desc["inputs"] = l2_note(nbytes)
+    return desc, {"model": model, "pcfg": pcfg, "dtype": dtype, "fmt": fmt, "bugs": bugs, "nbytes": nbytes}
+
+
+def l2_note(nbytes: int) -> str:
+    """How the timed steps treat the L2 (the same words in both arms)."""
+    if nbytes < 4 * L2_BYTES:
+        return (f"{nbytes / 1e6:.1f} MB of trace payload, under 4x the 126.5 MiB L2: L2 flushed before "
+                f"every step (a 2xL2+64 MiB memset outside the per-step events)")
+    return f"{nbytes / 1e9:.2f} GB of trace payload, far larger than the 126.5 MiB L2: no flush"
 
 
 def workload(name: str, rank: int = 0):
@@ -198,12 +237,32 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+CPU_SAMPLE_BYTES = 3 << 30      # ~15-30 s of single-core oracle work
+
+
+def _sample_ids(ids, size_of, stride: int, budget: int, max_id: int | None = None) -> set:
+    """Every `stride`-th id in trace order while the sample's payload bytes
+    stay within `budget` (ids that alone exceed what is left, or max_id, are
+    skipped)."""
+    out, total = set(), 0
+    for ident in ids[::stride]:
+        nb = size_of.get(ident, 0)
+        if total + nb <= budget and (max_id is None or nb <= max_id):
+            out.add(ident)
+            total += nb
+    return out
+
+
 def cpu_baseline(ref, cand, tol, fmt, stride: int):
-    """Time the oracle's check on every `stride`-th common id (host f32 copies)."""
+    """Time the oracle's check on a bounded sample of the common ids (host f32
+    copies), one thread (numpy), on this box's host CPU."""
     import numpy as np
     from oracle import traindiff_oracle as O
     ids = [i for i in dict.fromkeys(r.id.encode() for r in cand.records)]
-    sample = set(ids[::stride])
+    size_of: dict = {}
+    for r in list(ref.records) + list(cand.records):
+        size_of[r.id.encode()] = size_of.get(r.id.encode(), 0) + 2 * int(np.prod(r.shape))
+    sample = _sample_ids(ids, size_of, stride, CPU_SAMPLE_BYTES, REF_MAX_ID_BYTES)
 
     def host(recs):
         out = []
@@ -218,9 +277,13 @@ def cpu_baseline(ref, cand, tol, fmt, stride: int):
     t0 = time.perf_counter()
     doc = O.check(rr, cr, ref.header, cand.header, tol.responses, 3.0, fmt.value)
     dt = time.perf_counter() - t0
+    cpu = host_cpu()
     return {"value": nbytes / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
-            "sample": f"every {stride}th id ({len(sample)} ids, {nbytes / 1e9:.3f} GB of trace payload "
-                      f"counted at the workload's 2 B/elem), oracle/traindiff_oracle.check, 1 thread numpy",
+            "cpu_model": cpu["cpu_model"], "host_cores": cpu["cpu_count"],
+            "sample": f"every {stride}th id of at most {REF_MAX_ID_BYTES >> 20} MiB within a "
+                      f"{CPU_SAMPLE_BYTES >> 30} GiB budget ({len(sample)} ids, "
+                      f"{nbytes / 1e9:.3f} GB of trace payload counted at the workload's 2 B/elem), "
+                      f"oracle/traindiff_oracle.check, 1 thread numpy",
             "seconds": dt, "layer_checks_per_s": len(doc["entries"]) / dt}
 
 
@@ -243,6 +306,10 @@ def _reference_worker(args):
 
 
 _REF_SHARED = None
+
+
+REF_SAMPLE_BYTES = 1 << 30      # per reference-arm step (all host cores) ...
+REF_MAX_ID_BYTES = 320 << 20    # ... made of ids no larger than a TP=8 hidden activation
 
 
 def host_sample(name: str, stride: int):
@@ -280,7 +347,10 @@ def host_sample(name: str, stride: int):
     ref_specs = {s.ident: s for s in L.emit_records(model, L.ParallelConfig(microbatches=pcfg.microbatches))}
     cand_specs = L.emit_records(model, pcfg)
     ids = list(dict.fromkeys(s.ident for s in cand_specs))
-    sample = set(ids[::stride])
+    size_of: dict = {}
+    for sp in list(ref_specs.values()) + list(cand_specs):
+        size_of[sp.ident] = size_of.get(sp.ident, 0) + 2 * math.prod(sp.mapping.local_shape)
+    sample = _sample_ids(ids, size_of, stride, REF_SAMPLE_BYTES, REF_MAX_ID_BYTES)
     rng = np.random.default_rng(0)
     rr, cr = [], []
     for ident in ids:
@@ -416,10 +486,10 @@ def run_share(args, world: int, rank: int, local: int):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (N(0,sigma) per id rounded to bf16; candidate = Q(ref*(1+2^-8 u)))",
-                "config": dict(desc, inputs=f"{(ref.nbytes + cand.nbytes) / 1e9:.1f} GB resident on this GPU "
-                                            "(>> 126 MB L2, no flush)",
-                               algorithmic_bytes_per_step=alg_bytes, ids=n_ids,
-                               parallelism=f"{world} of the job's {share} GPUs live"),
+                "config": desc,
+                "workload_stats": {"algorithmic_bytes_per_step": alg_bytes, "ids": n_ids,
+                                   "resident_gb": (ref.nbytes + cand.nbytes) / 1e9,
+                                   "parallelism": f"{world} of the job's {share} GPUs live"},
                 "layer_checks_per_s": n_ids * world / (ms_step / 1e3),
                 "build_seconds": build_s, "plan_seconds": plan_s,
                 "share": {"candidate_gb": cand.nbytes / 1e9, "reference_gb": ref.nbytes / 1e9,
@@ -458,10 +528,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    stride = max(1, args.cpu_stride * 4)
+    stride = max(1, args.cpu_stride)
     rr, cr, fmt, n_sample = host_sample(args.config, stride)
     nbytes = sum(r.payload.size * 2 for r in rr) + sum(r.payload.size * 2 for r in cr)
-    cores = os.cpu_count() or 1
+    cores = host_cpu()["cpu_usable"]
     eps = 2.0 ** -24 if fmt == "FP32" else 2.0 ** -8
     _REF_SHARED = (rr, cr, eps)
     sample = sorted({r.ident for r in cr})
@@ -477,6 +547,7 @@ def run_reference(args):
                 times.append(dt)
     t = sum(times) / len(times)
     value = nbytes / t / 1e9
+    cpu = host_cpu()
     line = {"impl": "reference", "metric": "traced-tensor compare GB/s vs HBM roofline; layer-checks/sec",
             "value": value, "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
@@ -485,8 +556,11 @@ def run_reference(args):
             "config": describe(args.config)[0],
             "layer_checks_per_s": n_sample / t,
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
+                             "cpu_model": cpu["cpu_model"], "host_cores": cpu["cpu_count"],
                              "sampled_ids": n_sample,
-                             "sample": f"every {stride}th id of the workload ({n_sample} ids, "
+                             "sample": f"every {stride}th id of the workload of at most "
+                                       f"{REF_MAX_ID_BYTES >> 20} MiB, within a {REF_SAMPLE_BYTES >> 20} "
+                                       f"MiB budget ({n_sample} ids, "
                                        f"{nbytes / 1e9:.3f} GB at 2 B/elem), merge+rel_err per id on "
                                        f"{cores} processes"},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -563,7 +637,8 @@ def main():
     # inputs smaller than a few L2s (config 5's small tensors): L2 flushed
     # before every step, each step timed alone (the flush outside its events)
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
-    flush = torch.empty(2 * l2 + (64 << 20), dtype=torch.uint8, device="cuda") if alg_bytes < 4 * l2 else None
+    flush = torch.empty(2 * l2 + (64 << 20), dtype=torch.uint8, device="cuda") \
+        if alg_bytes < 4 * L2_BYTES else None
     step_ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)] \
         if flush is not None else None
     if world > 1:
@@ -632,8 +707,18 @@ def main():
         d2h = n_ids * N.ID_RESULT.itemsize
         del ref, cand
         torch.cuda.empty_cache()
-        check(href, hcand, tol, 3.0, fmt=fmt)        # warm-up
+        # the first call misses check()'s plan cache: it is timed as the cold
+        # e2e (host planning of the layout + everything the warm calls do)
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        check(href, hcand, tol, 3.0, fmt=fmt)
+        torch.cuda.synchronize()
+        t_cold = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t_cold, op=dist.ReduceOp.MAX)
+        t_cold = float(t_cold.item())
         times = []
         for _ in range(args.e2e_steps):
             if world > 1:
@@ -651,8 +736,11 @@ def main():
                "seconds_per_step": float(t_e2e.item()),
                "layer_checks_per_s": n_ids * world / float(t_e2e.item()),
                "verdicts": rep.counts,
-               "plan": "check()'s layout-keyed plan cache: planned by the warm-up call, reused by the "
-                       "timed calls (same layout every step; the payloads cross PCIe every step)"}
+               "plan": "check()'s layout-keyed plan cache: planned by the first (cold) call, reused by the "
+                       "timed calls (same layout every step; the payloads cross PCIe every step)",
+               "cold": {"value": alg_bytes * world / t_cold / 1e9, "unit": "GB/s", "seconds": t_cold,
+                        "what": "first check() of the layout: plan-cache miss (host planning) + the same "
+                                "H2D / kernels / D2H / report"}}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         if e2e is not None and e2e.get("value") is not None:
@@ -675,13 +763,11 @@ def main():
                 "dtype": "f64",   # arithmetic type: fp64 accumulation of bf16/f32 payloads
                 "data": "synthetic (N(0,sigma) per id rounded to the storage dtype; candidate = "
                         "Q(ref*(1+2^-8 u)), counter-based stream)",
-                "config": dict(desc, inputs=(f"{alg_bytes / 1e9:.2f} GB resident, larger than the L2 (no flush)"
-                                             if flush is None else
-                                             f"{alg_bytes / 1e6:.1f} MB resident; L2 flushed before every step "
-                                             f"({flush.numel() >> 20} MiB memset, outside the per-step events)"),
-                               algorithmic_bytes_per_step=alg_bytes, ids=n_ids,
-                               parallelism=f"dp{world} (independent id sets per rank, partial sums "
-                                           f"allreduced)" if world > 1 else "single GPU"),
+                "config": desc,
+                "workload_stats": {"algorithmic_bytes_per_step": alg_bytes, "ids": n_ids,
+                                   "l2_flush_per_step": flush is not None,
+                                   "parallelism": f"dp{world} (independent id sets per rank, partial sums "
+                                                  f"allreduced)" if world > 1 else "single GPU"},
                 "layer_checks_per_s": n_ids * world / (ms_step / 1e3),
                 "plan_seconds": plan_s,
                 "verdict_counts": {k: int((idres["verdict"] == v).sum()) for k, v in

@@ -412,6 +412,7 @@ def _one_group(ident, records, numeric):
 
 
 _REL_ERR_WORK: dict = {}
+_REL_ERR_LOCK = threading.Lock()
 
 
 def pair_sums(ta, tb) -> tuple[float, float, float]:
@@ -419,13 +420,19 @@ def pair_sums(ta, tb) -> tuple[float, float, float]:
     tensors: td_rel_err, one launch and one 24-byte D2H."""
     import torch
     dev = ta.device
-    work = _REL_ERR_WORK.get(dev)
-    if work is None:
-        work = _REL_ERR_WORK[dev] = (torch.zeros(N.REL_ERR_WORK_BYTES, dtype=torch.uint8, device=dev),
-                                     torch.zeros(3, dtype=torch.float64, device=dev))
+    # the kernel's partials + ticket are per (device, stream): launches on
+    # one stream are ordered, so they never share a workspace concurrently;
+    # the 3-double result is per call
+    stream = torch.cuda.current_stream(dev)
+    key = (dev, stream.cuda_stream)
+    with _REL_ERR_LOCK:
+        work = _REL_ERR_WORK.get(key)
+        if work is None:
+            work = _REL_ERR_WORK[key] = torch.zeros(N.REL_ERR_WORK_BYTES, dtype=torch.uint8, device=dev)
+    out = torch.empty(3, dtype=torch.float64, device=dev)
     N.call("td_rel_err", ta.data_ptr(), tb.data_ptr(), N.dtype_code(ta), ta.numel(),
-           work[0].data_ptr(), work[1].data_ptr(), N.stream_handle())
-    d2, a2, rel = work[1].tolist()
+           work.data_ptr(), out.data_ptr(), N.stream_handle(stream))
+    d2, a2, rel = out.tolist()
     return d2, a2, rel
 
 

@@ -23,6 +23,7 @@ from __future__ import annotations
 import functools
 import math
 import os
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -647,6 +648,7 @@ class Plan:
 
 
 _ONE_SEG = os.environ.get("TD_ONE_SEG", "1") != "0"      # A/B switch for by-value single segments
+_STAGING_LOCK = threading.Lock()
 
 
 class Prepared:
@@ -710,19 +712,23 @@ class Prepared:
         # one pinned staging buffer per plan, reused by every binding of it
         # (cudaHostAlloc per check cost ~ms); the previous copy out of it must
         # have completed before it is overwritten
-        staging, done = getattr(plan, "_staging", (None, None))
-        if staging is None or staging.numel() < blob.size:
-            staging = torch.empty(blob.size, dtype=torch.uint8).pin_memory()
-        elif done is not None:
-            done.synchronize()
-        host = staging[:blob.size]
-        host.numpy()[:] = blob
+        # (a plan cached by check() can be bound by several threads at once:
+        # the lock spans wait-for-previous-copy, fill and enqueue, so no
+        # binding overwrites the buffer before another's copy has read it)
         self.tables = torch.empty(blob.size, dtype=torch.uint8, device=dev)
-        with torch.cuda.stream(self.stream):
-            self.tables.copy_(host, non_blocking=True)
-            done = torch.cuda.Event()
-            done.record(self.stream)
-        plan._staging = (staging, done)
+        with _STAGING_LOCK:
+            staging, done = getattr(plan, "_staging", (None, None))
+            if staging is None or staging.numel() < blob.size:
+                staging = torch.empty(blob.size, dtype=torch.uint8).pin_memory()
+            elif done is not None:
+                done.synchronize()
+            host = staging[:blob.size]
+            host.numpy()[:] = blob
+            with torch.cuda.stream(self.stream):
+                self.tables.copy_(host, non_blocking=True)
+                done = torch.cuda.Event()
+                done.record(self.stream)
+            plan._staging = (staging, done)
         self._host_blob = host                    # keep the pinned source alive
         base = self.tables.data_ptr()
         self.seg_ptr = base + offsets[0]

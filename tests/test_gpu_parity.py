@@ -707,16 +707,52 @@ def test_concurrent_file_reads_and_host_checks(tmp_path, cases, golden_trace_byt
     threads reading traces to the device and checking host traces at the
     same time get the same results as one thread doing it alone."""
     import concurrent.futures
+    from paper_2506_09280_b200 import tracestore
     from paper_2506_09280_b200.tracestore import read_trace
     names = cases["traces"][:4]
     for name in names:
         (tmp_path / (name + ".ttrc")).write_bytes(golden_trace_bytes(name))
+    # 64 KiB ring slots x 4: every read spans many slots and wraps the ring,
+    # so a reader that refilled a slot before the previous caller's DMA out
+    # of it had finished would corrupt that caller's image
+    saved = tracestore._RING_PIECE, tracestore._RING_SLOTS, tracestore._RING
+    tracestore._RING_PIECE, tracestore._RING_SLOTS, tracestore._RING = 64 << 10, 4, None
+    try:
+        def job(name):
+            dev = read_trace(tmp_path / (name + ".ttrc"), device="cuda")
+            return [r.payload.cpu().numpy().tobytes() for r in dev.records]
+        want = {n: job(n) for n in names}
+        with concurrent.futures.ThreadPoolExecutor(4) as ex:
+            for _ in range(3):
+                got = dict(zip(names, ex.map(job, names)))
+                assert got == want
+    finally:
+        tracestore._RING_PIECE, tracestore._RING_SLOTS, tracestore._RING = saved
 
-    def job(name):
-        dev = read_trace(tmp_path / (name + ".ttrc"), device="cuda")
-        return [r.payload.cpu().numpy().tobytes() for r in dev.records]
-    want = {n: job(n) for n in names}
-    with concurrent.futures.ThreadPoolExecutor(4) as ex:
-        for _ in range(3):
-            got = dict(zip(names, ex.map(job, names)))
-            assert got == want
+
+def test_concurrent_checks_share_a_cached_plan(cases, golden_trace_bytes):
+    """check() caches one plan per layout, with one pinned staging buffer for
+    its tables: threads checking different payloads of the SAME layout at
+    once get exactly their own serial reports."""
+    import concurrent.futures
+    case = next(c for c in cases["checks"] if c["name"] == "clean_tp2_cp2_k3")
+    ref = trace_from_bytes(golden_trace_bytes(case["ref"]), device="cuda")
+    cand = trace_from_bytes(golden_trace_bytes(case["cand"]), device="cuda")
+    tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+    fmt = td.FloatFormat(case["fmt"])
+    variants = []
+    for k in range(6):
+        c = Trace(header=cand.header, raw_header=cand.raw_header)
+        for j, r in enumerate(cand.records):
+            p = r.payload.clone()
+            if j == (7 * k) % len(cand.records) and p.numel():
+                p.mul_(1.0 + 0.5 * k)
+            c.records.append(TraceRecord(r.id, r.rank_meta, r.mapping, r.replica_group_size, p, r.module_class))
+        variants.append(c)
+
+    def job(c):
+        return td.render_report(td.check(ref, c, tol, case["kappa"], fmt=fmt), "json")
+    want = [job(c) for c in variants]
+    with concurrent.futures.ThreadPoolExecutor(6) as ex:
+        for _ in range(4):
+            assert list(ex.map(job, variants)) == want
