@@ -29,6 +29,7 @@ S=1024, V=50304), single-device reference vs a TP=4 candidate, activations
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import math
 import os
@@ -107,10 +108,16 @@ def describe(name: str):
                 "storage_dtype": "bf16", "tensor_mib": mib, "maps": maps, "shards": g,
                 "inputs": l2_note(2 * (mib << 20))}
         return desc, {"sweep": (mib, maps, g), "fmt": FloatFormat.BF16, "nbytes": 2 * (mib << 20)}
+    # cfgN:S = config N at sequence length S (validation runs; the bench
+    # lines are quoted at the configs' own S)
+    name, _, s_over = name.partition(":")
+
+    def shaped(m):
+        return dataclasses.replace(m, seq_len=int(s_over)) if s_over else m
     if name == "cfg4":
-        model, pcfg = L.LLAMA3_8B, L.ParallelConfig(tp=2, dp=4, microbatches=4)
+        model, pcfg = shaped(L.LLAMA3_8B), L.ParallelConfig(tp=2, dp=4, microbatches=4)
         desc = {"workload": "config4 Llama-3-8B-shape bf16 full-step traces (L=32 d=4096 GQA 32/8 ff=14336 "
-                            "S=8192 V=128256), TP=2 x DP=4 candidate, M=4: this GPU's share of the "
+                            f"S={model.seq_len} V=128256), TP=2 x DP=4 candidate, M=4: this GPU's share of the "
                             "8-GPU check (rank r of 8: its candidate records, the reference slices of "
                             "the compares it runs, digests of its copies of cross-GPU replica groups)",
                 "trace_shapes": f"layers={model.layers} d={model.d_model} ff={model.d_ff} "
@@ -120,18 +127,19 @@ def describe(name: str):
                 "inputs": "~74 GB of trace payload per GPU share, far larger than the 126.5 MiB L2: no flush"}
         return desc, {"model": model, "pcfg": pcfg, "dtype": "bf16", "fmt": FloatFormat.BF16, "share": 8}
     if name == "cfg1":
-        model, pcfg, dtype, fmt = L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), "f32", FloatFormat.FP32
+        model, pcfg, dtype, fmt = shaped(L.GPT2_SMALL_L2), L.ParallelConfig(tp=2), "f32", FloatFormat.FP32
         label = "config1 GPT-2-small-shape L=2 fp32 traces, TP=2 candidate vs single-device reference"
     elif name == "cfg3":
-        model = L.LLAMA3_1B
+        model = shaped(L.LLAMA3_1B)
         pcfg, dtype, fmt = L.ParallelConfig(tp=8), "bf16", FloatFormat.BF16
-        label = ("config3 Llama-3-1B-shape bf16 traces (L=16 d=2048 GQA 32/8 ff=8192 SwiGLU S=8192 "
-                 "V=128256), TP=8 candidate vs single-device reference, injected bugs: wrong shard "
+        label = ("config3 Llama-3-1B-shape bf16 traces (L=16 d=2048 GQA 32/8 ff=8192 SwiGLU "
+                 f"S={model.seq_len} V=128256), TP=8 candidate vs single-device reference, injected bugs: wrong shard "
                  "order (lm_head logits), missing row-parallel allreduce (layers.7.attn output), "
                  "scale error (embedding output)")
     else:
-        model, pcfg, dtype, fmt = L.GPT2_MEDIUM, L.ParallelConfig(tp=4), "bf16", FloatFormat.BF16
-        label = ("config2 GPT-2-medium-shape bf16 traces (L=24 d=1024 ff=4096 S=1024 V=50304), TP=4 "
+        model, pcfg, dtype, fmt = shaped(L.GPT2_MEDIUM), L.ParallelConfig(tp=4), "bf16", FloatFormat.BF16
+        label = ("config2 GPT-2-medium-shape bf16 traces (L=24 d=1024 ff=4096 "
+                 f"S={model.seq_len} V=50304), TP=4 "
                  "candidate vs single-device reference, activations+grads+MainGrad+Param")
     bugs = None
     if name == "cfg3":
@@ -148,6 +156,12 @@ def describe(name: str):
     nbytes += sum(math.prod(s.mapping.local_shape) * esize for s in L.emit_records(model, pcfg))
     desc["inputs"] = l2_note(nbytes)
     return desc, {"model": model, "pcfg": pcfg, "dtype": dtype, "fmt": fmt, "bugs": bugs, "nbytes": nbytes}
+
+
+def scaling_of(name: str) -> str:
+    """Configs 1-3: one check split across the GPUs (total work fixed);
+    config 4: one 8-GPU job's shares, config 5: one tensor per GPU."""
+    return "weak" if name.startswith(("cfg4", "cfg5")) else "strong"
 
 
 def l2_note(nbytes: int) -> str:
@@ -334,15 +348,9 @@ def host_sample(name: str, stride: int):
         rr = [O.Rec("sweep", (0,) * 6, x.shape, x.shape, [(box[0], box[0])], 1, x)]
         cr = [O.Rec("sweep", (0,) * 6, y.shape, y.shape, [(box[0], box[0])], 1, y)]
         return rr, cr, "BF16", 1
-    if name == "cfg1":
-        model, pcfg, fmt = L.GPT2_SMALL_L2, L.ParallelConfig(tp=2), "FP32"
-    elif name == "cfg3":
-        model, pcfg, fmt = L.LLAMA3_1B, L.ParallelConfig(tp=8), "BF16"
-    elif name == "cfg4":
-        # the whole 8-GPU job's layout (the CPU reference has no GPU shares)
-        model, pcfg, fmt = L.LLAMA3_8B, L.ParallelConfig(tp=2, dp=4, microbatches=4), "BF16"
-    else:
-        model, pcfg, fmt = L.GPT2_MEDIUM, L.ParallelConfig(tp=4), "BF16"
+    # config 4: the whole 8-GPU job's layout (the CPU reference has no GPU shares)
+    _, spec = describe(name)
+    model, pcfg, fmt = spec["model"], spec["pcfg"], spec["fmt"].value
     eps = 2.0 ** -24 if fmt == "FP32" else 2.0 ** -8
     ref_specs = {s.ident: s for s in L.emit_records(model, L.ParallelConfig(microbatches=pcfg.microbatches))}
     cand_specs = L.emit_records(model, pcfg)
@@ -377,89 +385,88 @@ def host_sample(name: str, stride: int):
     return rr, cr, fmt, len(sample)
 
 
-def run_share(args, world: int, rank: int, local: int):
-    """Config 4: this GPU's share of the 8-GPU TP=2 x DP=4 check.  Rank r
-    (< world <= 8) holds virtual rank r's records (synthetic.ShareLayout) and
-    plans with every rank's metadata (StaticComm), so the same plan runs
-    whether the other 7 shares are live GPUs or absent.  A step = digests of
-    the local copies of cross-GPU replica groups (td_fingerprint, one launch)
-    + their table all_reduce + td_segnorm + slot reduction + the partial-sum
-    all_reduce + verdicts.  Weak scaling: N GPUs process N shares."""
+def run_distributed(args, world: int, rank: int, local: int):
+    """The check partitioned the way the candidate is.
+
+    Configs 1-3 at N > 1 GPUs: ONE check split across the GPUs by the
+    candidate's own TP ranks — TP rank t's records live on GPU floor(t*N/tp),
+    every compare runs where the copy it reads lives, with the reference
+    slices of its boxes (synthetic.ShareLayout = distributed.split_reference's
+    placement); strong scaling (the total work is the N=1 check's).
+    Config 4 at any N: GPU r holds virtual rank r of the 8-GPU TP=2 x DP=4
+    job (its records + the reference slices of its compares) and plans with
+    all 8 ranks' metadata (StaticComm), so N live GPUs run N of the 8 shares
+    (weak scaling; digests are compared among the live copies).
+
+    A step = the public distributed check end to end on resident payloads:
+    digests of the local copies of cross-GPU replica groups (fused in the
+    compare pass / one td_fingerprint launch), td_segnorm, slot reduction,
+    ONE all-gather of [slot sums | digests], td_combine (rank-order sums +
+    device digest compare), td_verdict, the one D2H of the verdicts — and,
+    only when a digest differed (config 3's missing allreduce spans GPUs),
+    the exact bug path (copies exchanged point to point, affected ids
+    re-run).  Time: CUDA events on the check's stream, max over ranks."""
     import torch
     import torch.distributed as dist
     from paper_2506_09280_b200 import _native as N
     from paper_2506_09280_b200 import synthetic
     from paper_2506_09280_b200.checker import ToleranceMap
-    from paper_2506_09280_b200.device import resolve_operands
-    from paper_2506_09280_b200.distributed import (DistributedCheckPlan, StaticComm, TorchComm,
-                                                   allreduce_partials)
+    from paper_2506_09280_b200.distributed import DistributedCheckPlan, StaticComm, TorchComm
     hbm, peak_kind = peaks()
-    desc, spec = describe("cfg4")
-    fmt, share = spec["fmt"], spec["share"]
-    if world > share:
-        raise SystemExit(f"config 4 is an {share}-GPU job: run it on at most {share} GPUs")
+    desc, spec = describe(args.config)
+    fmt, share = spec["fmt"], spec.get("share")
+    dtype = torch.float32 if spec["dtype"] == "f32" else torch.bfloat16
     t0 = time.perf_counter()
-    lay = synthetic.ShareLayout(spec["model"], spec["pcfg"], share)
-    ref, cand = lay.build(rank, seed=0, eps=fmt.eps)
+    if share:
+        if world > share:
+            raise SystemExit(f"config 4 is an {share}-GPU job: run it on at most {share} GPUs")
+        lay = synthetic.ShareLayout(spec["model"], spec["pcfg"], share)
+        ref, cand = lay.build(rank, seed=0, eps=fmt.eps, dtype=dtype)
+        ref_metas, cand_metas = lay.metas()
+        comm = StaticComm(rank, share, [ref_metas, cand_metas], inner=TorchComm() if world > 1 else None)
+        scaling, placement = "weak", f"{world} of the job's {share} GPU shares live"
+    else:
+        tp = spec["pcfg"].tp
+        lay = synthetic.ShareLayout(spec["model"], spec["pcfg"], world,
+                                    owner=lambda s, w=world, t=tp: s.rank[1] * w // t)
+        ref, cand = lay.build(rank, seed=0, eps=fmt.eps, dtype=dtype, bugs=spec.get("bugs"))
+        comm = TorchComm()
+        scaling, placement = "strong", f"one check split over {world} GPUs: TP rank t on GPU floor(t*{world}/{tp})"
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
-    ref_metas, cand_metas = lay.metas()
-    comm = StaticComm(rank, share, [ref_metas, cand_metas], inner=TorchComm() if world > 1 else None)
     tol = ToleranceMap({i: 2 * fmt.eps for i in lay.ids}, n_samples=1, eps_p=fmt.eps)
     t0 = time.perf_counter()
     dcp = DistributedCheckPlan(ref, cand, tol, 3.0, fmt=fmt, comm=comm)
     plan_s = time.perf_counter() - t0
-    digests, fps, where, n_fused = dcp.digests()
-    ptrs, keep = resolve_operands(dcp.plan.operands, dcp.plan.operand_dtypes)
-    prep = dcp.plan.prepare(ptrs, kappa=3.0, eps=fmt.eps, replica_eps=fmt.eps, digests=digests.data_ptr())
-    n_remote = len(dcp.plan.remote_groups)
-    table = torch.zeros((max(n_remote, 1), N.MAX_Z + 1, 2), dtype=torch.int64, device="cuda")
-    rows = torch.tensor([k for k, _ in where], dtype=torch.int64, device="cuda")
-    cols = torch.tensor([c for _, c in where], dtype=torch.int64, device="cuda")
-    stream = prep.stream
-    side = torch.cuda.Stream()
-    concurrent = os.environ.get("TD_DIGEST_CONCURRENT", "1") == "1"
-    # every byte this GPU holds, read once (SURVEY 8(d)): its candidate
-    # records (digested or compared) and the reference slices it compares
-    alg_bytes = ref.nbytes + cand.nbytes
+    b = dcp.bind()
+    stream = b.prep.stream
+    local_bytes = ref.nbytes + cand.nbytes          # every byte this GPU holds, read once
+    tot = torch.tensor([float(local_bytes)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot)
+    alg_bytes = int(tot.item())
+    n_ids = len(dcp.cand_view) + sum(1 for i in dcp.ref_view if i not in dcp.cand_view)
+    bug_steps = 0
 
-    def step(seg_events=None):
+    def step(ev=None):
+        nonlocal bug_steps
         sh = N.stream_handle(stream)
-        with torch.cuda.stream(stream):
-            if seg_events is not None:
-                seg_events[0].record(stream)
-            digests.zero_()
-            if concurrent:
-                # the digests of copies no compare reads stream beside the
-                # compare pass (both HBM-bound: fills each other's tails)
-                side.wait_stream(stream)
-                fps.run(side)
-                if seg_events is not None:
-                    seg_events[1].record(stream)
-                    seg_events[2].record(stream)
-                prep.segnorm(sh)
-                stream.wait_stream(side)
-            else:
-                fps.run(stream)
-                if seg_events is not None:
-                    seg_events[1].record(stream)
-                    seg_events[2].record(stream)
-                prep.segnorm(sh)          # compares; fills the fused digest slots
-            if seg_events is not None:
-                seg_events[3].record(stream)
-            if where:
-                table[rows, cols] = digests[:len(where)]
-            if world > 1:
-                dist.all_reduce(table)
-            prep.reduce(sh)
-            if world > 1:
-                allreduce_partials(prep)
-            prep.verdict(sh)
-
+        if ev is not None:
+            ev[0].record(stream)
+        b.digest_pass(sh)
+        if ev is not None:
+            ev[1].record(stream)
+        b.exchange(sh)
+        out = b.fetch()
+        if out[3]:
+            bug_steps += 1
+            out = dcp._bug_path(b) + (out[3],)
+        return out
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    bug_steps = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -467,55 +474,111 @@ def run_share(args, world: int, rank: int, local: int):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record(stream)
         for k in range(args.steps):
-            step(ev[k])
+            idres, gres, ties, n_diff = step(ev[k])
         end.record(stream)
         torch.cuda.synchronize()
-    idres, gres, ties = prep.fetch()
     t_local = torch.tensor([start.elapsed_time(end)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
     ms_step = float(t_local.item()) / args.steps
-    fp_ms = statistics.mean(a.elapsed_time(b) for a, b, _, _ in ev)
-    seg_ms = statistics.mean(c.elapsed_time(d) for _, _, c, d in ev)
-    pass_ms = statistics.mean(a.elapsed_time(d) for a, _, _, d in ev)   # digests + compares
-    seg_bytes = dcp.plan.algorithmic_bytes
-    n_ids = len(dcp.common)
+    pass_ms = statistics.mean(a.elapsed_time(c) for a, c in ev)       # digests + compares
+    pass_bytes = dcp.plan.algorithmic_bytes + b.fps.nbytes
+    counts = {k: int((idres["verdict"] == v).sum()) for k, v in
+              (("pass", 0), ("flag", 1), ("replica-mismatch", 2), ("merge-error", 3))}
+    launches = b.launches * args.steps
+    n_remote, n_fused, n_fps, stride = len(dcp.plan.remote_groups), dcp.n_fused, b.fps.n, dcp.stride
+    del b, dcp                                      # only `traces` holds the payloads now
+    traces = [ref, cand]
+    del ref, cand
+    e2e = None
+    if not args.no_e2e:
+        e2e = _distributed_e2e(args, world, rank, traces, tol, fmt, alg_bytes, n_ids,
+                               (lambda: StaticComm(rank, share, [ref_metas, cand_metas],
+                                                   inner=comm.inner)) if share else (lambda: comm))
     if rank == 0:
         line = {"metric": "traced-tensor compare GB/s vs HBM roofline; layer-checks/sec",
-                "value": alg_bytes * world / (ms_step / 1e3) / 1e9, "unit": "GB/s", "n_gpus": world,
+                "value": alg_bytes / (ms_step / 1e3) / 1e9, "unit": "GB/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic (N(0,sigma) per id rounded to bf16; candidate = Q(ref*(1+2^-8 u)))",
+                "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (N(0,sigma) per id rounded to the storage dtype; candidate = "
+                        "Q(ref*(1+2^-8 u)), counter-based stream)",
                 "config": desc,
                 "workload_stats": {"algorithmic_bytes_per_step": alg_bytes, "ids": n_ids,
-                                   "resident_gb": (ref.nbytes + cand.nbytes) / 1e9,
-                                   "parallelism": f"{world} of the job's {share} GPUs live"},
-                "layer_checks_per_s": n_ids * world / (ms_step / 1e3),
+                                   "local_bytes_rank0": local_bytes, "parallelism": placement},
+                "layer_checks_per_s": n_ids / (ms_step / 1e3) * (world if share else 1),
                 "build_seconds": build_s, "plan_seconds": plan_s,
-                "share": {"candidate_gb": cand.nbytes / 1e9, "reference_gb": ref.nbytes / 1e9,
-                          "digested_gb": fps.nbytes / 1e9, "compare_gb": seg_bytes / 1e9,
-                          "bytes_read_gb": (fps.nbytes + seg_bytes) / 1e9,
-                          "remote_replica_groups": n_remote, "digests_fused_in_compare": n_fused,
-                          "digest_kernel_concurrent_with_compares": concurrent}
-                         | ({} if concurrent else {"digest_ms": fp_ms,
-                                                   "digest_gbs": fps.nbytes / (fp_ms / 1e3) / 1e9}),
-                "verdict_counts_partial": {k: int((idres["verdict"] == v).sum()) for k, v in
-                                           (("pass", 0), ("flag", 1), ("replica-mismatch", 2),
-                                            ("merge-error", 3))},
+                "exchange": {"collective": "one all-gather of [slot sums | digest rows] per check",
+                             "bytes_per_rank": 8 * stride, "remote_replica_groups": n_remote,
+                             "digests_fused_in_compare": n_fused, "digested_by_fingerprint": n_fps,
+                             "steps_on_bug_path": bug_steps},
+                "verdict_counts" if not share or world == share else "verdict_counts_partial": counts,
                 "near_ties": ties,
-                "roofline": {"bound": "hbm", "achieved": (seg_bytes + fps.nbytes) / (pass_ms / 1e3) / 1e9,
+                "roofline": {"bound": "hbm", "achieved": pass_bytes / (pass_ms / 1e3) / 1e9,
                              "peak": hbm, "unit": "GB/s",
-                             "frac": (seg_bytes + fps.nbytes) / (pass_ms / 1e3) / 1e9 / hbm, "traffic": None,
-                             "kernel": "td_segnorm (k_segnorm_vec incl. digest classes) + td_fingerprint"
-                                       + (" on a side stream" if concurrent else ""),
+                             "frac": pass_bytes / (pass_ms / 1e3) / 1e9 / hbm, "traffic": None,
+                             "kernel": "td_segnorm (incl. digest classes) + td_fingerprint on a side stream, rank 0",
                              "kernel_ms": pass_ms, "peak_source": peak_kind},
-                "cpu_baseline": None, "e2e": None,
-                "gpu_launches": (prep.launches_per_run + 3) * args.steps,
+                "cpu_baseline": None, "e2e": e2e,
+                "gpu_launches": launches,
                 "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
-    del keep
     if world > 1:
         dist.destroy_process_group()
+
+
+def _distributed_e2e(args, world, rank, traces, tol, fmt, alg_bytes, n_ids, make_comm):
+    """e2e at N GPUs through the public collective API: every rank's share
+    copied to pinned host arenas, then per step DistributedCheckPlan.run on
+    the host traces (H2D of the share, the check, the verdicts' D2H, report
+    assembly), max over ranks.  The first call also plans (cold)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2506_09280_b200.device import stage_host_payloads
+    from paper_2506_09280_b200.distributed import DistributedCheckPlan
+    from paper_2506_09280_b200.tracestore import pack_pinned
+    try:
+        href, hcand = pack_pinned(traces[0]), pack_pinned(traces[1])
+        traces.clear()                              # the HBM copies go: staging needs the room
+        ok, why = 1, ""
+    except (RuntimeError, MemoryError) as exc:
+        href = hcand = None
+        ok, why = 0, str(exc).splitlines()[0][:200]
+    if world > 1:
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        ok = int(flag.item())
+    if not ok:
+        return {"value": None, "unit": "GB/s", "error": f"pinned host arenas unavailable: {why or 'another rank'}"}
+    torch.cuda.empty_cache()
+    h2d = torch.tensor([float(href.nbytes + hcand.nbytes)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(h2d)
+
+    def timed(plan):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        staged = stage_host_payloads([href, hcand])
+        plan = plan or DistributedCheckPlan(href, hcand, tol, 3.0, fmt=fmt, comm=make_comm())
+        rep = plan.run(staged=staged)
+        torch.cuda.synchronize()
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return plan, rep, float(t.item())
+    plan, rep, t_cold = timed(None)
+    times = []
+    for _ in range(args.e2e_steps):
+        _, rep, t = timed(plan)
+        times.append(t)
+    t_e2e = sum(times) / len(times)
+    return {"value": alg_bytes / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": int(h2d.item()),
+            "d2h_bytes_per_step": world * (n_ids * 32 + 8), "seconds_per_step": t_e2e,
+            "layer_checks_per_s": n_ids / t_e2e, "verdicts": rep.counts,
+            "plan": "DistributedCheckPlan built once (the cold call) and re-run on each step's staged payloads",
+            "cold": {"value": alg_bytes / t_cold / 1e9, "unit": "GB/s", "seconds": t_cold,
+                     "what": "first call: metadata exchange + host planning + the same H2D / check / D2H"}}
 
 
 def run_reference(args):
@@ -551,7 +614,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": "traced-tensor compare GB/s vs HBM roofline; layer-checks/sec",
             "value": value, "unit": "GB/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": scaling_of(args.config), "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (host numpy, same shapes/layout as the GPU arm)",
             "config": describe(args.config)[0],
             "layer_checks_per_s": n_sample / t,
@@ -591,8 +654,8 @@ def main():
     from paper_2506_09280_b200.checker import CheckPlan, check
     from paper_2506_09280_b200.device import resolve_operands
     from paper_2506_09280_b200.distributed import allreduce_partials
-    if args.config == "cfg4":
-        return run_share(args, world, rank, local)
+    if args.config == "cfg4" or (world > 1 and not args.config.startswith("cfg5")):
+        return run_distributed(args, world, rank, local)
     hbm, peak_kind = peaks()
 
     desc, ref, cand, tol, fmt = workload(args.config, rank)
@@ -759,7 +822,7 @@ def main():
         line = {"metric": "traced-tensor compare GB/s vs HBM roofline; layer-checks/sec",
                 "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None,
+                "scaling": scaling_of(args.config), "vs_baseline": None,
                 "dtype": "f64",   # arithmetic type: fp64 accumulation of bf16/f32 payloads
                 "data": "synthetic (N(0,sigma) per id rounded to the storage dtype; candidate = "
                         "Q(ref*(1+2^-8 u)), counter-based stream)",

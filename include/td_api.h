@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define TD_ABI_VERSION 1
+#define TD_ABI_VERSION 2
 
 /* element types of payload buffers */
 enum td_dtype { TD_F32 = 0, TD_BF16 = 1, TD_F16 = 2, TD_F64 = 3 };
@@ -220,6 +220,29 @@ int td_rel_err(const void* a, const void* b, int32_t dtype, int64_t n, void* wor
  * without it these return non-zero with td_last_error() set. */
 int td_allreduce_partials(void* nccl_comm, double* slots, int64_t n, void* stream);
 int td_allreduce_digests(void* nccl_comm, long long* table, int64_t n, void* stream);
+
+/* ---- the one-collective exchange (the distributed check's clean path) ----
+ * Each rank's exchange buffer is [slot sums: n_slots doubles (td_reduce_slots'
+ * id sums then group sums) | digest rows: 2 u64 per local copy of a cross-GPU
+ * replica group], padded to a common length `stride` (doubles).
+ * td_allgather_exchange: ncclAllGather of n = stride doubles per rank into
+ * recv (world * stride), one NCCL call for sums and digests alike.
+ * td_combine: slots[s] = sum over r < world of gathered[r*stride + s] in rank
+ * order (identical on every rank, independent of NCCL's algorithm; slots may
+ * alias gathered's own-rank row once the gather has completed); for copy c
+ * of a cross-GPU replica group (n_copies in all, copy_first[c] = index of its
+ * group's copy 0, copy_off[c] = offset in doubles of its digest row in
+ * gathered, < 0 if its holder is not part of the gather), differs[c] = 1 iff
+ * its 128-bit digest differs from copy 0's; *n_differ (reset here) counts
+ * them.  Equal digests mean identical copies, i.e. rel_err 0 exactly
+ * (canonical.py:236-242; the group's slot stays 0); a non-zero count sends
+ * the caller down the exact bug path (point-to-point copy exchange).
+ * Replaces the reference's emulated collectives (engine.py:100-142) on the
+ * compare path. */
+int td_allgather_exchange(void* nccl_comm, const double* send, double* recv, int64_t n, void* stream);
+int td_combine(const double* gathered, int32_t world, int64_t stride, int64_t n_slots, double* slots,
+               const int64_t* copy_off, const int32_t* copy_first, int64_t n_copies, int32_t* differs,
+               unsigned long long* n_differ, void* stream);
 
 /* ---- kernel 3: batched threshold compare -> per-id verdicts ----
  * eps = fmt.eps (threshold floor); replica_eps = fmt.eps for check_replicas.

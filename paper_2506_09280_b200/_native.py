@@ -84,6 +84,8 @@ SIGNATURES = {
     "td_rel_err": (ctypes.c_int, [_P, _P, _I32, _I64, _P, _P, _P]),
     "td_allreduce_partials": (ctypes.c_int, [_P, _P, _I64, _P]),
     "td_allreduce_digests": (ctypes.c_int, [_P, _P, _I64, _P]),
+    "td_allgather_exchange": (ctypes.c_int, [_P, _P, _P, _I64, _P]),
+    "td_combine": (ctypes.c_int, [_P, _I32, _I64, _I64, _P, _P, _P, _I64, _P, _P, _P]),
     "td_box_gather": (ctypes.c_int, [_P, _I32, _P, _P, _I32, _P]),
     "td_gather_bytes": (ctypes.c_int, [_P, _P, _P, _I64, _P]),
     "td_generate": (ctypes.c_int, [_P, _I64, _U64, _I32, _D, _D, _I64, _P, _I32, _P, _P, _I32, _P]),

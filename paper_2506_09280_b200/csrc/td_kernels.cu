@@ -1337,6 +1337,44 @@ __global__ void __launch_bounds__(256) k_gather_bytes(const unsigned char* __res
     }
 }
 
+// ---------------------------------------------------------------------------
+// Multi-GPU combine, after ONE all-gather of every live rank's
+// exchange buffer [slot sums: n_slots f64 | digest rows: 2 u64 each], rank r
+// at gathered + r * stride:
+//  * slot s = sum over ranks of gathered[r * stride + s], in rank order — a
+//    fixed order, so every rank computes bit-identical sums (and verdicts)
+//    whatever algorithm NCCL picks;
+//  * copy c of a cross-GPU replica group: differs[c] = its 128-bit digest !=
+//    copy 0's (first[c] = index of its group's copy 0; copies whose holder
+//    is not live have off[c] < 0 and compare equal), n_differ += 1 per
+//    differing copy.  Equal digests = identical copies (checker.py:184-191:
+//    rel_err 0, the group's slot stays zero); a differing copy sends the
+//    host down the exact bug path.
+__global__ void __launch_bounds__(256)
+k_combine(const double* __restrict__ gathered, int world, int64_t stride, int64_t n_slots,
+          double* __restrict__ slots, const int64_t* __restrict__ off, const int32_t* __restrict__ first,
+          int64_t n_copies, int32_t* __restrict__ differs, unsigned long long* __restrict__ n_differ) {
+    const int64_t n = n_slots > n_copies ? n_slots : n_copies;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < n_slots) {
+            double s = gathered[i];
+            for (int r = 1; r < world; ++r) s += gathered[(int64_t)r * stride + i];
+            slots[i] = s;
+        }
+        if (i < n_copies) {
+            const int64_t oc = off[i], o0 = off[first[i]];
+            int d = 0;
+            if (oc >= 0 && o0 >= 0) {
+                const unsigned long long* a = reinterpret_cast<const unsigned long long*>(gathered + oc);
+                const unsigned long long* b = reinterpret_cast<const unsigned long long*>(gathered + o0);
+                d = (a[0] != b[0]) | (a[1] != b[1]);
+            }
+            differs[i] = d;
+            if (d) atomicAdd(n_differ, 1ull);
+        }
+    }
+}
+
 // per-host-thread, per-device auxiliary streams for concurrent class launches
 struct AuxStreams {
     static constexpr int N = 7;
@@ -1661,6 +1699,21 @@ int td_generate(double* out, int64_t n, uint64_t seed, int32_t dist, double a, d
     return check_launch("td_generate");
 }
 
+int td_combine(const double* gathered, int32_t world, int64_t stride, int64_t n_slots, double* slots,
+               const int64_t* copy_off, const int32_t* copy_first, int64_t n_copies, int32_t* differs,
+               unsigned long long* n_differ, void* stream) {
+    if (world < 1 || stride < n_slots || n_slots < 0 || n_copies < 0 || (n_slots && (!gathered || !slots)) ||
+        (n_copies && (!gathered || !copy_off || !copy_first || !differs)) || !n_differ)
+        return fail("td_combine: invalid arguments");
+    if (cudaMemsetAsync(n_differ, 0, sizeof(unsigned long long), (cudaStream_t)stream) != cudaSuccess)
+        return fail("td_combine: cannot reset the mismatch counter");
+    const int64_t n = n_slots > n_copies ? n_slots : n_copies;
+    if (n == 0) return 0;
+    k_combine<<<grid_for(n, 256, 148 * 4), 256, 0, (cudaStream_t)stream>>>(
+        gathered, world, stride, n_slots, slots, copy_off, copy_first, n_copies, differs, n_differ);
+    return check_launch("td_combine");
+}
+
 int td_gather_bytes(const void* src, void* dst, const int64_t* ranges, int64_t n, void* stream) {
     if (n == 0) return 0;
     if (!src || !dst || !ranges || n < 0) return fail("td_gather_bytes: invalid arguments");
@@ -1688,6 +1741,16 @@ nccl_allreduce_fn nccl_allreduce() {
 }
 constexpr int NCCL_INT64 = 4, NCCL_FLOAT64 = 8, NCCL_SUM = 0;
 
+typedef int (*nccl_allgather_fn)(const void*, void*, size_t, int, void*, cudaStream_t);
+nccl_allgather_fn nccl_allgather() {
+    static nccl_allgather_fn fn = [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        return h ? reinterpret_cast<nccl_allgather_fn>(dlsym(h, "ncclAllGather")) : nullptr;
+    }();
+    return fn;
+}
+
 int allreduce_sum(void* comm, void* buf, int64_t n, int dtype, void* stream, const char* what) {
     if (n == 0) return 0;
     if (!comm || !buf || n < 0) return fail("%s: invalid arguments", what);
@@ -1706,6 +1769,15 @@ int td_allreduce_partials(void* nccl_comm, double* slots, int64_t n, void* strea
 
 int td_allreduce_digests(void* nccl_comm, long long* table, int64_t n, void* stream) {
     return allreduce_sum(nccl_comm, table, n, NCCL_INT64, stream, "td_allreduce_digests");
+}
+
+int td_allgather_exchange(void* nccl_comm, const double* send, double* recv, int64_t n, void* stream) {
+    if (n == 0) return 0;
+    if (!nccl_comm || !send || !recv || n < 0) return fail("td_allgather_exchange: invalid arguments");
+    nccl_allgather_fn fn = nccl_allgather();
+    if (!fn) return fail("td_allgather_exchange: libnccl.so.2 not found");
+    const int rc = fn(send, recv, (size_t)n, NCCL_FLOAT64, nccl_comm, (cudaStream_t)stream);
+    return rc ? fail("td_allgather_exchange: ncclAllGather returned %d", rc) : 0;
 }
 
 }  // extern "C"

@@ -1,26 +1,32 @@
-"""Multi-GPU check: one process per GPU, partial sums across NVLink.
+"""Multi-GPU check: one process per GPU, one collective per check.
 
 SURVEY §8(e).  A canonical id's compare is a sum over disjoint boxes, so:
 
 1. every rank publishes the METADATA of the records it holds (ids, maps,
-   replica sizes, dtypes, shapes — no payload) with one all_gather_object;
-   all ranks then hold the same global merge view (host, deterministic);
+   replica sizes, dtypes, shapes — no payload) with one all_gather_object
+   (once per layout); all ranks then hold the same global merge view;
 2. each rank plans only the work whose operands it holds (plan.Plan with
-   owner/me): compare runs on the rank holding the candidate's copy 0 (its
-   reference slice must be local), replica sums fused when a group's copies
-   are all on that rank;
+   owner/me): a compare runs on the rank holding the copy it reads (its
+   reference slices must be local), replica sums fused when a group's
+   copies are all on that rank;
 3. replica groups whose copies live on several ranks are decided by 128-bit
-   order-independent digests (td_fingerprint: every local copy in one
-   launch; one int64 all_reduce of a small table): equal digests = identical
-   copies = rel_err 0, so the group's slot stays zero, and the group's
-   compare may read any copy — plan.compare_copies spreads those compares
-   over the holders to balance bytes per GPU; on a mismatch (the bug path
-   only) the differing copies are sent point-to-point to copy 0's rank,
-   which computes the exact rel_err sums, and a compare that read another
-   copy is handed copy 0 instead;
-4. ONE all_reduce(sum, f64) of the per-id / per-group slot vector crosses
-   NVLink, then every rank runs td_verdict on identical sums and can render
-   the report.
+   order-independent digests (every local copy digested once: inside the
+   compare pass that reads it, or by one td_fingerprint launch beside it):
+   equal digests = identical copies = rel_err 0, so the group's slot stays
+   zero and its compare may read any copy — plan.compare_copies spreads
+   those compares over the holders to balance bytes per GPU;
+4. ONE collective per check: an all-gather of every rank's exchange buffer
+   [slot sums | digest rows]; td_combine then sums the slots in rank order
+   (bit-identical on every rank) and compares every copy's digest with copy
+   0's on the device, and td_verdict runs on the sums.  The clean path has no
+   host synchronisation until the one D2H of the verdicts (which carries the
+   digest-mismatch count), so a step can be captured in a CUDA graph;
+5. only when a digest differs (the bug path) does the host step in: the
+   differing copies travel point-to-point to copy 0's rank, which computes
+   the exact replica sums; a compare that read a differing copy is re-run,
+   for the affected ids only, reading copy 0; one more small exchange
+   patches those slots and td_verdict runs again — results are exactly the
+   reference's (checker.py:184-191, canonical.py:225-247).
 
 `Comm` abstracts the collectives: `TorchComm` wraps torch.distributed (NCCL
 on the GPU box, gloo for the CPU tests); `ThreadComm` runs N logical ranks
@@ -55,6 +61,15 @@ class Comm:
         """sends: [(dst, tensor)], recvs: [(src, tensor)] — matched in order."""
         raise NotImplementedError
 
+    def live_ranks(self) -> list:
+        """The ranks whose buffers all_gather_into collects, in row order."""
+        return list(range(self.world))
+
+    def all_gather_into(self, out, inp) -> None:
+        """out (len(live_ranks()) * inp.numel(), flat) <- every live rank's
+        inp, rank order, enqueued on torch's current stream."""
+        raise NotImplementedError
+
 
 class TorchComm(Comm):
     def __init__(self, group=None):
@@ -71,12 +86,29 @@ class TorchComm(Comm):
     def all_reduce_sum_(self, tensor) -> None:
         self.dist.all_reduce(tensor, op=self.dist.ReduceOp.SUM, group=self.group)
 
+    def all_gather_into(self, out, inp) -> None:
+        if inp.is_cuda and self.dist.get_backend(self.group) == "gloo":
+            # gloo (the CPU tests, same-device bench validation) gathers host tensors
+            host = out.new_empty(out.shape, device="cpu")
+            self.dist.all_gather_into_tensor(host, inp.cpu(), group=self.group)
+            out.copy_(host)
+            return
+        self.dist.all_gather_into_tensor(out, inp, group=self.group)
+
     def exchange(self, sends, recvs) -> None:
+        gloo = self.dist.get_backend(self.group) == "gloo"
+        if gloo:                           # gloo moves host tensors
+            sends = [(d, t.cpu()) for d, t in sends]
+            back = [(t, t.new_empty(t.shape, device="cpu")) for _, t in recvs]
+            recvs = [(s, h) for (s, _), (_, h) in zip(recvs, back)]
         ops = [self.dist.P2POp(self.dist.isend, t, self._g(d), self.group) for d, t in sends]
         ops += [self.dist.P2POp(self.dist.irecv, t, self._g(s), self.group) for s, t in recvs]
         if ops:
             for req in self.dist.batch_isend_irecv(ops):
                 req.wait()
+        if gloo:
+            for dev, host in back:
+                dev.copy_(host)
 
     def _g(self, r):
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
@@ -122,6 +154,14 @@ class ThreadComm(Comm):
         tensor.copy_(total)
         self._sync()
 
+    def all_gather_into(self, out, inp) -> None:
+        self.hub.slots[self.rank] = inp.clone()
+        self._sync()
+        rows = out.view(self.world, -1)
+        for r, t in enumerate(self.hub.slots):
+            rows[r].copy_(t)
+        self._sync()
+
     def exchange(self, sends, recvs) -> None:
         for k, (dst, t) in enumerate(sends):
             self.hub.mail[(self.rank, dst, k)] = t
@@ -165,6 +205,22 @@ class StaticComm(Comm):
             self.inner.exchange(sends, recvs)
         elif sends or recvs:
             raise N.NativeError("StaticComm: point-to-point traffic with ranks that are not running")
+
+    def live_ranks(self) -> list:
+        """Virtual ranks 0..inner.world-1 are the running ones (this process
+        alone: just this rank); the others' buffers are absent, so their
+        sums count 0 and their digests are not compared."""
+        if self.inner is None:
+            return [self.rank]
+        if self.rank >= self.inner.world:
+            raise N.NativeError("StaticComm: the running ranks must be virtual ranks 0..n-1")
+        return list(range(self.inner.world))
+
+    def all_gather_into(self, out, inp) -> None:
+        if self.inner is not None:
+            self.inner.all_gather_into(out, inp)
+        else:
+            out.copy_(inp)
 
 
 # ---------------------------------------------------------------------------
@@ -238,7 +294,9 @@ def global_trace(trace, comm: Comm, order_key=None) -> _MetaTrace:
 
 def allreduce_partials(prep, comm: Comm | None = None) -> None:
     """Sum the reduced slot vector of a Prepared plan across ranks, in place
-    (NCCL enqueues on torch's current stream)."""
+    (NCCL enqueues on torch's current stream).  The distributed check itself
+    exchanges sums and digests in one all-gather (DistributedCheckPlan); this
+    remains for callers that only need the sums."""
     import torch
     slots = prep.slot_sums
     if slots.numel() == 0:
@@ -269,14 +327,15 @@ class DistributedCheckPlan:
         self.ref_view = merge_view(gref)
         self.cand_view = merge_view(gcand)
         self.common = [i for i in self.cand_view if i in self.ref_view]
+        self._compare_copy = compare_copies(self.cand_view, lambda m: m.owner)
         self.plan = Plan([PlanEntry(i, x=self.ref_view[i], y=self.cand_view[i], x_rep=True,
                                     y_rep=True, tolerance=tol.get(i)) for i in self.common],
                          owner=lambda m: m.owner, me=comm.rank,
-                         compare_copy=compare_copies(self.cand_view, lambda m: m.owner), digest=True)
-        self._digest = None
+                         compare_copy=self._compare_copy, digest=True)
         self.mode = str(cand.header.get("mode", ""))
         self._report = CheckPlan.report
         self._report_rows = lambda: CheckPlan._report_rows(self)
+        self._layout_exchange()
 
     def _remote_group_records(self, slot_entry):
         _, ei, side, gi = slot_entry
@@ -284,66 +343,91 @@ class DistributedCheckPlan:
         meta = e.y if side == 0 else e.x
         return meta.groups[gi].records
 
-    def digests(self):
-        """(table, Fingerprints, where, F): the digest table of this rank's
-        copies of cross-rank replica groups.  Rows [0, F) are the digest
-        slots td_segnorm fills while comparing (plan.fused_digests), rows
-        [F, ...) the other local copies, digested by one td_fingerprint
-        launch; where[row] = (remote group index, copy index).  Staged once;
-        zero the table before each run."""
-        if self._digest is None:
-            import torch
-            from .device import Fingerprints
-            fused = list(self.plan.fused_digests)
-            done = set(fused)
-            where, tensors = list(fused), []
-            for k, entry in enumerate(self.plan.remote_groups):
-                for c, m in enumerate(self._remote_group_records(entry)):
-                    if m.owner == self.comm.rank and (k, c) not in done:
-                        where.append((k, c))
-                        tensors.append(m.device_payload().reshape(-1))
-            table = torch.zeros((max(len(where), 1), 2), dtype=torch.int64, device="cuda")
-            fps = Fingerprints(tensors, out=table[len(fused):])
-            self._digest = (table, fps, where, len(fused))
-        return self._digest
+    def _layout_exchange(self) -> None:
+        """The exchange buffer's layout, identical on every rank and derived
+        from the global metadata alone: [slot sums | digest rows], rank r's
+        digest rows being its copies of cross-rank groups in (remote group,
+        copy) order.  Per copy (flat over all remote groups): its digest
+        row's offset in the gathered buffer (-1 when its holder is not a live
+        rank) and the flat index of its group's copy 0."""
+        remote = self.plan.remote_groups
+        me = self.comm.rank
+        live = {r: i for i, r in enumerate(self.comm.live_ranks())}
+        self.n_live = len(live)
+        self.n_slots = 2 * len(self.plan.ids) + N.SLOT_STRIDE * len(self.plan.groups)
+        rows: dict = {}
+        canon = []                                # (owner, row) per flat copy
+        self.group_begin = [0]
+        first = []
+        for k, entry in enumerate(remote):
+            recs = self._remote_group_records(entry)
+            c0 = len(canon)
+            for m in recs:
+                r = rows.get(m.owner, 0)
+                rows[m.owner] = r + 1
+                canon.append((m.owner, r))
+                first.append(c0)
+            self.group_begin.append(len(canon))
+        self.n_rows = max(rows.values(), default=0)
+        self.stride = self.n_slots + 2 * self.n_rows
+        self.copy_first = np.asarray(first, np.int32)
+        self.copy_off = np.asarray([live[o] * self.stride + self.n_slots + 2 * r if o in live else -1
+                                    for o, r in canon], np.int64)
+        # this rank's digest table (td_segnorm's fused slots first, then the
+        # copies td_fingerprint digests) and each row's canonical row
+        flat = {}
+        for k in range(len(remote)):
+            for c in range(self.group_begin[k + 1] - self.group_begin[k]):
+                flat[(k, c)] = self.group_begin[k] + c
+        fused = list(self.plan.fused_digests)
+        done = set(fused)
+        self.where = list(fused)
+        for k, entry in enumerate(remote):
+            for c, m in enumerate(self._remote_group_records(entry)):
+                if m.owner == me and (k, c) not in done:
+                    self.where.append((k, c))
+        self.n_fused = len(fused)
+        self.canon_rows = np.asarray([canon[flat[kc]][1] for kc in self.where], np.int64)
 
-    def _resolve_remote(self, table, where):
-        """Exchange the digests (one all_reduce of a small table) and, on a
-        mismatch (bug path only):
-          * copy 0's rank receives the other copies and computes the exact
-            replica sums — returned as {group slot: 8 sums} to add;
-          * when the compare of that group reads a copy other than copy 0
-            (compare_copies) and that copy differs from copy 0, its rank
-            receives copy 0 and the compare must be re-run reading it —
-            returned as {id(record): tensor} operand overrides.
+    def bind(self, overrides: dict | None = None, staged: dict | None = None) -> "BoundCheck":
+        """Resolve this rank's payloads and stage every table: the result
+        runs the check step after step (BoundCheck.step).  staged: {id(trace
+        record): device tensor} copies already in flight
+        (device.stage_host_payloads of host traces)."""
+        return BoundCheck(self, overrides, staged)
+
+    def _bug_path(self, b: "BoundCheck"):
+        """Some copy's digest differs from its copy 0's (a real replica
+        divergence): exact sums for exactly the affected slots.
+          * copy 0's rank receives the differing copies and computes the
+            group's replica sums (y2, z2...) — canonical.py:236-242;
+          * an id whose compare read a differing copy (compare_copies) has
+            its compare re-run on every rank, for that id alone, reading
+            copy 0 (sent to the compare holder);
+        one small all-gather brings those sums to every rank (rank-order
+        sums), they replace the affected slots, and td_verdict runs again.
         Messages are issued in remote-group order on every rank, so each
         (source, destination) pair sees sends and receives in the same order."""
         import torch
         from .device import _Raw, _one_group, resolve_operands
         from .plan import Plan, PlanEntry
+        differs = b.differs.cpu().numpy()
         remote = self.plan.remote_groups
-        if not remote:
-            return {}, {}
-        full = torch.zeros((len(remote), N.MAX_Z + 1, 2), dtype=torch.int64, device="cuda")
-        if where:
-            rows = torch.tensor([k for k, _ in where], device="cuda")
-            cols = torch.tensor([c for _, c in where], device="cuda")
-            full[rows, cols] = table[:len(where)]
-        self.comm.all_reduce_sum_(full)
-        fp = full.cpu().numpy()
         compare_copy = {(ei, gi): c for ei, gi, c in self.plan.compare_reads}
         me = self.comm.rank
-        extra, overrides = {}, {}
-        sends, recvs, pending = [], [], []
+        flagged, pending, affected = [], [], set()
+        sends, recvs, overrides = [], [], {}
         for k, entry in enumerate(remote):
+            lo = self.group_begin[k]
             recs = self._remote_group_records(entry)
-            differs = [c for c in range(1, len(recs)) if not np.array_equal(fp[k, c], fp[k, 0])]
-            if not differs:
+            diff = [c for c in range(1, len(recs)) if differs[lo + c]]
+            if not diff:
                 continue
+            flagged.append(entry[0])
             y0 = recs[0]
             if y0.owner == me:
                 bufs = []
-                for c, m in enumerate(recs[1:], start=1):
+                for m in recs[1:]:
                     if m.owner == me:
                         bufs.append(m.device_payload().reshape(-1))
                     else:
@@ -351,14 +435,15 @@ class DistributedCheckPlan:
                                           device="cuda")
                         recvs.append((m.owner, buf))
                         bufs.append(buf)
-                pending.append((entry[0], y0, bufs))
+                pending.append((len(flagged) - 1, y0, bufs))
             else:
                 for m in recs[1:]:
                     if m.owner == me:
                         sends.append((y0.owner, m.device_payload().reshape(-1)))
             _, ei, side, gi = entry
             cc = compare_copy.get((ei, gi), 0) if side == 0 else 0
-            if cc and cc in differs:
+            if cc and cc in diff:
+                affected.add(ei)
                 holder = recs[cc]
                 if holder.owner == me and y0.owner == me:
                     overrides[id(holder)] = y0.device_payload()
@@ -369,59 +454,175 @@ class DistributedCheckPlan:
                 elif y0.owner == me:
                     sends.append((holder.owner, y0.device_payload().reshape(-1)))
         self.comm.exchange(sends, recvs)
-        for slot, y0, bufs in pending:
-            raws = [_Raw(y0.device_payload().reshape(-1))] + [_Raw(b) for b in bufs]
+        sub_ids = sorted(affected)
+        vec = np.zeros(2 * len(sub_ids) + N.SLOT_STRIDE * len(flagged), np.float64)
+        for j, y0, bufs in pending:
+            raws = [_Raw(y0.device_payload().reshape(-1))] + [_Raw(t) for t in bufs]
             mini = Plan([PlanEntry("remote", x=None, y=_one_group("remote", raws, True),
                                    x_rep=False, y_rep=True)])
             ptrs, keep = resolve_operands(mini.operands, mini.operand_dtypes)
             sums: dict = {}
             mini.run(ptrs, sums=sums)
-            extra[slot] = sums["group"][0]
-        return extra, overrides
+            vec[2 * len(sub_ids) + N.SLOT_STRIDE * j:2 * len(sub_ids) + N.SLOT_STRIDE * (j + 1)] = sums["group"][0]
+        if sub_ids:
+            sub = Plan([self.plan.entries[ei] for ei in sub_ids], owner=lambda m: m.owner, me=me,
+                       compare_copy=self._compare_copy, digest=False)
+            ptrs, keep = resolve_operands(sub.operands, sub.operand_dtypes, overrides)
+            sums = {}
+            sub.run(ptrs, sums=sums)
+            vec[:2 * len(sub_ids)] = sums["id"].reshape(-1)
+        # one small all-gather, sums in rank order (as td_combine does)
+        mine = torch.from_numpy(vec).to("cuda")
+        gathered = torch.empty(self.n_live * max(vec.size, 1), dtype=torch.float64, device="cuda")
+        if vec.size:
+            self.comm.all_gather_into(gathered, mine)
+        rows = gathered.view(self.n_live, -1).cpu().numpy()
+        total = rows[0].copy()
+        for r in range(1, self.n_live):
+            total += rows[r]
+        slots = b.prep.slot_sums.view(-1)
+        n_ids = len(self.plan.ids)
+        patch_idx, patch_val = [], []
+        for j, ei in enumerate(sub_ids):
+            patch_idx += [2 * ei, 2 * ei + 1]
+            patch_val += [total[2 * j], total[2 * j + 1]]
+        base = 2 * len(sub_ids)
+        for j, slot in enumerate(flagged):
+            g0 = 2 * n_ids + N.SLOT_STRIDE * slot
+            patch_idx += range(g0, g0 + N.SLOT_STRIDE)
+            patch_val += list(total[base + N.SLOT_STRIDE * j:base + N.SLOT_STRIDE * (j + 1)])
+        if patch_idx:
+            with torch.cuda.stream(b.prep.stream):
+                slots[torch.tensor(patch_idx, dtype=torch.int64, device="cuda")] = \
+                    torch.tensor(patch_val, dtype=torch.float64, device="cuda")
+        b.prep.verdict(N.stream_handle(b.prep.stream))
+        return b.prep.fetch()
 
-    def execute(self, timing: dict | None = None):
-        """Digests of the local copies of cross-rank groups (td_fingerprint +
-        the digest slots of the compare pass), td_segnorm, the digest
-        exchange, then — only when a compare read a copy that differs from
-        copy 0 — the compare pass again reading copy 0, slot reduction, the
-        partial-sum all_reduce and the verdicts."""
-        import torch
-        from .device import resolve_operands
-        table, fps, where, _ = self.digests()
-        ptrs, keep = resolve_operands(self.plan.operands, self.plan.operand_dtypes)
-        prep = self.plan.prepare(ptrs, kappa=self.kappa, eps=self.fmt.eps,
-                                 replica_eps=self.fmt.eps, digests=table.data_ptr())
-        sh = N.stream_handle(prep.stream)
-        with torch.cuda.stream(prep.stream):
-            table.zero_()
-        # copies no local compare reads are digested beside the compare pass
-        # (both stream HBM; each fills the other's tail)
-        side = torch.cuda.Stream()
-        side.wait_stream(prep.stream)
-        fps.run(side)
-        prep.segnorm(sh)
-        prep.stream.wait_stream(side)
-        extra, overrides = self._resolve_remote(table, where)
-        if overrides:
-            ptrs, keep2 = resolve_operands(self.plan.operands, self.plan.operand_dtypes, overrides)
-            prep = self.plan.prepare(ptrs, kappa=self.kappa, eps=self.fmt.eps,
-                                     replica_eps=self.fmt.eps, digests=table.data_ptr())
-            sh = N.stream_handle(prep.stream)
-            prep.segnorm(sh)
-        prep.reduce(sh)
-        if extra:
-            gsum = prep.slot_sums[2 * prep.n_ids:].view(-1, N.SLOT_STRIDE)
-            for slot, vals in extra.items():
-                gsum[slot] += torch.from_numpy(vals).to(gsum.device)
-        allreduce_partials(prep, self.comm)
-        prep.verdict(sh)
-        out = prep.fetch()
-        del keep
-        return out
+    def execute(self, timing: dict | None = None, staged: dict | None = None):
+        """One check: BoundCheck.step (digests, compares, slot reduction, the
+        one exchange, td_combine, verdicts), one D2H of the results; the bug
+        path only when td_combine counted a differing digest."""
+        b = self.bind(staged=staged)
+        return b.check()
 
-    def run(self, timing: dict | None = None):
-        idres, gres, ties = self.execute(timing)
+    def run(self, timing: dict | None = None, staged: dict | None = None):
+        idres, gres, ties = self.execute(timing, staged)
         return self._report(self, idres, gres, ties)
+
+
+class BoundCheck:
+    """A DistributedCheckPlan bound to this rank's payloads: step() enqueues
+    the whole clean-path check on the plan's stream with no host sync."""
+
+    def __init__(self, dcp: DistributedCheckPlan, overrides: dict | None = None, staged: dict | None = None):
+        import torch
+        from .device import Fingerprints, resolve_operands
+        self.dcp = dcp
+        plan = dcp.plan
+        smap = dict(overrides or {})
+        if staged:
+            for m in plan.operands:
+                rec = getattr(m, "record", None)
+                if rec is not None and id(rec) in staged and id(m) not in smap:
+                    smap[id(m)] = staged[id(rec)]
+        ptrs, self._keep = resolve_operands(plan.operands, plan.operand_dtypes, smap or None)
+        # rank-local digest table: td_segnorm's fused slots, then td_fingerprint's rows
+        self.table = torch.zeros((max(len(dcp.where), 1), 2), dtype=torch.int64, device="cuda")
+        self.prep = plan.prepare(ptrs, kappa=dcp.kappa, eps=dcp.fmt.eps, replica_eps=dcp.fmt.eps,
+                                 digests=self.table.data_ptr(), tail_words=2 * dcp.n_rows)
+        me = dcp.comm.rank
+        tensors = []
+        for k, c in dcp.where[dcp.n_fused:]:
+            m = dcp._remote_group_records(plan.remote_groups[k])[c]
+            assert m.owner == me
+            t = staged.get(id(m.record)) if staged and m.record is not None else None
+            tensors.append((t if t is not None else m.device_payload()).reshape(-1))
+        self.fps = Fingerprints(tensors, out=self.table[dcp.n_fused:])
+        self.canon = torch.from_numpy(dcp.canon_rows).to("cuda")
+        self.tail = self.prep.exchange[dcp.n_slots:].view(torch.int64).view(-1, 2)
+        n_copies = len(dcp.copy_off)
+        self.copy_off = torch.from_numpy(dcp.copy_off).to("cuda") if n_copies else None
+        self.copy_first = torch.from_numpy(dcp.copy_first).to("cuda") if n_copies else None
+        self.differs = torch.zeros(max(n_copies, 1), dtype=torch.int32, device="cuda")
+        self.n_copies = n_copies
+        self.gathered = self.prep.exchange if dcp.n_live == 1 else \
+            torch.empty(dcp.n_live * dcp.stride, dtype=torch.float64, device="cuda")
+        self.side = torch.cuda.Stream()
+        self.launches = self.prep.launches_per_run + 1 + (1 if tensors else 0) + (1 if len(dcp.where) else 0)
+
+    def digest_pass(self, sh) -> None:
+        """Digests of this rank's copies of cross-rank groups and the compare
+        pass: td_fingerprint on a side stream beside td_segnorm (both stream
+        HBM; each fills the other's tail)."""
+        import torch
+        prep = self.prep
+        with torch.cuda.stream(prep.stream):
+            if self.dcp.n_fused:
+                self.table[:self.dcp.n_fused].zero_()
+        if self.fps.n:
+            self.side.wait_stream(prep.stream)
+            self.fps.run(self.side)
+        prep.segnorm(sh)
+        if self.fps.n:
+            prep.stream.wait_stream(self.side)
+
+    def exchange(self, sh) -> None:
+        """Slot reduction, the digest rows into their canonical places, the
+        ONE collective, td_combine (rank-order sums + digest compare), verdicts."""
+        import torch
+        dcp, prep = self.dcp, self.prep
+        prep.reduce(sh)
+        with torch.cuda.stream(prep.stream):
+            if len(dcp.where):
+                self.tail.index_copy_(0, self.canon, self.table[:len(dcp.where)])
+            if dcp.n_live > 1:
+                dcp.comm.all_gather_into(self.gathered, prep.exchange)
+        N.call("td_combine", self.gathered.data_ptr(), dcp.n_live, dcp.stride, dcp.n_slots,
+               prep.slot_sums.data_ptr(), self.copy_off.data_ptr() if self.n_copies else 0,
+               self.copy_first.data_ptr() if self.n_copies else 0, self.n_copies, self.differs.data_ptr(),
+               prep.word_ptr, sh)
+        prep.verdict(sh)
+
+    def step(self) -> None:
+        sh = N.stream_handle(self.prep.stream)
+        self.digest_pass(sh)
+        self.exchange(sh)
+
+    def capture(self):
+        """The clean-path step as one CUDA graph (NCCL's all-gather included
+        when the communicator is torch.distributed's)."""
+        import torch
+        graph = torch.cuda.CUDAGraph()
+        prep = self.prep
+        cap = torch.cuda.Stream()
+        cap.wait_stream(prep.stream)
+        keep, prep.stream = prep.stream, cap
+        try:
+            with torch.cuda.graph(graph, stream=cap):
+                self.step()
+        finally:
+            prep.stream = keep
+        prep.stream.wait_stream(cap)
+        return graph
+
+    def check(self):
+        """step() + the one D2H, then the bug path only if a digest differed:
+        (id results, group results, near ties)."""
+        self.step()
+        idres, gres, ties, n_diff = self.fetch()
+        if n_diff:
+            idres, gres, ties = self.dcp._bug_path(self)
+        return idres, gres, ties
+
+    def fetch(self):
+        """(id results, group results, near ties, differing copies): one D2H."""
+        idres, gres, ties = self.prep.fetch()
+        return idres, gres, ties, self.prep.last_word
+
+    def local_digests(self) -> dict:
+        """{(remote group, copy): (h0, h1)} of this rank's copies after a step."""
+        t = self.table[:len(self.dcp.where)].cpu().numpy().view(np.uint64)
+        return {kc: (int(t[i, 0]), int(t[i, 1])) for i, kc in enumerate(self.dcp.where)}
 
 
 def _torch_dtype(code: int):
@@ -434,9 +635,11 @@ def check_distributed(ref, cand, tol, kappa: float = 3.0, *, fmt, comm: Comm | N
                       order_key=None):
     """Collective check(): each rank passes the records it holds.  Returns
     the full CheckReport on every rank."""
+    from .device import stage_host_payloads
     comm = comm or TorchComm()
+    staged = stage_host_payloads([ref, cand])      # host payloads start their DMA first
     return DistributedCheckPlan(ref, cand, tol, kappa, fmt=fmt, comm=comm,
-                                order_key=order_key).run()
+                                order_key=order_key).run(staged=staged)
 
 
 def split_reference(ref, cand_global, world: int):

@@ -639,12 +639,16 @@ class Plan:
         return out
 
     def prepare(self, pointers: np.ndarray, *, kappa: float = 3.0, eps: float = 0.0,
-                replica_eps: float = 0.0, stream=None, digests: int | None = None) -> "Prepared":
+                replica_eps: float = 0.0, stream=None, digests: int | None = None,
+                tail_words: int = 0) -> "Prepared":
         """Patch live addresses into the segment table and stage every
         device-side table and workspace; the result can be launched repeatedly.
         digests: device address of the (len(fused_digests), 2) u64 table the
-        digest classes accumulate into (the caller zeroes it per run)."""
-        return Prepared(self, pointers, kappa, eps, replica_eps, stream, digests)
+        digest classes accumulate into (the caller zeroes it per run).
+        tail_words: f64 words reserved right after the slot sums, so that
+        `exchange` = [slot sums | tail] is one contiguous buffer (the
+        multi-GPU exchange buffer: sums, then digest rows)."""
+        return Prepared(self, pointers, kappa, eps, replica_eps, stream, digests, tail_words)
 
 
 _ONE_SEG = os.environ.get("TD_ONE_SEG", "1") != "0"      # A/B switch for by-value single segments
@@ -654,7 +658,7 @@ _STAGING_LOCK = threading.Lock()
 class Prepared:
     """A plan bound to payload addresses, with its tables resident in HBM."""
 
-    def __init__(self, plan: Plan, pointers, kappa, eps, replica_eps, stream, digests=None):
+    def __init__(self, plan: Plan, pointers, kappa, eps, replica_eps, stream, digests=None, tail_words=0):
         import torch
         self.plan = plan
         self.kappa, self.eps, self.replica_eps = float(kappa), float(eps), float(replica_eps)
@@ -740,19 +744,25 @@ class Prepared:
         # the slot reduction then reads the chunk rows instead of the partials
         self.n_chunks = len(plan.chunks) if chunked else 0
         n_crow = self.n_chunks * N.WARPS_PER_TILE * N.PARTIAL_STRIDE
-        self.work = torch.empty(self.n_part + n_crow + 2 * n_ids + N.SLOT_STRIDE * n_groups,
-                                dtype=torch.float64, device=dev)
+        self.n_slots = 2 * n_ids + N.SLOT_STRIDE * n_groups
+        self.work = torch.empty(self.n_part + n_crow + self.n_slots + tail_words, dtype=torch.float64, device=dev)
         self.part_ptr = self.work.data_ptr()
         self.chunk_ptr = base + offsets[3 + n_cls] if chunked else 0
         self.red_ptr = self.part_ptr + 8 * self.n_part if chunked else self.part_ptr
         self.idsum_ptr = self.part_ptr + 8 * (self.n_part + n_crow)
-        # the slot-sum vector (id sums, then group sums): what crosses ranks
-        self.slot_sums = self.work[self.n_part + n_crow:]
+        # the slot-sum vector (id sums, then group sums): what crosses ranks;
+        # `exchange` extends it by the caller's tail (multi-GPU digests)
+        self.exchange = self.work[self.n_part + n_crow:]
+        self.slot_sums = self.exchange[:self.n_slots]
         self.gsum_ptr = self.idsum_ptr + 8 * 2 * n_ids
         self.res_bytes = N.ID_RESULT.itemsize * n_ids + N.GROUP_RESULT.itemsize * n_groups + 8
         self.res = torch.zeros(self.res_bytes, dtype=torch.uint8, device=dev)
         self.idres_ptr = self.res.data_ptr()
         self.gres_ptr = self.idres_ptr + N.ID_RESULT.itemsize * n_ids
+        # the last 8 bytes: a u64 a caller may have a kernel write (the
+        # multi-GPU digest-mismatch count), fetched with the results
+        self.word_ptr = self.idres_ptr + self.res_bytes - 8
+        self.last_word = 0
         # near ties are counted on the host from the per-id flags: no counter
         # reset between td_segnorm and the verdict kernel, which would keep
         # the verdict kernel from launching programmatically (PDL)
@@ -862,12 +872,13 @@ class Prepared:
         lo = N.ID_RESULT.itemsize * n_ids
         gres = raw[lo:lo + N.GROUP_RESULT.itemsize * n_groups].view(N.GROUP_RESULT)
         ties = int(idres["near_tie"].sum()) if n_ids else 0
+        self.last_word = int(raw[-8:].view(np.uint64)[0])
         return idres, gres, ties
 
     def sums(self) -> dict:
         """Per-id (d2, x2) and per-group (y2, z2...) sums, as reduced on the device."""
         with __import__("torch").cuda.stream(self.stream):
-            flat = self.work[self.n_part:].cpu().numpy()
+            flat = self.slot_sums.cpu().numpy()
         return {"id": flat[:2 * self.n_ids].reshape(self.n_ids, 2),
                 "group": flat[2 * self.n_ids:].reshape(self.n_groups, N.SLOT_STRIDE)}
 

@@ -212,14 +212,26 @@ class ShareLayout:
         return ref, cand
 
     def build(self, rank: int, *, dtype=None, seed: int = 0, eps: float = 2.0 ** -8,
-              header: dict | None = None):
+              header: dict | None = None, bugs: dict | None = None):
         """(reference trace, candidate trace) of `rank`, payloads in HBM.
         Values: as build() — every rank draws an id's logical tensors from
-        the same seed, so shards on different ranks fit together."""
+        the same seed, so shards on different ranks fit together.  bugs: as
+        build()'s ("scale" / "order" / "partial"), applied to the records
+        wherever they live ("order" swaps the id's first two TP shards'
+        payloads across ranks: each holder cuts its record through the
+        partner's map)."""
         import torch
         dtype = dtype or torch.bfloat16
+        bugs = bugs or {}
         hdr = header or {"digest": f"synthetic-{self.model}-{seed}", "mode": "cascade"}
         policy = "bf16" if dtype == torch.bfloat16 else "fp32"
+        partner: dict = {}                  # id(spec) -> spec whose map cuts its payload
+        for ident, bug in bugs.items():
+            if bug != "order":
+                continue
+            specs = [sp for sp in self.cand_specs if sp.ident == ident][:2]
+            if len(specs) == 2 and tuple(specs[0].mapping.local_shape) == tuple(specs[1].mapping.local_shape):
+                partner[id(specs[0])], partner[id(specs[1])] = specs[1], specs[0]
         ref, cand = Trace(header=dict(hdr)), Trace(header=dict(hdr))
         need = {i for i, _ in self.cand[rank]} | {i for i, *_ in self.ref[rank]}
         cand_by_id: dict = {}
@@ -242,10 +254,15 @@ class ShareLayout:
                 y = x if x.dim() == 0 else apply_perturbation(
                     x.reshape(-1, shape[-1]) if x.dim() > 1 else x.reshape(1, -1),
                     "cand|" + ident, PerturbSpec(0, eps), policy=policy).reshape(shape)
+                if bugs.get(ident) == "scale":
+                    y = (y.float() * self.pcfg.tp).to(dtype)
                 for pos in cand_by_id[ident]:
                     s = self.cand[rank][pos][1]
+                    payload = _shard(y, partner.get(id(s), s).mapping)
+                    if bugs.get(ident) == "partial" and payload.numel():
+                        payload = (payload.float() / self.pcfg.tp * (1 + s.rank[1])).to(dtype)
                     cand_recs[pos] = TraceRecord(parse_canonical(ident), RankMeta(*s.rank), s.mapping,
-                                                 s.replica, _shard(y, s.mapping), s.module_class)
+                                                 s.replica, payload, s.module_class)
                 del y
             for pos in ref_by_id.get(ident, ()):
                 _, k, m, mc = self.ref[rank][pos]

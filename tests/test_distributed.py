@@ -196,3 +196,29 @@ def test_distributed_check_over_nccl_world1():
     assert status == "ok", got
     from tests.test_gpu_parity import assert_reports_match
     assert_reports_match(got, want, "nccl world 1")
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_split_one_check():
+    """bench.py --gpus 2 on config 3's layout (at S=256): one check split over
+    two ranks by TP rank (gloo, both ranks on this GPU), the missing-allreduce
+    bug's TP replicas spanning the ranks (the exact bug path inside the timed
+    step) — the verdicts are config 3's: 720 pass, 2 flag, 1 replica-mismatch."""
+    import subprocess
+    import sys
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    env = dict(os.environ, TD_BENCH_BACKEND="gloo", TD_BENCH_SAME_DEVICE="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", "2",
+                          "--master-addr", "127.0.0.1", "--master-port", "29641",
+                          os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "cfg3:256",
+                          "--steps", "2", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong"
+    assert d["verdict_counts"] == {"pass": 720, "flag": 2, "replica-mismatch": 1, "merge-error": 0}
+    assert d["exchange"]["steps_on_bug_path"] == 2 and d["near_ties"] == 0
+    assert d["e2e"]["verdicts"]["replica-mismatch"] == 1 and d["e2e"]["verdicts"]["flag"] == 2

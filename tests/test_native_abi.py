@@ -23,7 +23,7 @@ def test_library_builds_and_loads():
     path = build.build()
     assert os.path.exists(path)
     lib = N.load_library()
-    assert lib.td_version() == 1
+    assert lib.td_version() == 2
 
 
 def test_every_declared_symbol_is_exported_and_typed():

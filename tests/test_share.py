@@ -166,28 +166,35 @@ def test_fingerprint_digests():
 @pytest.mark.gpu
 def test_digests_fused_in_compare_equal_fingerprints():
     """The digest slots td_segnorm fills while comparing a cross-GPU replica
-    group's copy equal td_fingerprint's digest of that copy."""
-    from paper_2506_09280_b200 import _native as N
-    from paper_2506_09280_b200.device import fingerprints, resolve_operands
+    group's copy equal td_fingerprint's digest of that copy, and the digest
+    rows land in the exchange buffer at the canonical offsets td_combine
+    reads (identical on every rank)."""
+    from paper_2506_09280_b200.device import fingerprints
     lay = synthetic.ShareLayout(SMALL, PCFG, WORLD)
     ref_metas, cand_metas = lay.metas()
     fused_total = 0
+    offsets = None
     for r in range(WORLD):
         ref, cand = lay.build(r)
         dcp = DistributedCheckPlan(ref, cand, _tol(lay), fmt=FloatFormat.BF16,
                                    comm=StaticComm(r, WORLD, [ref_metas, cand_metas]))
-        table, fps, where, nf = dcp.digests()
-        ptrs, keep = resolve_operands(dcp.plan.operands, dcp.plan.operand_dtypes)
-        prep = dcp.plan.prepare(ptrs, eps=FloatFormat.BF16.eps, digests=table.data_ptr())
-        table.zero_()
-        fps.run()
-        prep.segnorm(N.stream_handle(prep.stream))
+        if offsets is None:
+            offsets = (dcp.stride, dcp.group_begin, dcp.copy_first.tolist())
+        assert (dcp.stride, dcp.group_begin, dcp.copy_first.tolist()) == offsets
+        b = dcp.bind()
+        b.step()
         torch.cuda.synchronize()
+        got = b.local_digests()
         recs = [dcp._remote_group_records(dcp.plan.remote_groups[k])[c].device_payload().reshape(-1)
-                for k, c in where]
-        want = fingerprints(recs).cpu().numpy()
-        assert np.array_equal(table[:len(where)].cpu().numpy(), want), r
-        fused_total += nf
+                for k, c in dcp.where]
+        want = fingerprints(recs).cpu().numpy().view(np.uint64)
+        for i, kc in enumerate(dcp.where):
+            assert got[kc] == (int(want[i, 0]), int(want[i, 1])), (r, kc)
+        # canonical rows in the exchange tail (this rank is row 0 of a one-rank gather)
+        tail = b.prep.exchange[dcp.n_slots:].view(torch.int64).view(-1, 2).cpu().numpy().view(np.uint64)
+        for i, row in enumerate(dcp.canon_rows):
+            assert (int(tail[row, 0]), int(tail[row, 1])) == got[dcp.where[i]]
+        fused_total += dcp.n_fused
     assert fused_total > 0
 
 
@@ -240,3 +247,70 @@ def test_fingerprint_matches_numpy_restatement():
     got = fingerprints(views).cpu().numpy().view(np.uint64)
     for g, w in zip(got, want):
         assert (int(g[0]), int(g[1])) == w
+
+
+# config 4's layout (Llama-3-8B rules: L=32, GQA 32/8, SwiGLU w3, RMSNorm, no
+# position table; TP=2 x DP=4, M=4, 8 GPUs) at a width that fits all eight
+# shares plus the single-GPU union check on one device (d=1024, ff=3584,
+# V=32000, S=256 — the parameter-sized ids do not shrink with S)
+CFG4_SHAPE = L.ModelShape(layers=32, d_model=1024, n_heads=32, d_ff=3584, seq_len=256, vocab=32000,
+                          n_kv_heads=8, gated_mlp=True, norm_bias=False, position_table=False)
+CFG4_PCFG = L.ParallelConfig(tp=2, dp=4, microbatches=4)
+
+
+@pytest.mark.gpu
+def test_config4_layout_eight_shares_match_single_gpu_and_oracle():
+    """All 8 TP2 x DP4 shares of a config-4-layout check run as ThreadComm
+    ranks on one GPU (one all-gather per check, device digest compare), with
+    a swapped TP shard (the reference's wrong-order bug: a flag) and one
+    corrupted DP replica of a parameter (a cross-GPU digest mismatch: the
+    exact bug path, replica-mismatch).  Every rank's report equals a
+    single-GPU check() of the union of the shares, and a sample of ids —
+    the buggy ones included — equals the CPU oracle's report."""
+    import paper_2506_09280_b200 as td
+    from oracle import traindiff_oracle as O
+    from paper_2506_09280_b200.checker import check
+    swapped = "iter=0|mb=1|kind=ParamGrad|mod=model.layers.5.mlp.w1"
+    lay = synthetic.ShareLayout(CFG4_SHAPE, CFG4_PCFG, 8)
+    shares = [lay.build(r, bugs={swapped: "order"}) for r in range(8)]
+    tol = _tol(lay)
+    # a DP replica (copy 2 of a column-parallel parameter shard) corrupted
+    victim = "iter=0|mb=0|kind=Param|mod=model.layers.20.attn.wk"
+    hits = [(r, k) for r, (_, c) in enumerate(shares) for k, rec in enumerate(c.records)
+            if rec.id.encode() == victim and rec.rank_meta.dp == 2 and rec.rank_meta.tp == 1]
+    assert len(hits) == 1
+    r, k = hits[0]
+    shares[r][1].records[k].payload.view(torch.int16)[7] ^= 0x40
+
+    def body(rank, comm):
+        ref, cand = shares[rank]
+        plan = DistributedCheckPlan(ref, cand, tol, fmt=FloatFormat.BF16, comm=comm)
+        assert plan.plan.remote_groups
+        return json.loads(td.render_report(plan.run(), "json"))
+    reports = _run_threads(8, body)
+    ref_all, cand_all = _union(shares, shares[0][0].header)
+    want = json.loads(td.render_report(check(ref_all, cand_all, tol, fmt=FloatFormat.BF16), "json"))
+    from tests.test_gpu_parity import assert_reports_match
+    for rep in reports:
+        assert_reports_match(rep, want, "config-4 layout, 8 shares")
+    verdicts = {e["id"]: e["verdict"] for e in want["entries"]}
+    assert verdicts[swapped] == "flag" and verdicts[victim] == "replica-mismatch"
+    assert want["summary"]["flag"] == 1 and want["summary"]["replica-mismatch"] == 1
+    assert want["summary"]["pass"] == len(want["entries"]) - 2
+    # the CPU oracle on a sample of ids (every 97th, plus the two bugs)
+    ids = [e["id"] for e in want["entries"]]
+    sample = set(ids[::97]) | {swapped, victim}
+
+    def host(recs):
+        return [O.Rec(x.id.encode(), x.rank_meta.as_tuple(), x.mapping.local_shape, x.mapping.global_shape,
+                      [(lb.bounds, gb.bounds) for lb, gb in x.mapping.pairs], x.replica_group_size,
+                      x.payload.float().cpu().numpy()) for x in recs if x.id.encode() in sample]
+    doc = O.check(host(ref_all.records), host(cand_all.records), ref_all.header, cand_all.header,
+                  tol.responses, 3.0, "BF16")
+    got = {e["id"]: e for e in reports[0]["entries"]}
+    assert {e["id"] for e in doc["entries"]} == sample
+    for w in doc["entries"]:
+        g = got[w["id"]]
+        assert g["verdict"] == w["verdict"] and g["detail"] == w["detail"], (w["id"], g, w)
+        from tests.test_gpu_parity import _close
+        assert _close(g["observed"], w["observed"]), (w["id"], g["observed"], w["observed"])
