@@ -277,9 +277,7 @@ class CheckPlan:
                 continue
             if cand_kind[k] or ref_kind[k]:
                 if per_entry is None:
-                    per_entry = {}
-                    for row, (ei, side, gi) in zip(gres, self.plan.group_owner):
-                        per_entry.setdefault((ei, side), {})[gi] = row
+                    per_entry = self.plan.group_results(gres)
                 if cand_kind[k]:
                     detail = _side_detail(self.cand_view[ident], per_entry.get((k, 0), {}))
                 else:
@@ -335,9 +333,7 @@ def _check_key(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float, fmt: Fl
 
 def _strict_problem(view, plan: Plan, gres, side_of_entry: dict) -> str | None:
     """First id (view order) with a merge/replica problem, as 'id: detail'."""
-    per_entry: dict = {}
-    for row, (ei, side, gi) in zip(gres, plan.group_owner):
-        per_entry.setdefault((ei, side), {})[gi] = row
+    per_entry = plan.group_results(gres)
     for ident, meta in view.items():
         rows = per_entry.get(side_of_entry[ident], {})
         numeric = any(r["mismatch"] for r in rows.values())

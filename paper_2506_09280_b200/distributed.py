@@ -423,7 +423,8 @@ class DistributedCheckPlan:
             diff = [c for c in range(1, len(recs)) if differs[lo + c]]
             if not diff:
                 continue
-            flagged.append(entry[0])
+            first = len(flagged)
+            flagged.extend(self.plan.slots_of(entry[0]))        # one slot per chunk of MAX_Z copies
             y0 = recs[0]
             if y0.owner == me:
                 bufs = []
@@ -435,7 +436,7 @@ class DistributedCheckPlan:
                                           device="cuda")
                         recvs.append((m.owner, buf))
                         bufs.append(buf)
-                pending.append((len(flagged) - 1, y0, bufs))
+                pending.append((first, y0, bufs))
             else:
                 for m in recs[1:]:
                     if m.owner == me:
@@ -456,14 +457,17 @@ class DistributedCheckPlan:
         self.comm.exchange(sends, recvs)
         sub_ids = sorted(affected)
         vec = np.zeros(2 * len(sub_ids) + N.SLOT_STRIDE * len(flagged), np.float64)
-        for j, y0, bufs in pending:
+        base = 2 * len(sub_ids)
+        for first, y0, bufs in pending:
             raws = [_Raw(y0.device_payload().reshape(-1))] + [_Raw(t) for t in bufs]
             mini = Plan([PlanEntry("remote", x=None, y=_one_group("remote", raws, True),
                                    x_rep=False, y_rep=True)])
             ptrs, keep = resolve_operands(mini.operands, mini.operand_dtypes)
             sums: dict = {}
             mini.run(ptrs, sums=sums)
-            vec[2 * len(sub_ids) + N.SLOT_STRIDE * j:2 * len(sub_ids) + N.SLOT_STRIDE * (j + 1)] = sums["group"][0]
+            for j, row in enumerate(sums["group"]):         # the group's chunk slots, in order
+                at = base + N.SLOT_STRIDE * (first + j)
+                vec[at:at + N.SLOT_STRIDE] = row
         if sub_ids:
             sub = Plan([self.plan.entries[ei] for ei in sub_ids], owner=lambda m: m.owner, me=me,
                        compare_copy=self._compare_copy, digest=False)

@@ -338,8 +338,10 @@ class Plan:
         b = PlanBuilder(force_generic=static is not None)
         id_rows = []
         group_rows = []
-        self.group_owner = []     # (entry index, side, group index)
-        self.remote_groups = []   # (group slot, entry index, side, group index)
+        self.group_owner = []     # (entry index, side, group index) per group slot
+        self.group_offset = []    # per group slot: copy index of its first replica - 1
+        self.subslots = {}        # first group slot -> all slots of that group (> MAX_Z + 1 copies)
+        self.remote_groups = []   # (first group slot, entry index, side, group index)
         self.compare_reads = []   # (entry index, group index, copy index != 0)
         self.fused_digests = []   # digest slot -> (remote group index, copy index)
         compare_copy = compare_copy or {}
@@ -351,9 +353,6 @@ class Plan:
             if e.y is not None and not e.y.rank_problem:
                 for gi, g in enumerate(e.y.groups):
                     rep = e.y_rep and g.numeric
-                    if len(g.records) - 1 > N.MAX_Z and rep:
-                        raise NotImplementedError(
-                            f"{e.ident}: replica groups of more than {N.MAX_Z + 1} copies")
                     s0 = b.tile_cursor
                     y0 = g.records[0]
                     spans = rep and len({owner(r) for r in g.records}) > 1
@@ -366,10 +365,16 @@ class Plan:
                             self.compare_reads.append((ei, gi, c))
                     mine = is_local(y0)
                     together = rep and not spans and mine
+                    # replica copies in chunks of MAX_Z (one group slot each);
+                    # the compare reads copy 0 with the first chunk, every
+                    # further chunk re-reads copy 0 once
+                    chunks = _replica_chunks(len(g.records)) if rep else []
+                    zall = []
                     if mine:
                         gdt = _group_dtype(g.records) if together else y0.dtype_code
                         yop = b.operand(y0, gdt)
-                        zops = [b.operand(r, gdt) for r in g.records[1:]] if together else []
+                        zall = [b.operand(r, gdt) for r in g.records[1:]] if together else []
+                        zops = zall[:N.MAX_Z]
                         if has_compare:
                             fuse = digest and spans and static is None
                             first_seg = len(b.seg_rows)
@@ -385,30 +390,28 @@ class Plan:
                             n = math.prod(y0.shape)
                             b.add(None, 0, yop, 0, zops, 1, n, n, n)
                     if rep:
-                        group_rows.append((s0, b.tile_cursor, len(g.records) - 1))
-                        self.group_owner.append((ei, 0, gi))
+                        self._group_slots(b, group_rows, chunks, s0, yop if zall else None, zall,
+                                          math.prod(y0.shape), (ei, 0, gi))
             cg1 = len(group_rows)
             rg0 = len(group_rows)
             if e.x is not None and e.x_rep and not e.x.rank_problem:
                 for gi, g in enumerate(e.x.groups):
                     if not g.numeric:
                         continue
-                    if len(g.records) - 1 > N.MAX_Z:
-                        raise NotImplementedError(
-                            f"{e.ident}: replica groups of more than {N.MAX_Z + 1} copies")
                     s0 = b.tile_cursor
                     x0 = g.records[0]
                     mine = is_local(x0)
+                    chunks = _replica_chunks(len(g.records))
+                    zall, yop = [], None
+                    n = math.prod(x0.shape)
                     if len({owner(r) for r in g.records}) > 1:
                         self.remote_groups.append((len(group_rows), ei, 1, gi))
                     elif mine:
                         gdt = _group_dtype(g.records)
                         yop = b.operand(x0, gdt)
-                        zops = [b.operand(r, gdt) for r in g.records[1:]]
-                        n = math.prod(x0.shape)
-                        b.add(None, 0, yop, 0, zops, 1, n, n, n)
-                    group_rows.append((s0, b.tile_cursor, len(g.records) - 1))
-                    self.group_owner.append((ei, 1, gi))
+                        zall = [b.operand(r, gdt) for r in g.records[1:]]
+                        b.add(None, 0, yop, 0, zall[:N.MAX_Z], 1, n, n, n)
+                    self._group_slots(b, group_rows, chunks, s0, yop, zall, n, (ei, 1, gi))
             rg1 = len(group_rows)
             cand_host = 0
             if e.y is not None:
@@ -432,6 +435,46 @@ class Plan:
         self.tile_shift = self._retile()
         self._freeze_segments()
         self._chunk_slots()
+
+    def _group_slots(self, b: PlanBuilder, group_rows: list, chunks: list, s0: int, yop, zall: list,
+                     n: int, owner_key: tuple) -> None:
+        """Group slots of one replica group: chunk 0's tiles are those emitted
+        since s0 (the compare / first replica segments); each further chunk
+        gets a flat copy-0-vs-chunk segment of its own (when the copies are
+        local) and its own slot."""
+        first = len(group_rows)
+        for j, (lo, hi) in enumerate(chunks):
+            if j:
+                s0 = b.tile_cursor
+                if yop is not None:
+                    b.add(None, 0, yop, 0, zall[lo - 1:hi - 1], 1, n, n, n)
+            group_rows.append((s0, b.tile_cursor, hi - lo))
+            self.group_owner.append(owner_key)
+            self.group_offset.append(lo - 1)
+        if len(chunks) > 1:
+            self.subslots[first] = list(range(first, len(group_rows)))
+
+    def slots_of(self, first_slot: int) -> list:
+        """Every group slot of the replica group whose first slot is given."""
+        return self.subslots.get(first_slot, [first_slot])
+
+    def group_results(self, gres) -> dict:
+        """{(entry, side): {group index: {"worst", "worst_index", "mismatch"}}}
+        with a group's chunk slots folded the way check_replicas walks its
+        copies (canonical.py:236-242): strict > over copies 1..m in order,
+        so the first maximum wins and NaN never does."""
+        out: dict = {}
+        for row, key, off in zip(gres, self.group_owner, self.group_offset):
+            ei, side, gi = key
+            cur = out.setdefault((ei, side), {}).get(gi)
+            w, wi, mm = float(row["worst"]), int(row["worst_index"]), int(row["mismatch"])
+            if cur is None:
+                out[(ei, side)][gi] = {"worst": w, "worst_index": wi + off if wi > 0 else wi, "mismatch": mm}
+            else:
+                if wi > 0 and w > cur["worst"]:
+                    cur["worst"], cur["worst_index"] = w, wi + off
+                cur["mismatch"] |= mm
+        return out
 
     # tiles per SM worth aiming for before the default tile is shrunk
     TARGET_TILES = 148 * 8
@@ -917,6 +960,12 @@ def _run_blocks_uncached(ymap: ShardMapping, xmap: ShardMapping) -> tuple:
             xs = tuple(l0 + (c0 - g0) for (l0, _), (g0, _), (c0, _) in zip(xl.bounds, xg.bounds, cut))
             out.extend(_blocks(ext, xs, xmap.local_shape, ys, ymap.local_shape))
     return tuple(out)
+
+
+def _replica_chunks(n_copies: int) -> list:
+    """[(first copy, end copy)) ranges of at most MAX_Z replica copies (copy
+    0 is every chunk's reference), at least one."""
+    return [(lo, min(lo + N.MAX_Z, n_copies)) for lo in range(1, max(n_copies, 2), N.MAX_Z)]
 
 
 def _group_dtype(records) -> int:

@@ -222,3 +222,45 @@ def test_bench_two_ranks_split_one_check():
     assert d["verdict_counts"] == {"pass": 720, "flag": 2, "replica-mismatch": 1, "merge-error": 0}
     assert d["exchange"]["steps_on_bug_path"] == 2 and d["near_ties"] == 0
     assert d["e2e"]["verdicts"]["replica-mismatch"] == 1 and d["e2e"]["verdicts"]["flag"] == 2
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("corrupt", [(), ((13, 1.5),), ((2, 1.01), (9, 4.0))])
+def test_wide_replica_group_across_threads(corrupt):
+    """A 16-copy replica group spread over 4 ranks (4 copies each): the
+    digests decide the clean case; a differing copy takes the exact bug path
+    with the group's sums in chunks of 7 copies — the oracle's report."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_09280_b200 as td
+    from tests.test_gpu_parity import _oracle_report, _wide_replica_traces, assert_reports_match
+    ref, cand = _wide_replica_traces(16, corrupt)
+    tol = td.ToleranceMap({ref.records[0].id.encode(): 2.0 ** -8}, n_samples=1, eps_p=2.0 ** -8)
+    want = _oracle_report(ref, cand, tol)
+    world = 4
+    hub = ThreadComm.hub(world)
+    reports, errors = [None] * world, []
+    pos = {id(r): k for k, r in enumerate(cand.records)}
+    pos.update({id(r): k for k, r in enumerate(ref.records)})
+
+    def worker(rank):
+        try:
+            comm = ThreadComm(hub, rank)
+            cand_local = _local(cand, rank, world, lambda r: r.rank_meta.tp // 4)
+            gcand = global_trace(cand_local, comm, _order_key(pos))
+            refs = split_reference(ref, gcand, world)
+            plan = DistributedCheckPlan(refs[rank], cand_local, tol, 3.0, fmt=td.FloatFormat.BF16,
+                                        comm=comm, order_key=_order_key(pos))
+            reports[rank] = json.loads(td.render_report(plan.run(), "json"))
+        except Exception:  # pragma: no cover - surfaced below
+            import traceback
+            errors.append(traceback.format_exc())
+            hub.barrier.abort()
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=600)
+    assert not errors, errors[0]
+    for rep in reports:
+        assert_reports_match(rep, want, f"16 copies over 4 ranks {corrupt}")

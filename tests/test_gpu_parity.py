@@ -756,3 +756,46 @@ def test_concurrent_checks_share_a_cached_plan(cases, golden_trace_bytes):
     with concurrent.futures.ThreadPoolExecutor(6) as ex:
         for _ in range(4):
             assert list(ex.map(job, variants)) == want
+
+
+def _wide_replica_traces(n_copies, corrupt=(), dtype=None):
+    """A 16-copy (or any) replica group: reference = one (64, 96) id; the
+    candidate holds n_copies identity-mapped copies (replica_group_size =
+    n_copies, rank tp = copy index); corrupt = {copy: scale}."""
+    dtype = dtype or torch.bfloat16
+    ident = CanonicalId(0, 0, TensorKind.ACTIVATION_OUT, "model.layers.0.attn")
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn((64, 96), generator=g, device="cuda").to(dtype)
+    y = td.apply_perturbation(x, "cand|" + ident.encode(), td.PerturbSpec(0, 2.0 ** -8), policy="bf16")
+    hdr = {"digest": "wide", "mode": "cascade"}
+    ref = Trace(dict(hdr), [TraceRecord(ident, RankMeta(), identity_mapping((64, 96)), 1, x, "Attn")])
+    cand = Trace(dict(hdr), [])
+    for c in range(n_copies):
+        p = y.clone()
+        if c in dict(corrupt):
+            p = (p.float() * dict(corrupt)[c]).to(dtype)
+        cand.records.append(TraceRecord(ident, RankMeta(tp=c), identity_mapping((64, 96)), n_copies, p, "Attn"))
+    return ref, cand
+
+
+def _oracle_report(ref, cand, tol, fmt="BF16"):
+    def host(t):
+        return [O.Rec(r.id.encode(), r.rank_meta.as_tuple(), r.mapping.local_shape, r.mapping.global_shape,
+                      [(a.bounds, b.bounds) for a, b in r.mapping.pairs], r.replica_group_size,
+                      r.payload.float().cpu().numpy()) for r in t.records]
+    return O.check(host(ref), host(cand), ref.header, cand.header, tol.responses, 3.0, fmt)
+
+
+@pytest.mark.parametrize("n_copies,corrupt", [(16, ()), (16, ((11, 1.5),)), (16, ((3, 1.01), (12, 2.0))),
+                                              (9, ((8, 3.0),)), (23, ((15, 1.25), (22, 1.25)))])
+def test_replica_groups_beyond_eight_copies(n_copies, corrupt):
+    """Replica groups of more than 8 copies (check_replicas walks any number,
+    canonical.py:225-247): chunks of 7 replicas per group slot, copy 0
+    re-read per chunk, the worst folded with the reference's strict >
+    (first maximum wins).  Reports equal the CPU oracle's."""
+    ref, cand = _wide_replica_traces(n_copies, corrupt)
+    tol = td.ToleranceMap({ref.records[0].id.encode(): 2.0 ** -8}, n_samples=1, eps_p=2.0 ** -8)
+    got = json.loads(td.render_report(td.check(ref, cand, tol, fmt=td.FloatFormat.BF16), "json"))
+    want = _oracle_report(ref, cand, tol)
+    assert_reports_match(got, want, f"{n_copies} copies {corrupt}")
+    assert (got["summary"]["replica-mismatch"] == 1) == bool(corrupt)
