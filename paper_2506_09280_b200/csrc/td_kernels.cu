@@ -119,29 +119,33 @@ constexpr uint64_t GAMMA = 0x9E3779B97F4A7C15ull;
 constexpr uint64_t MIX1 = 0xBF58476D1CE4E5B9ull;
 constexpr uint64_t MIX2 = 0x94D049BB133111EBull;
 
-// One 8-byte word w with position key k = (j+1)*gamma (j = word index) into
-// a 128-bit digest: z = fold((w ^ k) * MIX1) — for a fixed key a bijection of
-// w, so a changed word always changes z — then h0 += z and h1 += hi32(z) *
-// lo32(z) (a non-linear second lane).  One 64-bit multiply and one 32x32
-// wide multiply per word: ncu showed the fmaheavy pipe (IMAD / IMAD.WIDE)
-// binding at 80% with the first, two-round version (5.6 TB/s).  Keys of
-// consecutive words differ by gamma, so callers step them with adds.
-__device__ __forceinline__ void fp_key_word(uint64_t w, uint64_t key, uint64_t& h0, uint64_t& h1) {
-    uint64_t z = (w ^ key) * MIX1;
-    z ^= z >> 32;
-    h0 += z;
-    h1 += (uint64_t)(uint32_t)(z >> 32) * (uint32_t)z;
+// Replica digests: 8-byte word w_j (j = its word index in the record) with
+// position key k_j = (j+1)*gamma goes into lane j & 1 as
+//     h[j & 1] += (w_j ^ k_j) * M[j & 1]      (mod 2^64, M odd)
+// — for a fixed key a bijection of w_j, so a changed word always changes its
+// lane's sum; position-keyed (permuted shards differ); order-independent (any
+// reduction order, atomics included, gives the same bits).  One 64-bit
+// multiply per word.  (The first version folded every word into both lanes,
+// z = fold((w ^ k) * MIX1), h0 += z, h1 += hi32(z) * lo32(z): ~12
+// instructions per word against 7, and the compare pass that digests its
+// copy is instruction-issue bound.)
+__device__ __forceinline__ void fp_key_word(uint64_t w, uint64_t key, uint64_t& h, uint64_t mult) {
+    h += (w ^ key) * mult;
 }
 
 __device__ __forceinline__ void fp_word(uint64_t w, uint64_t j, uint64_t& h0, uint64_t& h1) {
-    fp_key_word(w, (j + 1) * GAMMA, h0, h1);
+    if (j & 1) fp_key_word(w, (j + 1) * GAMMA, h1, MIX2);
+    else fp_key_word(w, (j + 1) * GAMMA, h0, MIX1);
 }
 
-// a 16-byte vector at word index j (words j, j+1)
+// a 16-byte vector at (even) word index j: words j -> lane 0, j+1 -> lane 1
+__device__ __forceinline__ void fp_vec_key(const uint4& v, uint64_t k0, uint64_t& h0, uint64_t& h1) {
+    fp_key_word(((uint64_t)v.y << 32) | v.x, k0, h0, MIX1);
+    fp_key_word(((uint64_t)v.w << 32) | v.z, k0 + GAMMA, h1, MIX2);
+}
+
 __device__ __forceinline__ void fp_vec(const uint4& v, uint64_t j, uint64_t& h0, uint64_t& h1) {
-    const uint64_t k0 = (j + 1) * GAMMA;
-    fp_key_word(((uint64_t)v.y << 32) | v.x, k0, h0, h1);
-    fp_key_word(((uint64_t)v.w << 32) | v.z, k0 + GAMMA, h0, h1);
+    fp_vec_key(v, (j + 1) * GAMMA, h0, h1);
 }
 
 #ifndef TD_REPLICA_SKIP
@@ -327,13 +331,19 @@ k_segnorm_vec(const td_segment* __restrict__ segs, const int64_t* __restrict__ t
                 }
             }
             if constexpr (DG) {
+                const bool flat = rd<ONE>(&g->rows) == 1;
 #pragma unroll
                 for (int k = 0; k < U; ++k) {
                     if (!ok[k]) continue;
                     const uint32_t u = base + k * BLOCK;
-                    const uint32_t row = udiv(u, S.div_m, S.div_p);
-                    const uint32_t cv = u - row * vpr;
-                    const uint64_t j = (uint64_t)(w0 + (((int64_t)row * S.ys + (int64_t)cv * 8) * ES >> 3));
+                    uint64_t j;
+                    if (flat) {
+                        j = (uint64_t)w0 + (uint64_t)u * (2 * Q);       // one row: 2Q words per unit
+                    } else {
+                        const uint32_t row = udiv(u, S.div_m, S.div_p);
+                        const uint32_t cv = u - row * vpr;
+                        j = (uint64_t)(w0 + (((int64_t)row * S.ys + (int64_t)cv * 8) * ES >> 3));
+                    }
 #pragma unroll
                     for (int q = 0; q < Q; ++q) fp_vec(yr[k][q], j + 2 * q, h0, h1);
                 }
@@ -454,6 +464,258 @@ k_segnorm_generic(const td_segment* __restrict__ segs, const int64_t* __restrict
 }
 
 typedef void (*segnorm_fn)(const td_segment*, const int64_t*, int64_t, double*, unsigned long long*, td_segment);
+
+// ---------------------------------------------------------------------------
+// Bulk-copy pipelined walker (compare classes, 2-byte payloads, nz = 0):
+// a warp-specialised CTA — warp 8 is a producer that moves each tile's x and
+// y bytes into a ring of shared-memory stages with cp.async.bulk (the TMA
+// engine, SASS UBLKCP), each stage's bytes tracked by an mbarrier
+// (complete_tx); warps 0-7 consume a stage from shared memory (fp64 norms,
+// and for DG the 128-bit digest of y) and release it with one arrive per
+// warp.  The loads hold no registers while in flight, so a CTA keeps
+// STAGES x 2 x CH x 16 bytes in flight whatever the consumers' register
+// budget — the LDG walker's digest class was latency-bound at 64 registers
+// (ncu: 42% warps active, 4.3 long-scoreboard stalls per issue).
+// Segment rows are cut into row pieces (16-B aligned, multiples of 16 B,
+// guaranteed by the vector class), one bulk copy per piece and operand,
+// issued by the producer warp's 32 lanes in parallel.  Partial rows and
+// digest slots are written exactly as by k_segnorm_vec (warp w of a tile
+// consumes units w*32+lane, +256, ... of every stage), so td_reduce_slots /
+// td_finalize are unchanged.
+#ifndef TD_BULK_CH
+#define TD_BULK_CH 1024             // units (16 B of each operand) per stage
+#endif
+#ifndef TD_BULK_STAGES
+#define TD_BULK_STAGES 6
+#endif
+#ifndef TD_BULK_MINB
+#define TD_BULK_MINB 1              // CTAs per SM
+#endif
+constexpr int BULK_THREADS = BLOCK + 32;
+constexpr uint32_t BULK_OPB = TD_BULK_CH * 16;   // bytes per operand per stage
+constexpr size_t BULK_SMEM = (size_t)TD_BULK_STAGES * 2 * BULK_OPB + 2 * TD_BULK_STAGES * sizeof(uint64_t);
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "TD_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra TD_WAIT;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+}
+
+#ifndef TD_BULK_ACC
+#define TD_BULK_ACC 2
+#endif
+#ifndef TD_BULK_ICONV
+#define TD_BULK_ICONV 0
+#endif
+
+// bf16 element e of a 16-B vector as f64 without F2F: its bits placed under
+// the f64 exponent field (value x * 2^-896, a double normal for bf16 normals
+// and a double subnormal for bf16 subnormals, zero for zero), then one exact
+// DMUL by 2^896.  Not for inf/NaN (exponent field 255): see bf16_any_infnan.
+__device__ __forceinline__ double bf16_f64_int(const uint4* q, int e) {
+    const uint32_t w = (&q[0].x)[e >> 1];
+    const uint32_t f = (e & 1) ? (w & 0xffff0000u) : (w << 16);      // f32 bits
+    const uint32_t hi = (f & 0x80000000u) | ((f & 0x7fffffffu) >> 3);
+    return __dmul_rn(__hiloint2double((int)hi, 0), 0x1p896);
+}
+
+__device__ __forceinline__ bool bf16_any_infnan(const uint4& a, const uint4& b) {
+    const uint32_t m = 0x7f807f80u;
+    uint32_t r = __vcmpeq2(a.x & m, m) | __vcmpeq2(a.y & m, m) | __vcmpeq2(a.z & m, m) | __vcmpeq2(a.w & m, m);
+    r |= __vcmpeq2(b.x & m, m) | __vcmpeq2(b.y & m, m) | __vcmpeq2(b.z & m, m) | __vcmpeq2(b.w & m, m);
+    return r != 0;
+}
+
+template <int DT, bool DG>
+__global__ void __launch_bounds__(BULK_THREADS, TD_BULK_MINB)
+k_segnorm_bulk(const td_segment* __restrict__ segs, const int64_t* __restrict__ tiles, int64_t n,
+               double* __restrict__ partials, unsigned long long* __restrict__ digests,
+               const __grid_constant__ td_segment seg1) {
+    static_assert(Vec<DT>::Q == 1, "2-byte payloads: 8 elements per 16-B unit");
+    constexpr int ES = 2;
+    constexpr int ST = TD_BULK_STAGES;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const uint32_t base = smem_addr(smem);
+    const uint32_t bars = base + ST * 2 * BULK_OPB;              // full[s], then empty[s]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(bars + 8 * s, 1);
+            mbar_init(bars + 8 * (ST + s), NWARP);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t stage = 0, phase = 0;
+    if (warp == NWARP) {
+        // ---- producer warp ----
+        uint64_t policy;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+        for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+            const int64_t e = __ldg(tiles + i);
+            const int64_t t = entry_tile(e);
+            const td_segment* g = segs + entry_seg(e);
+            const char* x = reinterpret_cast<const char*>(__ldg(&g->x));
+            const char* y = reinterpret_cast<const char*>(__ldg(&g->y));
+            const int64_t xs = __ldg(&g->x_stride), ys = __ldg(&g->y_stride);
+            const uint32_t vpr = (uint32_t)(__ldg(&g->cols) >> 3);
+            const uint32_t dm = __ldg(&g->div_m);
+            const int dp = __ldg(&g->div_p);
+            const int64_t tu = tile_units(g);
+            const int64_t first = (t - __ldg(&g->tile_begin)) * tu;
+            const uint32_t u0 = (uint32_t)first;
+            const uint32_t u1 = (uint32_t)min(first + tu, __ldg(&g->n_units));
+            for (uint32_t c0 = u0; c0 < u1; c0 += TD_BULK_CH) {
+                const uint32_t c1 = min(c0 + (uint32_t)TD_BULK_CH, u1);
+                const uint32_t full = bars + 8 * stage;
+                if (lane == 0) {
+                    mbar_wait(bars + 8 * (ST + stage), phase ^ 1);   // consumers released the slot
+                    mbar_expect_tx(full, 2u * (c1 - c0) * 16u);
+                }
+                __syncwarp();
+                const uint32_t xd = base + stage * 2 * BULK_OPB, yd = xd + BULK_OPB;
+                const uint32_t r0 = udiv(c0, dm, dp), r1 = udiv(c1 - 1, dm, dp);
+                for (uint32_t r = r0 + lane; r <= r1; r += 32) {
+                    const uint32_t a = max(c0, r * vpr), b = min(c1, (r + 1) * vpr);
+                    const uint32_t cv = a - r * vpr, bytes = (b - a) * 16u, so = (a - c0) * 16u;
+                    bulk_g2s(xd + so, x + ((int64_t)r * xs + (int64_t)cv * 8) * ES, bytes, full, policy);
+                    bulk_g2s(yd + so, y + ((int64_t)r * ys + (int64_t)cv * 8) * ES, bytes, full, policy);
+                }
+                if (++stage == ST) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else {
+        // ---- consumer warps ----
+        for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+            const int64_t e = __ldg(tiles + i);
+            const int64_t t = entry_tile(e);
+            const td_segment* g = segs + entry_seg(e);
+            const int64_t tu = tile_units(g);
+            const int64_t first = (t - __ldg(&g->tile_begin)) * tu;
+            const uint32_t u0 = (uint32_t)first;
+            const uint32_t u1 = (uint32_t)min(first + tu, __ldg(&g->n_units));
+            const uint32_t vpr = (uint32_t)(__ldg(&g->cols) >> 3);
+            const uint32_t dm = __ldg(&g->div_m);
+            const int dp = __ldg(&g->div_p);
+            const int64_t ys = __ldg(&g->y_stride);
+            const int64_t w0 = DG ? __ldg(&g->y_word0) : 0;
+            const bool flat = __ldg(&g->rows) == 1;
+            const uint64_t key0 = (uint64_t)(w0 + 1) * GAMMA;
+            // TD_BULK_ACC independent accumulator pairs (element e8 feeds pair
+            // e8 % ACC): the DFMA chains, not the loads, bound a consumer warp
+            constexpr int ACC = TD_BULK_ACC;
+            double d2[ACC], x2[ACC];
+#pragma unroll
+            for (int q = 0; q < ACC; ++q) d2[q] = x2[q] = 0.0;
+            uint64_t h0 = 0, h1 = 0;
+            for (uint32_t c0 = u0; c0 < u1; c0 += TD_BULK_CH) {
+                const uint32_t c1 = min(c0 + (uint32_t)TD_BULK_CH, u1);
+                mbar_wait(bars + 8 * stage, phase);
+                const unsigned char* xs_ = smem + stage * 2 * BULK_OPB;
+                const uint4* xv = reinterpret_cast<const uint4*>(xs_);
+                const uint4* yv = reinterpret_cast<const uint4*>(xs_ + BULK_OPB);
+                for (uint32_t k = threadIdx.x; k < c1 - c0; k += BLOCK) {
+                    const uint4 xr = xv[k], yr = yv[k];
+                    if constexpr (DG) {
+                        const uint32_t u = c0 + k;
+                        if (flat) {                  // one row: word index w0 + 2u
+                            fp_vec_key(yr, key0 + (uint64_t)u * (2 * GAMMA), h0, h1);
+                        } else {
+                            const uint32_t row = udiv(u, dm, dp);
+                            const uint32_t cv = u - row * vpr;
+                            fp_vec(yr, (uint64_t)(w0 + (((int64_t)row * ys + (int64_t)cv * 8) * ES >> 3)), h0, h1);
+                        }
+                    }
+                    if (TD_BULK_ICONV && DT == TD_BF16 && !bf16_any_infnan(xr, yr)) {
+                        // bf16 -> f64 on the integer pipe + one exact DMUL (no F2F on XU)
+#pragma unroll
+                        for (int e8 = 0; e8 < 8; ++e8) {
+                            const double a = bf16_f64_int(&xr, e8);
+                            const double d = a - bf16_f64_int(&yr, e8);
+                            d2[e8 % ACC] = fma(d, d, d2[e8 % ACC]);
+                            x2[e8 % ACC] = fma(a, a, x2[e8 % ACC]);
+                        }
+                    } else {
+#pragma unroll
+                        for (int e8 = 0; e8 < 8; ++e8) {
+                            const double a = Vec<DT>::at(&xr, e8);
+                            const double d = a - Vec<DT>::at(&yr, e8);
+                            d2[e8 % ACC] = fma(d, d, d2[e8 % ACC]);
+                            x2[e8 % ACC] = fma(a, a, x2[e8 % ACC]);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(bars + 8 * (ST + stage));
+                if (++stage == ST) { stage = 0; phase ^= 1; }
+            }
+            Acc a;
+            a.zero();
+#pragma unroll
+            for (int q = 0; q < ACC; ++q) {
+                a.d2 += d2[q];
+                a.x2 += x2[q];
+            }
+            write_warp_partial(a, 2, partials + (t * TD_WARPS_PER_TILE + warp) * TD_PARTIAL_STRIDE);
+            if constexpr (DG) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    h0 += __shfl_xor_sync(0xffffffffu, h0, o);
+                    h1 += __shfl_xor_sync(0xffffffffu, h1, o);
+                }
+                const int slot = __ldg(&g->digest_slot);
+                if (lane == 0 && slot >= 0) {
+                    atomicAdd(digests + 2 * slot, (unsigned long long)h0);
+                    atomicAdd(digests + 2 * slot + 1, (unsigned long long)h1);
+                }
+            }
+        }
+    }
+    griddep_launch_dependents();
+}
+
+// TD_BULK bit 0: digest classes take the bulk walker; bit 1: plain nz = 0
+// compare classes too (2-byte payloads).  Default: digest classes only.
+int bulk_mode() {
+    static const int m = [] {
+        const char* e = getenv("TD_BULK");
+        return e ? atoi(e) : 1;
+    }();
+    return m;
+}
+
+segnorm_fn pick_bulk(int dt, int nz, bool hx, bool dg) {
+    if (nz != 0 || !hx || (dt != TD_BF16 && dt != TD_F16)) return nullptr;
+    const int m = bulk_mode();
+    if (!(dg ? (m & 1) : (m & 2))) return nullptr;
+    if (dt == TD_BF16) return dg ? k_segnorm_bulk<TD_BF16, true> : k_segnorm_bulk<TD_BF16, false>;
+    return dg ? k_segnorm_bulk<TD_F16, true> : k_segnorm_bulk<TD_F16, false>;
+}
 
 static_assert(sizeof(td_segment) == 160, "td_segment layout");
 static_assert(BLOCK / 32 == TD_WARPS_PER_TILE, "one partial row per warp of a tile");
@@ -1141,7 +1403,7 @@ __global__ void k_quantize(const double* __restrict__ x, char* __restrict__ y, i
 // ---------------------------------------------------------------------------
 // Replica digests (multi-GPU replica groups): for each item, an
 // order-independent 128-bit digest of its bytes, sum over 8-byte words w_j
-// (tail zero-padded) of fp_key_word(w_j, (j+1)*gamma) mod 2^64 (see there).
+// (tail zero-padded) into two lanes by fp_word (see there).
 // Position-keyed, so permuted shards differ.
 // One launch covers every item: a flat list of 256 KB chunks (prefix sums of
 // per-item chunk counts, binary-searched per chunk), 16-byte streaming loads,
@@ -1182,8 +1444,7 @@ k_fingerprint(const td_fp_item* __restrict__ items, const int64_t* __restrict__ 
                     if (o < vend) {
                         // key of word o/8: base key + k * (2 * BLOCK) * gamma (adds only)
                         const uint64_t key = kbase + (uint64_t)k * (2ull * BLOCK * GAMMA);
-                        fp_key_word(((uint64_t)v[k].y << 32) | v[k].x, key, h0, h1);
-                        fp_key_word(((uint64_t)v[k].w << 32) | v[k].z, key + GAMMA, h0, h1);
+                        fp_vec_key(v[k], key, h0, h1);
                     }
                 }
             }
@@ -1520,7 +1781,22 @@ int td_segnorm(const td_segment* segs, const td_class* classes, int32_t n_classe
         td_segment seg1;
         if (C.host_seg) seg1 = *C.host_seg;
         else memset(&seg1, 0, sizeof(seg1));
-        fn<<<(unsigned)grid, BLOCK, 0, st>>>(segs, C.tiles, C.n_tiles, partials, C.digests, seg1);
+        if (segnorm_fn bulk = pick_bulk(C.dtype, C.nz, C.has_x != 0, C.digest != 0)) {
+            static thread_local bool attr_set[2][2] = {{false, false}, {false, false}};
+            bool& done = attr_set[C.dtype == TD_BF16][C.digest != 0];
+            if (!done) {
+                if (cudaFuncSetAttribute(bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BULK_SMEM) !=
+                    cudaSuccess)
+                    return fail("td_segnorm: cannot reserve %zu bytes of shared memory", BULK_SMEM);
+                done = true;
+            }
+            int64_t bgrid = (int64_t)sms * TD_BULK_MINB;
+            if (bgrid > C.n_tiles) bgrid = C.n_tiles;
+            bulk<<<(unsigned)bgrid, BULK_THREADS, BULK_SMEM, st>>>(segs, C.tiles, C.n_tiles, partials, C.digests,
+                                                                   seg1);
+        } else {
+            fn<<<(unsigned)grid, BLOCK, 0, st>>>(segs, C.tiles, C.n_tiles, partials, C.digests, seg1);
+        }
         if (int rc = check_launch("td_segnorm")) return rc;
         if (st != main_stream) join_aux(aux, k - 1, main_stream);
     }

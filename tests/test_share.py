@@ -214,18 +214,16 @@ def test_fuzzed_shares_match_single_gpu_check():
 
 
 def _digest_numpy(data: bytes):
-    """CPU restatement of the td_fingerprint digest (td_kernels.cu, fp_key_word):
-    8-byte little-endian words w_j (tail zero-padded), z = fold((w_j ^ (j+1)*gamma)
-    * MIX1), h0 = sum z, h1 = sum hi32(z) * lo32(z), all mod 2^64."""
+    """CPU restatement of the td_fingerprint digest (td_kernels.cu, fp_word):
+    8-byte little-endian words w_j (tail zero-padded), lane j % 2:
+    h[j % 2] = sum (w_j ^ (j+1)*gamma) * M[j % 2] mod 2^64, M = (MIX1, MIX2)."""
     pad = (-len(data)) % 8
     w = np.frombuffer(data + b"\0" * pad, dtype="<u8")
     with np.errstate(over="ignore"):
         j = np.arange(1, len(w) + 1, dtype=np.uint64)
-        key = j * np.uint64(0x9E3779B97F4A7C15)
-        z = (w ^ key) * np.uint64(0xBF58476D1CE4E5B9)
-        z ^= z >> np.uint64(32)
-        h0 = np.sum(z, dtype=np.uint64)
-        h1 = np.sum((z >> np.uint64(32)) * (z & np.uint64(0xFFFFFFFF)), dtype=np.uint64)
+        z = w ^ (j * np.uint64(0x9E3779B97F4A7C15))
+        h0 = np.sum(z[0::2] * np.uint64(0xBF58476D1CE4E5B9), dtype=np.uint64)
+        h1 = np.sum(z[1::2] * np.uint64(0x94D049BB133111EB), dtype=np.uint64)
     return int(h0), int(h1)
 
 
