@@ -1,0 +1,199 @@
+"""§8(f) #3: real-TP annotated captures from a live tensor-parallel run.
+
+A Megatron-style TP=2 GPT (tests/tp_gpt.py) runs as two real
+torch.distributed ranks (gloo); torchtap.layout_shard tags every capture
+with the reference emulator's map for that rank (engine.py:268-296).  The
+CPU tests check the annotated candidate against a single-device run with
+the CPU oracle (test infrastructure); the GPU tests run the same live job
+on cuda:0 (two processes, gloo on CUDA tensors), feed the device-resident
+captures to check() and to check_distributed() — each rank passing only its
+own records — and compare with the oracle.
+
+Bug site (reference test_checker.py:314-325): with the row-parallel
+all-reduce of `model.layers.1.attn` dropped (MC_TP_ROW_ALLREDUCE), the
+earliest divergence is that block's ActivationOut, a replica-mismatch whose
+observed error clears the tolerance floor by >= 10x.
+"""
+
+from __future__ import annotations
+
+import os
+import pickle
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+from oracle import traindiff_oracle as O
+from paper_2506_09280_b200 import torchtap
+from paper_2506_09280_b200.layout import Layout, ParallelConfig
+from paper_2506_09280_b200.torchtap import TapError
+
+from . import tp_gpt
+
+SHAPE = {"layers": 2, "d": 32, "heads": 4, "ff": 64, "seq": 16, "vocab": 64}
+BUG_SITE = "iter=0|mb=0|kind=ActivationOut|mod=model.layers.1.attn"
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _flat(rec) -> dict:
+    m = rec.mapping
+    return {"ident": rec.ident, "rank": tuple(rec.rank), "local": m.local_shape, "global": m.global_shape,
+            "pairs": [(l.bounds, g.bounds) for l, g in m.pairs], "replica": rec.replica,
+            "payload": rec.host(), "cls": rec.module_class}
+
+
+def _tp_worker(rank, world, port, out_dir, shape, device, dtype_name, skip, mode):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        if device == "cuda":
+            torch.cuda.set_device(0)
+        g = tp_gpt.TPGroup(rank, world)
+        h = tp_gpt.traced_step(shape, g, device=device, dtype=getattr(torch, dtype_name),
+                               skip_reduce=skip, precision=dtype_name)
+        result = {"records": [_flat(r) for r in h.records], "header": h.header()}
+        if mode == "distributed":
+            import paper_2506_09280_b200 as td
+            from paper_2506_09280_b200.distributed import TorchComm, global_trace, split_reference
+            ref_h = tp_gpt.traced_step(shape, tp_gpt.TPGroup(), device=device,
+                                       dtype=getattr(torch, dtype_name), precision=dtype_name)
+            comm = TorchComm()
+            cand = h.trace()
+            refs = split_reference(ref_h.trace(), global_trace(cand, comm), world)
+            tol = td.ToleranceMap({}, n_samples=1, eps_p=td.FloatFormat.BF16.eps)
+            rep = td.check_distributed(refs[rank], cand, tol, fmt=td.FloatFormat.BF16, comm=comm)
+            result["report"] = td.render_report(rep, "json")
+        with open(os.path.join(out_dir, f"rank{rank}.pkl"), "wb") as fh:
+            pickle.dump(result, fh)
+    finally:
+        dist.destroy_process_group()
+
+
+def run_tp(tmp_path, shape=SHAPE, world=2, device="cpu", dtype="float32", skip=(), mode="capture"):
+    mp.start_processes(_tp_worker, args=(world, _free_port(), str(tmp_path), shape, device, dtype,
+                                         tuple(skip), mode),
+                       nprocs=world, join=True, start_method="spawn")
+    out = []
+    for r in range(world):
+        with open(tmp_path / f"rank{r}.pkl", "rb") as fh:
+            out.append(pickle.load(fh))
+    return out
+
+
+def _oracle_recs(flat_records):
+    return [O.Rec(f["ident"], f["rank"], f["local"], f["global"], f["pairs"], f["replica"],
+                  f["payload"], f["cls"]) for f in flat_records]
+
+
+def _single_device(shape=SHAPE, device="cpu", dtype=torch.float32, precision="float32"):
+    return tp_gpt.traced_step(shape, tp_gpt.TPGroup(), device=device, dtype=dtype, precision=precision)
+
+
+def test_layout_shard_maps_are_the_layouts():
+    layout = Layout(tp_gpt.model_shape(SHAPE), ParallelConfig(tp=2))
+    shard = torchtap.layout_shard(layout, tp=1)
+    d, S, V = SHAPE["d"], SHAPE["seq"], SHAPE["vocab"]
+    m, rank, rep = shard("model.layers.0.attn.wq", "ParamGrad", torch.empty(d, d // 2))
+    assert m.pairs[0][1].bounds == ((0, d), (d // 2, d)) and rep == 1 and rank[1] == 1
+    m, _, rep = shard("model.layers.0.attn.wo", "ParamGrad", torch.empty(d // 2, d))
+    assert m.pairs[0][1].bounds == ((d // 2, d), (0, d)) and rep == 1
+    m, _, rep = shard("model.layers.1.mlp.norm.weight", "ParamGrad", torch.empty(d))
+    assert m.global_shape == (d,) and rep == 2
+    m, _, rep = shard("model.lm_head", "ActivationOut", torch.empty(S, V // 2))
+    assert m.pairs[0][1].bounds == ((0, S), (V // 2, V)) and rep == 1
+    m, _, rep = shard("model.layers.0.attn.norm", "ActivationOut", torch.empty(S, d))
+    assert m.global_shape == (S, d) and rep == 2
+    with pytest.raises(TapError, match="shape"):
+        shard("model.layers.0.attn.wq", "ParamGrad", torch.empty(d, d))
+    with pytest.raises(TapError, match="no ParamGrad map"):
+        shard("model.layers.0.attn.bogus", "ParamGrad", torch.empty(d))
+    with pytest.raises(TapError, match="outside"):
+        torchtap.layout_shard(layout, tp=2)
+
+
+def test_live_tp2_capture_matches_single_device(tmp_path):
+    ranks = run_tp(tmp_path)
+    ref = _single_device()
+    cand = [f for r in ranks for f in r["records"]]
+    # every capture carries its rank's map; copies of one id agree on the id set
+    assert {f["rank"][1] for f in cand} == {0, 1}
+    ids0 = [f["ident"] for f in ranks[0]["records"]]
+    assert sorted(ids0) == sorted(f["ident"] for f in ranks[1]["records"])
+    assert sorted(set(ids0)) == sorted(r.ident for r in ref.records)
+    doc = O.check(_oracle_recs([_flat(r) for r in ref.records]), _oracle_recs(cand),
+                  ref.header(), ranks[0]["header"], {}, 3.0, "BF16")
+    assert doc["exit_code"] == 0, doc["summary"]
+    assert doc["summary"]["pass"] == len(set(ids0)) and doc["summary"]["missing"] == 0
+    # fp32 host math: TP=2 differs from one device by reassociation only
+    assert max(e["observed"] for e in doc["entries"]) < 1e-5
+
+
+def test_live_tp2_missing_allreduce_is_a_replica_mismatch_at_the_site(tmp_path):
+    ranks = run_tp(tmp_path, skip=("model.layers.1.attn",))
+    ref = _single_device()
+    cand = [f for r in ranks for f in r["records"]]
+    doc = O.check(_oracle_recs([_flat(r) for r in ref.records]), _oracle_recs(cand),
+                  ref.header(), ranks[0]["header"], {}, 3.0, "BF16")
+    assert doc["earliest_divergence"] == BUG_SITE
+    entry = next(e for e in doc["entries"] if e["id"] == BUG_SITE)
+    assert entry["verdict"] == "replica-mismatch"
+    assert entry["observed"] >= 10 * O.eps_of("BF16")
+    assert doc["exit_code"] == 3
+    # everything the bug cannot reach stays clean
+    before = [e for e in doc["entries"] if "layers.0" in e["id"] and "ActivationOut" in e["id"]]
+    assert before and all(e["verdict"] == "pass" for e in before)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("skip", [(), ("model.layers.1.attn",)], ids=["clean", "missing_allreduce"])
+def test_live_tp2_on_gpu_feeds_check_and_check_distributed(tmp_path, skip):
+    """Two gloo ranks on cuda:0 run the bf16 TP model; their device-resident
+    captures go to check() (union) here and to check_distributed() inside the
+    job (each rank its own records); both reports equal the oracle's."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+
+    import paper_2506_09280_b200 as td
+    from paper_2506_09280_b200.tracestore import RankMeta, Trace, TraceRecord
+    from paper_2506_09280_b200.canonical import ShardMapping, SliceBox, parse_canonical
+    shape = {"layers": 2, "d": 256, "heads": 8, "ff": 1024, "seq": 128, "vocab": 512}
+    ranks = run_tp(tmp_path, shape=shape, device="cuda", dtype="bfloat16", skip=skip, mode="distributed")
+    ref_h = _single_device(shape, "cuda", torch.bfloat16, "bfloat16")
+    cand = Trace(header=ranks[0]["header"])
+    for f in (f for r in ranks for f in r["records"]):
+        pairs = tuple((SliceBox(tuple(map(tuple, l))), SliceBox(tuple(map(tuple, g)))) for l, g in f["pairs"])
+        payload = torch.from_numpy(f["payload"]).to("cuda", torch.bfloat16)
+        cand.records.append(TraceRecord(parse_canonical(f["ident"]), RankMeta(*f["rank"]),
+                                        ShardMapping(tuple(f["local"]), tuple(f["global"]), pairs),
+                                        f["replica"], payload, f["cls"]))
+    tol = td.ToleranceMap({}, n_samples=1, eps_p=td.FloatFormat.BF16.eps)
+    rep = td.check(ref_h.trace(), cand, tol, fmt=td.FloatFormat.BF16)
+    got = json.loads(td.render_report(rep, "json"))
+    want = O.check(_oracle_recs([_flat(r) for r in ref_h.records]),
+                   _oracle_recs([f for r in ranks for f in r["records"]]),
+                   ref_h.header(), ranks[0]["header"], {}, 3.0, "BF16")
+    assert got["summary"] == want["summary"] and got["exit_code"] == want["exit_code"]
+    assert got["earliest_divergence"] == want["earliest_divergence"]
+    for g, w in zip(got["entries"], want["entries"]):
+        assert (g["id"], g["verdict"]) == (w["id"], w["verdict"])
+        if isinstance(w["observed"], float):
+            assert abs(g["observed"] - w["observed"]) <= 1e-12 * max(abs(w["observed"]), 1e-300)
+    for r in ranks:
+        dist_doc = json.loads(r["report"])
+        assert dist_doc["summary"] == want["summary"]
+        assert [(e["id"], e["verdict"]) for e in dist_doc["entries"]] == \
+            [(e["id"], e["verdict"]) for e in want["entries"]]
+    if skip:
+        assert want["earliest_divergence"] == BUG_SITE and want["exit_code"] == 3
+    else:
+        assert want["exit_code"] == 0 and want["summary"]["missing"] == 0
