@@ -37,11 +37,26 @@ def _format_of(trace):
     return POLICIES[precision].storage
 
 
+def _hbm_fits(paths) -> bool:
+    """Reading a file to HBM holds its image and its unpacked payload arena
+    (about the file size each) until the unpack ends; the first trace's
+    arena stays while the second is read.  Peak ~ sum(sizes) + max(size)."""
+    import torch
+    if not torch.cuda.is_available():
+        return False
+    sizes = [p.stat().st_size for p in paths]
+    free, _ = torch.cuda.mem_get_info()
+    return sum(sizes) + max(sizes) + (256 << 20) <= free
+
+
 def _cmd_check(args) -> int:
     from .tracestore import read_trace
-    device = None if args.host else "cuda"
-    ref = read_trace(_resolve(args.ref), device=device)
-    cand = read_trace(_resolve(args.cand), device=device)
+    paths = [_resolve(args.ref), _resolve(args.cand)]
+    # device reads unless asked otherwise or the traces would not fit in HBM
+    # (then the host path: payloads are staged to the device by check())
+    device = None if args.host or not _hbm_fits(paths) else "cuda"
+    ref = read_trace(paths[0], device=device)
+    cand = read_trace(paths[1], device=device)
     try:
         blob = _resolve(args.tol).read_bytes()
     except OSError as exc:
@@ -69,7 +84,9 @@ def _parser() -> argparse.ArgumentParser:
     chk.add_argument("--tol", required=True)
     chk.add_argument("--k", type=float, default=3.0)
     chk.add_argument("--host", action="store_true",
-                     help="read payloads to host memory first (they are uploaded during check)")
+                     help="read payloads to host memory first (they are uploaded during check); "
+                          "the default reads them straight to HBM when both traces fit there "
+                          "(peak ~ ref + cand + the larger file), else falls back to this")
     view = chk.add_mutually_exclusive_group()
     view.add_argument("--json", action="store_true")
     view.add_argument("--text", action="store_true")

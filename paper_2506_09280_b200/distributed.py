@@ -36,12 +36,17 @@ included — is testable where only one GPU exists.
 
 from __future__ import annotations
 
+import os
 import threading
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _native as N
+
+# TD_SERIAL_FP=1: td_fingerprint runs on the check's stream before td_segnorm
+# instead of beside it on a side stream (A/B of the overlap)
+_SERIAL_FP = os.environ.get("TD_SERIAL_FP", "0") == "1"
 
 
 # ---------------------------------------------------------------------------
@@ -240,6 +245,7 @@ class RecordMeta:
     owner: int
     order: tuple
     record: object = None        # the local TraceRecord (None on other ranks)
+    exec_key: tuple | None = None  # layout.execution_key (default ordering only)
 
     def __getstate__(self):
         state = dict(self.__dict__)
@@ -265,18 +271,25 @@ class _MetaTrace:
 
 
 def _metas(trace, rank: int, order_key) -> list:
+    from .layout import execution_key
     out = []
     for pos, rec in enumerate(trace.records):
         key = order_key(rec, pos) if order_key is not None else (rank, pos)
+        ek = execution_key(rec.id, rec.rank_meta) if order_key is None else None
         out.append(RecordMeta(rec.id, rec.rank_meta, rec.mapping, rec.replica_group_size,
                               tuple(rec.shape), rec.dtype_code, rec.module_class, rank,
-                              tuple(key) if isinstance(key, (tuple, list)) else (key,), rec))
+                              tuple(key) if isinstance(key, (tuple, list)) else (key,), rec, ek))
     return out
 
 
 def global_trace(trace, comm: Comm, order_key=None) -> _MetaTrace:
-    """Every rank's record metadata, merged in global execution order
-    (order_key(record, local position); default: rank-major)."""
+    """Every rank's record metadata, merged in global execution order.
+
+    order_key(record, local position) gives the order explicitly.  By
+    default, when every record on every rank names a module or parameter of
+    the reference model, the order is the reference schedule's
+    (layout.execution_key: single-process execution order even when PP
+    stages or CP ranks hold disjoint ids); otherwise it is rank-major."""
     mine = _metas(trace, comm.rank, order_key)
     gathered = comm.all_gather_object(mine)
     allrecs = []
@@ -285,7 +298,10 @@ def global_trace(trace, comm: Comm, order_key=None) -> _MetaTrace:
             allrecs.extend(mine)          # keep the local payload links
         else:
             allrecs.extend(metas)
-    allrecs.sort(key=lambda m: m.order)
+    if order_key is None and all(m.exec_key is not None for m in allrecs):
+        allrecs.sort(key=lambda m: (m.exec_key, m.order))
+    else:
+        allrecs.sort(key=lambda m: m.order)
     return _MetaTrace(trace.header, allrecs)
 
 
@@ -563,11 +579,13 @@ class BoundCheck:
         with torch.cuda.stream(prep.stream):
             if self.dcp.n_fused:
                 self.table[:self.dcp.n_fused].zero_()
-        if self.fps.n:
+        if self.fps.n and _SERIAL_FP:
+            self.fps.run(prep.stream)
+        elif self.fps.n:
             self.side.wait_stream(prep.stream)
             self.fps.run(self.side)
         prep.segnorm(sh)
-        if self.fps.n:
+        if self.fps.n and not _SERIAL_FP:
             prep.stream.wait_stream(self.side)
 
     def exchange(self, sh) -> None:

@@ -355,3 +355,82 @@ LLAMA3_1B = ModelShape(layers=16, d_model=2048, n_heads=32, d_ff=8192, seq_len=8
                        n_kv_heads=8, gated_mlp=True, norm_bias=False, position_table=False)
 LLAMA3_8B = ModelShape(layers=32, d_model=4096, n_heads=32, d_ff=14336, seq_len=8192, vocab=128256,
                        n_kv_heads=8, gated_mlp=True, norm_bias=False, position_table=False)
+
+
+# -- execution order of a trace split across ranks ------------------------------
+
+_PARAM_SLOTS = {"attn.norm.weight": 0, "attn.norm.bias": 1, "attn.wq": 2, "attn.wk": 3, "attn.wv": 4,
+                "attn.wo": 5, "mlp.norm.weight": 6, "mlp.norm.bias": 7, "mlp.w1": 8, "mlp.w3": 9,
+                "mlp.w2": 10}
+_BIG = 1 << 40
+
+
+def _module_index(module: str):
+    """Forward position of a traced module: embedding, then per layer attn
+    and mlp, then final_norm and lm_head (engine.py:971-975)."""
+    if module == "model.embedding":
+        return 0
+    if module == "model.final_norm":
+        return _BIG
+    if module == "model.lm_head":
+        return _BIG + 1
+    parts = module.split(".")
+    if len(parts) == 4 and parts[0] == "model" and parts[1] == "layers" and parts[2].isdigit() \
+            and parts[3] in ("attn", "mlp"):
+        return 1 + 2 * int(parts[2]) + (parts[3] == "mlp")
+    return None
+
+
+def _param_index(path: str):
+    """Registration position of a parameter path (param_shapes order)."""
+    if path == "model.embedding.word":
+        return (0, 0, 0)
+    if path == "model.embedding.position":
+        return (0, 0, 1)
+    if path == "model.final_norm.weight":
+        return (2, 0, 0)
+    if path == "model.final_norm.bias":
+        return (2, 0, 1)
+    parts = path.split(".", 3)
+    if len(parts) == 4 and parts[0] == "model" and parts[1] == "layers" and parts[2].isdigit():
+        slot = _PARAM_SLOTS.get(parts[3])
+        if slot is not None:
+            return (1, int(parts[2]), slot)
+    return None
+
+
+_FWD = {"ActivationIn": 0, "ActivationOut": 1}
+_BWD = {"ActivationGradOut": 0, "ActivationGradIn": 1}
+
+
+def execution_key(ident, rank_meta):
+    """Sort key that puts the records of a trace split across ranks (PP
+    stages, CP/DP/TP ranks) back into the single-process execution order of
+    the reference schedule (Emulator.run_iteration, engine.py:966-979; the
+    order Layout.records emits): Param of the iteration, then per microbatch
+    its forward (modules in order, ActivationIn before ActivationOut), its
+    backward (modules reversed, GradOut before GradIn) and its ParamGrads
+    (registration order), then MainGrad, then the next iteration's Param;
+    copies of one id in (dp, cp, tp) rank order.  The order of first
+    occurrences is the report order (checker.py:205-206) and the order
+    within an id picks each replica group's copy 0 (checker.py:184-191).
+    None when the id is not one of the reference model's modules or
+    parameters (then the caller keeps rank-major order)."""
+    kind, module = ident.kind.value, ident.module_name
+    rank = (rank_meta.dp, rank_meta.cp, rank_meta.tp)
+    if kind in ("Param", "MainGrad"):
+        p = _param_index(module)
+        if p is None:
+            return None
+        return (ident.iteration, 0 if kind == "Param" else 2, 0, 0, p, rank)
+    if kind == "ParamGrad":
+        p = _param_index(module)
+        return None if p is None else (ident.iteration, 1, ident.microbatch, 2, p, rank)
+    m = _module_index(module)
+    if m is None:
+        return None
+    if kind in _FWD:
+        return (ident.iteration, 1, ident.microbatch, 0, (m, _FWD[kind]), rank)
+    if kind in _BWD:
+        return (ident.iteration, 1, ident.microbatch, 1, (-m, _BWD[kind]), rank)
+    return None

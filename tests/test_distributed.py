@@ -152,6 +152,98 @@ def test_distributed_check_threads_match_reference(world, cases, golden_trace_by
             assert_reports_match(rep, want, f"{name} world={world}")
 
 
+def _stage_owner(rec, world):
+    """PP stage / CP rank placement: ranks hold disjoint ids (pp) or disjoint rows (cp)."""
+    return (2 * rec.rank_meta.pp + rec.rank_meta.cp) % world
+
+
+def _global_order_threads(trace, world, owner):
+    hub = ThreadComm.hub(world)
+    out, errors = [None] * world, []
+
+    def worker(rank):
+        try:
+            out[rank] = global_trace(_local(trace, rank, world, lambda r: owner(r, world)), ThreadComm(hub, rank))
+        except Exception as exc:  # pragma: no cover
+            errors.append(repr(exc))
+            hub.barrier.abort()
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=120)
+    assert not errors, errors
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_global_trace_default_order_is_single_trace_execution_order(world, cases, golden_trace_bytes):
+    """With no order_key, a trace split by PP stage / CP rank (or by the
+    TP/DP owner rule) merges back into the single-process execution order:
+    the same first-occurrence id order (report order) and the same copy
+    order within every id (copy 0 of each replica group) as the reference
+    emulator's one trace (engine.py:966-979)."""
+    names = sorted({c["cand"] for c in cases["checks"]} | {c["ref"] for c in cases["checks"]})
+    assert "bf16_clean_dp2_cp2_pp2" in names
+    for name in names:
+        trace = trace_from_bytes(golden_trace_bytes(name))
+        want_ids = list(dict.fromkeys(r.id.encode() for r in trace.records))
+        want_within = {}
+        for r in trace.records:
+            want_within.setdefault(r.id.encode(), []).append(r.rank_meta.as_tuple())
+        for owner in (_stage_owner, _owner):
+            for g in _global_order_threads(trace, world, owner):
+                got_ids = list(dict.fromkeys(m.id.encode() for m in g.records))
+                assert got_ids == want_ids, (name, owner.__name__)
+                got_within = {}
+                for m in g.records:
+                    got_within.setdefault(m.id.encode(), []).append(m.rank_meta.as_tuple())
+                assert got_within == want_within, (name, owner.__name__)
+
+
+@pytest.mark.gpu
+def test_pp_cp_split_check_default_order_matches_reference(cases, golden_trace_bytes):
+    """The dp2*cp2*pp2 golden candidate split by PP stage and CP rank over 4
+    logical ranks, no order_key: every rank's report (earliest_flag and
+    earliest_divergence included) equals the reference's — also with an
+    injected bug whose site sits on the second PP stage."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_09280_b200 as td
+    from tests.test_gpu_parity import assert_reports_match  # noqa: E402
+    world = 4
+    for name in ("clean_dp2_cp2_pp2_k3", "bug_stale_input_k3", "bug_tp_row_allreduce_k3"):
+        case = next(c for c in cases["checks"] if c["name"] == name)
+        ref = trace_from_bytes(golden_trace_bytes(case["ref"]), device="cuda")
+        cand = trace_from_bytes(golden_trace_bytes(case["cand"]), device="cuda")
+        tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+        hub = ThreadComm.hub(world)
+        reports, errors = [None] * world, []
+
+        def worker(rank):
+            try:
+                comm = ThreadComm(hub, rank)
+                cand_local = _local(cand, rank, world, lambda r: _stage_owner(r, world))
+                refs = split_reference(ref, global_trace(cand_local, comm), world)
+                plan = DistributedCheckPlan(refs[rank], cand_local, tol, case["kappa"],
+                                            fmt=td.FloatFormat(case["fmt"]), comm=comm)
+                reports[rank] = json.loads(td.render_report(plan.run(), "json"))
+            except Exception as exc:  # pragma: no cover - surfaced below
+                errors.append(repr(exc))
+                hub.barrier.abort()
+        threads = [threading.Thread(target=worker, args=(r,)) for r in range(world)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join(timeout=600)
+        assert not errors, (name, errors)
+        want = json.loads(case["report"])
+        for rep in reports:
+            assert_reports_match(rep, want, f"{name} pp/cp split")
+            assert rep["earliest_flag"] == want["earliest_flag"]
+            assert rep["earliest_divergence"] == want["earliest_divergence"]
+
+
 def _nccl_world1(q):
     try:
         import paper_2506_09280_b200 as td

@@ -63,14 +63,15 @@ def _tp_worker(rank, world, port, out_dir, shape, device, dtype_name, skip, mode
         result = {"records": [_flat(r) for r in h.records], "header": h.header()}
         if mode == "distributed":
             import paper_2506_09280_b200 as td
-            from paper_2506_09280_b200.distributed import TorchComm, global_trace, split_reference
+            from paper_2506_09280_b200.distributed import (TorchComm, check_distributed, global_trace,
+                                                           split_reference)
             ref_h = tp_gpt.traced_step(shape, tp_gpt.TPGroup(), device=device,
                                        dtype=getattr(torch, dtype_name), precision=dtype_name)
             comm = TorchComm()
             cand = h.trace()
             refs = split_reference(ref_h.trace(), global_trace(cand, comm), world)
             tol = td.ToleranceMap({}, n_samples=1, eps_p=td.FloatFormat.BF16.eps)
-            rep = td.check_distributed(refs[rank], cand, tol, fmt=td.FloatFormat.BF16, comm=comm)
+            rep = check_distributed(refs[rank], cand, tol, fmt=td.FloatFormat.BF16, comm=comm)
             result["report"] = td.render_report(rep, "json")
         with open(os.path.join(out_dir, f"rank{rank}.pkl"), "wb") as fh:
             pickle.dump(result, fh)
