@@ -18,6 +18,8 @@ import math
 from dataclasses import dataclass, field
 from typing import Callable
 
+import numpy as np
+
 from . import _native as N
 from .device import resolve_operands
 from .errors import (ConfigInvalid, DigestMismatch, FormatError, ShapeMismatch,
@@ -555,10 +557,28 @@ def check_streaming(ref: Trace, run: Callable, tol: ToleranceMap, kappa: float =
             N.call("td_rel_err", x.data_ptr(), y.data_ptr(), N.dtype_code(x), x.numel(),
                    work.data_ptr(), sums[index[ident]].data_ptr(), N.stream_handle())
         else:                                           # mixed dtypes: widening path, synchronous
-            direct[ident] = pair_sums(x.double(), y.double())[2]
+            d2, a2, _ = pair_sums(x.double(), y.double())
+            sums[index[ident], 0], sums[index[ident], 1] = d2, a2
     run(sink)
-    rel = sums[:, 2].tolist()
+    # verdicts in the batched verdict kernel, as check()'s (td_verdict:
+    # precedence, threshold kappa * max(tol, eps), NaN passes, near ties)
     eps = fmt.eps
+    n = len(base)
+    desc = np.zeros(max(n, 1), dtype=N.ID_DESC)
+    seen = set(order)
+    for ident, k in index.items():
+        desc[k]["tolerance"] = tol.get(ident)
+        desc[k]["has_compare"] = int(ident in seen and ident not in shapes)
+        desc[k]["cand_host"] = N.MERGE if ident in shapes else 0
+    res = np.zeros(max(n, 1), dtype=N.ID_RESULT)
+    if n:
+        dev_desc = torch.from_numpy(desc.view(np.uint8)).to("cuda")
+        id_sums = sums[:, :2].contiguous()
+        dev_res = torch.zeros(res.nbytes, dtype=torch.uint8, device="cuda")
+        dev_ties = torch.zeros(1, dtype=torch.int64, device="cuda")
+        N.call("td_verdict", dev_desc.data_ptr(), n, 0, 0, id_sums.data_ptr(), 0, float(kappa), float(eps),
+               float(eps), dev_res.data_ptr(), 0, dev_ties.data_ptr(), N.stream_handle())
+        res = dev_res.cpu().numpy().view(N.ID_RESULT)
     entries, ties = [], 0
     for ident in order:
         tolerance = tol.get(ident)
@@ -567,16 +587,16 @@ def check_streaming(ref: Trace, run: Callable, tol: ToleranceMap, kappa: float =
         if entry is None:
             entries.append(CheckEntry(ident, VERDICT_MISSING, None, tolerance, threshold,
                                       "only in candidate trace"))
-        elif ident in shapes:
-            entries.append(CheckEntry(ident, VERDICT_MERGE, None, tolerance, threshold,
+            continue
+        row = res[index[ident]]
+        if ident in shapes:
+            entries.append(CheckEntry(ident, _NAME[int(row["verdict"])], None, tolerance, float(row["threshold"]),
                                       f"merged shapes differ: reference {tuple(entry[0].mapping.global_shape)} "
                                       f"vs candidate {shapes[ident]}"))
         else:
-            observed = direct.get(ident, rel[index[ident]])
-            verdict = VERDICT_FLAG if observed > threshold else VERDICT_PASS   # NaN -> pass
-            ties += abs(observed - threshold) <= 1e-12 * threshold
-            entries.append(CheckEntry(ident, verdict, observed, tolerance, threshold, ""))
-    seen = set(order)
+            ties += int(row["near_tie"])
+            entries.append(CheckEntry(ident, _NAME[int(row["verdict"])], float(row["observed"]), tolerance,
+                                      float(row["threshold"]), ""))
     for ident in base:
         if ident not in seen:
             tolerance = tol.get(ident)

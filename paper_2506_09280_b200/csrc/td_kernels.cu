@@ -121,16 +121,20 @@ constexpr uint64_t MIX2 = 0x94D049BB133111EBull;
 
 // Replica digests: 8-byte word w_j (j = its word index in the record) with
 // position key k_j = (j+1)*gamma goes into lane j & 1 as
-//     h[j & 1] += (w_j ^ k_j) * M[j & 1]      (mod 2^64, M odd)
+//     z = (w_j ^ k_j) * M[j & 1],   h[j & 1] += z ^ (z >> 32)   (mod 2^64, M odd)
 // — for a fixed key a bijection of w_j, so a changed word always changes its
 // lane's sum; position-keyed (permuted shards differ); order-independent (any
 // reduction order, atomics included, gives the same bits).  One 64-bit
-// multiply per word.  (The first version folded every word into both lanes,
-// z = fold((w ^ k) * MIX1), h0 += z, h1 += hi32(z) * lo32(z): ~12
-// instructions per word against 7, and the compare pass that digests its
-// copy is instruction-issue bound.)
+// multiply per word.  The fold (one LOP3: hi ^= into lo) keeps the lane sum
+// from being M * sum(w ^ k), a plain additive checksum in which two equal and
+// opposite word changes (e.g. a swap of two values whose keys agree on the
+// differing bits) cancel exactly; with it such a pair collides only if 32
+// nonlinear low bits cancel too.  (The first version folded every word into
+// both lanes, h0 += z, h1 += hi32(z) * lo32(z): ~12 instructions per word
+// against 8, and the compare pass that digests its copy is issue bound.)
 __device__ __forceinline__ void fp_key_word(uint64_t w, uint64_t key, uint64_t& h, uint64_t mult) {
-    h += (w ^ key) * mult;
+    const uint64_t z = (w ^ key) * mult;
+    h += z ^ (z >> 32);
 }
 
 __device__ __forceinline__ void fp_word(uint64_t w, uint64_t j, uint64_t& h0, uint64_t& h1) {
@@ -486,11 +490,11 @@ typedef void (*segnorm_fn)(const td_segment*, const int64_t*, int64_t, double*, 
 #define TD_BULK_CH 1024             // units (16 B of each operand) per stage
 #endif
 #ifndef TD_BULK_STAGES
-#define TD_BULK_STAGES 6
+#define TD_BULK_STAGES 3
 #endif
 #ifndef TD_BULK_MINB
-#define TD_BULK_MINB 1              // CTAs per SM
-#endif
+#define TD_BULK_MINB 2              // CTAs per SM (16 consumer warps per SM; ncu, config-4
+#endif                              // share: 4.58 ms vs 5.61 ms at 1 CTA x 6 stages)
 constexpr int BULK_THREADS = BLOCK + 32;
 constexpr uint32_t BULK_OPB = TD_BULK_CH * 16;   // bytes per operand per stage
 constexpr size_t BULK_SMEM = (size_t)TD_BULK_STAGES * 2 * BULK_OPB + 2 * TD_BULK_STAGES * sizeof(uint64_t);

@@ -298,11 +298,28 @@ def global_trace(trace, comm: Comm, order_key=None) -> _MetaTrace:
             allrecs.extend(mine)          # keep the local payload links
         else:
             allrecs.extend(metas)
-    if order_key is None and all(m.exec_key is not None for m in allrecs):
-        allrecs.sort(key=lambda m: (m.exec_key, m.order))
-    else:
-        allrecs.sort(key=lambda m: m.order)
+    sort_metas(allrecs)
     return _MetaTrace(trace.header, allrecs)
+
+
+def execution_sorted(records) -> list:
+    """Records of several ranks' traces (concatenated rank by rank) in the
+    order global_trace() gives them: the single-process trace they split."""
+    from .layout import execution_key
+    records = list(records)
+    keys = [execution_key(r.id, r.rank_meta) for r in records]
+    if any(k is None for k in keys):
+        return records
+    return [records[i] for i in sorted(range(len(records)), key=lambda i: (keys[i], i))]
+
+
+def sort_metas(metas: list) -> None:
+    """Global execution order of gathered record metadata, in place: the
+    reference schedule (exec_key) when every record has one, else `order`."""
+    if metas and all(m.exec_key is not None for m in metas):
+        metas.sort(key=lambda m: (m.exec_key, m.order))
+    else:
+        metas.sort(key=lambda m: m.order)
 
 
 # ---------------------------------------------------------------------------

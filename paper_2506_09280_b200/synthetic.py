@@ -158,7 +158,8 @@ class ShareLayout:
     def __init__(self, model: ModelShape, pcfg: ParallelConfig, world: int, owner=None,
                  dtype_code: int = 1):
         from .canonical import ShardMapping, SliceBox
-        from .distributed import RecordMeta, _MetaTrace
+        from .distributed import RecordMeta, _MetaTrace, sort_metas
+        from .layout import execution_key
         from .plan import compare_copies, merge_view
         self.model, self.pcfg, self.world = model, pcfg, world
         self.owner = owner or (lambda s: (s.rank[0] * pcfg.tp + s.rank[1] + pcfg.tp * pcfg.dp * s.rank[4]) % world)
@@ -174,10 +175,11 @@ class ShareLayout:
             o = self.owner(spec)
             pos = len(self.cand[o])
             self.cand[o].append((spec.ident, spec))
-            metas.append(RecordMeta(parse_canonical(spec.ident), RankMeta(*spec.rank), spec.mapping,
-                                    spec.replica, tuple(spec.mapping.local_shape), dtype_code,
-                                    spec.module_class, o, (o, pos)))
-        metas.sort(key=lambda m: m.order)
+            ident, rank = parse_canonical(spec.ident), RankMeta(*spec.rank)
+            metas.append(RecordMeta(ident, rank, spec.mapping, spec.replica, tuple(spec.mapping.local_shape),
+                                    dtype_code, spec.module_class, o, (o, pos), None,
+                                    execution_key(ident, rank)))
+        sort_metas(metas)            # the order global_trace() gives the live job
         view = merge_view(_MetaTrace({}, metas))
         choice = compare_copies(view, lambda m: m.owner)
         # reference slices: for every compared group, its global boxes on the
@@ -203,11 +205,15 @@ class ShareLayout:
         """(reference metas per rank, candidate metas per rank): what each
         rank's global_trace() publishes, in its local record order."""
         from .distributed import RecordMeta
-        ref = [[RecordMeta(parse_canonical(i), RankMeta(0, k, 0, 0, 0, 0), m, 1, tuple(m.local_shape),
-                           dtype_code, mc, r, (r, pos)) for pos, (i, k, m, mc) in enumerate(self.ref[r])]
+        from .layout import execution_key
+
+        def meta(i, rank, m, rep, mc, r, pos):
+            ident = parse_canonical(i)
+            return RecordMeta(ident, rank, m, rep, tuple(m.local_shape), dtype_code, mc, r, (r, pos), None,
+                              execution_key(ident, rank))
+        ref = [[meta(i, RankMeta(0, k, 0, 0, 0, 0), m, 1, mc, r, pos) for pos, (i, k, m, mc) in enumerate(self.ref[r])]
                for r in range(self.world)]
-        cand = [[RecordMeta(parse_canonical(i), RankMeta(*s.rank), s.mapping, s.replica,
-                            tuple(s.mapping.local_shape), dtype_code, s.module_class, r, (r, pos))
+        cand = [[meta(i, RankMeta(*s.rank), s.mapping, s.replica, s.module_class, r, pos)
                  for pos, (i, s) in enumerate(self.cand[r])] for r in range(self.world)]
         return ref, cand
 

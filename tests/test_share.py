@@ -91,10 +91,13 @@ def _run_threads(world, body):
 
 
 def _union(shares, header):
+    """The single-process traces the shares split (global execution order)."""
+    from paper_2506_09280_b200.distributed import execution_sorted
     ref, cand = Trace(header=dict(header)), Trace(header=dict(header))
     for r, c in shares:
         ref.records.extend(r.records)
         cand.records.extend(c.records)
+    ref.records, cand.records = execution_sorted(ref.records), execution_sorted(cand.records)
     return ref, cand
 
 
@@ -214,16 +217,19 @@ def test_fuzzed_shares_match_single_gpu_check():
 
 
 def _digest_numpy(data: bytes):
-    """CPU restatement of the td_fingerprint digest (td_kernels.cu, fp_word):
+    """CPU restatement of the td_fingerprint digest (td_kernels.cu, fp_key_word):
     8-byte little-endian words w_j (tail zero-padded), lane j % 2:
-    h[j % 2] = sum (w_j ^ (j+1)*gamma) * M[j % 2] mod 2^64, M = (MIX1, MIX2)."""
+    z_j = (w_j ^ (j+1)*gamma) * M[j % 2], h[j % 2] = sum z_j ^ (z_j >> 32)
+    mod 2^64, M = (MIX1, MIX2)."""
     pad = (-len(data)) % 8
     w = np.frombuffer(data + b"\0" * pad, dtype="<u8")
     with np.errstate(over="ignore"):
         j = np.arange(1, len(w) + 1, dtype=np.uint64)
         z = w ^ (j * np.uint64(0x9E3779B97F4A7C15))
-        h0 = np.sum(z[0::2] * np.uint64(0xBF58476D1CE4E5B9), dtype=np.uint64)
-        h1 = np.sum(z[1::2] * np.uint64(0x94D049BB133111EB), dtype=np.uint64)
+        z0 = z[0::2] * np.uint64(0xBF58476D1CE4E5B9)
+        z1 = z[1::2] * np.uint64(0x94D049BB133111EB)
+        h0 = np.sum(z0 ^ (z0 >> np.uint64(32)), dtype=np.uint64)
+        h1 = np.sum(z1 ^ (z1 >> np.uint64(32)), dtype=np.uint64)
     return int(h0), int(h1)
 
 
@@ -245,6 +251,39 @@ def test_fingerprint_matches_numpy_restatement():
     got = fingerprints(views).cpu().numpy().view(np.uint64)
     for g, w in zip(got, want):
         assert (int(g[0]), int(g[1])) == w
+    # an equal-and-opposite change of two same-lane words (one bit set in
+    # word 0 and cleared in word 2, where their position keys agree): a
+    # plain sum of (w ^ k) * M cannot tell the copies apart, the folded
+    # digest must
+    a, b = _same_lane_swap_pair()
+    da, db = fingerprints([torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()]).cpu().numpy().view(np.uint64)
+    assert tuple(da) != tuple(db)
+
+
+def _same_lane_swap_pair():
+    gamma = 0x9E3779B97F4A7C15
+    k0, k2 = gamma, (3 * gamma) & ((1 << 64) - 1)
+    bit = next(i for i in range(64) if ((k0 ^ k2) >> i) & 1 == 0)
+    words = np.random.default_rng(5).integers(0, 1 << 62, 8, dtype=np.uint64)
+    a, b = words.copy(), words.copy()
+    m = np.uint64(1 << bit)
+    a[0], a[2] = a[0] | m, a[2] & ~m
+    b[0], b[2] = b[0] & ~m, b[2] | m
+    return a.view(np.uint8), b.view(np.uint8)
+
+
+def test_digest_restatement_separates_a_same_lane_swap():
+    """The additive-checksum weakness the fold removes (td_kernels.cu,
+    fp_key_word), shown on the numpy restatement."""
+    a, b = _same_lane_swap_pair()
+    with np.errstate(over="ignore"):
+        def linear(x):
+            w = x.view(np.uint64)
+            j = np.arange(1, len(w) + 1, dtype=np.uint64)
+            return int(np.sum((w ^ (j * np.uint64(0x9E3779B97F4A7C15)))[0::2] * np.uint64(0xBF58476D1CE4E5B9),
+                              dtype=np.uint64))
+        assert linear(a) == linear(b)
+    assert _digest_numpy(a.tobytes()) != _digest_numpy(b.tobytes())
 
 
 # config 4's layout (Llama-3-8B rules: L=32, GQA 32/8, SwiGLU w3, RMSNorm, no

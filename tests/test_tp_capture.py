@@ -34,6 +34,8 @@ from paper_2506_09280_b200.torchtap import TapError
 from . import tp_gpt
 
 SHAPE = {"layers": 2, "d": 32, "heads": 4, "ff": 64, "seq": 16, "vocab": 64}
+# Llama-3 block rules (GQA 8/2, SwiGLU w3, RMSNorm, no position table)
+LLAMA = {"layers": 2, "d": 64, "heads": 8, "kv_heads": 2, "ff": 96, "seq": 16, "vocab": 64, "llama": True}
 BUG_SITE = "iter=0|mb=0|kind=ActivationOut|mod=model.layers.1.attn"
 
 
@@ -47,7 +49,7 @@ def _flat(rec) -> dict:
     m = rec.mapping
     return {"ident": rec.ident, "rank": tuple(rec.rank), "local": m.local_shape, "global": m.global_shape,
             "pairs": [(l.bounds, g.bounds) for l, g in m.pairs], "replica": rec.replica,
-            "payload": rec.host(), "cls": rec.module_class}
+            "payload": rec.host(), "cls": rec.module_class, "dtype": str(rec.payload.dtype).split(".")[-1]}
 
 
 def _tp_worker(rank, world, port, out_dir, shape, device, dtype_name, skip, mode):
@@ -121,9 +123,10 @@ def test_layout_shard_maps_are_the_layouts():
         torchtap.layout_shard(layout, tp=2)
 
 
-def test_live_tp2_capture_matches_single_device(tmp_path):
-    ranks = run_tp(tmp_path)
-    ref = _single_device()
+@pytest.mark.parametrize("shape", [SHAPE, LLAMA], ids=["gpt", "llama"])
+def test_live_tp2_capture_matches_single_device(tmp_path, shape):
+    ranks = run_tp(tmp_path, shape=shape)
+    ref = _single_device(shape)
     cand = [f for r in ranks for f in r["records"]]
     # every capture carries its rank's map; copies of one id agree on the id set
     assert {f["rank"][1] for f in cand} == {0, 1}
@@ -136,11 +139,19 @@ def test_live_tp2_capture_matches_single_device(tmp_path):
     assert doc["summary"]["pass"] == len(set(ids0)) and doc["summary"]["missing"] == 0
     # fp32 host math: TP=2 differs from one device by reassociation only
     assert max(e["observed"] for e in doc["entries"]) < 1e-5
+    # the layout's own id set for this model (layout.emit_records) covers
+    # every capture of the tapped kinds
+    kinds = ("ActivationIn", "ActivationOut", "ParamGrad")
+    want = {sp.ident for sp in Layout(tp_gpt.model_shape(shape), ParallelConfig(tp=2)).records()
+            if sp.kind in kinds}
+    got = {i for i in ids0 if not i.endswith(".norm")}
+    assert got == want
 
 
-def test_live_tp2_missing_allreduce_is_a_replica_mismatch_at_the_site(tmp_path):
-    ranks = run_tp(tmp_path, skip=("model.layers.1.attn",))
-    ref = _single_device()
+@pytest.mark.parametrize("shape", [SHAPE, LLAMA], ids=["gpt", "llama"])
+def test_live_tp2_missing_allreduce_is_a_replica_mismatch_at_the_site(tmp_path, shape):
+    ranks = run_tp(tmp_path, shape=shape, skip=("model.layers.1.attn",))
+    ref = _single_device(shape)
     cand = [f for r in ranks for f in r["records"]]
     doc = O.check(_oracle_recs([_flat(r) for r in ref.records]), _oracle_recs(cand),
                   ref.header(), ranks[0]["header"], {}, 3.0, "BF16")
@@ -154,9 +165,14 @@ def test_live_tp2_missing_allreduce_is_a_replica_mismatch_at_the_site(tmp_path):
     assert before and all(e["verdict"] == "pass" for e in before)
 
 
+GPU_GPT = {"layers": 2, "d": 256, "heads": 8, "ff": 1024, "seq": 128, "vocab": 512}
+GPU_LLAMA = {"layers": 2, "d": 256, "heads": 8, "kv_heads": 2, "ff": 768, "seq": 128, "vocab": 512, "llama": True}
+
+
 @pytest.mark.gpu
+@pytest.mark.parametrize("shape", [GPU_GPT, GPU_LLAMA], ids=["gpt", "llama"])
 @pytest.mark.parametrize("skip", [(), ("model.layers.1.attn",)], ids=["clean", "missing_allreduce"])
-def test_live_tp2_on_gpu_feeds_check_and_check_distributed(tmp_path, skip):
+def test_live_tp2_on_gpu_feeds_check_and_check_distributed(tmp_path, skip, shape):
     """Two gloo ranks on cuda:0 run the bf16 TP model; their device-resident
     captures go to check() (union) here and to check_distributed() inside the
     job (each rank its own records); both reports equal the oracle's."""
@@ -167,13 +183,12 @@ def test_live_tp2_on_gpu_feeds_check_and_check_distributed(tmp_path, skip):
     import paper_2506_09280_b200 as td
     from paper_2506_09280_b200.tracestore import RankMeta, Trace, TraceRecord
     from paper_2506_09280_b200.canonical import ShardMapping, SliceBox, parse_canonical
-    shape = {"layers": 2, "d": 256, "heads": 8, "ff": 1024, "seq": 128, "vocab": 512}
     ranks = run_tp(tmp_path, shape=shape, device="cuda", dtype="bfloat16", skip=skip, mode="distributed")
     ref_h = _single_device(shape, "cuda", torch.bfloat16, "bfloat16")
     cand = Trace(header=ranks[0]["header"])
     for f in (f for r in ranks for f in r["records"]):
         pairs = tuple((SliceBox(tuple(map(tuple, l))), SliceBox(tuple(map(tuple, g)))) for l, g in f["pairs"])
-        payload = torch.from_numpy(f["payload"]).to("cuda", torch.bfloat16)
+        payload = torch.from_numpy(f["payload"]).to("cuda", getattr(torch, f["dtype"]))
         cand.records.append(TraceRecord(parse_canonical(f["ident"]), RankMeta(*f["rank"]),
                                         ShardMapping(tuple(f["local"]), tuple(f["global"]), pairs),
                                         f["replica"], payload, f["cls"]))

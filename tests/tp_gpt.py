@@ -22,6 +22,14 @@ column-parallel input gradients.
 `skip_reduce` names blocks whose row-parallel all-reduce is dropped — the
 reference's MC_TP_ROW_ALLREDUCE injection (engine.py:504-529): each rank
 then keeps its partial sum and the block output's replicas disagree.
+
+shape["llama"] = True switches to the Llama-3 block the B200 layout rules
+extend the reference to (layout.py: `gated_mlp`, `n_kv_heads`,
+`norm_bias=False`, `position_table=False`): RMSNorm without bias, GQA with
+shape["kv_heads"] key/value heads (column-parallel by KV head), rotary
+position (no table), SwiGLU MLP with a column-parallel `w3`.  A live run of
+it pins those emission rules: every capture must fit the shard map
+layout_shard assigns it, and the TP run must agree with one device.
 """
 
 from __future__ import annotations
@@ -76,17 +84,38 @@ def full_params(shape: dict, seed: int = 1234, std: float = 0.02) -> dict:
     model.param_specs (depth-scaled std on the residual output projections)."""
     gen = torch.Generator().manual_seed(seed)
     d, ff, L, V, S = shape["d"], shape["ff"], shape["layers"], shape["vocab"], shape["seq"]
+    llama = shape.get("llama", False)
+    kv = d // shape["heads"] * shape.get("kv_heads", shape["heads"])
     res_std = std / math.sqrt(2.0 * L)
-    out = {"model.embedding.word": torch.randn(V, d, generator=gen) * std,
-           "model.embedding.position": torch.randn(S, d, generator=gen) * std}
+    out = {"model.embedding.word": torch.randn(V, d, generator=gen) * std}
+    if not llama:
+        out["model.embedding.position"] = torch.randn(S, d, generator=gen) * std
     for i in range(L):
         a, m = f"model.layers.{i}.attn", f"model.layers.{i}.mlp"
-        for w in ("wq", "wk", "wv"):
-            out[f"{a}.{w}"] = torch.randn(d, d, generator=gen) * std
+        out[f"{a}.wq"] = torch.randn(d, d, generator=gen) * std
+        for w in ("wk", "wv"):
+            out[f"{a}.{w}"] = torch.randn(d, kv, generator=gen) * std
         out[f"{a}.wo"] = torch.randn(d, d, generator=gen) * res_std
         out[f"{m}.w1"] = torch.randn(d, ff, generator=gen) * std
+        if llama:
+            out[f"{m}.w3"] = torch.randn(d, ff, generator=gen) * std
         out[f"{m}.w2"] = torch.randn(ff, d, generator=gen) * res_std
     return out
+
+
+def _norm(d: int, llama: bool):
+    return torch.nn.RMSNorm(d, eps=1e-5) if llama else torch.nn.LayerNorm(d, eps=1e-5)
+
+
+def _rotary(x):
+    """Rotary position embedding of (heads, S, dh), half-split pairs."""
+    h, S, dh = x.shape
+    half = dh // 2
+    inv = 1.0 / (10000.0 ** (torch.arange(half, device=x.device, dtype=torch.float32) / half))
+    ang = torch.arange(S, device=x.device, dtype=torch.float32)[:, None] * inv[None, :]
+    cos, sin = ang.cos().to(x.dtype), ang.sin().to(x.dtype)
+    a, b = x[..., :half], x[..., half:]
+    return torch.cat([a * cos - b * sin, a * sin + b * cos], dim=-1)
 
 
 def _shard(w: torch.Tensor, axis: int, g: TPGroup) -> torch.Tensor:
@@ -99,23 +128,28 @@ class Embedding(torch.nn.Module):
         super().__init__()
         self.g = g
         self.word = torch.nn.Parameter(_shard(word, 0, g))
-        self.position = torch.nn.Parameter(position.clone())
+        if position is not None:
+            self.position = torch.nn.Parameter(position.clone())
+        else:
+            self.position = None
 
     def forward(self, ids):
         v = self.word.shape[0]
         local = ids - self.g.rank * v
         inside = (local >= 0) & (local < v)
         rows = F.embedding(local.clamp(0, v - 1), self.word) * inside[:, None].to(self.word.dtype)
-        return _ReduceFromTP.apply(rows, self.g) + self.position
+        out = _ReduceFromTP.apply(rows, self.g)
+        return out + self.position if self.position is not None else out
 
 
 class AttentionBlock(torch.nn.Module):
-    def __init__(self, name, P, n_heads, g: TPGroup, skip_reduce=False):
+    def __init__(self, name, P, n_heads, g: TPGroup, skip_reduce=False, llama=False):
         super().__init__()
         d = P[f"{name}.wq"].shape[0]
-        self.g, self.skip_reduce = g, skip_reduce
+        self.g, self.skip_reduce, self.llama = g, skip_reduce, llama
         self.heads, self.dh = n_heads // g.world, d // n_heads
-        self.norm = torch.nn.LayerNorm(d, eps=1e-5)
+        self.kv_heads = P[f"{name}.wk"].shape[1] // self.dh // g.world
+        self.norm = _norm(d, llama)
         for w in ("wq", "wk", "wv"):
             setattr(self, w, torch.nn.Parameter(_shard(P[f"{name}.{w}"], 1, g)))
         self.wo = torch.nn.Parameter(_shard(P[f"{name}.wo"], 0, g))
@@ -123,7 +157,13 @@ class AttentionBlock(torch.nn.Module):
     def forward(self, x):
         S = x.shape[0]
         a = _CopyToTP.apply(self.norm(x), self.g)
-        q, k, v = ((a @ w).view(S, self.heads, self.dh).transpose(0, 1) for w in (self.wq, self.wk, self.wv))
+        q = (a @ self.wq).view(S, self.heads, self.dh).transpose(0, 1)
+        k, v = ((a @ w).view(S, self.kv_heads, self.dh).transpose(0, 1) for w in (self.wk, self.wv))
+        if self.llama:
+            q, k = _rotary(q), _rotary(k)
+        if self.kv_heads != self.heads:         # GQA: each KV head serves heads/kv_heads queries
+            k = k.repeat_interleave(self.heads // self.kv_heads, dim=0)
+            v = v.repeat_interleave(self.heads // self.kv_heads, dim=0)
         o = F.scaled_dot_product_attention(q[None], k[None], v[None], is_causal=True)[0]
         y = o.transpose(0, 1).reshape(S, self.heads * self.dh) @ self.wo
         if not self.skip_reduce:
@@ -132,27 +172,33 @@ class AttentionBlock(torch.nn.Module):
 
 
 class MlpBlock(torch.nn.Module):
-    def __init__(self, name, P, g: TPGroup, skip_reduce=False):
+    def __init__(self, name, P, g: TPGroup, skip_reduce=False, llama=False):
         super().__init__()
         d = P[f"{name}.w1"].shape[0]
-        self.g, self.skip_reduce = g, skip_reduce
-        self.norm = torch.nn.LayerNorm(d, eps=1e-5)
+        self.g, self.skip_reduce, self.llama = g, skip_reduce, llama
+        self.norm = _norm(d, llama)
         self.w1 = torch.nn.Parameter(_shard(P[f"{name}.w1"], 1, g))
+        if llama:
+            self.w3 = torch.nn.Parameter(_shard(P[f"{name}.w3"], 1, g))
         self.w2 = torch.nn.Parameter(_shard(P[f"{name}.w2"], 0, g))
 
     def forward(self, x):
         a = _CopyToTP.apply(self.norm(x), self.g)
-        y = F.gelu(a @ self.w1, approximate="tanh") @ self.w2
+        if self.llama:
+            y = (F.silu(a @ self.w1) * (a @ self.w3)) @ self.w2
+        else:
+            y = F.gelu(a @ self.w1, approximate="tanh") @ self.w2
         if not self.skip_reduce:
             y = _ReduceFromTP.apply(y, self.g)
         return x + y
 
 
 class Layer(torch.nn.Module):
-    def __init__(self, i, P, n_heads, g, skip):
+    def __init__(self, i, P, n_heads, g, skip, llama=False):
         super().__init__()
-        self.attn = AttentionBlock(f"model.layers.{i}.attn", P, n_heads, g, f"model.layers.{i}.attn" in skip)
-        self.mlp = MlpBlock(f"model.layers.{i}.mlp", P, g, f"model.layers.{i}.mlp" in skip)
+        self.attn = AttentionBlock(f"model.layers.{i}.attn", P, n_heads, g, f"model.layers.{i}.attn" in skip,
+                                   llama)
+        self.mlp = MlpBlock(f"model.layers.{i}.mlp", P, g, f"model.layers.{i}.mlp" in skip, llama)
 
     def forward(self, x):
         return self.mlp(self.attn(x))
@@ -174,11 +220,12 @@ class TPGPT(torch.nn.Module):
     def __init__(self, shape: dict, g: TPGroup, params: dict | None = None, skip_reduce=()):
         super().__init__()
         P = params if params is not None else full_params(shape)
+        llama = shape.get("llama", False)
         self.g = g
-        self.embedding = Embedding(P["model.embedding.word"], P["model.embedding.position"], g)
-        self.layers = torch.nn.ModuleList(Layer(i, P, shape["heads"], g, set(skip_reduce))
+        self.embedding = Embedding(P["model.embedding.word"], P.get("model.embedding.position"), g)
+        self.layers = torch.nn.ModuleList(Layer(i, P, shape["heads"], g, set(skip_reduce), llama)
                                           for i in range(shape["layers"]))
-        self.final_norm = torch.nn.LayerNorm(shape["d"], eps=1e-5)
+        self.final_norm = _norm(shape["d"], llama)
         self.lm_head = TiedLMHead(self.embedding, g)
 
     def forward(self, ids):
@@ -210,8 +257,11 @@ PATTERNS = ("embedding", "layers.*.attn", "layers.*.attn.norm", "layers.*.mlp",
 
 def model_shape(shape: dict):
     from paper_2506_09280_b200.layout import ModelShape
+    llama = shape.get("llama", False)
     return ModelShape(layers=shape["layers"], d_model=shape["d"], n_heads=shape["heads"],
-                      d_ff=shape["ff"], seq_len=shape["seq"], vocab=shape["vocab"])
+                      d_ff=shape["ff"], seq_len=shape["seq"], vocab=shape["vocab"],
+                      n_kv_heads=shape.get("kv_heads"), gated_mlp=llama, norm_bias=not llama,
+                      position_table=not llama)
 
 
 def traced_step(shape: dict, g: TPGroup, *, device="cpu", dtype=torch.float32, skip_reduce=(),

@@ -64,6 +64,9 @@ def run_case(rnd, k):
     for r, c in shares:
         ref_all.records.extend(r.records)
         cand_all.records.extend(c.records)
+    # the single-process traces the shares split: global execution order
+    from paper_2506_09280_b200.distributed import execution_sorted
+    ref_all.records, cand_all.records = execution_sorted(ref_all.records), execution_sorted(cand_all.records)
     want = json.loads(td.render_report(check(ref_all, cand_all, tol, fmt=td.FloatFormat.BF16), "json"))
     from tests.test_gpu_parity import assert_reports_match
     for rep in reports:
