@@ -25,7 +25,7 @@ from .device import resolve_operands
 from .errors import (ConfigInvalid, DigestMismatch, FormatError, ShapeMismatch,
                      TraindiffError)
 from .perturb import PerturbSpec
-from .plan import Plan, PlanEntry, merge_view
+from .plan import Plan, PlanEntry, gc_paused, merge_view
 from .tensor import FloatFormat
 from .tracestore import Trace, canonical_json
 
@@ -181,6 +181,7 @@ def _side_detail(meta, group_rows) -> str:
 class CheckPlan:
     """check() split into plan (metadata, once per layout) and run (GPU)."""
 
+    @gc_paused
     def __init__(self, ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float = 3.0, *,
                  fmt: FloatFormat):
         if kappa <= 0:

@@ -20,7 +20,9 @@ once for a layout can be re-run on every step's fresh payloads.
 
 from __future__ import annotations
 
+import contextlib
 import functools
+import gc
 import math
 import os
 import threading
@@ -35,6 +37,31 @@ VERDICT_NAMES = {N.PASS: "pass", N.FLAG: "flag", N.REPLICA: "replica-mismatch",
                  N.MERGE: "merge-error", N.MISSING: "missing"}
 MAX_UNITS = 1 << 30          # per-segment unit cap (kernel uses 32-bit unit indices)
 _VEC_DTYPES = (N.F32, N.BF16, N.F16)
+
+
+@contextlib.contextmanager
+def no_gc():
+    """Cyclic GC paused while a plan is built: planning allocates tens of
+    thousands of small tuples, and a full collection over a process holding
+    big traces (every record, every payload handle) costs more than the
+    planning itself (config 2: 131 ms vs 28 ms for the segment tables).
+    Nothing built here is cyclic garbage; reference counting frees it."""
+    if not gc.isenabled():
+        yield
+        return
+    gc.disable()
+    try:
+        yield
+    finally:
+        gc.enable()
+
+
+def gc_paused(fn):
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        with no_gc():
+            return fn(*args, **kwargs)
+    return wrapper
 
 
 # ---------------------------------------------------------------------------
@@ -119,6 +146,7 @@ def _merge_detail(mappings: tuple, hull: tuple, shapes: tuple) -> str | None:
     return None if err is None else str(err)
 
 
+@gc_paused
 def merge_view(trace, replica_check: bool = True) -> dict[str, IdMeta]:
     """Per-id merge metadata in first-appearance order (checker.py:201-211)."""
     view = {}
@@ -197,13 +225,13 @@ class PlanBuilder:
         """Register `owner`'s payload, to be presented to the kernel as `dtype`
         (a widening cast at resolution time when the stored dtype differs)."""
         key = (id(owner), dtype)
-        slot = self._operand_index.get(key)
-        if slot is None:
-            slot = len(self.operands)
+        op = self._operand_index.get(key)
+        if op is None:
+            op = _Operand(len(self.operands), dtype, N.DTYPE_SIZE[dtype])
             self.operands.append(owner)
             self.operand_dtypes.append(dtype)
-            self._operand_index[key] = slot
-        return _Operand(slot, dtype, N.DTYPE_SIZE[dtype])
+            self._operand_index[key] = op
+        return op
 
     def add(self, x: _Operand | None, x_off: int, y: _Operand, y_off: int, zs: list,
             rows: int, cols: int, rx: int, ry: int) -> None:
@@ -311,6 +339,7 @@ class PlanEntry:
 class Plan:
     """Frozen layout of one comparison; `run()` executes it on the GPU."""
 
+    @gc_paused
     def __init__(self, entries: list[PlanEntry], static: tuple[float, float] | None = None,
                  owner=None, me: int = 0, compare_copy: dict | None = None, digest: bool = False):
         """static=(atol, rtol) builds compare_static's plan: the elementwise

@@ -1,10 +1,13 @@
 """BASELINE configs at full size.  Configs 1 and 2 (2.8 GB, 8.2 GB) run the CPU
 oracle on the whole trace: identical reports.  Config 3 (Llama-3-1B shape, S=8192, TP=8, 69 GB
 of bf16 traces in HBM) with the three injected bugs.  Too big for the CPU
-oracle, so the checks are size-independent: the verdicts are exactly the
-injections, and the observed rel_err of the bug ids and of a sample of clean
-ids equals an independent torch fp64 computation over the materialised
-merges (copy 0 of every shard group, reference semantics) within 1e-12."""
+oracle as a whole, so: the verdicts are exactly the injections; the CPU
+oracle re-checks a sample of ids (every 16th id under 256 MB of reference
+payload, plus the replica and scale bugs — each id's report entry is
+independent of the others') and its entries equal ours; and the observed
+rel_err of the bug ids (the 2.1 GB logits included) equals an independent
+torch fp64 computation over the materialised merges (copy 0 of every shard
+group, reference semantics) within 1e-12."""
 
 import pytest
 import torch
@@ -69,6 +72,28 @@ def test_config3_full_size_injections_and_fp64_norms():
     # the scale bug multiplies by tp = 8 exactly: rel_err of 8x vs x is 7 up
     # to the simulated round-off
     assert abs(verdicts[[k for k, v in BUGS.items() if v == "scale"][0]].observed - 7.0) < 0.1
+    # the CPU oracle on a sample of ids
+    from oracle import traindiff_oracle as O
+    from tests.test_gpu_parity import _close
+    ref_bytes = {}
+    for r in ref.records:
+        ref_bytes[r.id.encode()] = ref_bytes.get(r.id.encode(), 0) + r.nbytes
+    ids = [e.ident for e in rep.entries]
+    sample = {i for i in ids[::16] if ref_bytes.get(i, 0) < (256 << 20)}
+    sample |= {k for k, v in BUGS.items() if v != "order"}
+    assert len(sample) >= 30
+
+    def host(trace):
+        return [O.Rec(r.id.encode(), r.rank_meta.as_tuple(), r.mapping.local_shape, r.mapping.global_shape,
+                      [(lb.bounds, gb.bounds) for lb, gb in r.mapping.pairs], r.replica_group_size,
+                      r.payload.float().cpu().numpy()) for r in trace.records if r.id.encode() in sample]
+    doc = O.check(host(ref), host(cand), ref.header, cand.header, tol.responses, 3.0, "BF16")
+    assert {e["id"] for e in doc["entries"]} == sample
+    for w in doc["entries"]:
+        g = verdicts[w["id"]]
+        assert (g.verdict, g.detail) == (w["verdict"], w["detail"]), (w["id"], g, w)
+        assert _close(g.observed, w["observed"]), (w["id"], g.observed, w["observed"])
+        assert _close(g.threshold, w["threshold"])
 
 
 def test_config1_full_size_against_cpu_oracle():

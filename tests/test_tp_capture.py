@@ -52,7 +52,7 @@ def _flat(rec) -> dict:
             "payload": rec.host(), "cls": rec.module_class, "dtype": str(rec.payload.dtype).split(".")[-1]}
 
 
-def _tp_worker(rank, world, port, out_dir, shape, device, dtype_name, skip, mode):
+def _tp_worker(rank, world, port, out_dir, shape, device, dtype_name, skip, mode, responses=None):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -72,7 +72,7 @@ def _tp_worker(rank, world, port, out_dir, shape, device, dtype_name, skip, mode
             comm = TorchComm()
             cand = h.trace()
             refs = split_reference(ref_h.trace(), global_trace(cand, comm), world)
-            tol = td.ToleranceMap({}, n_samples=1, eps_p=td.FloatFormat.BF16.eps)
+            tol = td.ToleranceMap(dict(responses or {}), n_samples=3, eps_p=td.FloatFormat.BF16.eps)
             rep = check_distributed(refs[rank], cand, tol, fmt=td.FloatFormat.BF16, comm=comm)
             result["report"] = td.render_report(rep, "json")
         with open(os.path.join(out_dir, f"rank{rank}.pkl"), "wb") as fh:
@@ -81,9 +81,10 @@ def _tp_worker(rank, world, port, out_dir, shape, device, dtype_name, skip, mode
         dist.destroy_process_group()
 
 
-def run_tp(tmp_path, shape=SHAPE, world=2, device="cpu", dtype="float32", skip=(), mode="capture"):
+def run_tp(tmp_path, shape=SHAPE, world=2, device="cpu", dtype="float32", skip=(), mode="capture",
+           responses=None):
     mp.start_processes(_tp_worker, args=(world, _free_port(), str(tmp_path), shape, device, dtype,
-                                         tuple(skip), mode),
+                                         tuple(skip), mode, responses),
                        nprocs=world, join=True, start_method="spawn")
     out = []
     for r in range(world):
@@ -183,7 +184,19 @@ def test_live_tp2_on_gpu_feeds_check_and_check_distributed(tmp_path, skip, shape
     import paper_2506_09280_b200 as td
     from paper_2506_09280_b200.tracestore import RankMeta, Trace, TraceRecord
     from paper_2506_09280_b200.canonical import ShardMapping, SliceBox, parse_canonical
-    ranks = run_tp(tmp_path, shape=shape, device="cuda", dtype="bfloat16", skip=skip, mode="distributed")
+    # tolerances the reference way: responses of the single-device bf16 run
+    # to an eps-nudge of the embedding output (estimate_tolerance, n=3)
+    eps = td.FloatFormat.BF16.eps
+
+    def runner(spec):
+        pert = None if spec is None else \
+            (lambda out, ident: td.apply_perturbation(out, ident, spec, policy="bf16"))
+        return tp_gpt.traced_step(shape, tp_gpt.TPGroup(), device="cuda", dtype=torch.bfloat16,
+                                  precision="bfloat16", perturb=pert).trace()
+    tol = td.estimate_tolerance(runner, n_samples=3, eps_p=eps)
+    assert max(tol.responses.values()) > 0
+    ranks = run_tp(tmp_path, shape=shape, device="cuda", dtype="bfloat16", skip=skip, mode="distributed",
+                   responses=dict(tol.responses))
     ref_h = _single_device(shape, "cuda", torch.bfloat16, "bfloat16")
     cand = Trace(header=ranks[0]["header"])
     for f in (f for r in ranks for f in r["records"]):
@@ -192,12 +205,11 @@ def test_live_tp2_on_gpu_feeds_check_and_check_distributed(tmp_path, skip, shape
         cand.records.append(TraceRecord(parse_canonical(f["ident"]), RankMeta(*f["rank"]),
                                         ShardMapping(tuple(f["local"]), tuple(f["global"]), pairs),
                                         f["replica"], payload, f["cls"]))
-    tol = td.ToleranceMap({}, n_samples=1, eps_p=td.FloatFormat.BF16.eps)
     rep = td.check(ref_h.trace(), cand, tol, fmt=td.FloatFormat.BF16)
     got = json.loads(td.render_report(rep, "json"))
     want = O.check(_oracle_recs([_flat(r) for r in ref_h.records]),
                    _oracle_recs([f for r in ranks for f in r["records"]]),
-                   ref_h.header(), ranks[0]["header"], {}, 3.0, "BF16")
+                   ref_h.header(), ranks[0]["header"], dict(tol.responses), 3.0, "BF16")
     assert got["summary"] == want["summary"] and got["exit_code"] == want["exit_code"]
     assert got["earliest_divergence"] == want["earliest_divergence"]
     for g, w in zip(got["entries"], want["entries"]):

@@ -40,13 +40,18 @@ def main(name="cfg2", profile=False):
     ref = meta_trace(L.emit_records(model, L.ParallelConfig(microbatches=pcfg.microbatches)), hdr)
     cand = meta_trace(L.emit_records(model, pcfg), hdr)
     tol = ToleranceMap({}, n_samples=1, eps_p=2.0 ** -8)
-    best = None
-    for _ in range(3):
+    from paper_2506_09280_b200 import plan as PL
+    times = []
+    for _ in range(7):
+        PL._MERGE_DETAIL.clear()          # cold: no memoised merge witnesses
+        PL._RUN_BLOCKS.clear()
+        PL._run_blocks.cache_clear()
         t0 = time.perf_counter()
         CheckPlan(ref, cand, tol, fmt=FloatFormat.BF16)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    print(f"{name}: {len(ref.records)} ref + {len(cand.records)} cand records, cold plan {best * 1e3:.1f} ms")
+        times.append(time.perf_counter() - t0)
+    times.sort()
+    print(f"{name}: {len(ref.records)} ref + {len(cand.records)} cand records, cold plan "
+          f"min {times[0] * 1e3:.1f} ms, median {times[3] * 1e3:.1f} ms")
     if profile:
         pr = cProfile.Profile()
         pr.enable()
