@@ -78,6 +78,35 @@ def apply_perturbation(x, ident, spec: PerturbSpec | None, *, full_cols: int | N
     return y
 
 
+_STRAIGHT = None
+
+
+def straight_through(x, value):
+    """`value` in the forward pass, the gradient handed to `x` unchanged in
+    the backward: how a perturbed (or regenerated) tensor stands in for a
+    live activation.  The reference's backward uses the gradient of the
+    module's output as is for the upstream chain and the embedding's
+    parameters (engine.py:886-908, 383-385) — the (1 + u*eps) factor is an
+    input nudge, not part of the differentiated function.  A plain
+    td_perturb output has no autograd history, so returning it from a hook
+    would cut the graph: no gradient would reach anything upstream."""
+    global _STRAIGHT
+    import torch
+    if not (torch.is_grad_enabled() and x.requires_grad):
+        return value
+    if _STRAIGHT is None:
+        class StraightThrough(torch.autograd.Function):
+            @staticmethod
+            def forward(ctx, inp, val):
+                return val.clone()
+
+            @staticmethod
+            def backward(ctx, grad):
+                return grad, None
+        _STRAIGHT = StraightThrough.apply
+    return _STRAIGHT(x, value)
+
+
 def perturb_hook(ident, spec: PerturbSpec | None, *, policy: str = "fp32", row_positions=None,
                  generator: str = "splitmix64"):
     """A torch forward hook that replaces a module's output with its
@@ -86,8 +115,8 @@ def perturb_hook(ident, spec: PerturbSpec | None, *, policy: str = "fp32", row_p
     def hook(module, args, output):
         if spec is None or spec.eps == 0.0:
             return output
-        return apply_perturbation(output, ident, spec, policy=policy,
-                                  row_positions=row_positions, generator=generator)
+        return straight_through(output, apply_perturbation(output, ident, spec, policy=policy,
+                                                           row_positions=row_positions, generator=generator))
     return hook
 
 
@@ -100,5 +129,5 @@ def perturb_pre_hook(ident, spec: PerturbSpec | None, *, policy: str = "fp32", r
             return None
         first = apply_perturbation(args[0], ident, spec, policy=policy,
                                    row_positions=row_positions, generator=generator)
-        return (first,) + tuple(args[1:])
+        return (straight_through(args[0], first),) + tuple(args[1:])
     return hook

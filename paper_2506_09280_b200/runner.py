@@ -17,7 +17,7 @@ from typing import Callable
 import torch
 
 from .errors import NonFinite
-from .perturb import PerturbSpec, apply_perturbation
+from .perturb import PerturbSpec, apply_perturbation, straight_through
 from .torchtap import TapConfig, attach, detach
 from .torchtap.writer import encode_id
 
@@ -63,12 +63,15 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
                                                    check=False, nonfinite=nonfinite)
                     # the module reads `value`; its input gradient still flows
                     # back to the chain unchanged (engine.py:383-385)
-                    return (_replace(x, value),) + tuple(args[1:])
+                    return (straight_through(x, value),) + tuple(args[1:])
                 hooks.append(model.get_submodule(name).register_forward_pre_hook(regen, prepend=True))
         if spec is not None and spec.eps != 0.0:
             def out_hook(module, args, output):
-                return apply_perturbation(output, emb_id, spec, policy=policy, generator=generator,
-                                          check=False, nonfinite=nonfinite)
+                # the nudged output replaces the live one; gradients pass
+                # through unchanged (straight_through)
+                return straight_through(output, apply_perturbation(output, emb_id, spec, policy=policy,
+                                                                   generator=generator, check=False,
+                                                                   nonfinite=nonfinite))
             hooks.append(emb.register_forward_hook(out_hook, prepend=True))
             for name in (() if rewrite else module_inputs):
                 ident = encode_id(tap.iteration, tap.microbatch, "ActivationIn", tap.canonical_name(name))
@@ -76,8 +79,9 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
                 def pre_hook(module, args, _ident=ident):
                     if not args:
                         return None
-                    return (apply_perturbation(args[0], _ident, spec, policy=policy, generator=generator,
-                                               check=False, nonfinite=nonfinite),) + tuple(args[1:])
+                    return (straight_through(args[0], apply_perturbation(args[0], _ident, spec, policy=policy,
+                                                                         generator=generator, check=False,
+                                                                         nonfinite=nonfinite)),) + tuple(args[1:])
                 hooks.append(model.get_submodule(name).register_forward_pre_hook(pre_hook, prepend=True))
         handle = attach(model, tap, sink=sink)
         try:
@@ -94,28 +98,6 @@ def torch_runner(model, step: Callable, *, embedding: str, tap: TapConfig,
         hdr = header if header is not None else dict(handle.header(), mode="module-wise" if module_inputs else "cascade")
         return handle.trace(hdr)
     return runner
-
-
-_REPLACE = None
-
-
-def _replace(x, value):
-    """autograd-aware substitution: forward yields `value`, backward hands the
-    gradient to the replaced input `x` unchanged."""
-    global _REPLACE
-    if _REPLACE is None:
-        import torch
-
-        class Replace(torch.autograd.Function):
-            @staticmethod
-            def forward(ctx, inp, val):
-                return val.clone()
-
-            @staticmethod
-            def backward(ctx, grad):
-                return grad, None
-        _REPLACE = Replace.apply
-    return _REPLACE(x, value)
 
 
 def _regenerate(ident: str, shape: tuple, std: float, policy: str):

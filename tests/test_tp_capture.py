@@ -72,8 +72,9 @@ def _tp_worker(rank, world, port, out_dir, shape, device, dtype_name, skip, mode
             comm = TorchComm()
             cand = h.trace()
             refs = split_reference(ref_h.trace(), global_trace(cand, comm), world)
-            tol = td.ToleranceMap(dict(responses or {}), n_samples=3, eps_p=td.FloatFormat.BF16.eps)
-            rep = check_distributed(refs[rank], cand, tol, fmt=td.FloatFormat.BF16, comm=comm)
+            fmt = td.FloatFormat.BF16 if dtype_name == "bfloat16" else td.FloatFormat.FP32
+            tol = td.ToleranceMap(dict(responses or {}), n_samples=3, eps_p=fmt.eps)
+            rep = check_distributed(refs[rank], cand, tol, fmt=fmt, comm=comm)
             result["report"] = td.render_report(rep, "json")
         with open(os.path.join(out_dir, f"rank{rank}.pkl"), "wb") as fh:
             pickle.dump(result, fh)
@@ -177,27 +178,46 @@ def test_live_tp2_on_gpu_feeds_check_and_check_distributed(tmp_path, skip, shape
     """Two gloo ranks on cuda:0 run the bf16 TP model; their device-resident
     captures go to check() (union) here and to check_distributed() inside the
     job (each rank its own records); both reports equal the oracle's."""
+    _gpu_live_case(tmp_path, shape, "bfloat16", skip, n_samples=3)
+
+
+# config 1 as BASELINE.json names it: the 2-layer GPT-2-small shape (d=768,
+# 12 heads, ff=3072, S=1024, V=50304), fp32, a TP=2 candidate against the
+# single-device run, tolerances from perturbation runs (n=5, eps_p = FP32
+# eps; config.py:138-141) — here both runs are live PyTorch executions
+CFG1 = {"layers": 2, "d": 768, "heads": 12, "ff": 3072, "seq": 1024, "vocab": 50304}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("skip", [(), ("model.layers.1.attn",)], ids=["clean", "missing_allreduce"])
+def test_config1_live_gpt2_small_tp2_fp32(tmp_path, skip):
+    _gpu_live_case(tmp_path, CFG1, "float32", skip, n_samples=5)
+
+
+def _gpu_live_case(tmp_path, shape, dtype, skip, n_samples):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import json
 
     import paper_2506_09280_b200 as td
-    from paper_2506_09280_b200.tracestore import RankMeta, Trace, TraceRecord
     from paper_2506_09280_b200.canonical import ShardMapping, SliceBox, parse_canonical
-    # tolerances the reference way: responses of the single-device bf16 run
-    # to an eps-nudge of the embedding output (estimate_tolerance, n=3)
-    eps = td.FloatFormat.BF16.eps
+    from paper_2506_09280_b200.tracestore import RankMeta, Trace, TraceRecord
+    fmt = td.FloatFormat.BF16 if dtype == "bfloat16" else td.FloatFormat.FP32
+    policy = "bf16" if dtype == "bfloat16" else "fp32"
+    tdt = getattr(torch, dtype)
+    # tolerances the reference way: responses of the single-device run to an
+    # eps-nudge of the embedding output (estimate_tolerance)
 
     def runner(spec):
         pert = None if spec is None else \
-            (lambda out, ident: td.apply_perturbation(out, ident, spec, policy="bf16"))
-        return tp_gpt.traced_step(shape, tp_gpt.TPGroup(), device="cuda", dtype=torch.bfloat16,
-                                  precision="bfloat16", perturb=pert).trace()
-    tol = td.estimate_tolerance(runner, n_samples=3, eps_p=eps)
+            (lambda out, ident: td.apply_perturbation(out, ident, spec, policy=policy))
+        return tp_gpt.traced_step(shape, tp_gpt.TPGroup(), device="cuda", dtype=tdt,
+                                  precision=dtype, perturb=pert).trace()
+    tol = td.estimate_tolerance(runner, n_samples=n_samples, eps_p=fmt.eps)
     assert max(tol.responses.values()) > 0
-    ranks = run_tp(tmp_path, shape=shape, device="cuda", dtype="bfloat16", skip=skip, mode="distributed",
+    ranks = run_tp(tmp_path, shape=shape, device="cuda", dtype=dtype, skip=skip, mode="distributed",
                    responses=dict(tol.responses))
-    ref_h = _single_device(shape, "cuda", torch.bfloat16, "bfloat16")
+    ref_h = _single_device(shape, "cuda", tdt, dtype)
     cand = Trace(header=ranks[0]["header"])
     for f in (f for r in ranks for f in r["records"]):
         pairs = tuple((SliceBox(tuple(map(tuple, l))), SliceBox(tuple(map(tuple, g)))) for l, g in f["pairs"])
@@ -205,11 +225,11 @@ def test_live_tp2_on_gpu_feeds_check_and_check_distributed(tmp_path, skip, shape
         cand.records.append(TraceRecord(parse_canonical(f["ident"]), RankMeta(*f["rank"]),
                                         ShardMapping(tuple(f["local"]), tuple(f["global"]), pairs),
                                         f["replica"], payload, f["cls"]))
-    rep = td.check(ref_h.trace(), cand, tol, fmt=td.FloatFormat.BF16)
+    rep = td.check(ref_h.trace(), cand, tol, fmt=fmt)
     got = json.loads(td.render_report(rep, "json"))
     want = O.check(_oracle_recs([_flat(r) for r in ref_h.records]),
                    _oracle_recs([f for r in ranks for f in r["records"]]),
-                   ref_h.header(), ranks[0]["header"], dict(tol.responses), 3.0, "BF16")
+                   ref_h.header(), ranks[0]["header"], dict(tol.responses), 3.0, fmt.value)
     assert got["summary"] == want["summary"] and got["exit_code"] == want["exit_code"]
     assert got["earliest_divergence"] == want["earliest_divergence"]
     for g, w in zip(got["entries"], want["entries"]):
@@ -223,5 +243,7 @@ def test_live_tp2_on_gpu_feeds_check_and_check_distributed(tmp_path, skip, shape
             [(e["id"], e["verdict"]) for e in want["entries"]]
     if skip:
         assert want["earliest_divergence"] == BUG_SITE and want["exit_code"] == 3
+        entry = next(e for e in want["entries"] if e["id"] == BUG_SITE)
+        assert entry["observed"] >= 10 * max(entry["tolerance"], fmt.eps)
     else:
         assert want["exit_code"] == 0 and want["summary"]["missing"] == 0

@@ -281,7 +281,9 @@ def traced_step(shape: dict, g: TPGroup, *, device="cpu", dtype=torch.float32, s
         ident = "iter=0|mb=0|kind=ActivationOut|mod=model.embedding"
         # prepended: runs before the tap's output hook, which then captures
         # (and the model consumes) the perturbed embedding output
-        model.embedding.register_forward_hook(lambda mod, args, out: perturb(out, ident), prepend=True)
+        from paper_2506_09280_b200.perturb import straight_through
+        model.embedding.register_forward_hook(lambda mod, args, out: straight_through(out, perturb(out, ident)),
+                                              prepend=True)
     ids = torch.randint(0, shape["vocab"], (shape["seq"],),
                         generator=torch.Generator().manual_seed(seed_tokens)).to(device)
     model.loss(ids).backward()
