@@ -267,6 +267,29 @@ def _sample_ids(ids, size_of, stride: int, budget: int, max_id: int | None = Non
     return out
 
 
+def _row_prefix(records, keep: int) -> list:
+    """Oracle records of global rows [0, keep) of one id's records: every
+    (local, global) pair cut to those rows, one record per surviving pair
+    (same rank metadata and replica size, so replica groups stay groups)."""
+    from oracle import traindiff_oracle as O
+    out = []
+    for r in records:
+        for lb, gb in r.mapping.pairs:
+            (g0, g1), (l0, _) = gb.bounds[0], lb.bounds[0]
+            hi = min(g1, keep)
+            if hi <= g0:
+                continue
+            n = hi - g0
+            loc = ((0, n),) + tuple((0, b - a) for a, b in lb.bounds[1:])
+            glob = ((g0, hi),) + tuple(gb.bounds[1:])
+            sl = (slice(l0, l0 + n),) + tuple(slice(a, b) for a, b in lb.bounds[1:])
+            payload = r.payload[sl].float().cpu().numpy()
+            out.append(O.Rec(r.id.encode(), r.rank_meta.as_tuple(), payload.shape,
+                             (keep,) + tuple(r.mapping.global_shape[1:]), [(loc, glob)], r.replica_group_size,
+                             payload))
+    return out
+
+
 def cpu_baseline(ref, cand, tol, fmt, stride: int):
     """Time the oracle's check on a bounded sample of the common ids (host f32
     copies), one thread (numpy), on this box's host CPU."""
@@ -286,7 +309,18 @@ def cpu_baseline(ref, cand, tol, fmt, stride: int):
                                  r.mapping.global_shape, [(l.bounds, g.bounds) for l, g in r.mapping.pairs],
                                  r.replica_group_size, r.payload.float().cpu().numpy()))
         return out
-    rr, cr = host(ref.records), host(cand.records)
+    if sample:
+        rr, cr = host(ref.records), host(cand.records)
+        what = f"every {stride}th id of at most {REF_MAX_ID_BYTES >> 20} MiB within a " \
+               f"{CPU_SAMPLE_BYTES >> 30} GiB budget ({len(sample)} ids"
+    else:
+        # one id larger than the budget (config 5): a leading row block of it
+        ident = ids[0]
+        rows_all = next(r.mapping.global_shape[0] for r in ref.records if r.id.encode() == ident)
+        keep = max(1, int(rows_all * CPU_SAMPLE_BYTES // max(size_of[ident], 1)))
+        rr = _row_prefix([r for r in ref.records if r.id.encode() == ident], keep)
+        cr = _row_prefix([r for r in cand.records if r.id.encode() == ident], keep)
+        what = f"rows [0, {keep}) of the {rows_all}-row id (1 id"
     nbytes = sum(r.payload.size * 2 for r in rr) + sum(r.payload.size * 2 for r in cr)
     t0 = time.perf_counter()
     doc = O.check(rr, cr, ref.header, cand.header, tol.responses, 3.0, fmt.value)
@@ -294,10 +328,8 @@ def cpu_baseline(ref, cand, tol, fmt, stride: int):
     cpu = host_cpu()
     return {"value": nbytes / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "port",
             "cpu_model": cpu["cpu_model"], "host_cores": cpu["cpu_count"],
-            "sample": f"every {stride}th id of at most {REF_MAX_ID_BYTES >> 20} MiB within a "
-                      f"{CPU_SAMPLE_BYTES >> 30} GiB budget ({len(sample)} ids, "
-                      f"{nbytes / 1e9:.3f} GB of trace payload counted at the workload's 2 B/elem), "
-                      f"oracle/traindiff_oracle.check, 1 thread numpy",
+            "sample": f"{what}, {nbytes / 1e9:.3f} GB of trace payload counted at the workload's "
+                      f"2 B/elem), oracle/traindiff_oracle.check, 1 thread numpy",
             "seconds": dt, "layer_checks_per_s": len(doc["entries"]) / dt}
 
 

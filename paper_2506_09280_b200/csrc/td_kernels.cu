@@ -1305,8 +1305,20 @@ k_perturb_vec8(const char* x, char* y, int dt_in, int dt_out, int64_t rows, int6
 // 2^(32-s) (IMAD.HI + IMAD.WIDE instead of two SHF) was measured per shift
 // site: every mix of sites lost 2-31% (fmaheavy saturates first; each
 // IMAD.HI/WIDE costs ~2.6x the SHF it replaces), so the shifts stay on ALU.
+#ifndef TD_PERTURB_F32RT
+#define TD_PERTURB_F32RT 1
+#endif
+#ifndef TD_PERTURB_I2F
+#define TD_PERTURB_I2F 0        // I2F variant: 96 registers unbounded, no faster at 64 (A/B in DESIGN §3)
+#endif
+#ifndef TD_PERTURB_ACC
+#define TD_PERTURB_ACC 1
+#endif
+#ifndef TD_PERTURB_MINB
+#define TD_PERTURB_MINB 1
+#endif
 template <int GEN>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, TD_PERTURB_MINB)
 k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows, uint32_t gpr,
                int64_t full_cols, int64_t col0, const int64_t* __restrict__ row_pos, int64_t row0,
                uint64_t seed, double eps, uint32_t div_m, int div_p,
@@ -1325,6 +1337,10 @@ k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows,
         uint32_t out_of_range = 0;
         const uint64_t z0 = seed + (kb + 1) * GAMMA;
         uint4 blk;
+#if TD_PERTURB_F32RT
+        float fpair[2];
+        uint32_t span_max = 0, tie_min = 0xffffffffu;
+#endif
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const uint32_t xb = (j & 1) ? (iw[j >> 1] & 0xffff0000u) : (iw[j >> 1] << 16);
@@ -1339,11 +1355,44 @@ k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows,
                 } else {
                     w = splitmix_mix(z0 + (uint64_t)j * GAMMA);
                 }
+#if TD_PERTURB_I2F
+                // 2u - 1 = m * 2^-52 - 1 for the 53-bit m = w >> 11: m converts to
+                // f64 exactly (I2F on the XU pipe, which this kernel leaves idle)
+                // and the FMA's one rounding is exact (the result has <= 52
+                // significant bits) — numpy's 2.0*u - 1.0 bit for bit
+                u = __fma_rn(__ull2double_rn(w >> 11), 0x1p-52, -1.0);
+#else
                 const uint64_t m = w >> 11;
                 const double one_m = __longlong_as_double((long long)(0x3FF0000000000000ull | (m & 0xFFFFFFFFFFFFFull)));
                 u = __dsub_rn(one_m, (m >> 52) ? 1.0 : 2.0);
+#endif
             }
             const double v = __dmul_rn(xv, __dadd_rn(1.0, __dmul_rn(u, eps)));
+#if TD_PERTURB_F32RT
+            // Q_bf16 through one XU conversion: f = RN_f32(v), then RN_bf16(f)
+            // (cvt.rn.bf16x2.f32, one instruction per pair).  Rounding twice
+            // equals rounding once unless f is exactly a bf16 midpoint (low
+            // half-word 0x8000) — those, and anything outside [2^-125, bf16
+            // max + half an ulp) (bf16-subnormal range, the reference's
+            // clamp to max_finite, inf/NaN), take the exact path below.
+            const float f = __double2float_rn(v);
+            const uint32_t fb = __float_as_uint(f);
+            // two running extremes instead of per-element tests: 2|f| - 2^-125's
+            // bits must stay below the span to bf16 max + half an ulp (max over
+            // the group), and (f ^ 0x8000) & 0xffff is 0 only at a midpoint (min)
+#if TD_PERTURB_ACC
+            span_max = max(span_max, fb + fb - 0x02000000u);
+            tie_min = min(tie_min, (fb ^ 0x8000u) & 0xffffu);
+#else
+            out_of_range |= (((fb & 0x7fffffffu) - 0x01000000u) < (0x7f7f8000u - 0x01000000u) ? 0u : 1u)
+                            | ((fb & 0xffffu) == 0x8000u ? 1u : 0u);
+#endif
+            fpair[j & 1] = f;
+            if (j & 1) {
+                const __nv_bfloat162 h2 = __floats2bfloat162_rn(fpair[0], fpair[1]);
+                ow[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+            }
+#else
             const uint64_t b = (uint64_t)__double_as_longlong(v);
             const uint32_t hi = (uint32_t)(b >> 32);
             const uint64_t rb = (b & 0x7fffffffffffffffull) + 0xfffffffffffull + ((hi >> 13) & 1u);
@@ -1352,7 +1401,11 @@ k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows,
             const uint32_t t = (((rh << 3) - (896u << 23)) & 0x7fff0000u) | (hi & 0x80000000u);
             if (j & 1) ow[j >> 1] = __byte_perm(ow[j >> 1], t, 0x7632);
             else ow[j >> 1] = t;
+#endif
         }
+#if TD_PERTURB_F32RT && TD_PERTURB_ACC
+        out_of_range = (span_max >= 0xfeff0000u - 0x02000000u) | (tie_min == 0u);
+#endif
         if (out_of_range) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
