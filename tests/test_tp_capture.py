@@ -150,6 +150,47 @@ def test_live_tp2_capture_matches_single_device(tmp_path, shape):
     assert got == want
 
 
+def _dp_tp_worker(rank, world, port, out_dir, shape, tp):
+    """Rank r of a dp x tp job: TP group {d*tp .. d*tp+tp-1}, microbatch d."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dp = world // tp
+        groups = [dist.new_group(list(range(d * tp, (d + 1) * tp))) for d in range(dp)]
+        d, t = divmod(rank, tp)
+        h = tp_gpt.traced_step(shape, tp_gpt.TPGroup(t, tp, groups[d]), dp=dp, dp_rank=d, microbatch=d)
+        with open(os.path.join(out_dir, f"rank{rank}.pkl"), "wb") as fh:
+            pickle.dump({"records": [_flat(r) for r in h.records], "header": h.header()}, fh)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_live_dp2_tp2_microbatches_match_single_device(tmp_path):
+    """DP=2 x TP=2 live job (4 gloo ranks, TP sub-groups): DP rank d runs
+    microbatch d; every capture carries its (dp, tp) rank and the layout's
+    map (ids iter=0|mb=d|...); the union equals a single device running both
+    microbatches, per the CPU oracle, and covers the layout's id set."""
+    world, tp = 4, 2
+    mp.start_processes(_dp_tp_worker, args=(world, _free_port(), str(tmp_path), SHAPE, tp),
+                       nprocs=world, join=True, start_method="spawn")
+    ranks = []
+    for r in range(world):
+        with open(tmp_path / f"rank{r}.pkl", "rb") as fh:
+            ranks.append(pickle.load(fh))
+    cand = [f for r in ranks for f in r["records"]]
+    assert {(f["rank"][0], f["rank"][1]) for f in cand} == {(0, 0), (0, 1), (1, 0), (1, 1)}
+    assert {f["ident"].split("|")[1] for f in cand} == {"mb=0", "mb=1"}
+    ref = [_flat(r) for mb in (0, 1) for r in tp_gpt.traced_step(SHAPE, tp_gpt.TPGroup(), microbatch=mb).records]
+    doc = O.check(_oracle_recs(ref), _oracle_recs(cand), ranks[0]["header"], ranks[0]["header"], {}, 3.0, "BF16")
+    assert doc["exit_code"] == 0 and doc["summary"]["missing"] == 0, doc["summary"]
+    assert max(e["observed"] for e in doc["entries"]) < 1e-5
+    kinds = ("ActivationIn", "ActivationOut", "ParamGrad")
+    want = {sp.ident for sp in Layout(tp_gpt.model_shape(SHAPE), ParallelConfig(tp=2, dp=2, microbatches=2)).records()
+            if sp.kind in kinds}
+    assert {f["ident"] for f in cand if not f["ident"].endswith(".norm")} == want
+
+
 @pytest.mark.parametrize("shape", [SHAPE, LLAMA], ids=["gpt", "llama"])
 def test_live_tp2_missing_allreduce_is_a_replica_mismatch_at_the_site(tmp_path, shape):
     ranks = run_tp(tmp_path, shape=shape, skip=("model.layers.1.attn",))

@@ -265,27 +265,30 @@ def model_shape(shape: dict):
 
 
 def traced_step(shape: dict, g: TPGroup, *, device="cpu", dtype=torch.float32, skip_reduce=(),
-                perturb=None, precision="fp32", seed_tokens: int = 99):
-    """One forward+backward of rank g.rank, traced with that rank's real-TP
-    maps (torchtap.layout_shard).  perturb(tensor, ident, rows) -> tensor is
-    applied to the embedding output (the reference's perturbation site,
+                perturb=None, precision="fp32", seed_tokens: int = 99, dp: int = 1, dp_rank: int = 0,
+                microbatch: int = 0):
+    """One forward+backward of TP rank g.rank (of DP rank dp_rank when the
+    job is dp x tp), traced with that rank's real maps
+    (torchtap.layout_shard) under microbatch `microbatch` (its tokens are
+    seeded by seed_tokens + microbatch).  perturb(tensor, ident) -> tensor
+    is applied to the embedding output (the reference's perturbation site,
     engine.py:466-471).  Returns the TapHandle."""
     from paper_2506_09280_b200 import torchtap
     from paper_2506_09280_b200.layout import Layout, ParallelConfig
     model = TPGPT(shape, g, skip_reduce=skip_reduce).to(device=device, dtype=dtype)
-    layout = Layout(model_shape(shape), ParallelConfig(tp=g.world))
-    cfg = torchtap.TapConfig(patterns=PATTERNS, precision=precision,
-                             shard=torchtap.layout_shard(layout, tp=g.rank))
+    layout = Layout(model_shape(shape), ParallelConfig(tp=g.world, dp=dp, microbatches=dp))
+    cfg = torchtap.TapConfig(patterns=PATTERNS, precision=precision, microbatch=microbatch,
+                             shard=torchtap.layout_shard(layout, dp=dp_rank, tp=g.rank))
     handle = torchtap.attach(model, cfg)
     if perturb is not None:
-        ident = "iter=0|mb=0|kind=ActivationOut|mod=model.embedding"
+        ident = f"iter=0|mb={microbatch}|kind=ActivationOut|mod=model.embedding"
         # prepended: runs before the tap's output hook, which then captures
         # (and the model consumes) the perturbed embedding output
         from paper_2506_09280_b200.perturb import straight_through
         model.embedding.register_forward_hook(lambda mod, args, out: straight_through(out, perturb(out, ident)),
                                               prepend=True)
     ids = torch.randint(0, shape["vocab"], (shape["seq"],),
-                        generator=torch.Generator().manual_seed(seed_tokens)).to(device)
+                        generator=torch.Generator().manual_seed(seed_tokens + microbatch)).to(device)
     model.loss(ids).backward()
     torchtap.detach(handle)
     return handle
