@@ -297,3 +297,31 @@ def _gpu_live_case(tmp_path, shape, dtype, skip, n_samples, kappa=3.0):
     else:
         bad = [(e["id"], e["observed"], e["threshold"]) for e in want["entries"] if e["verdict"] != "pass"]
         assert want["exit_code"] == 0 and want["summary"]["missing"] == 0, bad
+
+
+@pytest.mark.parametrize("pcfg", [ParallelConfig(tp=2, sp=True, microbatches=2),
+                                  ParallelConfig(tp=2, cp=2, microbatches=2),
+                                  ParallelConfig(dp=2, tp=2, pp=2, microbatches=4),
+                                  ParallelConfig(tp=4, pp=2, vp=2, microbatches=2)],
+                         ids=["tp2sp", "tp2cp2", "dp2tp2pp2", "tp4pp2vp2"])
+def test_layout_shard_reproduces_every_emitted_map(pcfg):
+    """For every rank of SP / CP / PP / VP layouts, layout_shard answers each
+    (module, kind) the layout emits for that rank with exactly the emitted
+    ShardMapping, RankMeta 6-tuple and declared replica size."""
+    shape = dict(SHAPE, layers=4)
+    layout = Layout(tp_gpt.model_shape(shape), pcfg)
+    specs = list(layout.records())
+    n = 0
+    for dr in range(pcfg.dp):
+        for c in range(pcfg.cp):
+            for t in range(pcfg.tp):
+                shard = torchtap.layout_shard(layout, dp=dr, tp=t, cp=c)
+                for sp in specs:
+                    if (sp.rank[0], sp.rank[1], sp.rank[4]) != (dr, t, c) or sp.kind not in \
+                            ("ActivationIn", "ActivationOut", "ParamGrad"):
+                        continue
+                    module = sp.ident.split("|mod=", 1)[1]
+                    m, rank, rep = shard(module, sp.kind, torch.empty(sp.mapping.local_shape))
+                    assert (m, tuple(rank), rep) == (sp.mapping, sp.rank, sp.replica), sp.ident
+                    n += 1
+    assert n > 100
