@@ -33,6 +33,10 @@ import numpy as np
 from . import _native as N
 from .canonical import ShardMapping, merge_problem
 
+# per-structure templates in merge_view and Plan (TD_PLAN_TEMPLATES=0: the
+# general path for every id; tests/test_plan_templates.py checks they agree)
+_TEMPLATES = os.environ.get("TD_PLAN_TEMPLATES", "1") != "0"
+
 VERDICT_NAMES = {N.PASS: "pass", N.FLAG: "flag", N.REPLICA: "replica-mismatch",
                  N.MERGE: "merge-error", N.MISSING: "missing"}
 MAX_UNITS = 1 << 30          # per-segment unit cap (kernel uses 32-bit unit indices)
@@ -82,6 +86,7 @@ class IdMeta:
     global_shape: tuple | None = None
     rank_problem: bool = False
     merge_detail: str | None = None
+    struct_key: tuple | None = None   # merge_view's structure key + copy dtypes (plan templates)
 
     @property
     def merge_ok(self) -> bool:
@@ -148,10 +153,38 @@ def _merge_detail(mappings: tuple, hull: tuple, shapes: tuple) -> str | None:
 
 @gc_paused
 def merge_view(trace, replica_check: bool = True) -> dict[str, IdMeta]:
-    """Per-id merge metadata in first-appearance order (checker.py:201-211)."""
+    """Per-id merge metadata in first-appearance order (checker.py:201-211).
+
+    id_meta reads only each record's mapping and declared replica size, so
+    ids whose records carry the same (mapping signature, replica size)
+    sequence share one result shape: it is computed once per structure and
+    re-instantiated with each id's own records (`_TEMPLATES`)."""
     view = {}
+    memo: dict | None = {} if _TEMPLATES else None
     for ident, entries in trace.by_id().items():
-        view[ident] = id_meta(ident, sorted(entries, key=lambda p: p[0]), replica_check)
+        # by_id lists an id's records in trace order: already sorted by position
+        if memo is None:
+            view[ident] = id_meta(ident, entries, replica_check)
+            continue
+        key = tuple((rec.mapping.sig_id, rec.replica_group_size, rec.dtype_code) for _, rec in entries)
+        hit = memo.get(key)
+        if hit is None:
+            meta = view[ident] = id_meta(ident, entries, replica_check)
+            pos = {id(rec): k for k, (_, rec) in enumerate(entries)}
+            if len(pos) != len(entries):         # one record object listed twice: no template
+                continue
+            hit = memo[key] = (meta.rank_problem, meta.global_shape, meta.merge_detail,
+                               [([pos[id(r)] for r in g.records], g.declared_detail, g.numeric)
+                                for g in meta.groups])
+        else:
+            rank_problem, hull, detail, groups = hit
+            meta = view[ident] = IdMeta(ident=ident, exec_index=entries[0][0], global_shape=hull,
+                                        rank_problem=rank_problem, merge_detail=detail)
+            meta.groups = [GroupMeta(records=[entries[k][1] for k in idx], declared_detail=d, numeric=num)
+                           for idx, d, num in groups]
+        # the groups are a function of `key`, which also holds the copies'
+        # dtypes: everything the per-entry planner reads (plan templates)
+        meta.struct_key = (replica_check, key)
     return view
 
 
@@ -362,6 +395,7 @@ class Plan:
         per digest slot, the other local copies still need td_fingerprint."""
         self.entries = entries
         self.static = static
+        owner_given = owner
         owner = owner if owner is not None else (lambda rec: me)
         is_local = (lambda rec: owner(rec) == me)
         b = PlanBuilder(force_generic=static is not None)
@@ -374,88 +408,26 @@ class Plan:
         self.compare_reads = []   # (entry index, group index, copy index != 0)
         self.fused_digests = []   # digest slot -> (remote group index, copy index)
         compare_copy = compare_copy or {}
+        # per-entry templates (single-GPU plans): ids of one layout repeat a
+        # few structures (every hidden activation, every weight of a shape);
+        # the first id of a structure is planned in full and its output
+        # recorded relative to its own operands / tiles / group slots, later
+        # ids of the same structure replay it with their own records
+        templates = {} if (_TEMPLATES and owner_given is None and not compare_copy and not digest) else None
+        shared = _shared_entries(entries) if templates is not None else set()
         for ei, e in enumerate(entries):
-            t0 = b.tile_cursor
-            has_compare = (e.x is not None and e.y is not None and e.x.merge_ok and e.y.merge_ok
-                           and e.x.global_shape == e.y.global_shape)
-            cg0 = len(group_rows)
-            if e.y is not None and not e.y.rank_problem:
-                for gi, g in enumerate(e.y.groups):
-                    rep = e.y_rep and g.numeric
-                    s0 = b.tile_cursor
-                    y0 = g.records[0]
-                    spans = rep and len({owner(r) for r in g.records}) > 1
-                    c = 0
-                    if spans:
-                        self.remote_groups.append((len(group_rows), ei, 0, gi))
-                        c = compare_copy.get((e.ident, gi), 0)
-                        if c:
-                            y0 = g.records[c]
-                            self.compare_reads.append((ei, gi, c))
-                    mine = is_local(y0)
-                    together = rep and not spans and mine
-                    # replica copies in chunks of MAX_Z (one group slot each);
-                    # the compare reads copy 0 with the first chunk, every
-                    # further chunk re-reads copy 0 once
-                    chunks = _replica_chunks(len(g.records)) if rep else []
-                    zall = []
-                    if mine:
-                        gdt = _group_dtype(g.records) if together else y0.dtype_code
-                        yop = b.operand(y0, gdt)
-                        zall = [b.operand(r, gdt) for r in g.records[1:]] if together else []
-                        zops = zall[:N.MAX_Z]
-                        if has_compare:
-                            fuse = digest and spans and static is None
-                            first_seg = len(b.seg_rows)
-                            if fuse:
-                                b.digest_slot = len(self.fused_digests)
-                            self._compare_runs(b, e.x, y0, yop, zops, is_local)
-                            b.digest_slot = -1
-                            if fuse:
-                                self._settle_digest(b, first_seg, y0, yop, len(self.remote_groups) - 1, c)
-                            if zops:
-                                self._replica_remainder(b, y0, yop, zops)
-                        elif zops:
-                            n = math.prod(y0.shape)
-                            b.add(None, 0, yop, 0, zops, 1, n, n, n)
-                    if rep:
-                        self._group_slots(b, group_rows, chunks, s0, yop if zall else None, zall,
-                                          math.prod(y0.shape), (ei, 0, gi))
-            cg1 = len(group_rows)
-            rg0 = len(group_rows)
-            if e.x is not None and e.x_rep and not e.x.rank_problem:
-                for gi, g in enumerate(e.x.groups):
-                    if not g.numeric:
-                        continue
-                    s0 = b.tile_cursor
-                    x0 = g.records[0]
-                    mine = is_local(x0)
-                    chunks = _replica_chunks(len(g.records))
-                    zall, yop = [], None
-                    n = math.prod(x0.shape)
-                    if len({owner(r) for r in g.records}) > 1:
-                        self.remote_groups.append((len(group_rows), ei, 1, gi))
-                    elif mine:
-                        gdt = _group_dtype(g.records)
-                        yop = b.operand(x0, gdt)
-                        zall = [b.operand(r, gdt) for r in g.records[1:]]
-                        b.add(None, 0, yop, 0, zall[:N.MAX_Z], 1, n, n, n)
-                    self._group_slots(b, group_rows, chunks, s0, yop, zall, n, (ei, 1, gi))
-            rg1 = len(group_rows)
-            cand_host = 0
-            if e.y is not None:
-                if e.y.declared_problem is not None:
-                    cand_host = N.REPLICA
-                elif not e.y.merge_ok:
-                    cand_host = N.MERGE
-            ref_host = 0
-            if e.x is not None:
-                if e.x.declared_problem is not None:
-                    ref_host = N.REPLICA
-                elif not e.x.merge_ok:
-                    ref_host = N.MERGE
-            id_rows.append((t0, b.tile_cursor, cg0, cg1, rg0, rg1, int(has_compare),
-                            cand_host, ref_host, 0, float(e.tolerance)))
+            if templates is None:
+                self._plan_entry(b, ei, e, group_rows, id_rows, owner, is_local, compare_copy, digest, static)
+                continue
+            key = None if ei in shared else (e.x_rep, e.y_rep, _meta_key(e.x), _meta_key(e.y))
+            tpl = templates.get(key) if key is not None else None
+            if tpl is not None:
+                self._replay_entry(b, ei, e, tpl, group_rows, id_rows)
+                continue
+            mark = (len(b.operands), len(b.seg_rows), b.n_tiles, len(group_rows), len(self.group_owner))
+            self._plan_entry(b, ei, e, group_rows, id_rows, owner, is_local, compare_copy, digest, static)
+            if key is not None:
+                templates[key] = self._record_entry(b, e, mark, group_rows, id_rows)
         self.builder = b
         self.n_tiles = b.n_tiles
         self.ids = np.array(id_rows, dtype=N.ID_DESC) if id_rows else np.zeros(0, N.ID_DESC)
@@ -464,6 +436,155 @@ class Plan:
         self.tile_shift = self._retile()
         self._freeze_segments()
         self._chunk_slots()
+
+    def _plan_entry(self, b: PlanBuilder, ei: int, e: PlanEntry, group_rows: list, id_rows: list, owner,
+                    is_local, compare_copy: dict, digest: bool, static) -> None:
+        """Segments, group slots and the id row of one entry (the general path)."""
+        t0 = b.tile_cursor
+        has_compare = (e.x is not None and e.y is not None and e.x.merge_ok and e.y.merge_ok
+                       and e.x.global_shape == e.y.global_shape)
+        cg0 = len(group_rows)
+        if e.y is not None and not e.y.rank_problem:
+            for gi, g in enumerate(e.y.groups):
+                rep = e.y_rep and g.numeric
+                s0 = b.tile_cursor
+                y0 = g.records[0]
+                spans = rep and len({owner(r) for r in g.records}) > 1
+                c = 0
+                if spans:
+                    self.remote_groups.append((len(group_rows), ei, 0, gi))
+                    c = compare_copy.get((e.ident, gi), 0)
+                    if c:
+                        y0 = g.records[c]
+                        self.compare_reads.append((ei, gi, c))
+                mine = is_local(y0)
+                together = rep and not spans and mine
+                # replica copies in chunks of MAX_Z (one group slot each);
+                # the compare reads copy 0 with the first chunk, every
+                # further chunk re-reads copy 0 once
+                chunks = _replica_chunks(len(g.records)) if rep else []
+                zall = []
+                if mine:
+                    gdt = _group_dtype(g.records) if together else y0.dtype_code
+                    yop = b.operand(y0, gdt)
+                    zall = [b.operand(r, gdt) for r in g.records[1:]] if together else []
+                    zops = zall[:N.MAX_Z]
+                    if has_compare:
+                        fuse = digest and spans and static is None
+                        first_seg = len(b.seg_rows)
+                        if fuse:
+                            b.digest_slot = len(self.fused_digests)
+                        self._compare_runs(b, e.x, y0, yop, zops, is_local)
+                        b.digest_slot = -1
+                        if fuse:
+                            self._settle_digest(b, first_seg, y0, yop, len(self.remote_groups) - 1, c)
+                        if zops:
+                            self._replica_remainder(b, y0, yop, zops)
+                    elif zops:
+                        n = math.prod(y0.shape)
+                        b.add(None, 0, yop, 0, zops, 1, n, n, n)
+                if rep:
+                    self._group_slots(b, group_rows, chunks, s0, yop if zall else None, zall,
+                                      math.prod(y0.shape), (ei, 0, gi))
+        cg1 = len(group_rows)
+        rg0 = len(group_rows)
+        if e.x is not None and e.x_rep and not e.x.rank_problem:
+            for gi, g in enumerate(e.x.groups):
+                if not g.numeric:
+                    continue
+                s0 = b.tile_cursor
+                x0 = g.records[0]
+                mine = is_local(x0)
+                chunks = _replica_chunks(len(g.records))
+                zall, yop = [], None
+                n = math.prod(x0.shape)
+                if len({owner(r) for r in g.records}) > 1:
+                    self.remote_groups.append((len(group_rows), ei, 1, gi))
+                elif mine:
+                    gdt = _group_dtype(g.records)
+                    yop = b.operand(x0, gdt)
+                    zall = [b.operand(r, gdt) for r in g.records[1:]]
+                    b.add(None, 0, yop, 0, zall[:N.MAX_Z], 1, n, n, n)
+                self._group_slots(b, group_rows, chunks, s0, yop, zall, n, (ei, 1, gi))
+        rg1 = len(group_rows)
+        cand_host = 0
+        if e.y is not None:
+            if e.y.declared_problem is not None:
+                cand_host = N.REPLICA
+            elif not e.y.merge_ok:
+                cand_host = N.MERGE
+        ref_host = 0
+        if e.x is not None:
+            if e.x.declared_problem is not None:
+                ref_host = N.REPLICA
+            elif not e.x.merge_ok:
+                ref_host = N.MERGE
+        id_rows.append((t0, b.tile_cursor, cg0, cg1, rg0, rg1, int(has_compare),
+                        cand_host, ref_host, 0, float(e.tolerance)))
+
+    def _record_entry(self, b: PlanBuilder, e: PlanEntry, mark: tuple, group_rows: list, id_rows: list):
+        """The output of the entry just planned, relative to where it started
+        (None when it cannot be replayed: an operand shared with another
+        entry)."""
+        n_ops, n_rows, tiles0, g0, o0 = mark
+        role = {}
+        for side, meta in ((0, e.y), (1, e.x)):
+            if meta is None:
+                continue
+            for gi, g in enumerate(meta.groups):
+                for ri, r in enumerate(g.records):
+                    role[id(r)] = (side, gi, ri)
+        ops = []
+        for owner_rec, dt in zip(b.operands[n_ops:], b.operand_dtypes[n_ops:]):
+            where = role.get(id(owner_rec))
+            if where is None:
+                return None
+            ops.append((where, dt))
+
+        def rel(op):
+            k = op.slot - n_ops
+            if k < 0:
+                raise LookupError
+            return k
+        try:
+            rows = [(None if x is None else rel(x), xo, rel(y), yo, tuple(rel(z) for z in zs), r, c, rx, ry,
+                     tb - tiles0, nu, vec, ds)
+                    for x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec, ds in b.seg_rows[n_rows:]]
+        except LookupError:
+            return None
+        groups = [(s0 - tiles0, s1 - tiles0, nz) for s0, s1, nz in group_rows[g0:]]
+        owners = [(side, gi) for _, side, gi in self.group_owner[o0:]]
+        offsets = self.group_offset[o0:]
+        subs = {k - g0: [j - g0 for j in v] for k, v in self.subslots.items() if k >= g0}
+        t0, t1, cg0, cg1, rg0, rg1, hc, ch, rh, pad, _ = id_rows[-1]
+        idrow = (t0 - tiles0, t1 - tiles0, cg0 - g0, cg1 - g0, rg0 - g0, rg1 - g0, hc, ch, rh, pad)
+        return ops, rows, b.n_tiles - tiles0, groups, owners, offsets, subs, idrow
+
+    def _replay_entry(self, b: PlanBuilder, ei: int, e: PlanEntry, tpl, group_rows: list, id_rows: list) -> None:
+        ops_t, rows, n_tiles, groups, owners, offsets, subs, idrow = tpl
+        ops = []
+        index, operands, dtypes = b._operand_index, b.operands, b.operand_dtypes
+        for (side, gi, ri), dt in ops_t:
+            rec = (e.y if side == 0 else e.x).groups[gi].records[ri]
+            op = _Operand(len(operands), dt, N.DTYPE_SIZE[dt])    # a new record: no de-duplication to do
+            operands.append(rec)
+            dtypes.append(dt)
+            index[(id(rec), dt)] = op
+            ops.append(op)
+        tiles0, g0 = b.n_tiles, len(group_rows)
+        append = b.seg_rows.append
+        for xi, xo, yi, yo, zis, r, c, rx, ry, tb, nu, vec, ds in rows:
+            append((None if xi is None else ops[xi], xo, ops[yi], yo, [ops[k] for k in zis], r, c, rx, ry,
+                    tiles0 + tb, nu, vec, ds))
+        b.n_tiles += n_tiles
+        group_rows.extend((tiles0 + s0, tiles0 + s1, nz) for s0, s1, nz in groups)
+        self.group_owner.extend((ei, side, gi) for side, gi in owners)
+        self.group_offset.extend(offsets)
+        for k, v in subs.items():
+            self.subslots[g0 + k] = [g0 + j for j in v]
+        t0, t1, cg0, cg1, rg0, rg1, hc, ch, rh, pad = idrow
+        id_rows.append((tiles0 + t0, tiles0 + t1, g0 + cg0, g0 + cg1, g0 + rg0, g0 + rg1, hc, ch, rh, pad,
+                        float(e.tolerance)))
 
     def _group_slots(self, b: PlanBuilder, group_rows: list, chunks: list, s0: int, yop, zall: list,
                      n: int, owner_key: tuple) -> None:
@@ -644,55 +765,77 @@ class Plan:
     # -- device tables ----------------------------------------------------------
 
     def _freeze_segments(self) -> None:
+        """The device segment table, tile -> segment map and per-class tile
+        lists, built column-wise (numpy over the builder's rows)."""
         rows = self.builder.seg_rows
         n = len(rows)
         segs = np.zeros(n, dtype=N.SEGMENT)
-        self.seg_xslot = np.full(n, -1, np.int64)
-        self.seg_xoff = np.zeros(n, np.int64)     # bytes
-        self.seg_yslot = np.zeros(n, np.int64)
-        self.seg_yoff = np.zeros(n, np.int64)
         self.seg_zslot = np.full((n, N.MAX_Z), -1, np.int64)
-        tile_seg = np.zeros(self.n_tiles, np.int32)
-        class_tiles: dict = {}
-        cols = {k: [0] * n for k in ("x_stride", "y_stride", "rows", "cols", "tile_begin", "n_units", "x_dtype",
-                                     "y_dtype", "nz", "flags", "div_m", "div_p", "y_word0", "digest_slot")}
-        xslot, xoff, yslot, yoff = [-1] * n, [0] * n, [0] * n, [0] * n
-        shift_bits = self.tile_shift << N.SEG_TILE_SHIFT_POS
-        for i, (x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec, ds) in enumerate(rows):
-            cols["x_stride"][i], cols["y_stride"][i], cols["rows"][i], cols["cols"][i] = rx, ry, r, c
-            cols["tile_begin"][i], cols["n_units"][i] = tb, nu
-            cols["x_dtype"][i] = x.dtype if x is not None else y.dtype
-            cols["y_dtype"][i], cols["nz"][i] = y.dtype, len(zs)
-            cols["flags"][i] = ((N.SEG_HAS_X if x is not None else 0) | (N.SEG_VEC if vec else 0) | shift_bits)
-            cols["div_m"][i], cols["div_p"][i] = _magic(c // 8 if vec else c)
-            cols["y_word0"][i], cols["digest_slot"][i] = (yo * y.esize) // 8, ds
-            if x is not None:
-                xslot[i], xoff[i] = x.slot, xo * x.esize
-            yslot[i], yoff[i] = y.slot, yo * y.esize
-            for j, z in enumerate(zs):
-                self.seg_zslot[i, j] = z.slot
-            nt = -(-nu // self.tile_units)
-            tile_seg[tb:tb + nt] = i
-            key = (bool(vec), y.dtype, len(zs), x is not None, ds >= 0)
-            class_tiles.setdefault(key, []).append((tb, nt))
-        if n:
-            for k, v in cols.items():
-                segs[k] = v
-            self.seg_xslot[:], self.seg_xoff[:] = xslot, xoff
-            self.seg_yslot[:], self.seg_yoff[:] = yslot, yoff
-        self.segs = segs
-        self.tile_seg = tile_seg
-        self.class_keys = sorted(class_tiles)
-        self.class_segs = [[int(tile_seg[tb]) for tb, _ in class_tiles[k]] for k in self.class_keys]
-        # packed (segment << 32 | tile) entries, grid-stride walked by the kernels
-        self.class_lists = [np.concatenate([(np.int64(tile_seg[tb]) << 32) + np.arange(tb, tb + nt, dtype=np.int64)
-                                            for tb, nt in class_tiles[k]]) for k in self.class_keys]
         self.operands = self.builder.operands
         self.operand_dtypes = self.builder.operand_dtypes
-        self.algorithmic_bytes = 0
-        for x, _, y, _, zs, r, c, *_ in rows:
-            per = y.esize * (1 + len(zs)) + (x.esize if x is not None else 0)
-            self.algorithmic_bytes += r * c * per
+        if n == 0:
+            self.seg_xslot = np.full(0, -1, np.int64)
+            self.seg_xoff = self.seg_yslot = self.seg_yoff = np.zeros(0, np.int64)
+            self.segs, self.tile_seg = segs, np.zeros(self.n_tiles, np.int32)
+            self.class_keys, self.class_segs, self.class_lists = [], [], []
+            self.algorithmic_bytes = 0
+            return
+        xs, xo, ys, yo, zss, r, c, rx, ry, tb, nu, vec, ds = zip(*rows)
+        i64 = np.int64
+        has_x = np.fromiter((x is not None for x in xs), bool, n)
+        x_es = np.fromiter((x.esize if x is not None else 0 for x in xs), i64, n)
+        x_slot = np.fromiter((x.slot if x is not None else -1 for x in xs), i64, n)
+        x_dt = np.fromiter((x.dtype if x is not None else y.dtype for x, y in zip(xs, ys)), np.int32, n)
+        y_es = np.fromiter((y.esize for y in ys), i64, n)
+        y_slot = np.fromiter((y.slot for y in ys), i64, n)
+        y_dt = np.fromiter((y.dtype for y in ys), np.int32, n)
+        nz = np.fromiter((len(z) for z in zss), np.int32, n)
+        for i in np.flatnonzero(nz):
+            for j, z in enumerate(zss[i]):
+                self.seg_zslot[i, j] = z.slot
+        r, c, tb, nu = (np.asarray(v, i64) for v in (r, c, tb, nu))
+        xo, yo = np.asarray(xo, i64), np.asarray(yo, i64)
+        vec = np.asarray(vec, bool)
+        ds = np.asarray(ds, np.int32)
+        segs["x_stride"], segs["y_stride"], segs["rows"], segs["cols"] = rx, ry, r, c
+        segs["tile_begin"], segs["n_units"] = tb, nu
+        segs["x_dtype"], segs["y_dtype"], segs["nz"] = x_dt, y_dt, nz
+        segs["flags"] = ((has_x * N.SEG_HAS_X) | (vec * N.SEG_VEC)
+                         | (self.tile_shift << N.SEG_TILE_SHIFT_POS)).astype(np.uint32)
+        # _magic(d) for every row: p = 31 + bit_length(d - 1), m = ceil(2^p / d)
+        d = np.where(vec, c // 8, c)
+        _, e = np.frexp((d - 1).astype(np.float64))
+        p = 31 + np.where(d > 1, e, 0).astype(i64)
+        big = np.left_shift(np.ones(n, i64), p)
+        m = big // d + (big % d != 0)
+        segs["div_m"], segs["div_p"] = m.astype(np.uint32), p.astype(np.int32)
+        segs["y_word0"], segs["digest_slot"] = (yo * y_es) // 8, ds
+        self.seg_xslot, self.seg_xoff = x_slot, np.where(has_x, xo * x_es, 0)
+        self.seg_yslot, self.seg_yoff = y_slot, yo * y_es
+        nt = -(-nu // self.tile_units)
+        tile_seg = np.zeros(self.n_tiles, np.int32)
+        seg_of_tile = np.repeat(np.arange(n, dtype=np.int32), nt)
+        first = np.repeat(tb - np.concatenate([[0], np.cumsum(nt)[:-1]]), nt)
+        tiles = first + np.arange(len(seg_of_tile), dtype=i64)     # tile index of each (segment, k)
+        tile_seg[tiles] = seg_of_tile
+        keys = list(zip(vec.tolist(), y_dt.tolist(), nz.tolist(), has_x.tolist(), (ds >= 0).tolist()))
+        members: dict = {}
+        for i, k in enumerate(keys):
+            members.setdefault(k, []).append(i)
+        self.segs = segs
+        self.tile_seg = tile_seg
+        self.class_keys = sorted(members)
+        self.class_segs = [members[k] for k in self.class_keys]
+        owner = seg_of_tile.astype(i64) << 32
+        self.class_lists = []
+        for k in self.class_keys:
+            idx = np.asarray(members[k], i64)
+            pick = np.repeat(idx, nt[idx])
+            base = np.repeat(tb[idx] - np.concatenate([[0], np.cumsum(nt[idx])[:-1]]), nt[idx])
+            t = base + np.arange(len(pick), dtype=i64)
+            self.class_lists.append((pick << 32) + t)
+        del owner
+        self.algorithmic_bytes = int((r * c * (y_es * (1 + nz) + x_es)).sum())
 
     # -- execution ----------------------------------------------------------------
 
@@ -723,8 +866,29 @@ class Plan:
         return Prepared(self, pointers, kappa, eps, replica_eps, stream, digests, tail_words)
 
 
-_ONE_SEG = os.environ.get("TD_ONE_SEG", "1") != "0"      # A/B switch for by-value single segments
-_STAGING_LOCK = threading.Lock()
+_ONE_SEG = os.environ.get("TD_ONE_SEG", "1") != "0"
+
+
+def _meta_key(meta):
+    """Everything of an IdMeta the per-entry planner reads, as a hashable
+    key: problems, hull, and per group its replica flags and every copy's
+    (mapping signature id, dtype)."""
+    if meta is None:
+        return None
+    if meta.struct_key is not None:
+        return meta.struct_key
+    return (meta.rank_problem, meta.merge_ok, meta.global_shape,
+            tuple((g.numeric, g.declared_detail is None,
+                   tuple((r.mapping.sig_id, r.dtype_code) for r in g.records)) for g in meta.groups))
+
+
+def _shared_entries(entries) -> set:
+    """Entries whose two sides hold the same record object (a trace checked
+    against itself): operand de-duplication then differs from entry to entry,
+    so they are planned without templates."""
+    xs = {id(r) for e in entries if e.x is not None for g in e.x.groups for r in g.records}
+    return {ei for ei, e in enumerate(entries)
+            if e.y is not None and any(id(r) in xs for g in e.y.groups for r in g.records)}
 
 
 class Prepared:
