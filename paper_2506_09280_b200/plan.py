@@ -866,7 +866,8 @@ class Plan:
         return Prepared(self, pointers, kappa, eps, replica_eps, stream, digests, tail_words)
 
 
-_ONE_SEG = os.environ.get("TD_ONE_SEG", "1") != "0"
+_ONE_SEG = os.environ.get("TD_ONE_SEG", "1") != "0"      # A/B switch for by-value single segments
+_STAGING_LOCK = threading.Lock()
 
 
 def _meta_key(meta):
