@@ -23,6 +23,7 @@ from __future__ import annotations
 import contextlib
 import functools
 import gc
+import itertools
 import math
 import os
 import threading
@@ -86,7 +87,7 @@ class IdMeta:
     global_shape: tuple | None = None
     rank_problem: bool = False
     merge_detail: str | None = None
-    struct_key: tuple | None = None   # merge_view's structure key + copy dtypes (plan templates)
+    struct_key: int | None = None     # interned merge_view structure (copy signatures, sizes, dtypes)
 
     @property
     def merge_ok(self) -> bool:
@@ -173,18 +174,19 @@ def merge_view(trace, replica_check: bool = True) -> dict[str, IdMeta]:
             pos = {id(rec): k for k, (_, rec) in enumerate(entries)}
             if len(pos) != len(entries):         # one record object listed twice: no template
                 continue
+            # the groups are a function of `key`, which also holds the copies'
+            # dtypes: everything the per-entry planner reads (plan templates);
+            # interned to a small int so entry keys hash cheaply
             hit = memo[key] = (meta.rank_problem, meta.global_shape, meta.merge_detail,
                                [([pos[id(r)] for r in g.records], g.declared_detail, g.numeric)
-                                for g in meta.groups])
+                                for g in meta.groups], _intern_struct((replica_check, key)))
         else:
-            rank_problem, hull, detail, groups = hit
+            rank_problem, hull, detail, groups, _ = hit
             meta = view[ident] = IdMeta(ident=ident, exec_index=entries[0][0], global_shape=hull,
                                         rank_problem=rank_problem, merge_detail=detail)
             meta.groups = [GroupMeta(records=[entries[k][1] for k in idx], declared_detail=d, numeric=num)
                            for idx, d, num in groups]
-        # the groups are a function of `key`, which also holds the copies'
-        # dtypes: everything the per-entry planner reads (plan templates)
-        meta.struct_key = (replica_check, key)
+        meta.struct_key = hit[4]
     return view
 
 
@@ -233,11 +235,14 @@ def _blocks(ext, x_start, x_shape, y_start, y_shape):
         yield ox, oy, rows, cols, rx, ry
 
 
-@dataclass
 class _Operand:
-    slot: int        # index into the plan's operand table
-    dtype: int
-    esize: int
+    """A registered payload: slot in the plan's operand table, the dtype it
+    is read as, that dtype's size."""
+
+    __slots__ = ("slot", "dtype", "esize")
+
+    def __init__(self, slot: int, dtype: int, esize: int):
+        self.slot, self.dtype, self.esize = slot, dtype, esize
 
 
 class PlanBuilder:
@@ -562,26 +567,27 @@ class Plan:
 
     def _replay_entry(self, b: PlanBuilder, ei: int, e: PlanEntry, tpl, group_rows: list, id_rows: list) -> None:
         ops_t, rows, n_tiles, groups, owners, offsets, subs, idrow = tpl
-        ops = []
         index, operands, dtypes = b._operand_index, b.operands, b.operand_dtypes
+        sides = (e.y, e.x)
+        ops = []
         for (side, gi, ri), dt in ops_t:
-            rec = (e.y if side == 0 else e.x).groups[gi].records[ri]
+            rec = sides[side].groups[gi].records[ri]
             op = _Operand(len(operands), dt, N.DTYPE_SIZE[dt])    # a new record: no de-duplication to do
             operands.append(rec)
             dtypes.append(dt)
             index[(id(rec), dt)] = op
             ops.append(op)
         tiles0, g0 = b.n_tiles, len(group_rows)
-        append = b.seg_rows.append
-        for xi, xo, yi, yo, zis, r, c, rx, ry, tb, nu, vec, ds in rows:
-            append((None if xi is None else ops[xi], xo, ops[yi], yo, [ops[k] for k in zis], r, c, rx, ry,
-                    tiles0 + tb, nu, vec, ds))
+        b.seg_rows.extend((None if xi is None else ops[xi], xo, ops[yi], yo, [ops[k] for k in zis] if zis else [],
+                           r, c, rx, ry, tiles0 + tb, nu, vec, ds)
+                          for xi, xo, yi, yo, zis, r, c, rx, ry, tb, nu, vec, ds in rows)
         b.n_tiles += n_tiles
-        group_rows.extend((tiles0 + s0, tiles0 + s1, nz) for s0, s1, nz in groups)
-        self.group_owner.extend((ei, side, gi) for side, gi in owners)
-        self.group_offset.extend(offsets)
-        for k, v in subs.items():
-            self.subslots[g0 + k] = [g0 + j for j in v]
+        if groups:
+            group_rows.extend((tiles0 + s0, tiles0 + s1, nz) for s0, s1, nz in groups)
+            self.group_owner.extend((ei, side, gi) for side, gi in owners)
+            self.group_offset.extend(offsets)
+            for k, v in subs.items():
+                self.subslots[g0 + k] = [g0 + j for j in v]
         t0, t1, cg0, cg1, rg0, rg1, hc, ch, rh, pad = idrow
         id_rows.append((tiles0 + t0, tiles0 + t1, g0 + cg0, g0 + cg1, g0 + rg0, g0 + rg1, hc, ch, rh, pad,
                         float(e.tolerance)))
@@ -881,6 +887,19 @@ def _meta_key(meta):
     return (meta.rank_problem, meta.merge_ok, meta.global_shape,
             tuple((g.numeric, g.declared_detail is None,
                    tuple((r.mapping.sig_id, r.dtype_code) for r in g.records)) for g in meta.groups))
+
+
+_STRUCT_IDS: dict = {}
+_STRUCT_COUNTER = itertools.count(1)
+
+
+def _intern_struct(key: tuple) -> int:
+    sid = _STRUCT_IDS.get(key)
+    if sid is None:
+        if len(_STRUCT_IDS) > (1 << 16):    # bound the table; ids stay unique (counter)
+            _STRUCT_IDS.clear()
+        sid = _STRUCT_IDS.setdefault(key, next(_STRUCT_COUNTER))
+    return sid
 
 
 def _shared_entries(entries) -> set:
