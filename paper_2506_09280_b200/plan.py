@@ -418,18 +418,25 @@ class Plan:
         # the first id of a structure is planned in full and its output
         # recorded relative to its own operands / tiles / group slots, later
         # ids of the same structure replay it with their own records
-        templates = {} if (_TEMPLATES and owner_given is None and not compare_copy and not digest) else None
+        templates = {} if _TEMPLATES else None
         shared = _shared_entries(entries) if templates is not None else set()
         for ei, e in enumerate(entries):
             if templates is None:
                 self._plan_entry(b, ei, e, group_rows, id_rows, owner, is_local, compare_copy, digest, static)
                 continue
             key = None if ei in shared else (e.x_rep, e.y_rep, _meta_key(e.x), _meta_key(e.y))
+            if key is not None and owner_given is not None:
+                # multi-GPU plans also depend on where every copy lives and on
+                # which copy each cross-rank group's compare reads
+                key = (key, _owners_key(e.y, owner), _owners_key(e.x, owner),
+                       tuple(compare_copy.get((e.ident, gi), 0) for gi in range(len(e.y.groups)))
+                       if compare_copy and e.y is not None else ())
             tpl = templates.get(key) if key is not None else None
             if tpl is not None:
                 self._replay_entry(b, ei, e, tpl, group_rows, id_rows)
                 continue
-            mark = (len(b.operands), len(b.seg_rows), b.n_tiles, len(group_rows), len(self.group_owner))
+            mark = (len(b.operands), len(b.seg_rows), b.n_tiles, len(group_rows), len(self.group_owner),
+                    len(self.remote_groups), len(self.compare_reads), len(self.fused_digests))
             self._plan_entry(b, ei, e, group_rows, id_rows, owner, is_local, compare_copy, digest, static)
             if key is not None:
                 templates[key] = self._record_entry(b, e, mark, group_rows, id_rows)
@@ -531,7 +538,7 @@ class Plan:
         """The output of the entry just planned, relative to where it started
         (None when it cannot be replayed: an operand shared with another
         entry)."""
-        n_ops, n_rows, tiles0, g0, o0 = mark
+        n_ops, n_rows, tiles0, g0, o0, rg0_, cr0, fd0 = mark
         role = {}
         for side, meta in ((0, e.y), (1, e.x)):
             if meta is None:
@@ -553,20 +560,24 @@ class Plan:
             return k
         try:
             rows = [(None if x is None else rel(x), xo, rel(y), yo, tuple(rel(z) for z in zs), r, c, rx, ry,
-                     tb - tiles0, nu, vec, ds)
+                     tb - tiles0, nu, vec, ds if ds < 0 else ds - fd0)
                     for x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec, ds in b.seg_rows[n_rows:]]
         except LookupError:
             return None
+        remote = [(slot - g0, side, gi) for slot, _, side, gi in self.remote_groups[rg0_:]]
+        reads = [(gi, c) for _, gi, c in self.compare_reads[cr0:]]
+        fused = [(k - rg0_, c) for k, c in self.fused_digests[fd0:]]
         groups = [(s0 - tiles0, s1 - tiles0, nz) for s0, s1, nz in group_rows[g0:]]
         owners = [(side, gi) for _, side, gi in self.group_owner[o0:]]
         offsets = self.group_offset[o0:]
         subs = {k - g0: [j - g0 for j in v] for k, v in self.subslots.items() if k >= g0}
         t0, t1, cg0, cg1, rg0, rg1, hc, ch, rh, pad, _ = id_rows[-1]
         idrow = (t0 - tiles0, t1 - tiles0, cg0 - g0, cg1 - g0, rg0 - g0, rg1 - g0, hc, ch, rh, pad)
-        return ops, rows, b.n_tiles - tiles0, groups, owners, offsets, subs, idrow
+        return ops, rows, b.n_tiles - tiles0, groups, owners, offsets, subs, idrow, remote, reads, fused
 
     def _replay_entry(self, b: PlanBuilder, ei: int, e: PlanEntry, tpl, group_rows: list, id_rows: list) -> None:
-        ops_t, rows, n_tiles, groups, owners, offsets, subs, idrow = tpl
+        ops_t, rows, n_tiles, groups, owners, offsets, subs, idrow, remote, reads, fused = tpl
+        fd0, rg0 = len(self.fused_digests), len(self.remote_groups)
         index, operands, dtypes = b._operand_index, b.operands, b.operand_dtypes
         sides = (e.y, e.x)
         ops = []
@@ -579,8 +590,12 @@ class Plan:
             ops.append(op)
         tiles0, g0 = b.n_tiles, len(group_rows)
         b.seg_rows.extend((None if xi is None else ops[xi], xo, ops[yi], yo, [ops[k] for k in zis] if zis else [],
-                           r, c, rx, ry, tiles0 + tb, nu, vec, ds)
+                           r, c, rx, ry, tiles0 + tb, nu, vec, ds if ds < 0 else fd0 + ds)
                           for xi, xo, yi, yo, zis, r, c, rx, ry, tb, nu, vec, ds in rows)
+        if remote:
+            self.remote_groups.extend((g0 + slot, ei, side, gi) for slot, side, gi in remote)
+            self.compare_reads.extend((ei, gi, c) for gi, c in reads)
+            self.fused_digests.extend((rg0 + k, c) for k, c in fused)
         b.n_tiles += n_tiles
         if groups:
             group_rows.extend((tiles0 + s0, tiles0 + s1, nz) for s0, s1, nz in groups)
@@ -900,6 +915,12 @@ def _intern_struct(key: tuple) -> int:
             _STRUCT_IDS.clear()
         sid = _STRUCT_IDS.setdefault(key, next(_STRUCT_COUNTER))
     return sid
+
+
+def _owners_key(meta, owner):
+    if meta is None:
+        return None
+    return tuple(tuple(owner(r) for r in g.records) for g in meta.groups)
 
 
 def _shared_entries(entries) -> set:
