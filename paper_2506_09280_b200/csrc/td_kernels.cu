@@ -1305,20 +1305,11 @@ k_perturb_vec8(const char* x, char* y, int dt_in, int dt_out, int64_t rows, int6
 // 2^(32-s) (IMAD.HI + IMAD.WIDE instead of two SHF) was measured per shift
 // site: every mix of sites lost 2-31% (fmaheavy saturates first; each
 // IMAD.HI/WIDE costs ~2.6x the SHF it replaces), so the shifts stay on ALU.
-#ifndef TD_PERTURB_F32RT
-#define TD_PERTURB_F32RT 1
-#endif
-#ifndef TD_PERTURB_I2F
-#define TD_PERTURB_I2F 0        // I2F variant: 96 registers unbounded, no faster at 64 (A/B in DESIGN §3)
-#endif
-#ifndef TD_PERTURB_ACC
-#define TD_PERTURB_ACC 1
-#endif
-#ifndef TD_PERTURB_MINB
-#define TD_PERTURB_MINB 1
+#ifndef TD_PERTURB_CVT
+#define TD_PERTURB_CVT 1        // 0: the integer RNE of round 1 (A/B)
 #endif
 template <int GEN>
-__global__ void __launch_bounds__(256, TD_PERTURB_MINB)
+__global__ void __launch_bounds__(256)
 k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows, uint32_t gpr,
                int64_t full_cols, int64_t col0, const int64_t* __restrict__ row_pos, int64_t row0,
                uint64_t seed, double eps, uint32_t div_m, int div_p,
@@ -1337,9 +1328,8 @@ k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows,
         uint32_t out_of_range = 0;
         const uint64_t z0 = seed + (kb + 1) * GAMMA;
         uint4 blk;
-#if TD_PERTURB_F32RT
-        float fpair[2];
-        uint32_t span_max = 0, tie_min = 0xffffffffu;
+#if TD_PERTURB_CVT
+        uint32_t hlo = 0, emin = 0xffffffffu, emax = 0u;
 #endif
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -1355,42 +1345,30 @@ k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows,
                 } else {
                     w = splitmix_mix(z0 + (uint64_t)j * GAMMA);
                 }
-#if TD_PERTURB_I2F
-                // 2u - 1 = m * 2^-52 - 1 for the 53-bit m = w >> 11: m converts to
-                // f64 exactly (I2F on the XU pipe, which this kernel leaves idle)
-                // and the FMA's one rounding is exact (the result has <= 52
-                // significant bits) — numpy's 2.0*u - 1.0 bit for bit
-                u = __fma_rn(__ull2double_rn(w >> 11), 0x1p-52, -1.0);
-#else
                 const uint64_t m = w >> 11;
                 const double one_m = __longlong_as_double((long long)(0x3FF0000000000000ull | (m & 0xFFFFFFFFFFFFFull)));
                 u = __dsub_rn(one_m, (m >> 52) ? 1.0 : 2.0);
-#endif
             }
             const double v = __dmul_rn(xv, __dadd_rn(1.0, __dmul_rn(u, eps)));
-#if TD_PERTURB_F32RT
-            // Q_bf16 through one XU conversion: f = RN_f32(v), then RN_bf16(f)
-            // (cvt.rn.bf16x2.f32, one instruction per pair).  Rounding twice
-            // equals rounding once unless f is exactly a bf16 midpoint (low
-            // half-word 0x8000) — those, and anything outside [2^-125, bf16
-            // max + half an ulp) (bf16-subnormal range, the reference's
-            // clamp to max_finite, inf/NaN), take the exact path below.
-            const float f = __double2float_rn(v);
-            const uint32_t fb = __float_as_uint(f);
-            // two running extremes instead of per-element tests: 2|f| - 2^-125's
-            // bits must stay below the span to bf16 max + half an ulp (max over
-            // the group), and (f ^ 0x8000) & 0xffff is 0 only at a midpoint (min)
-#if TD_PERTURB_ACC
-            span_max = max(span_max, fb + fb - 0x02000000u);
-            tie_min = min(tie_min, (fb ^ 0x8000u) & 0xffffu);
-#else
-            out_of_range |= (((fb & 0x7fffffffu) - 0x01000000u) < (0x7f7f8000u - 0x01000000u) ? 0u : 1u)
-                            | ((fb & 0xffffu) == 0x8000u ? 1u : 0u);
-#endif
-            fpair[j & 1] = f;
-            if (j & 1) {
-                const __nv_bfloat162 h2 = __floats2bfloat162_rn(fpair[0], fpair[1]);
-                ow[j >> 1] = *reinterpret_cast<const uint32_t*>(&h2);
+#if TD_PERTURB_CVT
+            // Q_bf16 as ONE XU conversion: F2F.BF16.F64 is IEEE round-to-nearest-
+            // even from f64 straight to bf16 — the reference's quantizer wherever
+            // the result is a bf16 normal.  The two halves of each packed pair
+            // are range-tested together (16x2 min/max of the exponent fields):
+            // a zero or subnormal result (exponent 0), an overflow to inf or a
+            // NaN (exponent 0xff: the reference clamps to max_finite instead)
+            // sends the group to the exact path below.
+            {
+                const uint32_t hb = __bfloat16_as_ushort(__double2bfloat16(v));
+                if (j & 1) {
+                    const uint32_t w = (hb << 16) | hlo;
+                    const uint32_t t = w & 0x7f807f80u;
+                    emin = __vminu2(emin, t);
+                    emax = __vmaxu2(emax, t);
+                    ow[j >> 1] = w;
+                } else {
+                    hlo = hb;
+                }
             }
 #else
             const uint64_t b = (uint64_t)__double_as_longlong(v);
@@ -1403,8 +1381,9 @@ k_perturb_bf16(const uint4* __restrict__ x, uint4* __restrict__ y, int64_t rows,
             else ow[j >> 1] = t;
 #endif
         }
-#if TD_PERTURB_F32RT && TD_PERTURB_ACC
-        out_of_range = (span_max >= 0xfeff0000u - 0x02000000u) | (tie_min == 0u);
+#if TD_PERTURB_CVT
+        out_of_range = ((emin & 0xffffu) < 0x0080u) | ((emin >> 16) < 0x0080u) |
+                       ((emax & 0xffffu) > 0x7f00u) | ((emax >> 16) > 0x7f00u);
 #endif
         if (out_of_range) {
 #pragma unroll
