@@ -440,22 +440,71 @@ class DistributedCheckPlan:
         one small all-gather brings those sums to every rank (rank-order
         sums), they replace the affected slots, and td_verdict runs again.
         Messages are issued in remote-group order on every rank, so each
-        (source, destination) pair sees sends and receives in the same order."""
+        (source, destination) pair sees sends and receives in the same order.
+
+        The work for one pattern of differing copies (receive buffers, the
+        bound mini-plans, the patch index) is built once per bound check and
+        reused while the pattern repeats — every step of a run whose bug
+        persists — so a repeat costs the transfers and launches alone."""
+        import torch
+        differs = b.differs.cpu().numpy()
+        remote = self.plan.remote_groups
+        pattern = []
+        for k, entry in enumerate(remote):
+            lo, hi = self.group_begin[k], self.group_begin[k + 1]
+            diff = tuple(c for c in range(1, hi - lo) if differs[lo + c])
+            if diff:
+                pattern.append((k, diff))
+        cache = b.__dict__.setdefault("_bug_cache", {})
+        work = cache.get(tuple(pattern))
+        if work is None:
+            if len(cache) > 8:
+                cache.clear()
+            work = cache[tuple(pattern)] = self._bug_work(pattern)
+        sends, recvs, preps, sub_prep, n_sub, flagged, patch_idx, gathered, mine = work
+        self.comm.exchange(sends, recvs)
+        vec = np.zeros(mine.numel(), np.float64)
+        base = 2 * n_sub
+        for first, prep in preps:
+            prep.launch()
+            prep.fetch()
+            for j, row in enumerate(prep.sums()["group"]):    # the group's chunk slots, in order
+                at = base + N.SLOT_STRIDE * (first + j)
+                vec[at:at + N.SLOT_STRIDE] = row
+        if sub_prep is not None:
+            sub_prep.launch()
+            sub_prep.fetch()
+            vec[:2 * n_sub] = sub_prep.sums()["id"].reshape(-1)
+        # one small all-gather, sums in rank order (as td_combine does)
+        mine.copy_(torch.from_numpy(vec))
+        if vec.size:
+            self.comm.all_gather_into(gathered, mine)
+        rows = gathered.view(self.n_live, -1)
+        total = rows[0].clone()
+        for r in range(1, self.n_live):
+            total += rows[r]
+        if patch_idx is not None:
+            slots = b.prep.slot_sums.view(-1)
+            b.prep.stream.wait_stream(torch.cuda.current_stream())   # the gathered sums
+            with torch.cuda.stream(b.prep.stream):
+                slots[patch_idx[0]] = total[patch_idx[1]]
+        b.prep.verdict(N.stream_handle(b.prep.stream))
+        return b.prep.fetch()
+
+    def _bug_work(self, pattern):
+        """Transfers, bound mini-plans and patch indices for one pattern of
+        differing copies [(remote group, differing copy indices)]."""
         import torch
         from .device import _Raw, _one_group, resolve_operands
         from .plan import Plan, PlanEntry
-        differs = b.differs.cpu().numpy()
         remote = self.plan.remote_groups
         compare_copy = {(ei, gi): c for ei, gi, c in self.plan.compare_reads}
         me = self.comm.rank
         flagged, pending, affected = [], [], set()
         sends, recvs, overrides = [], [], {}
-        for k, entry in enumerate(remote):
-            lo = self.group_begin[k]
+        for k, diff in pattern:
+            entry = remote[k]
             recs = self._remote_group_records(entry)
-            diff = [c for c in range(1, len(recs)) if differs[lo + c]]
-            if not diff:
-                continue
             first = len(flagged)
             flagged.extend(self.plan.slots_of(entry[0]))        # one slot per chunk of MAX_Z copies
             y0 = recs[0]
@@ -487,53 +536,41 @@ class DistributedCheckPlan:
                     overrides[id(holder)] = buf
                 elif y0.owner == me:
                     sends.append((holder.owner, y0.device_payload().reshape(-1)))
-        self.comm.exchange(sends, recvs)
         sub_ids = sorted(affected)
-        vec = np.zeros(2 * len(sub_ids) + N.SLOT_STRIDE * len(flagged), np.float64)
-        base = 2 * len(sub_ids)
+        preps = []
         for first, y0, bufs in pending:
             raws = [_Raw(y0.device_payload().reshape(-1))] + [_Raw(t) for t in bufs]
             mini = Plan([PlanEntry("remote", x=None, y=_one_group("remote", raws, True),
                                    x_rep=False, y_rep=True)])
             ptrs, keep = resolve_operands(mini.operands, mini.operand_dtypes)
-            sums: dict = {}
-            mini.run(ptrs, sums=sums)
-            for j, row in enumerate(sums["group"]):         # the group's chunk slots, in order
-                at = base + N.SLOT_STRIDE * (first + j)
-                vec[at:at + N.SLOT_STRIDE] = row
+            prep = mini.prepare(ptrs)
+            prep._keep = (keep, raws)
+            preps.append((first, prep))
+        sub_prep = None
         if sub_ids:
             sub = Plan([self.plan.entries[ei] for ei in sub_ids], owner=lambda m: m.owner, me=me,
                        compare_copy=self._compare_copy, digest=False)
             ptrs, keep = resolve_operands(sub.operands, sub.operand_dtypes, overrides)
-            sums = {}
-            sub.run(ptrs, sums=sums)
-            vec[:2 * len(sub_ids)] = sums["id"].reshape(-1)
-        # one small all-gather, sums in rank order (as td_combine does)
-        mine = torch.from_numpy(vec).to("cuda")
-        gathered = torch.empty(self.n_live * max(vec.size, 1), dtype=torch.float64, device="cuda")
-        if vec.size:
-            self.comm.all_gather_into(gathered, mine)
-        rows = gathered.view(self.n_live, -1).cpu().numpy()
-        total = rows[0].copy()
-        for r in range(1, self.n_live):
-            total += rows[r]
-        slots = b.prep.slot_sums.view(-1)
+            sub_prep = sub.prepare(ptrs)
+            sub_prep._keep = keep
+        n = 2 * len(sub_ids) + N.SLOT_STRIDE * len(flagged)
+        mine = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
+        gathered = torch.empty(self.n_live * max(n, 1), dtype=torch.float64, device="cuda")
         n_ids = len(self.plan.ids)
-        patch_idx, patch_val = [], []
+        dst, src = [], []
         for j, ei in enumerate(sub_ids):
-            patch_idx += [2 * ei, 2 * ei + 1]
-            patch_val += [total[2 * j], total[2 * j + 1]]
+            dst += [2 * ei, 2 * ei + 1]
+            src += [2 * j, 2 * j + 1]
         base = 2 * len(sub_ids)
         for j, slot in enumerate(flagged):
             g0 = 2 * n_ids + N.SLOT_STRIDE * slot
-            patch_idx += range(g0, g0 + N.SLOT_STRIDE)
-            patch_val += list(total[base + N.SLOT_STRIDE * j:base + N.SLOT_STRIDE * (j + 1)])
-        if patch_idx:
-            with torch.cuda.stream(b.prep.stream):
-                slots[torch.tensor(patch_idx, dtype=torch.int64, device="cuda")] = \
-                    torch.tensor(patch_val, dtype=torch.float64, device="cuda")
-        b.prep.verdict(N.stream_handle(b.prep.stream))
-        return b.prep.fetch()
+            dst += range(g0, g0 + N.SLOT_STRIDE)
+            src += range(base + N.SLOT_STRIDE * j, base + N.SLOT_STRIDE * (j + 1))
+        patch_idx = None
+        if dst:
+            patch_idx = (torch.tensor(dst, dtype=torch.int64, device="cuda"),
+                         torch.tensor(src, dtype=torch.int64, device="cuda"))
+        return sends, recvs, preps, sub_prep, len(sub_ids), flagged, patch_idx, gathered, mine
 
     def execute(self, timing: dict | None = None, staged: dict | None = None):
         """One check: BoundCheck.step (digests, compares, slot reduction, the
