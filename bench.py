@@ -267,6 +267,17 @@ def _sample_ids(ids, size_of, stride: int, budget: int, max_id: int | None = Non
     return out
 
 
+def _ncu_traffic(config: str):
+    """DRAM bytes (read + write) per step of the roofline kernel(s), from the
+    committed ncu capture of this config (profiles/segnorm_traffic.json)."""
+    prof = os.path.join(ROOT, "profiles", "segnorm_traffic.json")
+    if not os.path.exists(prof):
+        return None
+    with open(prof) as fh:
+        entry = json.load(fh).get("configs", {}).get(config)
+    return entry.get("dram_bytes_per_step") if entry else None
+
+
 def _pageable_e2e(href, hcand, tol, fmt, alg_bytes):
     """The same check() from ordinary (pageable) host tensors, the form a
     reference user's traces arrive in: check() stages them through its
@@ -580,7 +591,8 @@ def run_distributed(args, world: int, rank: int, local: int):
                 "near_ties": ties,
                 "roofline": {"bound": "hbm", "achieved": pass_bytes / (pass_ms / 1e3) / 1e9,
                              "peak": hbm, "unit": "GB/s",
-                             "frac": pass_bytes / (pass_ms / 1e3) / 1e9 / hbm, "traffic": None,
+                             "frac": pass_bytes / (pass_ms / 1e3) / 1e9 / hbm,
+                             "traffic": _ncu_traffic(args.config) if world == 1 else None,
                              "kernel": "td_segnorm (incl. digest classes) + td_fingerprint on a side stream, rank 0",
                              "kernel_ms": pass_ms, "peak_source": peak_kind},
                 "cpu_baseline": None, "e2e": e2e,
@@ -877,14 +889,7 @@ def main():
             cpu = cpu_baseline(href, hcand, tol, fmt, args.cpu_stride)
         else:
             cpu = cpu_baseline(ref, cand, tol, fmt, args.cpu_stride)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "segnorm_traffic.json")
-    if os.path.exists(prof):
-        with open(prof) as fh:
-            doc = json.load(fh)
-        entry = doc.get("configs", {}).get(args.config)
-        if entry:
-            traffic = entry.get("dram_bytes_per_step")
+    traffic = _ncu_traffic(args.config)
     if rank == 0:
         line = {"metric": "traced-tensor compare GB/s vs HBM roofline; layer-checks/sec",
                 "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
