@@ -1634,6 +1634,77 @@ __global__ void __launch_bounds__(256) k_gather_bytes(const unsigned char* __res
     }
 }
 
+// The same gather through shared memory: per 16 KiB piece one elected thread
+// moves the piece's source bytes, widened to the enclosing aligned 16-byte
+// blocks, with ONE cp.async.bulk (the TMA engine; 16-B aligned by
+// construction whatever the record's offset) into a shared-memory stage,
+// tracked by an mbarrier's transaction count; the CTA writes aligned uint4s
+// built from 4-byte shared-memory words funnel-shifted into place (any source
+// misalignment), with bytewise heads / tails.  Bulk copies hold no registers
+// in flight, so the 8 resident CTAs of an SM keep 128 KiB of loads
+// outstanding (a second stage per CTA, the next piece's copy overlapping
+// this one's stores, measured slower: 33 KiB per CTA leaves 6 resident).
+// The widened block never reaches past the 16-B block holding the range's
+// last byte (same page), as the LDG kernel's aligned words.
+#ifndef TD_GATHER_STAGE
+#define TD_GATHER_STAGE (16 << 10)
+#endif
+constexpr int GATHER_SMEM = TD_GATHER_STAGE + 64 + 16;
+__global__ void __launch_bounds__(256) k_gather_staged(const unsigned char* __restrict__ src,
+                                                       unsigned char* __restrict__ dst,
+                                                       const int64_t* __restrict__ ranges, int64_t n) {
+    extern __shared__ __align__(128) unsigned char sm[];
+    const uint32_t sbase = smem_addr(sm);
+    const uint32_t sbar = smem_addr(sm + TD_GATHER_STAGE + 64);
+    uint64_t policy = 0;
+    if (threadIdx.x == 0) {
+        mbar_init(sbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    }
+    __syncthreads();
+    const uint32_t* sw = reinterpret_cast<const uint32_t*>(sm);
+    uint32_t phase = 0;
+    const int64_t grid = gridDim.x;
+    int64_t base = 0;
+    for (int64_t r = 0; r < n; ++r) {
+        const int64_t so = ranges[3 * r], dof = ranges[3 * r + 1], nb = ranges[3 * r + 2];
+        const int64_t pieces = (nb + TD_GATHER_STAGE - 1) / TD_GATHER_STAGE;
+        int64_t k = ((int64_t)blockIdx.x - base % grid + grid) % grid;
+        base += pieces;
+        for (; k < pieces; k += grid) {
+            const int64_t lo = k * TD_GATHER_STAGE;
+            const uint32_t len = (uint32_t)(nb - lo < TD_GATHER_STAGE ? nb - lo : TD_GATHER_STAGE);
+            const unsigned char* s = src + so + lo;
+            unsigned char* d = dst + dof + lo;
+            const uint32_t mis0 = (uint32_t)(reinterpret_cast<uintptr_t>(s) & 15);
+            const uint32_t bytes = (mis0 + len + 15u) & ~15u;
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // earlier reads before the refill
+                mbar_expect_tx(sbar, bytes);
+                bulk_g2s(sbase, s - mis0, bytes, sbar, policy);
+            }
+            mbar_wait(sbar, phase);
+            phase ^= 1u;
+            uint32_t head = (16u - (uint32_t)(reinterpret_cast<uintptr_t>(d) & 15)) & 15u;
+            if (head > len) head = len;
+            if (threadIdx.x < head) d[threadIdx.x] = sm[mis0 + threadIdx.x];
+            const uint32_t off = mis0 + head;               // staged byte of output byte `head`
+            const uint32_t v = (len - head) >> 4;
+            const uint32_t q = off >> 2, sh = 8u * (off & 3u);
+            uint4* d16 = reinterpret_cast<uint4*>(d + head);
+            for (uint32_t i = threadIdx.x; i < v; i += blockDim.x) {
+                const uint32_t* w = sw + q + 4 * i;
+                const uint32_t w0 = w[0], w1 = w[1], w2 = w[2], w3 = w[3], w4 = w[4];
+                d16[i] = make_uint4(__funnelshift_r(w0, w1, sh), __funnelshift_r(w1, w2, sh),
+                                    __funnelshift_r(w2, w3, sh), __funnelshift_r(w3, w4, sh));
+            }
+            for (uint32_t i = head + 16 * v + threadIdx.x; i < len; i += blockDim.x) d[i] = sm[mis0 + i];
+            __syncthreads();                                 // the stage is free again
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Multi-GPU combine, after ONE all-gather of every live rank's
 // exchange buffer [slot sums: n_slots f64 | digest rows: 2 u64 each], rank r
@@ -1699,6 +1770,16 @@ AuxStreams* aux_streams(int dev) {
 void join_aux(AuxStreams* a, int k, cudaStream_t main_stream) {
     cudaEventRecord(a->join[k], a->stream[k]);
     cudaStreamWaitEvent(main_stream, a->join[k], 0);
+}
+
+// TD_GATHER_STAGED=0: td_gather_bytes on the LDG walker instead of the
+// shared-memory staged one (A/B)
+bool gather_staged() {
+    static const bool on = [] {
+        const char* e = getenv("TD_GATHER_STAGED");
+        return e == nullptr || e[0] != '0';
+    }();
+    return on;
 }
 
 bool serial_classes() {
@@ -2030,6 +2111,11 @@ int td_gather_bytes(const void* src, void* dst, const int64_t* ranges, int64_t n
     if (n == 0) return 0;
     if (!src || !dst || !ranges || n < 0) return fail("td_gather_bytes: invalid arguments");
     const int grid = 148 * 8;
+    if (gather_staged()) {
+        k_gather_staged<<<grid, 256, GATHER_SMEM, (cudaStream_t)stream>>>(
+            static_cast<const unsigned char*>(src), static_cast<unsigned char*>(dst), ranges, n);
+        return check_launch("td_gather_bytes");
+    }
     k_gather_bytes<<<grid, 256, 0, (cudaStream_t)stream>>>(static_cast<const unsigned char*>(src),
                                                            static_cast<unsigned char*>(dst), ranges, n);
     return check_launch("td_gather_bytes");
