@@ -166,13 +166,14 @@ def _dp_tp_worker(rank, world, port, out_dir, shape, tp):
         dist.destroy_process_group()
 
 
-def test_live_dp2_tp2_microbatches_match_single_device(tmp_path):
+@pytest.mark.parametrize("shape", [SHAPE, LLAMA], ids=["gpt", "llama"])
+def test_live_dp2_tp2_microbatches_match_single_device(tmp_path, shape):
     """DP=2 x TP=2 live job (4 gloo ranks, TP sub-groups): DP rank d runs
     microbatch d; every capture carries its (dp, tp) rank and the layout's
     map (ids iter=0|mb=d|...); the union equals a single device running both
     microbatches, per the CPU oracle, and covers the layout's id set."""
     world, tp = 4, 2
-    mp.start_processes(_dp_tp_worker, args=(world, _free_port(), str(tmp_path), SHAPE, tp),
+    mp.start_processes(_dp_tp_worker, args=(world, _free_port(), str(tmp_path), shape, tp),
                        nprocs=world, join=True, start_method="spawn")
     ranks = []
     for r in range(world):
@@ -181,12 +182,12 @@ def test_live_dp2_tp2_microbatches_match_single_device(tmp_path):
     cand = [f for r in ranks for f in r["records"]]
     assert {(f["rank"][0], f["rank"][1]) for f in cand} == {(0, 0), (0, 1), (1, 0), (1, 1)}
     assert {f["ident"].split("|")[1] for f in cand} == {"mb=0", "mb=1"}
-    ref = [_flat(r) for mb in (0, 1) for r in tp_gpt.traced_step(SHAPE, tp_gpt.TPGroup(), microbatch=mb).records]
+    ref = [_flat(r) for mb in (0, 1) for r in tp_gpt.traced_step(shape, tp_gpt.TPGroup(), microbatch=mb).records]
     doc = O.check(_oracle_recs(ref), _oracle_recs(cand), ranks[0]["header"], ranks[0]["header"], {}, 3.0, "BF16")
     assert doc["exit_code"] == 0 and doc["summary"]["missing"] == 0, doc["summary"]
     assert max(e["observed"] for e in doc["entries"]) < 1e-5
     kinds = ("ActivationIn", "ActivationOut", "ParamGrad")
-    want = {sp.ident for sp in Layout(tp_gpt.model_shape(SHAPE), ParallelConfig(tp=2, dp=2, microbatches=2)).records()
+    want = {sp.ident for sp in Layout(tp_gpt.model_shape(shape), ParallelConfig(tp=2, dp=2, microbatches=2)).records()
             if sp.kind in kinds}
     assert {f["ident"] for f in cand if not f["ident"].endswith(".norm")} == want
 
