@@ -351,3 +351,36 @@ def test_config4_layout_eight_shares_match_single_gpu_and_oracle():
         assert g["verdict"] == w["verdict"] and g["detail"] == w["detail"], (w["id"], g, w)
         from tests.test_gpu_parity import _close
         assert _close(g["observed"], w["observed"]), (w["id"], g["observed"], w["observed"])
+
+
+@pytest.mark.gpu
+def test_distributed_clean_step_replays_as_one_cuda_graph():
+    """The multi-GPU clean path (digests fused in the compare pass and by
+    td_fingerprint on a side stream, td_segnorm, slot reduction, the
+    exchange, td_combine, td_verdict) has no host synchronisation, so one
+    GPU's share of a config-4-layout job captures into ONE CUDA graph;
+    replays give the eager step's verdicts, sums and digest table bit for
+    bit."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2506_09280_b200.distributed import StaticComm
+    lay = synthetic.ShareLayout(CFG4_SHAPE, CFG4_PCFG, 8)
+    ref, cand = lay.build(0)
+    rm, cm = lay.metas()
+    plan = DistributedCheckPlan(ref, cand, _tol(lay), fmt=FloatFormat.BF16, comm=StaticComm(0, 8, [rm, cm]))
+    assert plan.plan.remote_groups and plan.plan.fused_digests
+    b = plan.bind()
+    b.step()
+    idres, gres, ties, n_diff = b.fetch()
+    digests = b.local_digests()
+    sums = b.prep.slot_sums.clone()
+    graph = b.capture()
+    for _ in range(3):
+        b.prep.slot_sums.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        idres2, gres2, ties2, n_diff2 = b.fetch()
+        assert idres2.tobytes() == idres.tobytes() and gres2.tobytes() == gres.tobytes()
+        assert (ties2, n_diff2) == (ties, n_diff) == (0, 0)
+        assert torch.equal(b.prep.slot_sums, sums)
+        assert b.local_digests() == digests
