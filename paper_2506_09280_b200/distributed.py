@@ -461,23 +461,19 @@ class DistributedCheckPlan:
             if len(cache) > 8:
                 cache.clear()
             work = cache[tuple(pattern)] = self._bug_work(pattern)
-        sends, recvs, preps, sub_prep, n_sub, flagged, patch_idx, gathered, mine = work
+        sends, recvs, assembly, patch_idx, gathered, mine, n_sums = work
         self.comm.exchange(sends, recvs)
-        vec = np.zeros(mine.numel(), np.float64)
-        base = 2 * n_sub
-        for first, prep in preps:
+        # the mini-plans run on this stream and their sums are moved into the
+        # exchange vector on the device: no host round trip for them
+        cur = torch.cuda.current_stream()
+        for prep, src, dst in assembly:
             prep.launch()
-            prep.fetch()
-            for j, row in enumerate(prep.sums()["group"]):    # the group's chunk slots, in order
-                at = base + N.SLOT_STRIDE * (first + j)
-                vec[at:at + N.SLOT_STRIDE] = row
-        if sub_prep is not None:
-            sub_prep.launch()
-            sub_prep.fetch()
-            vec[:2 * n_sub] = sub_prep.sums()["id"].reshape(-1)
-        # one small all-gather, sums in rank order (as td_combine does)
-        mine.copy_(torch.from_numpy(vec))
-        if vec.size:
+            cur.wait_stream(prep.stream)
+            mine[dst] = prep.slot_sums[src]
+        # one small all-gather, sums in rank order (as td_combine does); every
+        # rank takes part (its vector may hold zeros only: not every rank runs
+        # a mini-plan)
+        if n_sums:
             self.comm.all_gather_into(gathered, mine)
         rows = gathered.view(self.n_live, -1)
         total = rows[0].clone()
@@ -537,7 +533,8 @@ class DistributedCheckPlan:
                 elif y0.owner == me:
                     sends.append((holder.owner, y0.device_payload().reshape(-1)))
         sub_ids = sorted(affected)
-        preps = []
+        base = 2 * len(sub_ids)
+        assembly = []             # (bound mini-plan, its slot-sum indices, exchange-vector indices)
         for first, y0, bufs in pending:
             raws = [_Raw(y0.device_payload().reshape(-1))] + [_Raw(t) for t in bufs]
             mini = Plan([PlanEntry("remote", x=None, y=_one_group("remote", raws, True),
@@ -545,14 +542,18 @@ class DistributedCheckPlan:
             ptrs, keep = resolve_operands(mini.operands, mini.operand_dtypes)
             prep = mini.prepare(ptrs)
             prep._keep = (keep, raws)
-            preps.append((first, prep))
-        sub_prep = None
+            width = N.SLOT_STRIDE * len(mini.groups)      # the group's chunk slots, in order
+            src = 2 * len(mini.ids) + torch.arange(width, device="cuda")
+            dst = base + N.SLOT_STRIDE * first + torch.arange(width, device="cuda")
+            assembly.append((prep, src, dst))
         if sub_ids:
             sub = Plan([self.plan.entries[ei] for ei in sub_ids], owner=lambda m: m.owner, me=me,
                        compare_copy=self._compare_copy, digest=False)
             ptrs, keep = resolve_operands(sub.operands, sub.operand_dtypes, overrides)
             sub_prep = sub.prepare(ptrs)
             sub_prep._keep = keep
+            idx = torch.arange(2 * len(sub_ids), device="cuda")
+            assembly.append((sub_prep, idx, idx))
         n = 2 * len(sub_ids) + N.SLOT_STRIDE * len(flagged)
         mine = torch.zeros(max(n, 1), dtype=torch.float64, device="cuda")
         gathered = torch.empty(self.n_live * max(n, 1), dtype=torch.float64, device="cuda")
@@ -570,7 +571,7 @@ class DistributedCheckPlan:
         if dst:
             patch_idx = (torch.tensor(dst, dtype=torch.int64, device="cuda"),
                          torch.tensor(src, dtype=torch.int64, device="cuda"))
-        return sends, recvs, preps, sub_prep, len(sub_ids), flagged, patch_idx, gathered, mine
+        return sends, recvs, assembly, patch_idx, gathered, mine, n
 
     def execute(self, timing: dict | None = None, staged: dict | None = None):
         """One check: BoundCheck.step (digests, compares, slot reduction, the
