@@ -66,6 +66,10 @@ class Comm:
         """sends: [(dst, tensor)], recvs: [(src, tensor)] — matched in order."""
         raise NotImplementedError
 
+    def broadcast_(self, tensor, src: int) -> None:
+        """tensor <- rank src's tensor on every rank (CUDA, current stream)."""
+        raise NotImplementedError
+
     def live_ranks(self) -> list:
         """The ranks whose buffers all_gather_into collects, in row order."""
         return list(range(self.world))
@@ -99,6 +103,14 @@ class TorchComm(Comm):
             out.copy_(host)
             return
         self.dist.all_gather_into_tensor(out, inp, group=self.group)
+
+    def broadcast_(self, tensor, src: int) -> None:
+        if tensor.is_cuda and self.dist.get_backend(self.group) == "gloo":
+            host = tensor.cpu()                # gloo moves host tensors
+            self.dist.broadcast(host, src=self._g(src), group=self.group)
+            tensor.copy_(host)
+            return
+        self.dist.broadcast(tensor, src=self._g(src), group=self.group)
 
     def exchange(self, sends, recvs) -> None:
         gloo = self.dist.get_backend(self.group) == "gloo"
@@ -167,6 +179,14 @@ class ThreadComm(Comm):
             rows[r].copy_(t)
         self._sync()
 
+    def broadcast_(self, tensor, src: int) -> None:
+        if self.rank == src:
+            self.hub.slots[src] = tensor
+        self._sync()
+        if self.rank != src:
+            tensor.copy_(self.hub.slots[src])
+        self._sync()
+
     def exchange(self, sends, recvs) -> None:
         for k, (dst, t) in enumerate(sends):
             self.hub.mail[(self.rank, dst, k)] = t
@@ -210,6 +230,12 @@ class StaticComm(Comm):
             self.inner.exchange(sends, recvs)
         elif sends or recvs:
             raise N.NativeError("StaticComm: point-to-point traffic with ranks that are not running")
+
+    def broadcast_(self, tensor, src: int) -> None:
+        if self.inner is not None:
+            self.inner.broadcast_(tensor, src)
+        elif src != self.rank:
+            raise N.NativeError("StaticComm: broadcast from a rank that is not running")
 
     def live_ranks(self) -> list:
         """Virtual ranks 0..inner.world-1 are the running ones (this process
@@ -432,18 +458,22 @@ class DistributedCheckPlan:
     def _bug_path(self, b: "BoundCheck"):
         """Some copy's digest differs from its copy 0's (a real replica
         divergence): exact sums for exactly the affected slots.
-          * copy 0's rank receives the differing copies and computes the
-            group's replica sums (y2, z2...) — canonical.py:236-242;
+          * copy 0 of each differing group is broadcast from its holder to
+            every rank (one NCCL broadcast per group, in remote-group order);
+          * every rank holding a differing copy computes that copy's replica
+            sum against it, copy 0's holder the group's y2 (copies whose
+            digests matched add exactly 0) — canonical.py:236-242;
           * an id whose compare read a differing copy (compare_copies) has
-            its compare re-run on every rank, for that id alone, reading
-            copy 0 (sent to the compare holder);
+            its compare re-run on every rank, for that id alone, reading the
+            broadcast copy 0;
         one small all-gather brings those sums to every rank (rank-order
-        sums), they replace the affected slots, and td_verdict runs again.
-        Messages are issued in remote-group order on every rank, so each
-        (source, destination) pair sees sends and receives in the same order.
+        sums, each slot written by exactly one rank), they replace the
+        affected slots, and td_verdict runs again.  Every rank receives each
+        differing group's copy 0 once, instead of copy 0's rank receiving
+        every copy.
 
-        The work for one pattern of differing copies (receive buffers, the
-        bound mini-plans, the patch index) is built once per bound check and
+        The work for one pattern of differing copies (broadcast buffers, the
+        bound mini-plans, the index maps) is built once per bound check and
         reused while the pattern repeats — every step of a run whose bug
         persists — so a repeat costs the transfers and launches alone."""
         import torch
@@ -461,8 +491,9 @@ class DistributedCheckPlan:
             if len(cache) > 8:
                 cache.clear()
             work = cache[tuple(pattern)] = self._bug_work(pattern)
-        sends, recvs, assembly, patch_idx, gathered, mine, n_sums = work
-        self.comm.exchange(sends, recvs)
+        casts, assembly, patch_idx, gathered, mine, n_sums = work
+        for tensor, src in casts:
+            self.comm.broadcast_(tensor, src)
         # the mini-plans run on this stream and their sums are moved into the
         # exchange vector on the device: no host round trip for them
         cur = torch.cuda.current_stream()
@@ -471,8 +502,7 @@ class DistributedCheckPlan:
             cur.wait_stream(prep.stream)
             mine[dst] = prep.slot_sums[src]
         # one small all-gather, sums in rank order (as td_combine does); every
-        # rank takes part (its vector may hold zeros only: not every rank runs
-        # a mini-plan)
+        # rank takes part (its vector may hold zeros only)
         if n_sums:
             self.comm.all_gather_into(gathered, mine)
         rows = gathered.view(self.n_live, -1)
@@ -488,64 +518,59 @@ class DistributedCheckPlan:
         return b.prep.fetch()
 
     def _bug_work(self, pattern):
-        """Transfers, bound mini-plans and patch indices for one pattern of
-        differing copies [(remote group, differing copy indices)]."""
+        """Broadcast buffers, bound mini-plans and index maps for one pattern
+        of differing copies [(remote group, differing copy indices)]."""
         import torch
         from .device import _Raw, _one_group, resolve_operands
         from .plan import Plan, PlanEntry
         remote = self.plan.remote_groups
         compare_copy = {(ei, gi): c for ei, gi, c in self.plan.compare_reads}
-        me = self.comm.rank
-        flagged, pending, affected = [], [], set()
-        sends, recvs, overrides = [], [], {}
+        me, Z, S = self.comm.rank, N.MAX_Z, N.SLOT_STRIDE
+        flagged, tasks, affected, casts, overrides = [], [], set(), [], {}
         for k, diff in pattern:
             entry = remote[k]
             recs = self._remote_group_records(entry)
             first = len(flagged)
-            flagged.extend(self.plan.slots_of(entry[0]))        # one slot per chunk of MAX_Z copies
+            n_chunks = len(self.plan.slots_of(entry[0]))       # one slot per chunk of MAX_Z copies
+            flagged.extend(self.plan.slots_of(entry[0]))
             y0 = recs[0]
             if y0.owner == me:
-                bufs = []
-                for m in recs[1:]:
-                    if m.owner == me:
-                        bufs.append(m.device_payload().reshape(-1))
-                    else:
-                        buf = torch.empty(int(np.prod(m.shape)), dtype=_torch_dtype(m.dtype_code),
-                                          device="cuda")
-                        recvs.append((m.owner, buf))
-                        bufs.append(buf)
-                pending.append((first, y0, bufs))
+                y0t = y0.device_payload()
             else:
-                for m in recs[1:]:
-                    if m.owner == me:
-                        sends.append((y0.owner, m.device_payload().reshape(-1)))
+                y0t = torch.empty(tuple(y0.shape), dtype=_torch_dtype(y0.dtype_code), device="cuda")
+            casts.append((y0t.reshape(-1), y0.owner))
+            mine_copies = [c for c in diff if recs[c].owner == me]
+            if y0.owner == me or mine_copies:
+                tasks.append((first, n_chunks, y0.owner == me, y0t, [(c, recs[c]) for c in mine_copies]))
             _, ei, side, gi = entry
             cc = compare_copy.get((ei, gi), 0) if side == 0 else 0
             if cc and cc in diff:
                 affected.add(ei)
-                holder = recs[cc]
-                if holder.owner == me and y0.owner == me:
-                    overrides[id(holder)] = y0.device_payload()
-                elif holder.owner == me:
-                    buf = torch.empty(tuple(y0.shape), dtype=_torch_dtype(y0.dtype_code), device="cuda")
-                    recvs.append((y0.owner, buf.view(-1)))
-                    overrides[id(holder)] = buf
-                elif y0.owner == me:
-                    sends.append((holder.owner, y0.device_payload().reshape(-1)))
+                if recs[cc].owner == me:
+                    overrides[id(recs[cc])] = y0t
         sub_ids = sorted(affected)
         base = 2 * len(sub_ids)
         assembly = []             # (bound mini-plan, its slot-sum indices, exchange-vector indices)
-        for first, y0, bufs in pending:
-            raws = [_Raw(y0.device_payload().reshape(-1))] + [_Raw(t) for t in bufs]
-            mini = Plan([PlanEntry("remote", x=None, y=_one_group("remote", raws, True),
+        for first, n_chunks, owner, y0t, copies in tasks:
+            y0r = _Raw(y0t.reshape(-1))
+            # copy 0 itself stands in when this rank holds no differing copy:
+            # its slot's y2 is what copy 0's holder owes the group
+            zs = [_Raw(m.device_payload().reshape(-1)) for _, m in copies] or [y0r]
+            mini = Plan([PlanEntry("remote", x=None, y=_one_group("remote", [y0r] + zs, True),
                                    x_rep=False, y_rep=True)])
             ptrs, keep = resolve_operands(mini.operands, mini.operand_dtypes)
             prep = mini.prepare(ptrs)
-            prep._keep = (keep, raws)
-            width = N.SLOT_STRIDE * len(mini.groups)      # the group's chunk slots, in order
-            src = 2 * len(mini.ids) + torch.arange(width, device="cuda")
-            dst = base + N.SLOT_STRIDE * first + torch.arange(width, device="cuda")
-            assembly.append((prep, src, dst))
+            prep._keep = (keep, y0r, zs)
+            g0 = 2 * len(mini.ids)                         # the mini-plan's first group slot
+            src, dst = [], []
+            for pos, (c, _) in enumerate(copies):          # z of copy c, its own global slot
+                src.append(g0 + S * (pos // Z) + 1 + pos % Z)
+                dst.append(base + S * (first + (c - 1) // Z) + 1 + (c - 1) % Z)
+            if owner:                                      # y2 into every chunk slot of the group
+                for j in range(n_chunks):
+                    src.append(g0)
+                    dst.append(base + S * (first + j))
+            assembly.append((prep, torch.tensor(src, device="cuda"), torch.tensor(dst, device="cuda")))
         if sub_ids:
             sub = Plan([self.plan.entries[ei] for ei in sub_ids], owner=lambda m: m.owner, me=me,
                        compare_copy=self._compare_copy, digest=False)
@@ -571,7 +596,7 @@ class DistributedCheckPlan:
         if dst:
             patch_idx = (torch.tensor(dst, dtype=torch.int64, device="cuda"),
                          torch.tensor(src, dtype=torch.int64, device="cuda"))
-        return sends, recvs, assembly, patch_idx, gathered, mine, n
+        return casts, assembly, patch_idx, gathered, mine, n
 
     def execute(self, timing: dict | None = None, staged: dict | None = None):
         """One check: BoundCheck.step (digests, compares, slot reduction, the
