@@ -21,12 +21,13 @@ SURVEY §8(e).  A canonical id's compare is a sum over disjoint boxes, so:
    0's on the device, and td_verdict runs on the sums.  The clean path has no
    host synchronisation until the one D2H of the verdicts (which carries the
    digest-mismatch count), so a step can be captured in a CUDA graph;
-5. only when a digest differs (the bug path) does the host step in: the
-   differing copies travel point-to-point to copy 0's rank, which computes
-   the exact replica sums; a compare that read a differing copy is re-run,
-   for the affected ids only, reading copy 0; one more small exchange
-   patches those slots and td_verdict runs again — results are exactly the
-   reference's (checker.py:184-191, canonical.py:225-247).
+5. only when a digest differs (the bug path) does the host step in: copy
+   0 of each differing group is broadcast to every rank, each holder of a
+   differing copy computes that copy's exact replica sum where it lives
+   (copy 0's holder the group's y2); a compare that read a differing copy
+   is re-run, for the affected ids only, reading copy 0; one more small
+   all-gather patches those slots and td_verdict runs again — results are
+   exactly the reference's (checker.py:184-191, canonical.py:225-247).
 
 `Comm` abstracts the collectives: `TorchComm` wraps torch.distributed (NCCL
 on the GPU box, gloo for the CPU tests); `ThreadComm` runs N logical ranks
