@@ -542,7 +542,6 @@ def check_streaming(ref: Trace, run: Callable, tol: ToleranceMap, kappa: float =
     work = torch.zeros(N.REL_ERR_WORK_BYTES, dtype=torch.uint8, device="cuda")
     order: list = []
     shapes: dict = {}
-    direct: dict = {}
 
     def sink(ident, tensor, module_class):
         order.append(ident)

@@ -63,10 +63,6 @@ class Comm:
     def all_reduce_sum_(self, tensor) -> None:
         raise NotImplementedError
 
-    def exchange(self, sends: list, recvs: list) -> None:
-        """sends: [(dst, tensor)], recvs: [(src, tensor)] — matched in order."""
-        raise NotImplementedError
-
     def broadcast_(self, tensor, src: int) -> None:
         """tensor <- rank src's tensor on every rank (CUDA, current stream)."""
         raise NotImplementedError
@@ -113,21 +109,6 @@ class TorchComm(Comm):
             return
         self.dist.broadcast(tensor, src=self._g(src), group=self.group)
 
-    def exchange(self, sends, recvs) -> None:
-        gloo = self.dist.get_backend(self.group) == "gloo"
-        if gloo:                           # gloo moves host tensors
-            sends = [(d, t.cpu()) for d, t in sends]
-            back = [(t, t.new_empty(t.shape, device="cpu")) for _, t in recvs]
-            recvs = [(s, h) for (s, _), (_, h) in zip(recvs, back)]
-        ops = [self.dist.P2POp(self.dist.isend, t, self._g(d), self.group) for d, t in sends]
-        ops += [self.dist.P2POp(self.dist.irecv, t, self._g(s), self.group) for s, t in recvs]
-        if ops:
-            for req in self.dist.batch_isend_irecv(ops):
-                req.wait()
-        if gloo:
-            for dev, host in back:
-                dev.copy_(host)
-
     def _g(self, r):
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
 
@@ -137,7 +118,6 @@ class _ThreadHub:
         self.world = world
         self.barrier = threading.Barrier(world)
         self.slots = [None] * world
-        self.mail: dict = {}
 
 
 class ThreadComm(Comm):
@@ -188,22 +168,6 @@ class ThreadComm(Comm):
             tensor.copy_(self.hub.slots[src])
         self._sync()
 
-    def exchange(self, sends, recvs) -> None:
-        for k, (dst, t) in enumerate(sends):
-            self.hub.mail[(self.rank, dst, k)] = t
-        self._sync()
-        counters: dict = {}
-        for src, t in recvs:
-            k = counters.get(src, 0)
-            # sends from `src` to me are numbered in src's send order, skipping other dsts
-            mine = sorted(key for key in self.hub.mail if key[0] == src and key[1] == self.rank)
-            t.copy_(self.hub.mail[mine[k]])
-            counters[src] = k + 1
-        self._sync()
-        if self.rank == 0:
-            self.hub.mail.clear()
-        self._sync()
-
 
 class StaticComm(Comm):
     """A rank of a job whose record metadata is known in advance
@@ -225,12 +189,6 @@ class StaticComm(Comm):
     def all_reduce_sum_(self, tensor) -> None:
         if self.inner is not None:
             self.inner.all_reduce_sum_(tensor)
-
-    def exchange(self, sends, recvs) -> None:
-        if self.inner is not None:
-            self.inner.exchange(sends, recvs)
-        elif sends or recvs:
-            raise N.NativeError("StaticComm: point-to-point traffic with ranks that are not running")
 
     def broadcast_(self, tensor, src: int) -> None:
         if self.inner is not None:
