@@ -356,3 +356,35 @@ def test_wide_replica_group_across_threads(corrupt):
     assert not errors, errors[0]
     for rep in reports:
         assert_reports_match(rep, want, f"16 copies over 4 ranks {corrupt}")
+
+
+def test_global_trace_falls_back_to_rank_major_for_foreign_module_names():
+    """Ids that are not the reference model's modules (an arbitrary torchtap
+    model) have no schedule position: the merged order is rank-major, with
+    each rank's own record order kept."""
+    import torch
+    from paper_2506_09280_b200.canonical import identity_mapping, parse_canonical
+    from paper_2506_09280_b200.layout import execution_key
+    from paper_2506_09280_b200.tracestore import RankMeta, TraceRecord
+    names = ["model.layers.0.attn", "model.encoder.block3", "model.layers.1.mlp"]
+    assert execution_key(parse_canonical(f"iter=0|mb=0|kind=ActivationOut|mod={names[1]}"), RankMeta()) is None
+    traces = []
+    for r in range(2):
+        t = Trace(header={"digest": "d", "mode": "cascade"})
+        for name in (names if r == 0 else names[::-1]):
+            t.records.append(TraceRecord(parse_canonical(f"iter=0|mb=0|kind=ActivationOut|mod={name}"),
+                                         RankMeta(tp=r), identity_mapping((2, 2)), 2, torch.zeros(2, 2), "M"))
+        traces.append(t)
+    hub = ThreadComm.hub(2)
+    out = [None, None]
+
+    def worker(rank):
+        out[rank] = global_trace(traces[rank], ThreadComm(hub, rank))
+    threads = [threading.Thread(target=worker, args=(r,)) for r in range(2)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=60)
+    for g in out:
+        assert [(m.rank_meta.tp, m.id.module_name) for m in g.records] == \
+            [(0, n) for n in names] + [(1, n) for n in names[::-1]]
