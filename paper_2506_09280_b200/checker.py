@@ -299,10 +299,20 @@ def check(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float = 3.0, *,
     kappa * max(tolerance, fmt.eps).
 
     Host-resident payloads start their H2D copies before planning, so the
-    metadata work overlaps the DMA."""
+    metadata work overlaps the DMA.  Host traces larger than the device's
+    free memory are checked in consecutive batches of ids (the reference
+    checks host traces of any size), with the same report."""
     if kappa <= 0:
         raise ConfigInvalid("kappa must be positive")
     _require_same_setup(ref, cand)
+    budget = _hbm_budget()
+    if budget is not None and _host_bytes(ref) + _host_bytes(cand) > budget:
+        return _check_in_batches(ref, cand, tol, kappa, fmt, budget)
+    return _check_direct(ref, cand, tol, kappa, fmt)
+
+
+def _check_direct(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float, fmt: FloatFormat) -> CheckReport:
+    """check() with every payload staged on the device at once."""
     from .device import stage_host_payloads
     staged = stage_host_payloads([ref, cand])
     key = _check_key(ref, cand, tol, kappa, fmt)
@@ -319,6 +329,82 @@ def check(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float = 3.0, *,
         _PLAN_CACHE.pop(next(iter(_PLAN_CACHE)))
     _PLAN_CACHE[key] = (cp, cp.detach())
     return report
+
+
+def _host_bytes(trace: Trace) -> int:
+    """Payload bytes check() would have to bring to the device."""
+    total = 0
+    for r in trace.records:
+        p = r.payload
+        if not (getattr(p, "is_cuda", False)):
+            total += r.nbytes
+    return total
+
+
+def _hbm_budget() -> int | None:
+    """Device bytes a check may stage at once: TD_HBM_BUDGET_BYTES, else the
+    free HBM less a margin for plan tables and workspace (None without a
+    GPU: check() then fails loudly further down, as before)."""
+    import os
+    env = os.environ.get("TD_HBM_BUDGET_BYTES")
+    if env:
+        return int(env)
+    try:
+        import torch
+        if not torch.cuda.is_available():
+            return None
+        free, _ = torch.cuda.mem_get_info()
+        free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()   # the allocator's cache
+    except Exception:  # pragma: no cover - no driver
+        return None
+    return int(free * 0.9) - (1 << 30)
+
+
+def _check_in_batches(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float, fmt: FloatFormat,
+                      budget: int) -> CheckReport:
+    """check() of host traces larger than the device: the candidate's ids,
+    in execution order, are cut into consecutive batches whose payloads (both
+    sides) fit `budget`; each batch is an ordinary check of the two traces
+    restricted to its ids (every id's verdict depends on its own records
+    only), and the entries are concatenated in the same order — candidate
+    execution order, then reference-only ids — so the report is the one
+    check() of the whole traces gives (checker.py:328-365)."""
+    cand_ids = cand.by_id()
+    ref_ids = ref.by_id()
+    size = {}
+    for trace in (ref, cand):
+        for r in trace.records:
+            if not getattr(r.payload, "is_cuda", False):
+                ident = r.id.encode()
+                size[ident] = size.get(ident, 0) + r.nbytes
+    batches, cur, used = [], [], 0
+    for ident in cand_ids:
+        nb = size.get(ident, 0)
+        if cur and used + nb > budget:
+            batches.append(cur)
+            cur, used = [], 0
+        cur.append(ident)
+        used += nb
+    if cur:
+        batches.append(cur)
+    entries, ties = [], 0
+    for ids in batches:
+        keep = set(ids)
+        sub_ref = Trace(header=ref.header, raw_header=ref.raw_header,
+                        records=[r for r in ref.records if r.id.encode() in keep])
+        sub_cand = Trace(header=cand.header, raw_header=cand.raw_header,
+                         records=[r for r in cand.records if r.id.encode() in keep])
+        rep = _check_direct(sub_ref, sub_cand, tol, kappa, fmt)
+        entries.extend(rep.entries)
+        ties += rep.near_ties
+    eps = fmt.eps
+    for ident in ref_ids:
+        if ident not in cand_ids:
+            tolerance = tol.get(ident)
+            entries.append(CheckEntry(ident, VERDICT_MISSING, None, tolerance, kappa * max(tolerance, eps),
+                                      "only in reference trace"))
+    return CheckReport(entries=tuple(entries), mode=str(cand.header.get("mode", "")), kappa=kappa, fmt=fmt,
+                       near_ties=ties)
 
 
 # check() plans are pure functions of the traces' metadata, the tolerances,

@@ -85,6 +85,30 @@ def test_check_reproduces_reference_reports(cases, golden_trace_bytes, payloads)
     assert near == 0
 
 
+@pytest.mark.parametrize("budget", [1 << 20, 64 << 10])
+def test_check_in_batches_when_host_traces_exceed_the_device(monkeypatch, cases, golden_trace_bytes, budget):
+    """Host traces larger than the device budget (forced small here) are
+    checked in consecutive batches of ids: every golden scenario's report —
+    order, verdicts, missing ids, earliest flag — is still the reference's."""
+    from paper_2506_09280_b200 import checker
+    calls = []
+    real = checker._check_direct
+    monkeypatch.setattr(checker, "_check_direct", lambda *a: calls.append(1) or real(*a))
+    monkeypatch.setenv("TD_HBM_BUDGET_BYTES", str(budget))
+    split = 0
+    for case in cases["checks"]:
+        ref = trace_from_bytes(golden_trace_bytes(case["ref"]))
+        cand = trace_from_bytes(golden_trace_bytes(case["cand"]))
+        tol = td.ToleranceMap.from_json(cases["tols"][case["tol"]])
+        calls.clear()
+        rep = td.check(ref, cand, tol, case["kappa"], fmt=td.FloatFormat(case["fmt"]))
+        if checker._host_bytes(ref) + checker._host_bytes(cand) > budget:
+            assert len(calls) > 1, case["name"]        # it did split
+            split += 1
+        assert_reports_match(json.loads(td.render_report(rep, "json")), json.loads(case["report"]), case["name"])
+    assert split >= 10
+
+
 def test_estimate_tolerance_reproduces_reference(cases, golden_trace_bytes):
     for est in cases["estimates"]:
         base = trace_from_bytes(golden_trace_bytes(est["base"]), device="cuda")
