@@ -1790,6 +1790,17 @@ bool serial_classes() {
     return serial;
 }
 
+// TD_BLOCKS_PER_SM=<n>: td_segnorm's resident CTAs per SM when the caller
+// passes 0 (A/B knob; default 4)
+int default_blocks_per_sm() {
+    static const int n = [] {
+        const char* e = getenv("TD_BLOCKS_PER_SM");
+        const int v = e ? atoi(e) : 0;
+        return v > 0 && v <= 8 ? v : 4;
+    }();
+    return n;
+}
+
 int grid_for(int64_t n, int per_block, int cap) {
     int64_t g = (n + per_block - 1) / per_block;
     if (g < 1) g = 1;
@@ -1847,7 +1858,7 @@ int td_segnorm(const td_segment* segs, const td_class* classes, int32_t n_classe
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int per_sm = blocks_per_sm > 0 ? blocks_per_sm : 4;
+    const int per_sm = blocks_per_sm > 0 ? blocks_per_sm : default_blocks_per_sm();
     // Classes run concurrently: the largest on the caller's stream, the others
     // forked onto this thread's auxiliary streams, so each kernel's tail is
     // filled by the next kernel's CTAs instead of idling SMs (joined below).

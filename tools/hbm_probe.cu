@@ -17,6 +17,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
+#include <string>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1); } } while (0)
 
@@ -155,7 +157,56 @@ __global__ void __launch_bounds__(256, 1) bulk_fp64(const char* x, const char* y
     if (d2 == 123.0 && x2 == 456.0) out[0] = d2;
 }
 
+// "small": per-size read ceiling with L2 flushed (256 MiB memset) before each
+// timed rep, one launch per rep between events — the regime of config 5's
+// small tensors (td_segnorm there: 1 MiB 5.3 us, 16 MiB 11.5 us, 64 MiB
+// 27.7 us per ncu).
+static int small_sizes() {
+    const size_t maxb = 256ull << 20;
+    char *x, *y, *fl;
+    unsigned* uout;
+    CK(cudaMalloc(&x, maxb));
+    CK(cudaMalloc(&y, maxb));
+    CK(cudaMalloc(&fl, 256ull << 20));
+    CK(cudaMalloc(&uout, 64));
+    CK(cudaMemset(x, 1, maxb));
+    CK(cudaMemset(y, 2, maxb));
+    int sms;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    for (size_t mib : {1, 4, 16, 64, 256}) {
+        const size_t bytes = mib << 20, n16 = bytes / 16;
+        auto time_it = [&](const char* name, auto launch) {
+            std::vector<float> v;
+            for (int r = 0; r < 23; ++r) {
+                CK(cudaMemset(fl, r, 256ull << 20));
+                cudaEventRecord(a);
+                launch();
+                cudaEventRecord(b);
+                CK(cudaEventSynchronize(b));
+                float ms;
+                cudaEventElapsedTime(&ms, a, b);
+                if (r >= 3) v.push_back(ms);
+            }
+            std::sort(v.begin(), v.end());
+            const float med = v[v.size() / 2];
+            printf("%4zu MiB x2  %-26s %8.2f us  %8.1f GB/s\n", mib, name, med * 1e3, 2.0 * bytes / (med / 1e3) / 1e9);
+        };
+        for (int per : {2, 4, 8}) {
+            char nm[64];
+            snprintf(nm, sizeof nm, "read_xor U=4 %d/SM", per);
+            time_it(nm, [&] { read_xor<4><<<sms * per, 256>>>((const uint4*)x, (const uint4*)y, n16, uout); });
+            snprintf(nm, sizeof nm, "read_xor U=8 %d/SM", per);
+            time_it(nm, [&] { read_xor<8><<<sms * per, 256>>>((const uint4*)x, (const uint4*)y, n16, uout); });
+        }
+    }
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc > 1 && std::string(argv[1]) == "small") return small_sizes();
     double gib = argc > 1 ? atof(argv[1]) : 4.0;
     size_t bytes = (size_t)(gib * (1ull << 30));
     bytes &= ~((size_t)(1 << 20) - 1);
