@@ -132,3 +132,18 @@ def test_maximum_size_identities(gib):
         assert rep.entries[0].observed == want
         del cand, y
         torch.cuda.empty_cache()
+
+
+def test_injected_faults_match_oracle():
+    """Error and edge paths on random layouts (tools/fuzz_faults.py): dropped
+    / duplicated / re-declared replica copies, missing and extra ids, moved
+    and enlarged shard boxes, rank changes, NaN/inf elements, zero payloads
+    — every report equals the CPU oracle's.  40 seeded cases here; the
+    committed run covers 3000 (profiles/r2_fuzz_faults.txt)."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import fuzz_faults
+    stats = fuzz_faults.run(40, seed=2024)
+    assert stats["cases"] == 40
+    assert stats.get("merge-error", 0) + stats.get("replica-mismatch", 0) > 0
