@@ -38,7 +38,6 @@ def test_cpu_baseline_row_prefix_of_one_big_id():
     leading row block: the cut records still merge into that block (column
     shards and row stripes alike) and the oracle's rel_err over the block
     equals a direct computation."""
-    import numpy as np
     import torch
     sys.path.insert(0, ROOT)
     import bench

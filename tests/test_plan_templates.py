@@ -5,8 +5,6 @@ slot — over the golden traces of the reference (all check scenarios, bugs
 included), randomised shardings, and the BASELINE configs' layouts built
 from metadata alone (meta-device payloads)."""
 
-import gzip
-import json
 import os
 
 import numpy as np

@@ -21,7 +21,6 @@ import os
 import pickle
 import socket
 
-import numpy as np
 import pytest
 import torch
 import torch.multiprocessing as mp

@@ -3,10 +3,15 @@
 
     python tools/dplan_profile.py [prof]
 """
-import sys, time, gc, cProfile, pstats
-sys.path.insert(0,'/root/repo')
+import cProfile
+import os
+import pstats
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-from paper_2506_09280_b200 import layout as L, synthetic, plan as PL
+from paper_2506_09280_b200 import layout as L, synthetic
 from paper_2506_09280_b200.canonical import parse_canonical
 from paper_2506_09280_b200.tracestore import Trace, TraceRecord, RankMeta
 from paper_2506_09280_b200.distributed import DistributedCheckPlan, StaticComm

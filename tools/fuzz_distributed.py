@@ -26,7 +26,6 @@ sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 
 def run_case(rnd, k, faults=False):
-    import torch
     import paper_2506_09280_b200 as td
     from paper_2506_09280_b200 import synthetic
     from paper_2506_09280_b200.checker import check
