@@ -524,15 +524,20 @@ def run_distributed(args, world: int, rank: int, local: int):
     n_ids = len(dcp.cand_view) + sum(1 for i in dcp.ref_view if i not in dcp.cand_view)
     bug_steps = 0
 
+    gstep = None
+
     def step(ev=None):
         nonlocal bug_steps
-        sh = N.stream_handle(stream)
-        if ev is not None:
-            ev[0].record(stream)
-        b.digest_pass(sh)
-        if ev is not None:
-            ev[1].record(stream)
-        b.exchange(sh)
+        if gstep is not None:
+            gstep.replay(ev)
+        else:
+            sh = N.stream_handle(stream)
+            if ev is not None:
+                ev[0].record(stream)
+            b.digest_pass(sh)
+            if ev is not None:
+                ev[1].record(stream)
+            b.exchange(sh)
         out = b.fetch()
         if out[3]:
             bug_steps += 1
@@ -541,6 +546,15 @@ def run_distributed(args, world: int, rank: int, local: int):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # the clean-path step replayed as CUDA graphs around the eager all-gather
+    # (BoundCheck.capture_parts: one host call per part instead of a launch
+    # per kernel); the roofline's kernel time: events around the first graph
+    # (digests + compare pass + slot reduction; one GPU: the whole step)
+    if os.environ.get("TD_BENCH_GRAPH", "1") != "0":
+        gstep = b.capture_parts()
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     bug_steps = 0
     if world > 1:
@@ -563,7 +577,8 @@ def run_distributed(args, world: int, rank: int, local: int):
               (("pass", 0), ("flag", 1), ("replica-mismatch", 2), ("merge-error", 3))}
     launches = b.launches * args.steps
     n_remote, n_fused, n_fps, stride = len(dcp.plan.remote_groups), dcp.n_fused, b.fps.n, dcp.stride
-    del b, dcp                                      # only `traces` holds the payloads now
+    graphed = gstep is not None
+    del b, dcp, gstep                               # only `traces` holds the payloads now
     traces = [ref, cand]
     del ref, cand
     e2e = None
@@ -586,14 +601,18 @@ def run_distributed(args, world: int, rank: int, local: int):
                 "exchange": {"collective": "one all-gather of [slot sums | digest rows] per check",
                              "bytes_per_rank": 8 * stride, "remote_replica_groups": n_remote,
                              "digests_fused_in_compare": n_fused, "digested_by_fingerprint": n_fps,
-                             "steps_on_bug_path": bug_steps},
+                             "steps_on_bug_path": bug_steps,
+                             "step_launch": "CUDA graphs around the eager all-gather" if graphed
+                             else "eager launches"},
                 "verdict_counts" if not share or world == share else "verdict_counts_partial": counts,
                 "near_ties": ties,
                 "roofline": {"bound": "hbm", "achieved": pass_bytes / (pass_ms / 1e3) / 1e9,
                              "peak": hbm, "unit": "GB/s",
                              "frac": pass_bytes / (pass_ms / 1e3) / 1e9 / hbm,
                              "traffic": _ncu_traffic(args.config) if world == 1 else None,
-                             "kernel": "td_segnorm (incl. digest classes) + td_fingerprint on a side stream, rank 0",
+                             "kernel": "td_segnorm (incl. digest classes) + td_fingerprint on a side stream, rank 0"
+                                       + ("; timed as the step's first CUDA graph (+ slot reduction"
+                                          + (", combine, verdict)" if world == 1 else ")") if graphed else ""),
                              "kernel_ms": pass_ms, "peak_source": peak_kind},
                 "cpu_baseline": None, "e2e": e2e,
                 "gpu_launches": launches,

@@ -630,14 +630,26 @@ class BoundCheck:
     def exchange(self, sh) -> None:
         """Slot reduction, the digest rows into their canonical places, the
         ONE collective, td_combine (rank-order sums + digest compare), verdicts."""
+        self._pre_collective(sh)
+        self._collective()
+        self._post_collective(sh)
+
+    def _pre_collective(self, sh) -> None:
         import torch
         dcp, prep = self.dcp, self.prep
         prep.reduce(sh)
-        with torch.cuda.stream(prep.stream):
-            if len(dcp.where):
+        if len(dcp.where):
+            with torch.cuda.stream(prep.stream):
                 self.tail.index_copy_(0, self.canon, self.table[:len(dcp.where)])
-            if dcp.n_live > 1:
-                dcp.comm.all_gather_into(self.gathered, prep.exchange)
+
+    def _collective(self) -> None:
+        import torch
+        if self.dcp.n_live > 1:
+            with torch.cuda.stream(self.prep.stream):
+                self.dcp.comm.all_gather_into(self.gathered, self.prep.exchange)
+
+    def _post_collective(self, sh) -> None:
+        dcp, prep = self.dcp, self.prep
         N.call("td_combine", self.gathered.data_ptr(), dcp.n_live, dcp.stride, dcp.n_slots,
                prep.slot_sums.data_ptr(), self.copy_off.data_ptr() if self.n_copies else 0,
                self.copy_first.data_ptr() if self.n_copies else 0, self.n_copies, self.differs.data_ptr(),
@@ -649,9 +661,7 @@ class BoundCheck:
         self.digest_pass(sh)
         self.exchange(sh)
 
-    def capture(self):
-        """The clean-path step as one CUDA graph (NCCL's all-gather included
-        when the communicator is torch.distributed's)."""
+    def _capture(self, fn):
         import torch
         graph = torch.cuda.CUDAGraph()
         prep = self.prep
@@ -660,11 +670,30 @@ class BoundCheck:
         keep, prep.stream = prep.stream, cap
         try:
             with torch.cuda.graph(graph, stream=cap):
-                self.step()
+                fn(N.stream_handle(cap))
         finally:
             prep.stream = keep
         prep.stream.wait_stream(cap)
         return graph
+
+    def capture(self):
+        """The clean-path step as one CUDA graph (NCCL's all-gather included
+        when the communicator is torch.distributed's)."""
+        return self._capture(lambda sh: self.step())
+
+    def capture_parts(self) -> "GraphStep":
+        """The clean-path step as CUDA graphs around an eager collective:
+        everything before the exchange (digests, compares, slot reduction,
+        digest rows) in one graph, td_combine + td_verdict in another, the
+        all-gather launched between them — one host call per part, without
+        capturing the communicator.  One graph when no other rank is live."""
+        if self.dcp.n_live == 1:
+            return GraphStep(self, self.capture(), None)
+
+        def pre(sh):
+            self.digest_pass(sh)
+            self._pre_collective(sh)
+        return GraphStep(self, self._capture(pre), self._capture(self._post_collective))
 
     def check(self):
         """step() + the one D2H, then the bug path only if a digest differed:
@@ -684,6 +713,29 @@ class BoundCheck:
         """{(remote group, copy): (h0, h1)} of this rank's copies after a step."""
         t = self.table[:len(self.dcp.where)].cpu().numpy().view(np.uint64)
         return {kc: (int(t[i, 0]), int(t[i, 1])) for i, kc in enumerate(self.dcp.where)}
+
+
+class GraphStep:
+    """BoundCheck.capture_parts(): replay() enqueues one clean-path step on
+    the check's stream (then BoundCheck.fetch / the bug path as usual)."""
+
+    def __init__(self, bound: BoundCheck, pre, post):
+        self.bound, self.pre, self.post = bound, pre, post
+
+    def replay(self, events=None) -> None:
+        """events: an optional (start, end) CUDA-event pair recorded around
+        the first graph (digests, compares and the slot reduction)."""
+        import torch
+        stream = self.bound.prep.stream
+        with torch.cuda.stream(stream):
+            if events is not None:
+                events[0].record(stream)
+            self.pre.replay()
+            if events is not None:
+                events[1].record(stream)
+            if self.post is not None:
+                self.bound._collective()
+                self.post.replay()
 
 
 def _torch_dtype(code: int):

@@ -384,3 +384,50 @@ def test_distributed_clean_step_replays_as_one_cuda_graph():
         assert (ties2, n_diff2) == (ties, n_diff) == (0, 0)
         assert torch.equal(b.prep.slot_sums, sums)
         assert b.local_digests() == digests
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("corrupt", [False, True])
+def test_graph_step_around_eager_collective_matches_eager_step(corrupt):
+    """BoundCheck.capture_parts (what bench.py --gpus N replays): the
+    clean-path step as a graph before the all-gather and one after it, the
+    collective eager between them — every rank's verdicts, sums and
+    digest-mismatch count equal the eager step's, step after step, and the
+    bug path run after a replay gives the eager bug path's results."""
+    lay = synthetic.ShareLayout(SMALL, PCFG, WORLD)
+    shares = [lay.build(r) for r in range(WORLD)]
+    if corrupt:
+        rec = next(r for r in shares[WORLD - 1][1].records if r.replica_group_size > 1)
+        rec.payload.mul_(2)
+    tol = _tol(lay)
+    lock = threading.Lock()
+
+    def body(rank, comm):
+        ref, cand = shares[rank]
+        dcp = DistributedCheckPlan(ref, cand, tol, fmt=FloatFormat.BF16, comm=comm)
+        b = dcp.bind()
+        b.step()
+        idres, gres, ties, n_diff = b.fetch()
+        sums = b.prep.slot_sums.clone()
+        want = dcp._bug_path(b) if n_diff else (idres, gres, ties)
+        comm.hub.barrier.wait()
+        with lock:                     # one capture at a time: no other thread's CUDA work meanwhile
+            torch.cuda.synchronize()
+            g = b.capture_parts()
+            torch.cuda.synchronize()
+        comm.hub.barrier.wait()
+        for _ in range(2):
+            b.prep.slot_sums.zero_()
+            g.replay()
+            idres2, gres2, ties2, n_diff2 = b.fetch()
+            assert (idres2.tobytes(), gres2.tobytes(), ties2, n_diff2) == \
+                (idres.tobytes(), gres.tobytes(), ties, n_diff)
+            assert torch.equal(b.prep.slot_sums, sums)
+            got = dcp._bug_path(b) if n_diff2 else (idres2, gres2, ties2)
+            assert got[0].tobytes() == want[0].tobytes() and got[1].tobytes() == want[1].tobytes()
+        return int(n_diff), int((want[0]["verdict"] == 2).sum())
+    out = _run_threads(WORLD, body)
+    if corrupt:
+        assert all(n > 0 for n, _ in out) and all(m == 1 for _, m in out)
+    else:
+        assert out == [(0, 0)] * WORLD
