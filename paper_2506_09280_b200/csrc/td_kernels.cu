@@ -33,6 +33,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <vector>
 
 namespace {
 
@@ -95,10 +97,6 @@ template <> struct Vec<TD_F32> {
         return (double)__uint_as_float((&q[0].x)[e]);
     }
 };
-
-__host__ __device__ __forceinline__ int dtype_size(int dt) {
-    return dt == TD_F32 ? 4 : (dt == TD_F64 ? 8 : 2);
-}
 
 __device__ __forceinline__ double load_elem(const char* base, int dt, int64_t idx) {
     switch (dt) {
@@ -1749,22 +1747,72 @@ struct AuxStreams {
     cudaStream_t stream[N];
     cudaEvent_t join[N];
     cudaEvent_t fork;
-    bool ready = false;
+    int dev = -1;
+};
+
+// Auxiliary stream sets are per host thread (two threads' td_segnorm calls
+// must not share fork/join events) but outlive it: a thread's sets go back
+// to a process-wide free list when the thread exits and the next new thread
+// on that device takes one, so services that run checks on short-lived
+// threads hold at most one set per concurrently live thread instead of
+// creating streams without bound.  Nothing is destroyed (no CUDA calls at
+// thread or process exit); the list and its lock are never freed.
+std::mutex& aux_lock() {
+    static std::mutex* m = new std::mutex;
+    return *m;
+}
+std::vector<AuxStreams*>& aux_free() {
+    static std::vector<AuxStreams*>* v = new std::vector<AuxStreams*>;
+    return *v;
+}
+
+struct AuxLocal {
+    AuxStreams* per_dev[16] = {};
+    ~AuxLocal() {
+        std::lock_guard<std::mutex> g(aux_lock());
+        for (AuxStreams* a : per_dev)
+            if (a) aux_free().push_back(a);
+    }
 };
 
 AuxStreams* aux_streams(int dev) {
-    thread_local AuxStreams pool[16];
+    thread_local AuxLocal local;
     if (dev < 0 || dev >= 16) return nullptr;
-    AuxStreams& a = pool[dev];
-    if (!a.ready) {
-        for (int k = 0; k < AuxStreams::N; ++k) {
-            if (cudaStreamCreateWithFlags(&a.stream[k], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-            if (cudaEventCreateWithFlags(&a.join[k], cudaEventDisableTiming) != cudaSuccess) return nullptr;
-        }
-        if (cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-        a.ready = true;
+    if (AuxStreams* a = local.per_dev[dev]) return a;
+    {
+        std::lock_guard<std::mutex> g(aux_lock());
+        auto& pool = aux_free();
+        for (size_t i = 0; i < pool.size(); ++i)
+            if (pool[i]->dev == dev) {
+                local.per_dev[dev] = pool[i];
+                pool.erase(pool.begin() + i);
+                return local.per_dev[dev];
+            }
     }
-    return &a;
+    AuxStreams* a = new AuxStreams;
+    int made = 0;
+    bool ok = true;
+    for (; made < AuxStreams::N && ok; ++made) {
+        ok = cudaStreamCreateWithFlags(&a->stream[made], cudaStreamNonBlocking) == cudaSuccess;
+        if (ok && cudaEventCreateWithFlags(&a->join[made], cudaEventDisableTiming) != cudaSuccess) {
+            cudaStreamDestroy(a->stream[made]);
+            ok = false;
+        }
+        if (!ok) break;
+    }
+    if (ok) ok = cudaEventCreateWithFlags(&a->fork, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) {                                   // fall back to serial classes on this call
+        for (int k = 0; k < made; ++k) {
+            cudaStreamDestroy(a->stream[k]);
+            cudaEventDestroy(a->join[k]);
+        }
+        delete a;
+        cudaGetLastError();
+        return nullptr;
+    }
+    a->dev = dev;
+    local.per_dev[dev] = a;
+    return a;
 }
 
 void join_aux(AuxStreams* a, int k, cudaStream_t main_stream) {
