@@ -20,7 +20,8 @@ injected into the reference or the candidate trace:
 
 Every case: td.check's report on the device traces == the CPU oracle's on
 host copies (verdicts, details, thresholds exact; observed within 1e-12,
-NaN == NaN), or both raise.
+NaN == NaN), or both raise; about a third of the cases also compare
+td.compare_static's verdicts with the oracle's on the same traces.
 
     python tools/fuzz_faults.py [--cases 500] [--seed 0]      (GPU)
 """
@@ -162,6 +163,13 @@ def run(cases: int, seed: int) -> dict:
             assert_reports_match(got, want, label)
             for v, n in got["summary"].items():
                 stats[v] += n
+        if rnd.random() < 0.3:
+            # compare_static (elementwise |c - r| <= atol + rtol |r|) on the same faulted traces
+            atol, rtol = rnd.choice([(0.0, 0.0), (0.0, 1e-2), (1e-3, 1e-1), (10.0, 10.0)])
+            got_s = [(e.ident, e.verdict) for e in td.compare_static(ref, cand, atol, rtol).entries]
+            want_s = O.compare_static(_oracle_recs(ref), _oracle_recs(cand), atol, rtol)
+            assert got_s == want_s, (label, "compare_static", atol, rtol)
+            stats["static_cases"] += 1
         stats["cases"] += 1
     out = dict(stats)
     out["faults"] = dict(faults_seen)
