@@ -25,7 +25,7 @@ from .device import resolve_operands
 from .errors import (ConfigInvalid, DigestMismatch, FormatError, ShapeMismatch,
                      TraindiffError)
 from .perturb import PerturbSpec
-from .plan import Plan, PlanEntry, gc_paused, merge_view
+from .plan import Plan, PlanEntry, gc_paused, merge_view, no_gc
 from .tensor import FloatFormat
 from .tracestore import Trace, canonical_json
 
@@ -432,9 +432,16 @@ def _strict_problem(view, plan: Plan, gres, side_of_entry: dict) -> str | None:
 
 
 def _layout_key(trace) -> tuple:
-    """Everything a plan depends on, per record, in trace order."""
-    return tuple((r.id.encode(), r.rank_meta.as_tuple(), r.mapping.signature(), r.dtype_code,
-                  r.payload.shape, r.replica_group_size) for r in trace.records)
+    """Everything a plan depends on, per record, in trace order: ids, rank
+    metas, mapping signatures (as their interned ids: equal ids = equal
+    signatures), dtypes, payload shapes, replica sizes — column by column
+    (no tuple per record) and with the cyclic GC paused: every check() of a
+    cached layout builds and compares this key before it launches anything."""
+    recs = trace.records
+    with no_gc():
+        return (tuple([r.id.encode() for r in recs]), tuple([r.rank_meta.as_tuple() for r in recs]),
+                tuple([r.mapping.sig_id for r in recs]), tuple([r.dtype_code for r in recs]),
+                tuple([r.payload.shape for r in recs]), tuple([r.replica_group_size for r in recs]))
 
 
 def _forget_payloads(view, plan: Plan, keep_ids) -> None:
