@@ -305,9 +305,11 @@ def check(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float = 3.0, *,
     if kappa <= 0:
         raise ConfigInvalid("kappa must be positive")
     _require_same_setup(ref, cand)
-    budget = _hbm_budget()
-    if budget is not None and _host_bytes(ref) + _host_bytes(cand) > budget:
-        return _check_in_batches(ref, cand, tol, kappa, fmt, budget)
+    host = _host_bytes(ref) + _host_bytes(cand)
+    if host:                          # device-resident traces skip the free-memory query
+        budget = _hbm_budget()
+        if budget is not None and host > budget:
+            return _check_in_batches(ref, cand, tol, kappa, fmt, budget)
     return _check_direct(ref, cand, tol, kappa, fmt)
 
 
