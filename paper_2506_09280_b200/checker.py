@@ -307,7 +307,7 @@ def check(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float = 3.0, *,
     _require_same_setup(ref, cand)
     host = _host_bytes(ref) + _host_bytes(cand)
     if host:                          # device-resident traces skip the free-memory query
-        budget = _hbm_budget()
+        budget = _hbm_budget(host)
         if budget is not None and host > budget:
             return _check_in_batches(ref, cand, tol, kappa, fmt, budget)
     return _check_direct(ref, cand, tol, kappa, fmt)
@@ -343,10 +343,13 @@ def _host_bytes(trace: Trace) -> int:
     return total
 
 
-def _hbm_budget() -> int | None:
+def _hbm_budget(host_bytes: int = 0) -> int | None:
     """Device bytes a check may stage at once: TD_HBM_BUDGET_BYTES, else the
     free HBM less a margin for plan tables and workspace (None without a
-    GPU: check() then fails loudly further down, as before)."""
+    GPU: check() then fails loudly further down, as before).  The driver's
+    free-memory query costs 10-20 ms per call on a loaded device, so it is
+    made only when the host bytes could come near the limit: below half of
+    what this process has not allocated, the answer cannot be 'batch'."""
     import os
     env = os.environ.get("TD_HBM_BUDGET_BYTES")
     if env:
@@ -355,6 +358,10 @@ def _hbm_budget() -> int | None:
         import torch
         if not torch.cuda.is_available():
             return None
+        dev = torch.cuda.current_device()
+        headroom = torch.cuda.get_device_properties(dev).total_memory - torch.cuda.memory_allocated(dev)
+        if 2 * host_bytes + (4 << 30) < headroom:
+            return headroom
         free, _ = torch.cuda.mem_get_info()
         free += torch.cuda.memory_reserved() - torch.cuda.memory_allocated()   # the allocator's cache
     except Exception:  # pragma: no cover - no driver
