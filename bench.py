@@ -278,6 +278,39 @@ def _ncu_traffic(config: str):
     return entry.get("dram_bytes_per_step") if entry else None
 
 
+def _h2d_ceiling(traces, e2e_seconds):
+    """The e2e's own roofline: the same pinned arenas copied to HBM with
+    nothing else (one DMA per trace on one stream, CUDA events), this run,
+    this box.  frac = that copy's time / the e2e step's time."""
+    import torch
+    arenas = []
+    for t in traces:
+        if t.records:
+            st = t.records[0].payload.untyped_storage()
+            arenas.append(torch.empty(0, dtype=torch.uint8).set_(st))
+    n = sum(a.numel() for a in arenas)
+    try:
+        dev = [torch.empty(a.numel(), dtype=torch.uint8, device="cuda") for a in arenas]
+    except torch.OutOfMemoryError:
+        return {"h2d_gbs": None, "error": "no device memory for the probe"}
+    best = None
+    for _ in range(2):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for d, a in zip(dev, arenas):
+            d.copy_(a, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    del dev
+    torch.cuda.empty_cache()
+    return {"h2d_gbs": n / (best / 1e3) / 1e9, "bytes": n, "seconds": best / 1e3,
+            "frac": (best / 1e3) / e2e_seconds,
+            "what": "the same pinned arenas copied host->HBM alone (no check): the PCIe roofline of e2e"}
+
+
 def _pageable_e2e(href, hcand, tol, fmt, alg_bytes):
     """The same check() from ordinary (pageable) host tensors, the form a
     reference user's traces arrive in: check() stages them through its
@@ -902,6 +935,7 @@ def main():
                                 "H2D / kernels / D2H / report"}}
         if world == 1:
             e2e["pageable"] = _pageable_e2e(href, hcand, tol, fmt, alg_bytes)
+            e2e["pcie"] = _h2d_ceiling([href, hcand], e2e["seconds_per_step"])
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         if e2e is not None and e2e.get("value") is not None:
