@@ -43,6 +43,19 @@ VERDICT_NAMES = {N.PASS: "pass", N.FLAG: "flag", N.REPLICA: "replica-mismatch",
 MAX_UNITS = 1 << 30          # per-segment unit cap (kernel uses 32-bit unit indices)
 _VEC_DTYPES = (N.F32, N.BF16, N.F16)
 
+# column layout of a plan's segment rows once frozen to int64 (Plan._columns):
+# x slot (-1: none), x offset, y slot, y offset, MAX_Z z slots (-1 padded),
+# nz, rows, cols, x row stride, y row stride, first tile, units, vector flag,
+# digest slot (-1: none); offsets / strides in elements
+_C_X, _C_XO, _C_Y, _C_YO, _C_Z = 0, 1, 2, 3, 4
+_C_NZ = _C_Z + N.MAX_Z
+_C_R, _C_C, _C_RX, _C_RY, _C_TB, _C_NU, _C_VEC, _C_DS = range(_C_NZ + 1, _C_NZ + 9)
+_TPL_NCOLS = _C_DS + 1
+_SLOT_COLS = [_C_X, _C_Y] + list(range(_C_Z, _C_Z + N.MAX_Z))
+_ESIZE = np.zeros(max(N.DTYPE_SIZE) + 1, np.int64)
+for _code, _size in N.DTYPE_SIZE.items():
+    _ESIZE[_code] = _size
+
 
 @contextlib.contextmanager
 def no_gc():
@@ -419,6 +432,8 @@ class Plan:
         # recorded relative to its own operands / tiles / group slots, later
         # ids of the same structure replay it with their own records
         templates = {} if _TEMPLATES else None
+        self._tpl_rows = []       # template k -> its segment rows (int64, _TPL_COLS)
+        self._replays = []        # (template, first operand, first tile, digest base) per replayed entry
         shared = _shared_entries(entries) if templates is not None else set()
         for ei, e in enumerate(entries):
             if templates is None:
@@ -445,6 +460,7 @@ class Plan:
         self.ids = np.array(id_rows, dtype=N.ID_DESC) if id_rows else np.zeros(0, N.ID_DESC)
         self.groups = (np.array(group_rows, dtype=[("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")])
                        if group_rows else np.zeros(0, [("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")]))
+        self._columns()
         self.tile_shift = self._retile()
         self._freeze_segments()
         self._chunk_slots()
@@ -559,9 +575,14 @@ class Plan:
                 raise LookupError
             return k
         try:
-            rows = [(None if x is None else rel(x), xo, rel(y), yo, tuple(rel(z) for z in zs), r, c, rx, ry,
-                     tb - tiles0, nu, vec, ds if ds < 0 else ds - fd0)
-                    for x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec, ds in b.seg_rows[n_rows:]]
+            # one int64 row per segment (_TPL_COLS), operand slots / tiles /
+            # digest slots relative to the entry's start: replayed column-wise
+            # for every later id of the structure in _columns()
+            rows = np.array([(-1 if x is None else rel(x), xo, rel(y), yo,
+                              *[rel(z) for z in zs], *([-1] * (N.MAX_Z - len(zs))), len(zs),
+                              r, c, rx, ry, tb - tiles0, nu, int(vec), ds if ds < 0 else ds - fd0)
+                             for x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec, ds in b.seg_rows[n_rows:]],
+                            np.int64).reshape(-1, _TPL_NCOLS)
         except LookupError:
             return None
         remote = [(slot - g0, side, gi) for slot, _, side, gi in self.remote_groups[rg0_:]]
@@ -573,25 +594,23 @@ class Plan:
         subs = {k - g0: [j - g0 for j in v] for k, v in self.subslots.items() if k >= g0}
         t0, t1, cg0, cg1, rg0, rg1, hc, ch, rh, pad, _ = id_rows[-1]
         idrow = (t0 - tiles0, t1 - tiles0, cg0 - g0, cg1 - g0, rg0 - g0, rg1 - g0, hc, ch, rh, pad)
-        return ops, rows, b.n_tiles - tiles0, groups, owners, offsets, subs, idrow, remote, reads, fused
+        self._tpl_rows.append(rows)
+        return (tuple(w for w, _ in ops), tuple(dt for _, dt in ops), len(self._tpl_rows) - 1,
+                b.n_tiles - tiles0, groups, owners, offsets, subs, idrow, remote, reads, fused)
 
     def _replay_entry(self, b: PlanBuilder, ei: int, e: PlanEntry, tpl, group_rows: list, id_rows: list) -> None:
-        ops_t, rows, n_tiles, groups, owners, offsets, subs, idrow, remote, reads, fused = tpl
+        where, dts, tpl_k, n_tiles, groups, owners, offsets, subs, idrow, remote, reads, fused = tpl
         fd0, rg0 = len(self.fused_digests), len(self.remote_groups)
-        index, operands, dtypes = b._operand_index, b.operands, b.operand_dtypes
         sides = (e.y, e.x)
-        ops = []
-        for (side, gi, ri), dt in ops_t:
-            rec = sides[side].groups[gi].records[ri]
-            op = _Operand(len(operands), dt, N.DTYPE_SIZE[dt])    # a new record: no de-duplication to do
-            operands.append(rec)
-            dtypes.append(dt)
-            index[(id(rec), dt)] = op
-            ops.append(op)
+        # a replayed entry's records are its own (shared records take the
+        # general path, _shared_entries), so its operands need no
+        # de-duplication entry: they are appended as one block
+        op0 = len(b.operands)
+        b.operands.extend([sides[side].groups[gi].records[ri] for side, gi, ri in where])
+        b.operand_dtypes.extend(dts)
         tiles0, g0 = b.n_tiles, len(group_rows)
-        b.seg_rows.extend((None if xi is None else ops[xi], xo, ops[yi], yo, [ops[k] for k in zis] if zis else [],
-                           r, c, rx, ry, tiles0 + tb, nu, vec, ds if ds < 0 else fd0 + ds)
-                          for xi, xo, yi, yo, zis, r, c, rx, ry, tb, nu, vec, ds in rows)
+        # the segments themselves are instantiated column-wise in _columns()
+        self._replays.append((tpl_k, op0, tiles0, fd0))
         if remote:
             self.remote_groups.extend((g0 + slot, ei, side, gi) for slot, side, gi in remote)
             self.compare_reads.extend((ei, gi, c) for gi, c in reads)
@@ -663,11 +682,12 @@ class Plan:
         they are remapped boundary to boundary.  Returns the shift stored in
         the flags (0 = the library default)."""
         b = self.builder
+        cols = self._cols
         self.tile_units = N.TILE_UNITS
         default = N.TILE_UNITS.bit_length() - 1
-        if not b.seg_rows or (1 << default) != N.TILE_UNITS:
+        if not len(cols) or (1 << default) != N.TILE_UNITS:
             return 0
-        units = np.array([r[10] for r in b.seg_rows], np.int64)
+        units = cols[:, _C_NU]
         shift = default
         while shift > self.MIN_TILE_SHIFT and int((-(-units // (1 << shift))).sum()) < self.TARGET_TILES:
             shift -= 1
@@ -676,8 +696,8 @@ class Plan:
         self.tile_units = 1 << shift
         counts = -(-units // self.tile_units)
         new_begin = np.concatenate([[0], np.cumsum(counts)])
-        old_begin = np.array([r[9] for r in b.seg_rows] + [b.n_tiles], np.int64)
-        b.seg_rows = [r[:9] + (int(new_begin[i]),) + r[10:] for i, r in enumerate(b.seg_rows)]
+        old_begin = np.append(cols[:, _C_TB], b.n_tiles)
+        cols[:, _C_TB] = new_begin[:-1]
         b.n_tiles = self.n_tiles = int(new_begin[-1])
 
         def remap(v):
@@ -785,39 +805,73 @@ class Plan:
 
     # -- device tables ----------------------------------------------------------
 
+    def _columns(self) -> None:
+        """The segment rows as one int64 array (_TPL_NCOLS columns) in
+        emission order: the general path's rows, and every replayed entry's
+        template rows instantiated column-wise — per template, all of its
+        replays at once, with their operand slots, first tile and digest slot
+        offset — then merged back into emission order."""
+        b = self.builder
+        gen = np.array([(-1 if x is None else x.slot, xo, y.slot, yo,
+                         *[z.slot for z in zs], *([-1] * (N.MAX_Z - len(zs))), len(zs),
+                         r, c, rx, ry, tb, nu, int(vec), ds)
+                        for x, xo, y, yo, zs, r, c, rx, ry, tb, nu, vec, ds in b.seg_rows],
+                       np.int64).reshape(-1, _TPL_NCOLS)
+        if not self._replays:
+            self._cols = gen
+            return
+        rp = np.array(self._replays, np.int64)          # template, op0, tiles0, fd0
+        pieces = [gen]
+        order = np.argsort(rp[:, 0], kind="stable")
+        cuts = np.flatnonzero(np.diff(rp[order, 0])) + 1
+        for sel in np.split(order, cuts):
+            rows = self._tpl_rows[int(rp[sel[0], 0])]
+            m = len(rows)
+            if m == 0:
+                continue
+            k = len(sel)
+            R = np.repeat(rows[None, :, :], k, axis=0)
+            S = R[:, :, _SLOT_COLS]
+            R[:, :, _SLOT_COLS] = np.where(S >= 0, S + rp[sel, 1][:, None, None], S)
+            R[:, :, _C_TB] += rp[sel, 2][:, None]
+            D = R[:, :, _C_DS]
+            R[:, :, _C_DS] = np.where(D >= 0, D + rp[sel, 3][:, None], D)
+            pieces.append(R.reshape(k * m, _TPL_NCOLS))
+        cols = np.concatenate(pieces)
+        # every segment spans >= 1 tile and tiles are handed out in emission
+        # order, so the first tile orders the segments as they were emitted
+        self._cols = cols[np.argsort(cols[:, _C_TB], kind="stable")]
+
     def _freeze_segments(self) -> None:
         """The device segment table, tile -> segment map and per-class tile
-        lists, built column-wise (numpy over the builder's rows)."""
-        rows = self.builder.seg_rows
-        n = len(rows)
+        lists, built column-wise from _columns()' array."""
+        cols = self._cols
+        n = len(cols)
         segs = np.zeros(n, dtype=N.SEGMENT)
-        self.seg_zslot = np.full((n, N.MAX_Z), -1, np.int64)
         self.operands = self.builder.operands
         self.operand_dtypes = self.builder.operand_dtypes
         if n == 0:
+            self.seg_zslot = np.full((0, N.MAX_Z), -1, np.int64)
             self.seg_xslot = np.full(0, -1, np.int64)
             self.seg_xoff = self.seg_yslot = self.seg_yoff = np.zeros(0, np.int64)
             self.segs, self.tile_seg = segs, np.zeros(self.n_tiles, np.int32)
             self.class_keys, self.class_segs, self.class_lists = [], [], []
             self.algorithmic_bytes = 0
             return
-        xs, xo, ys, yo, zss, r, c, rx, ry, tb, nu, vec, ds = zip(*rows)
         i64 = np.int64
-        has_x = np.fromiter((x is not None for x in xs), bool, n)
-        x_es = np.fromiter((x.esize if x is not None else 0 for x in xs), i64, n)
-        x_slot = np.fromiter((x.slot if x is not None else -1 for x in xs), i64, n)
-        x_dt = np.fromiter((x.dtype if x is not None else y.dtype for x, y in zip(xs, ys)), np.int32, n)
-        y_es = np.fromiter((y.esize for y in ys), i64, n)
-        y_slot = np.fromiter((y.slot for y in ys), i64, n)
-        y_dt = np.fromiter((y.dtype for y in ys), np.int32, n)
-        nz = np.fromiter((len(z) for z in zss), np.int32, n)
-        for i in np.flatnonzero(nz):
-            for j, z in enumerate(zss[i]):
-                self.seg_zslot[i, j] = z.slot
-        r, c, tb, nu = (np.asarray(v, i64) for v in (r, c, tb, nu))
-        xo, yo = np.asarray(xo, i64), np.asarray(yo, i64)
-        vec = np.asarray(vec, bool)
-        ds = np.asarray(ds, np.int32)
+        op_dt = np.asarray(self.operand_dtypes, np.int32)
+        x_slot, y_slot = cols[:, _C_X].copy(), cols[:, _C_Y].copy()
+        has_x = x_slot >= 0
+        y_dt = op_dt[y_slot]
+        y_es = _ESIZE[y_dt]
+        x_dt = np.where(has_x, op_dt[np.maximum(x_slot, 0)], y_dt)
+        x_es = np.where(has_x, _ESIZE[x_dt], 0)
+        nz = cols[:, _C_NZ].astype(np.int32)
+        self.seg_zslot = cols[:, _C_Z:_C_Z + N.MAX_Z].copy()
+        r, c, rx, ry, tb, nu = (cols[:, k] for k in (_C_R, _C_C, _C_RX, _C_RY, _C_TB, _C_NU))
+        xo, yo = cols[:, _C_XO], cols[:, _C_YO]
+        vec = cols[:, _C_VEC] != 0
+        ds = cols[:, _C_DS].astype(np.int32)
         segs["x_stride"], segs["y_stride"], segs["rows"], segs["cols"] = rx, ry, r, c
         segs["tile_begin"], segs["n_units"] = tb, nu
         segs["x_dtype"], segs["y_dtype"], segs["nz"] = x_dt, y_dt, nz
@@ -839,23 +893,26 @@ class Plan:
         first = np.repeat(tb - np.concatenate([[0], np.cumsum(nt)[:-1]]), nt)
         tiles = first + np.arange(len(seg_of_tile), dtype=i64)     # tile index of each (segment, k)
         tile_seg[tiles] = seg_of_tile
-        keys = list(zip(vec.tolist(), y_dt.tolist(), nz.tolist(), has_x.tolist(), (ds >= 0).tolist()))
-        members: dict = {}
-        for i, k in enumerate(keys):
-            members.setdefault(k, []).append(i)
+        # tile classes: (vector, y dtype, nz, has x, digest), sorted as tuples
+        # packed one field per byte (every field < 256), so integer order is
+        # the tuples' order
+        code = ((((vec.astype(i64) << 8 | y_dt) << 8 | nz) << 8 | has_x) << 8) | (ds >= 0)
+        uniq, inverse = np.unique(code, return_inverse=True)
+        inverse = inverse.reshape(-1)
         self.segs = segs
         self.tile_seg = tile_seg
-        self.class_keys = sorted(members)
-        self.class_segs = [members[k] for k in self.class_keys]
-        owner = seg_of_tile.astype(i64) << 32
+        self.class_keys = [(bool(k >> 32), int((k >> 24) & 255), int((k >> 16) & 255), bool((k >> 8) & 255),
+                            bool(k & 255)) for k in uniq.tolist()]
+        by_class = np.argsort(inverse, kind="stable")
+        bounds = np.concatenate([[0], np.cumsum(np.bincount(inverse, minlength=len(uniq)))])
+        self.class_segs = [by_class[bounds[k]:bounds[k + 1]].tolist() for k in range(len(uniq))]
         self.class_lists = []
-        for k in self.class_keys:
-            idx = np.asarray(members[k], i64)
+        for k in range(len(uniq)):
+            idx = by_class[bounds[k]:bounds[k + 1]].astype(i64)
             pick = np.repeat(idx, nt[idx])
             base = np.repeat(tb[idx] - np.concatenate([[0], np.cumsum(nt[idx])[:-1]]), nt[idx])
             t = base + np.arange(len(pick), dtype=i64)
             self.class_lists.append((pick << 32) + t)
-        del owner
         self.algorithmic_bytes = int((r * c * (y_es * (1 + nz) + x_es)).sum())
 
     # -- execution ----------------------------------------------------------------
@@ -928,6 +985,8 @@ def _shared_entries(entries) -> set:
     against itself): operand de-duplication then differs from entry to entry,
     so they are planned without templates."""
     xs = {id(r) for e in entries if e.x is not None for g in e.x.groups for r in g.records}
+    if xs.isdisjoint([id(r) for e in entries if e.y is not None for g in e.y.groups for r in g.records]):
+        return set()            # the usual case: two distinct traces
     return {ei for ei, e in enumerate(entries)
             if e.y is not None and any(id(r) in xs for g in e.y.groups for r in g.records)}
 
