@@ -463,6 +463,7 @@ class Plan:
         self._columns()
         self.tile_shift = self._retile()
         self._freeze_segments()
+        del self._cols, self._replays, self._tpl_rows     # planning scratch (cached plans stay lean)
         self._chunk_slots()
 
     def _plan_entry(self, b: PlanBuilder, ei: int, e: PlanEntry, group_rows: list, id_rows: list, owner,
