@@ -117,6 +117,26 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     return lib
 
 
+_HOST_EXT = None
+
+
+def host_ext():
+    """The warm-check record walks in C++ (csrc/td_host.cpp, built in-tree by
+    build.build_host), or None: they are host metadata walks with a Python
+    twin, so a missing or disabled (TD_HOST_EXT=0) module only costs time."""
+    global _HOST_EXT
+    if _HOST_EXT is None:
+        mod = False
+        if os.environ.get("TD_HOST_EXT", "1") != "0":
+            try:
+                import torch  # noqa: F401  -- libtorch_python resident first
+                from . import _td_host as mod
+            except ImportError:
+                mod = False
+        _HOST_EXT = mod
+    return _HOST_EXT or None
+
+
 def lib() -> ctypes.CDLL:
     """The library, on a machine that can actually run it."""
     import torch

@@ -42,7 +42,44 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > out_m for p in deps)
 
 
+HOST_SOURCE = os.path.join(HERE, "csrc", "td_host.cpp")
+
+
+def host_output() -> str:
+    import sysconfig
+    return os.path.join(HERE, "_td_host" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_host(force: bool = False, verbose: bool = False) -> str:
+    """The warm-check record walks (csrc/td_host.cpp) as a CPython extension
+    against the installed torch (host code only, g++)."""
+    import sysconfig
+
+    import torch
+    from torch.utils import cpp_extension
+    out = host_output()
+    if not force and os.path.exists(out) and os.path.getmtime(out) > max(
+            os.path.getmtime(HOST_SOURCE), os.path.getmtime(__file__)):
+        return out
+    libdirs = cpp_extension.library_paths()
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-shared", "-fPIC", "-w",
+           f"-D_GLIBCXX_USE_CXX11_ABI={int(torch._C._GLIBCXX_USE_CXX11_ABI)}",
+           "-I", sysconfig.get_paths()["include"],
+           *[f for d in cpp_extension.include_paths() for f in ("-I", d)],
+           HOST_SOURCE, "-o", out + ".tmp",
+           *[f"-L{d}" for d in libdirs], *[f"-Wl,-rpath,{d}" for d in libdirs],
+           "-lc10", "-ltorch", "-ltorch_cpu", "-ltorch_python"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"g++ failed ({proc.returncode}):\n{proc.stderr}")
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_host(force=force, verbose=verbose)
     if not force and not needs_build():
         return OUTPUT
     tmp = OUTPUT + ".tmp"

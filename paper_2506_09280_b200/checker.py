@@ -310,13 +310,15 @@ def check(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float = 3.0, *,
         budget = _hbm_budget(host)
         if budget is not None and host > budget:
             return _check_in_batches(ref, cand, tol, kappa, fmt, budget)
-    return _check_direct(ref, cand, tol, kappa, fmt)
+    return _check_direct(ref, cand, tol, kappa, fmt, resident=not host)
 
 
-def _check_direct(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float, fmt: FloatFormat) -> CheckReport:
-    """check() with every payload staged on the device at once."""
+def _check_direct(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float, fmt: FloatFormat,
+                  resident: bool = False) -> CheckReport:
+    """check() with every payload staged on the device at once (resident:
+    every payload is already in device memory, nothing to stage)."""
     from .device import stage_host_payloads
-    staged = stage_host_payloads([ref, cand])
+    staged = {} if resident else stage_host_payloads([ref, cand])
     key = _check_key(ref, cand, tol, kappa, fmt)
     hit = _PLAN_CACHE.get(key)
     if hit is not None:
@@ -335,6 +337,15 @@ def _check_direct(ref: Trace, cand: Trace, tol: ToleranceMap, kappa: float, fmt:
 
 def _host_bytes(trace: Trace) -> int:
     """Payload bytes check() would have to bring to the device."""
+    ext = N.host_ext()
+    if ext is not None:
+        total = ext.host_bytes(trace.records)
+        if total is not None:
+            return total
+    return _host_bytes_py(trace)
+
+
+def _host_bytes_py(trace: Trace) -> int:
     total = 0
     for r in trace.records:
         p = r.payload
@@ -446,6 +457,13 @@ def _layout_key(trace) -> tuple:
     signatures), dtypes, payload shapes, replica sizes — column by column
     (no tuple per record) and with the cyclic GC paused: every check() of a
     cached layout builds and compares this key before it launches anything."""
+    ext = N.host_ext()
+    if ext is not None:
+        return ext.layout_key(trace.records)
+    return _layout_key_py(trace)
+
+
+def _layout_key_py(trace) -> tuple:
     recs = trace.records
     with no_gc():
         return (tuple([r.id.encode() for r in recs]), tuple([r.rank_meta.as_tuple() for r in recs]),

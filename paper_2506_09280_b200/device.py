@@ -370,9 +370,19 @@ def _resolve_resident(operands, dtypes, staged):
     traces: torchtap captures, read_trace(device="cuda")): pointers in one
     pass, alignment checked in bulk.  None when any operand needs the general
     path (host payload, staged copy, widening, misalignment)."""
-    import torch
     if staged or dtypes is None:
         return None
+    ext = N.host_ext()
+    if ext is not None:
+        got = ext.resident_ptrs(operands, bytes(dtypes))
+        if got is None:
+            return None
+        return np.frombuffer(got[0], dtype=np.uint64).copy(), got[1]
+    return _resolve_resident_py(operands, dtypes)
+
+
+def _resolve_resident_py(operands, dtypes):
+    import torch
     try:
         payloads = [o.payload for o in operands]
     except AttributeError:
