@@ -32,6 +32,8 @@ PyObject* s_mapping;
 PyObject* s_sig_id;
 PyObject* s_replica;
 PyObject* s_dtype_code;
+PyObject* s_text;
+PyObject* s_t;
 
 // td dtype code of a tensor (td_api.h TD_F32/BF16/F16/F64), -1 otherwise
 int td_code(const at::Tensor& t) {
@@ -58,6 +60,17 @@ struct Seq {
     ~Seq() { Py_XDECREF(fast); }
 };
 
+// obj.<cache> when the immutable object already memoised it (CanonicalId
+// keeps its encoded text in _text, RankMeta its tuple in _t), else
+// obj.<method>(), which memoises it: no Python frame on the warm path.
+PyObject* cached_or_call(PyObject* obj, PyObject* cache, PyObject* method) {
+    PyObject* v = PyObject_GetAttr(obj, cache);
+    if (v) return v;
+    if (!PyErr_ExceptionMatches(PyExc_AttributeError)) return nullptr;
+    PyErr_Clear();
+    return PyObject_CallMethodNoArgs(obj, method);
+}
+
 // layout_key(records) -> (ids, rank tuples, signature ids, dtype codes,
 // shapes, replica sizes): six tuples in record order, equal to
 // checker._layout_key's (torch.Size compares and hashes as its tuple).
@@ -71,10 +84,10 @@ PyObject* layout_key(PyObject*, PyObject* arg) {
     for (Py_ssize_t k = 0; ok && k < n; ++k) {
         PyObject* rec = recs.items[k];
         PyObject* id = PyObject_GetAttr(rec, s_id);
-        PyObject* enc = id ? PyObject_CallMethodNoArgs(id, s_encode) : nullptr;
+        PyObject* enc = id ? cached_or_call(id, s_text, s_encode) : nullptr;
         Py_XDECREF(id);
         PyObject* rm = PyObject_GetAttr(rec, s_rank_meta);
-        PyObject* rt = rm ? PyObject_CallMethodNoArgs(rm, s_as_tuple) : nullptr;
+        PyObject* rt = rm ? cached_or_call(rm, s_t, s_as_tuple) : nullptr;
         Py_XDECREF(rm);
         PyObject* mp = PyObject_GetAttr(rec, s_mapping);
         PyObject* sig = mp ? PyObject_GetAttr(mp, s_sig_id) : nullptr;
@@ -222,5 +235,7 @@ PyMODINIT_FUNC PyInit__td_host() {
     s_sig_id = PyUnicode_InternFromString("sig_id");
     s_replica = PyUnicode_InternFromString("replica_group_size");
     s_dtype_code = PyUnicode_InternFromString("dtype_code");
+    s_text = PyUnicode_InternFromString("_text");
+    s_t = PyUnicode_InternFromString("_t");
     return PyModule_Create(&module);
 }

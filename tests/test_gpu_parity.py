@@ -93,7 +93,7 @@ def test_check_in_batches_when_host_traces_exceed_the_device(monkeypatch, cases,
     from paper_2506_09280_b200 import checker
     calls = []
     real = checker._check_direct
-    monkeypatch.setattr(checker, "_check_direct", lambda *a: calls.append(1) or real(*a))
+    monkeypatch.setattr(checker, "_check_direct", lambda *a, **k: calls.append(1) or real(*a, **k))
     monkeypatch.setenv("TD_HBM_BUDGET_BYTES", str(budget))
     split = 0
     for case in cases["checks"]:
