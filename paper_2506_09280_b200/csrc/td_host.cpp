@@ -132,6 +132,84 @@ PyObject* layout_key(PyObject*, PyObject* arg) {
     return res;
 }
 
+// td dtype code of a record's payload as a new int (rec.dtype_code's value;
+// non-torch payloads and unsupported dtypes go through the property, which
+// raises as Python does)
+PyObject* record_code(PyObject* rec, PyObject* payload) {
+    if (THPVariable_Check(payload)) {
+        const int c = td_code(THPVariable_Unpack(payload));
+        if (c >= 0) return PyLong_FromLong(c);
+    }
+    return PyObject_GetAttr(rec, s_dtype_code);
+}
+
+// group_by_id(records) -> (ids, positions, keys): the encoded ids in first
+// appearance order (Trace.by_id's order), each id's record positions in
+// trace order, and each id's merge_view structure key — the tuple of
+// (mapping signature id, replica group size, dtype code) of its records.
+PyObject* group_by_id(PyObject*, PyObject* arg) {
+    Seq recs(arg);
+    if (!recs.fast) return nullptr;
+    PyObject* index = PyDict_New();
+    PyObject* ids = PyList_New(0);
+    PyObject* pos = PyList_New(0);
+    PyObject* atoms = PyList_New(0);
+    bool ok = index && ids && pos && atoms;
+    for (Py_ssize_t k = 0; ok && k < recs.n; ++k) {
+        PyObject* rec = recs.items[k];
+        PyObject* id = PyObject_GetAttr(rec, s_id);
+        PyObject* enc = id ? cached_or_call(id, s_text, s_encode) : nullptr;
+        Py_XDECREF(id);
+        PyObject* mp = enc ? PyObject_GetAttr(rec, s_mapping) : nullptr;
+        PyObject* sig = mp ? PyObject_GetAttr(mp, s_sig_id) : nullptr;
+        Py_XDECREF(mp);
+        PyObject* rep = sig ? PyObject_GetAttr(rec, s_replica) : nullptr;
+        PyObject* payload = rep ? PyObject_GetAttr(rec, s_payload) : nullptr;
+        PyObject* code = payload ? record_code(rec, payload) : nullptr;
+        Py_XDECREF(payload);
+        PyObject* atom = code ? PyTuple_Pack(3, sig, rep, code) : nullptr;
+        Py_XDECREF(sig); Py_XDECREF(rep); Py_XDECREF(code);
+        PyObject* kk = atom ? PyLong_FromSsize_t(k) : nullptr;
+        if (!kk) {
+            Py_XDECREF(enc); Py_XDECREF(atom);
+            ok = false;
+            break;
+        }
+        PyObject* slot = PyDict_GetItemWithError(index, enc);     // borrowed
+        if (slot) {
+            const Py_ssize_t j = PyLong_AsSsize_t(slot);
+            ok = PyList_Append(PyList_GET_ITEM(pos, j), kk) == 0 &&
+                 PyList_Append(PyList_GET_ITEM(atoms, j), atom) == 0;
+        } else if (!PyErr_Occurred()) {
+            PyObject* j = PyLong_FromSsize_t(PyList_GET_SIZE(ids));
+            PyObject* pl = PyList_New(1);
+            PyObject* al = PyList_New(1);
+            ok = j && pl && al && PyDict_SetItem(index, enc, j) == 0 && PyList_Append(ids, enc) == 0;
+            if (ok) {
+                Py_INCREF(kk); PyList_SET_ITEM(pl, 0, kk);
+                Py_INCREF(atom); PyList_SET_ITEM(al, 0, atom);
+                ok = PyList_Append(pos, pl) == 0 && PyList_Append(atoms, al) == 0;
+            }
+            Py_XDECREF(j); Py_XDECREF(pl); Py_XDECREF(al);
+        } else {
+            ok = false;
+        }
+        Py_DECREF(enc); Py_DECREF(atom); Py_DECREF(kk);
+    }
+    PyObject* keys = ok ? PyList_New(PyList_GET_SIZE(atoms)) : nullptr;
+    for (Py_ssize_t j = 0; keys && j < PyList_GET_SIZE(atoms); ++j) {
+        PyObject* t = PyList_AsTuple(PyList_GET_ITEM(atoms, j));
+        if (!t) {
+            Py_CLEAR(keys);
+            break;
+        }
+        PyList_SET_ITEM(keys, j, t);
+    }
+    PyObject* res = keys ? PyTuple_Pack(3, ids, pos, keys) : nullptr;
+    Py_XDECREF(index); Py_XDECREF(ids); Py_XDECREF(pos); Py_XDECREF(atoms); Py_XDECREF(keys);
+    return res;
+}
+
 // host_bytes(records) -> bytes of payloads not resident on a CUDA device
 // (checker._host_bytes), or None when a payload is not a torch tensor (numpy
 // payloads: the Python walk sums record.nbytes).
@@ -216,6 +294,7 @@ PyObject* resident_ptrs(PyObject*, PyObject* args) {
 
 PyMethodDef methods[] = {
     {"layout_key", layout_key, METH_O, "checker._layout_key over a record list"},
+    {"group_by_id", group_by_id, METH_O, "Trace.by_id positions + merge_view structure keys"},
     {"host_bytes", host_bytes, METH_O, "checker._host_bytes over a record list (None: not torch payloads)"},
     {"resident_ptrs", resident_ptrs, METH_VARARGS, "device._resolve_resident's fast case"},
     {nullptr, nullptr, 0, nullptr},

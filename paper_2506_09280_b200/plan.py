@@ -173,6 +173,10 @@ def merge_view(trace, replica_check: bool = True) -> dict[str, IdMeta]:
     ids whose records carry the same (mapping signature, replica size)
     sequence share one result shape: it is computed once per structure and
     re-instantiated with each id's own records (`_TEMPLATES`)."""
+    from .tracestore import Trace
+    ext = N.host_ext()
+    if _TEMPLATES and ext is not None and type(trace).by_id is Trace.by_id:
+        return _merge_view_grouped(trace, ext.group_by_id(trace.records), replica_check)
     view = {}
     memo: dict | None = {} if _TEMPLATES else None
     for ident, entries in trace.by_id().items():
@@ -198,6 +202,34 @@ def merge_view(trace, replica_check: bool = True) -> dict[str, IdMeta]:
             meta = view[ident] = IdMeta(ident=ident, exec_index=entries[0][0], global_shape=hull,
                                         rank_problem=rank_problem, merge_detail=detail)
             meta.groups = [GroupMeta(records=[entries[k][1] for k in idx], declared_detail=d, numeric=num)
+                           for idx, d, num in groups]
+        meta.struct_key = hit[4]
+    return view
+
+
+def _merge_view_grouped(trace, grouped, replica_check: bool) -> dict[str, IdMeta]:
+    """merge_view's template path over _td_host.group_by_id's output (ids in
+    first-appearance order, their record positions, their structure keys):
+    the same metadata, without the per-record Python walks."""
+    recs = trace.records
+    view = {}
+    memo: dict = {}
+    for ident, ks, key in zip(*grouped):
+        hit = memo.get(key)
+        if hit is None:
+            entries = [(k, recs[k]) for k in ks]
+            meta = view[ident] = id_meta(ident, entries, replica_check)
+            pos = {id(rec): k for k, (_, rec) in enumerate(entries)}
+            if len(pos) != len(entries):         # one record object listed twice: no template
+                continue
+            hit = memo[key] = (meta.rank_problem, meta.global_shape, meta.merge_detail,
+                               [([pos[id(r)] for r in g.records], g.declared_detail, g.numeric)
+                                for g in meta.groups], _intern_struct((replica_check, key)))
+        else:
+            rank_problem, hull, detail, groups, _ = hit
+            meta = view[ident] = IdMeta(ident=ident, exec_index=ks[0], global_shape=hull,
+                                        rank_problem=rank_problem, merge_detail=detail)
+            meta.groups = [GroupMeta(records=[recs[ks[k]] for k in idx], declared_detail=d, numeric=num)
                            for idx, d, num in groups]
         meta.struct_key = hit[4]
     return view

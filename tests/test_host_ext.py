@@ -121,3 +121,28 @@ def test_check_reports_equal_with_and_without_the_extension(cases, golden_trace_
             finally:
                 N._HOST_EXT = saved
         assert runs[0] == runs[1] == runs[2], case["name"]
+
+
+def _view_signature(view):
+    return [(ident, m.exec_index, m.global_shape, m.rank_problem, m.merge_detail, m.struct_key,
+             [([id(r) for r in g.records], g.declared_detail, g.numeric) for g in m.groups])
+            for ident, m in view.items()]
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "*.ttrc.gz"))))
+def test_grouped_merge_view_equals_python(path):
+    """merge_view over _td_host.group_by_id == merge_view's Python walk
+    (every golden trace: TP/SP/CP/PP/DP layouts, replica groups, shard maps)."""
+    from paper_2506_09280_b200 import plan as P
+    _ext()
+    t = trace_from_bytes(gzip.open(path).read())
+    grouped = P.merge_view(t)
+    saved = N._HOST_EXT
+    N._HOST_EXT = False
+    try:
+        plain = P.merge_view(t)
+    finally:
+        N._HOST_EXT = saved
+    assert _view_signature(grouped) == _view_signature(plain)
+    ids, pos, keys = N.host_ext().group_by_id(t.records)
+    assert ids == list(t.by_id()) and pos == [[k for k, _ in e] for e in t.by_id().values()]
