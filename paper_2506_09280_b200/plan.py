@@ -451,7 +451,7 @@ class Plan:
         b = PlanBuilder(force_generic=static is not None)
         id_rows = []
         group_rows = []
-        self.group_owner = []     # (entry index, side, group index) per group slot
+        self._group_owner = []     # (entry index, side, group index) per group slot
         self.group_offset = []    # per group slot: copy index of its first replica - 1
         self.subslots = {}        # first group slot -> all slots of that group (> MAX_Z + 1 copies)
         self.remote_groups = []   # (first group slot, entry index, side, group index)
@@ -465,7 +465,12 @@ class Plan:
         # ids of the same structure replay it with their own records
         templates = {} if _TEMPLATES else None
         self._tpl_rows = []       # template k -> its segment rows (int64, _TPL_COLS)
-        self._replays = []        # (template, first operand, first tile, digest base) per replayed entry
+        self._tpl_groups = []     # template k -> its group rows (tile begin, tile end relative; nz)
+        self._tpl_ids = []        # template k -> its id row, relative
+        self._replays = []        # (template, first operand, first tile, digest base, first group slot,
+        #                            id row) per replayed entry
+        self._id_tol = []         # tolerance per replayed entry, replay order
+        self._owner_fill = []     # (first group slot, entry, ((side, group index), ...)) per replay
         shared = _shared_entries(entries) if templates is not None else set()
         for ei, e in enumerate(entries):
             if templates is None:
@@ -482,20 +487,18 @@ class Plan:
             if tpl is not None:
                 self._replay_entry(b, ei, e, tpl, group_rows, id_rows)
                 continue
-            mark = (len(b.operands), len(b.seg_rows), b.n_tiles, len(group_rows), len(self.group_owner),
+            mark = (len(b.operands), len(b.seg_rows), b.n_tiles, len(group_rows), len(self._group_owner),
                     len(self.remote_groups), len(self.compare_reads), len(self.fused_digests))
             self._plan_entry(b, ei, e, group_rows, id_rows, owner, is_local, compare_copy, digest, static)
             if key is not None:
                 templates[key] = self._record_entry(b, e, mark, group_rows, id_rows)
         self.builder = b
         self.n_tiles = b.n_tiles
-        self.ids = np.array(id_rows, dtype=N.ID_DESC) if id_rows else np.zeros(0, N.ID_DESC)
-        self.groups = (np.array(group_rows, dtype=[("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")])
-                       if group_rows else np.zeros(0, [("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")]))
+        self._fill_replayed_rows(id_rows, group_rows)
         self._columns()
         self.tile_shift = self._retile()
         self._freeze_segments()
-        del self._cols, self._replays, self._tpl_rows     # planning scratch (cached plans stay lean)
+        del self._cols, self._replays, self._tpl_rows, self._tpl_groups, self._tpl_ids, self._id_tol
         self._chunk_slots()
 
     def _plan_entry(self, b: PlanBuilder, ei: int, e: PlanEntry, group_rows: list, id_rows: list, owner,
@@ -622,17 +625,19 @@ class Plan:
         reads = [(gi, c) for _, gi, c in self.compare_reads[cr0:]]
         fused = [(k - rg0_, c) for k, c in self.fused_digests[fd0:]]
         groups = [(s0 - tiles0, s1 - tiles0, nz) for s0, s1, nz in group_rows[g0:]]
-        owners = [(side, gi) for _, side, gi in self.group_owner[o0:]]
+        owners = [(side, gi) for _, side, gi in self._group_owner[o0:]]
         offsets = self.group_offset[o0:]
         subs = {k - g0: [j - g0 for j in v] for k, v in self.subslots.items() if k >= g0}
         t0, t1, cg0, cg1, rg0, rg1, hc, ch, rh, pad, _ = id_rows[-1]
         idrow = (t0 - tiles0, t1 - tiles0, cg0 - g0, cg1 - g0, rg0 - g0, rg1 - g0, hc, ch, rh, pad)
         self._tpl_rows.append(rows)
+        self._tpl_groups.append(np.array(groups, np.int64).reshape(-1, 3))
+        self._tpl_ids.append(idrow)
         return (tuple(w for w, _ in ops), tuple(dt for _, dt in ops), len(self._tpl_rows) - 1,
-                b.n_tiles - tiles0, groups, owners, offsets, subs, idrow, remote, reads, fused)
+                b.n_tiles - tiles0, (None,) * len(groups), tuple(owners), offsets, subs, remote, reads, fused)
 
     def _replay_entry(self, b: PlanBuilder, ei: int, e: PlanEntry, tpl, group_rows: list, id_rows: list) -> None:
-        where, dts, tpl_k, n_tiles, groups, owners, offsets, subs, idrow, remote, reads, fused = tpl
+        where, dts, tpl_k, n_tiles, holes, owners, offsets, subs, remote, reads, fused = tpl
         fd0, rg0 = len(self.fused_digests), len(self.remote_groups)
         sides = (e.y, e.x)
         # a replayed entry's records are its own (shared records take the
@@ -642,22 +647,79 @@ class Plan:
         b.operands.extend([sides[side].groups[gi].records[ri] for side, gi, ri in where])
         b.operand_dtypes.extend(dts)
         tiles0, g0 = b.n_tiles, len(group_rows)
-        # the segments themselves are instantiated column-wise in _columns()
-        self._replays.append((tpl_k, op0, tiles0, fd0))
+        # segments, group rows and the id row are instantiated column-wise
+        # later (_columns, _fill_replayed_rows); here only their slots
+        self._replays.append((tpl_k, op0, tiles0, fd0, g0, len(id_rows)))
         if remote:
             self.remote_groups.extend((g0 + slot, ei, side, gi) for slot, side, gi in remote)
             self.compare_reads.extend((ei, gi, c) for gi, c in reads)
             self.fused_digests.extend((rg0 + k, c) for k, c in fused)
         b.n_tiles += n_tiles
-        if groups:
-            group_rows.extend((tiles0 + s0, tiles0 + s1, nz) for s0, s1, nz in groups)
-            self.group_owner.extend((ei, side, gi) for side, gi in owners)
+        if holes:
+            group_rows.extend(holes)
+            self._group_owner.extend(holes)           # (ei, side, gi) filled on demand (_owners)
+            self._owner_fill.append((g0, ei, owners))
             self.group_offset.extend(offsets)
             for k, v in subs.items():
                 self.subslots[g0 + k] = [g0 + j for j in v]
-        t0, t1, cg0, cg1, rg0, rg1, hc, ch, rh, pad = idrow
-        id_rows.append((tiles0 + t0, tiles0 + t1, g0 + cg0, g0 + cg1, g0 + rg0, g0 + rg1, hc, ch, rh, pad,
-                        float(e.tolerance)))
+        id_rows.append(None)
+        self._id_tol.append(e.tolerance)
+
+    _GROUP_DT = [("tile_begin", "<i8"), ("tile_end", "<i8"), ("nz", "<i4")]
+
+    def _fill_replayed_rows(self, id_rows: list, group_rows: list) -> None:
+        """self.ids / self.groups: the general path's rows as built, every
+        replayed entry's rows from its template, offset column-wise by the
+        entry's first tile / first group slot (per template, all replays at
+        once)."""
+        ids = np.zeros(len(id_rows), N.ID_DESC)
+        groups = np.zeros(len(group_rows), self._GROUP_DT)
+        gen_ids = [k for k, r in enumerate(id_rows) if r is not None]
+        if gen_ids:
+            ids[gen_ids] = np.array([id_rows[k] for k in gen_ids], N.ID_DESC)
+        gen_groups = [k for k, r in enumerate(group_rows) if r is not None]
+        if gen_groups:
+            groups[gen_groups] = np.array([group_rows[k] for k in gen_groups], self._GROUP_DT)
+        if self._replays:
+            rp = np.array(self._replays, np.int64)   # template, op0, tiles0, fd0, g0, id row
+            tol = np.array(self._id_tol, np.float64)
+            order = np.argsort(rp[:, 0], kind="stable")
+            for sel in np.split(order, np.flatnonzero(np.diff(rp[order, 0])) + 1):
+                k = int(rp[sel[0], 0])
+                t0, t1, cg0, cg1, rg0, rg1, hc, ch, rh, pad = self._tpl_ids[k]
+                tiles0, g0, row = rp[sel, 2], rp[sel, 4], rp[sel, 5]
+                ids["tile_begin"][row], ids["tile_end"][row] = tiles0 + t0, tiles0 + t1
+                ids["cgroup_begin"][row], ids["cgroup_end"][row] = g0 + cg0, g0 + cg1
+                ids["rgroup_begin"][row], ids["rgroup_end"][row] = g0 + rg0, g0 + rg1
+                ids["has_compare"][row], ids["cand_host"][row], ids["ref_host"][row] = hc, ch, rh
+                ids["pad"][row] = pad
+                ids["tolerance"][row] = tol[sel]
+                G = self._tpl_groups[k]
+                if len(G):
+                    slots = (g0[:, None] + np.arange(len(G))).reshape(-1)
+                    groups["tile_begin"][slots] = (tiles0[:, None] + G[:, 0]).reshape(-1)
+                    groups["tile_end"][slots] = (tiles0[:, None] + G[:, 1]).reshape(-1)
+                    groups["nz"][slots] = np.tile(G[:, 2], len(sel))
+        self.ids, self.groups = ids, groups
+
+    @property
+    def group_owner(self) -> list:
+        """(entry index, side, group index) per group slot."""
+        self._owners()
+        return self._group_owner
+
+    def _owners(self) -> None:
+        """Fill the (entry, side, group index) owners of replayed groups
+        (cached plans are shared across threads: the fill list is emptied
+        only once every owner is in place)."""
+        if not self._owner_fill:
+            return
+        with _OWNER_LOCK:
+            owner = self._group_owner
+            for g0, ei, owners in self._owner_fill:
+                for j, (side, gi) in enumerate(owners):
+                    owner[g0 + j] = (ei, side, gi)
+            self._owner_fill = []
 
     def _group_slots(self, b: PlanBuilder, group_rows: list, chunks: list, s0: int, yop, zall: list,
                      n: int, owner_key: tuple) -> None:
@@ -672,7 +734,7 @@ class Plan:
                 if yop is not None:
                     b.add(None, 0, yop, 0, zall[lo - 1:hi - 1], 1, n, n, n)
             group_rows.append((s0, b.tile_cursor, hi - lo))
-            self.group_owner.append(owner_key)
+            self._group_owner.append(owner_key)
             self.group_offset.append(lo - 1)
         if len(chunks) > 1:
             self.subslots[first] = list(range(first, len(group_rows)))
@@ -979,6 +1041,7 @@ class Plan:
 
 _ONE_SEG = os.environ.get("TD_ONE_SEG", "1") != "0"      # A/B switch for by-value single segments
 _STAGING_LOCK = threading.Lock()
+_OWNER_LOCK = threading.Lock()
 
 
 def _meta_key(meta):
@@ -1017,8 +1080,9 @@ def _shared_entries(entries) -> set:
     """Entries whose two sides hold the same record object (a trace checked
     against itself): operand de-duplication then differs from entry to entry,
     so they are planned without templates."""
-    xs = {id(r) for e in entries if e.x is not None for g in e.x.groups for r in g.records}
-    if xs.isdisjoint([id(r) for e in entries if e.y is not None for g in e.y.groups for r in g.records]):
+    chain = itertools.chain.from_iterable
+    xs = set(map(id, chain(g.records for e in entries if e.x is not None for g in e.x.groups)))
+    if xs.isdisjoint(map(id, chain(g.records for e in entries if e.y is not None for g in e.y.groups))):
         return set()            # the usual case: two distinct traces
     return {ei for ei, e in enumerate(entries)
             if e.y is not None and any(id(r) in xs for g in e.y.groups for r in g.records)}
