@@ -191,8 +191,10 @@ class CheckPlan:
         self.ref_view = merge_view(ref)
         self.cand_view = merge_view(cand)
         self.common = [i for i in self.cand_view if i in self.ref_view]
+        disjoint = set(map(id, ref.records)).isdisjoint(map(id, cand.records))
         self.plan = Plan([PlanEntry(i, x=self.ref_view[i], y=self.cand_view[i], x_rep=True,
-                                    y_rep=True, tolerance=tol.get(i)) for i in self.common])
+                                    y_rep=True, tolerance=tol.get(i)) for i in self.common],
+                         disjoint=disjoint)
         self.mode = str(cand.header.get("mode", ""))
 
     @property
@@ -229,8 +231,7 @@ class CheckPlan:
         sources = [pos[id(o)] for o in self.plan.operands]
         for view in (self.ref_view, self.cand_view):
             for meta in view.values():
-                for g in meta.groups:
-                    g.records = [None] * len(g.records)
+                meta.drop_records()
         self.plan.operands[:] = [None] * len(self.plan.operands)
         self.ref = self.cand = None
         return sources
@@ -475,8 +476,7 @@ def _forget_payloads(view, plan: Plan, keep_ids) -> None:
     """Drop a sample trace's record references from a cached view / plan
     (the cached path re-binds operands by position and reads only metadata)."""
     for meta in view.values():
-        for g in meta.groups:
-            g.records = [None] * len(g.records)
+        meta.drop_records()
     plan.operands[:] = [o if id(o) in keep_ids else None for o in plan.operands]
 
 

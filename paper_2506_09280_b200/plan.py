@@ -92,15 +92,62 @@ class GroupMeta:
     numeric: bool                 # copies need the device rel_err check
 
 
-@dataclass
 class IdMeta:
-    ident: str
-    exec_index: int
-    groups: list = field(default_factory=list)
-    global_shape: tuple | None = None
-    rank_problem: bool = False
-    merge_detail: str | None = None
-    struct_key: int | None = None     # interned merge_view structure (copy signatures, sizes, dtypes)
+    """Merge metadata of one id: its shard groups (copies of one shard) and
+    problems.  merge_view's template path leaves `groups` lazy — (trace
+    records, the id's record positions, the structure's group template) —
+    until something reads them: the planner's replay takes records straight
+    from the template (record_at) and only problem ids are ever detailed."""
+
+    __slots__ = ("ident", "exec_index", "global_shape", "rank_problem", "merge_detail", "struct_key",
+                 "_groups", "_lazy")
+
+    def __init__(self, ident: str, exec_index: int, groups: list | None = None,
+                 global_shape: tuple | None = None, rank_problem: bool = False,
+                 merge_detail: str | None = None, struct_key: int | None = None):
+        self.ident, self.exec_index = ident, exec_index
+        self.global_shape, self.rank_problem, self.merge_detail = global_shape, rank_problem, merge_detail
+        self.struct_key = struct_key          # interned merge_view structure (copy signatures, sizes, dtypes)
+        self._groups = [] if groups is None else groups
+        self._lazy = None                     # (records, positions, [(idx, declared detail, numeric)])
+
+    @property
+    def groups(self) -> list:
+        lazy = self._lazy
+        if lazy is not None:
+            recs, ks, tgroups = lazy
+            self._groups = [GroupMeta(records=[None if recs is None else recs[ks[k]] for k in idx],
+                                      declared_detail=d, numeric=num) for idx, d, num in tgroups]
+            self._lazy = None
+        return self._groups
+
+    @groups.setter
+    def groups(self, value: list) -> None:
+        self._groups, self._lazy = value, None
+
+    def record_at(self, gi: int, ri: int):
+        """groups[gi].records[ri] without materialising the groups."""
+        lazy = self._lazy
+        if lazy is None:
+            return self._groups[gi].records[ri]
+        recs, ks, tgroups = lazy
+        return recs[ks[tgroups[gi][0][ri]]]
+
+    def all_records(self):
+        """Every record of the id's groups (any order)."""
+        lazy = self._lazy
+        if lazy is not None and lazy[0] is not None:
+            recs = lazy[0]
+            return [recs[k] for k in lazy[1]]
+        return itertools.chain.from_iterable(g.records for g in self._groups)
+
+    def drop_records(self) -> None:
+        """Forget the trace's records (cached plans keep metadata only)."""
+        if self._lazy is not None:
+            self._lazy = (None, self._lazy[1], self._lazy[2])
+        else:
+            for g in self._groups:
+                g.records = [None] * len(g.records)
 
     @property
     def merge_ok(self) -> bool:
@@ -108,10 +155,19 @@ class IdMeta:
 
     @property
     def declared_problem(self) -> str | None:
-        for g in self.groups:
+        if self._lazy is not None:
+            for _, d, _ in self._lazy[2]:
+                if d is not None:
+                    return d
+            return None
+        for g in self._groups:
             if g.declared_detail is not None:
                 return g.declared_detail
         return None
+
+    def __repr__(self) -> str:
+        return (f"IdMeta(ident={self.ident!r}, exec_index={self.exec_index}, global_shape={self.global_shape}, "
+                f"groups={len(self.groups)})")
 
 
 def id_meta(ident: str, entries: list, replica_check: bool = True) -> IdMeta:
@@ -176,7 +232,8 @@ def merge_view(trace, replica_check: bool = True) -> dict[str, IdMeta]:
     from .tracestore import Trace
     ext = N.host_ext()
     if _TEMPLATES and ext is not None and type(trace).by_id is Trace.by_id:
-        return _merge_view_grouped(trace, ext.group_by_id(trace.records), replica_check)
+        recs = list(trace.records)       # the lazy metas resolve positions against this snapshot
+        return _merge_view_grouped(recs, ext.group_by_id(recs), replica_check)
     view = {}
     memo: dict | None = {} if _TEMPLATES else None
     for ident, entries in trace.by_id().items():
@@ -207,11 +264,11 @@ def merge_view(trace, replica_check: bool = True) -> dict[str, IdMeta]:
     return view
 
 
-def _merge_view_grouped(trace, grouped, replica_check: bool) -> dict[str, IdMeta]:
+def _merge_view_grouped(recs: list, grouped, replica_check: bool) -> dict[str, IdMeta]:
     """merge_view's template path over _td_host.group_by_id's output (ids in
     first-appearance order, their record positions, their structure keys):
-    the same metadata, without the per-record Python walks."""
-    recs = trace.records
+    the same metadata, without the per-record Python walks; ids that repeat
+    a structure keep their groups lazy (IdMeta.groups)."""
     view = {}
     memo: dict = {}
     for ident, ks, key in zip(*grouped):
@@ -229,8 +286,7 @@ def _merge_view_grouped(trace, grouped, replica_check: bool) -> dict[str, IdMeta
             rank_problem, hull, detail, groups, _ = hit
             meta = view[ident] = IdMeta(ident=ident, exec_index=ks[0], global_shape=hull,
                                         rank_problem=rank_problem, merge_detail=detail)
-            meta.groups = [GroupMeta(records=[recs[ks[k]] for k in idx], declared_detail=d, numeric=num)
-                           for idx, d, num in groups]
+            meta._lazy = (recs, ks, groups)
         meta.struct_key = hit[4]
     return view
 
@@ -424,7 +480,8 @@ class Plan:
 
     @gc_paused
     def __init__(self, entries: list[PlanEntry], static: tuple[float, float] | None = None,
-                 owner=None, me: int = 0, compare_copy: dict | None = None, digest: bool = False):
+                 owner=None, me: int = 0, compare_copy: dict | None = None, digest: bool = False,
+                 disjoint: bool = False):
         """static=(atol, rtol) builds compare_static's plan: the elementwise
         failure count replaces d2 (generic walker, no replica checks).
 
@@ -471,7 +528,8 @@ class Plan:
         #                            id row) per replayed entry
         self._id_tol = []         # tolerance per replayed entry, replay order
         self._owner_fill = []     # (first group slot, entry, ((side, group index), ...)) per replay
-        shared = _shared_entries(entries) if templates is not None else set()
+        # disjoint: the caller knows the two sides hold no record in common
+        shared = _shared_entries(entries) if templates is not None and not disjoint else set()
         for ei, e in enumerate(entries):
             if templates is None:
                 self._plan_entry(b, ei, e, group_rows, id_rows, owner, is_local, compare_copy, digest, static)
@@ -644,7 +702,7 @@ class Plan:
         # general path, _shared_entries), so its operands need no
         # de-duplication entry: they are appended as one block
         op0 = len(b.operands)
-        b.operands.extend([sides[side].groups[gi].records[ri] for side, gi, ri in where])
+        b.operands.extend([sides[side].record_at(gi, ri) for side, gi, ri in where])
         b.operand_dtypes.extend(dts)
         tiles0, g0 = b.n_tiles, len(group_rows)
         # segments, group rows and the id row are instantiated column-wise
@@ -1081,8 +1139,8 @@ def _shared_entries(entries) -> set:
     against itself): operand de-duplication then differs from entry to entry,
     so they are planned without templates."""
     chain = itertools.chain.from_iterable
-    xs = set(map(id, chain(g.records for e in entries if e.x is not None for g in e.x.groups)))
-    if xs.isdisjoint(map(id, chain(g.records for e in entries if e.y is not None for g in e.y.groups))):
+    xs = set(map(id, chain(e.x.all_records() for e in entries if e.x is not None)))
+    if xs.isdisjoint(map(id, chain(e.y.all_records() for e in entries if e.y is not None))):
         return set()            # the usual case: two distinct traces
     return {ei for ei, e in enumerate(entries)
             if e.y is not None and any(id(r) in xs for g in e.y.groups for r in g.records)}
