@@ -877,11 +877,13 @@ class Plan:
         `groups_chunked` carry chunk ranges in place of tile ranges.  Sets
         self.chunks = None when one level suffices."""
         W = N.WARPS_PER_TILE
-        spans = [(int(tb) * W, int(te) * W, 0, 2) for tb, te in zip(self.ids["tile_begin"], self.ids["tile_end"])]
-        spans += [(int(tb) * W, int(te) * W, 2, 1 + int(nz)) for tb, te, nz in
-                  zip(self.groups["tile_begin"], self.groups["tile_end"], self.groups["nz"])]
+        rb = np.concatenate([self.ids["tile_begin"], self.groups["tile_begin"]]).astype(np.int64) * W
+        re = np.concatenate([self.ids["tile_end"], self.groups["tile_end"]]).astype(np.int64) * W
+        n_ids = len(self.ids)
+        k0 = np.repeat(np.array([0, 2], np.int32), [n_ids, len(self.groups)])
+        nk = np.concatenate([np.full(n_ids, 2, np.int32), 1 + self.groups["nz"].astype(np.int32)])
         self.chunks = None
-        longest = max((re - rb for rb, re, _, _ in spans), default=0)
+        longest = int((re - rb).max()) if len(rb) else 0
         if longest < self.CHUNK_MIN_ROWS:
             return
         # chunks of CHUNK_ROWS for big slots; for mid-size plans (a few k rows,
@@ -889,20 +891,23 @@ class Plan:
         # longest slot spreads over ~32 CTAs instead of one
         step = self.CHUNK_ROWS if longest >= 32 * self.CHUNK_ROWS else \
             min(self.CHUNK_ROWS, max(256, 1 << max(0, (longest // 32 - 1).bit_length())))
-        rows, ranges = [], []
-        for rb, re, k0, nk in spans:
-            c0 = len(rows)
-            rows.extend((r, min(r + step, re), k0, nk) for r in range(rb, re, step))
-            ranges.append((c0, len(rows)))
-        self.chunks = np.array(rows, dtype=N.CHUNK) if rows else np.zeros(0, N.CHUNK)
-        ranges = np.array(ranges, np.int64).reshape(-1, 2)
-        n_ids = len(self.ids)
+        # slot j -> chunks [c0[j], c1[j]) covering rows rb[j], rb[j]+step, ... < re[j]
+        count = np.maximum(0, -(-(re - rb) // step))
+        c1 = np.cumsum(count)
+        c0 = c1 - count
+        owner = np.repeat(np.arange(len(rb)), count)
+        r0 = rb[owner] + (np.arange(int(c1[-1]) if len(c1) else 0, dtype=np.int64) - c0[owner]) * step
+        chunks = np.zeros(len(r0), N.CHUNK)
+        names = chunks.dtype.names
+        chunks[names[0]], chunks[names[1]] = r0, np.minimum(r0 + step, re[owner])
+        chunks[names[2]], chunks[names[3]] = k0[owner], nk[owner]
+        self.chunks = chunks
         self.ids_chunked = self.ids.copy()
-        self.ids_chunked["tile_begin"], self.ids_chunked["tile_end"] = ranges[:n_ids, 0], ranges[:n_ids, 1]
+        self.ids_chunked["tile_begin"], self.ids_chunked["tile_end"] = c0[:n_ids], c1[:n_ids]
         self.groups_chunked = self.groups.copy()
         if len(self.groups):
-            self.groups_chunked["tile_begin"] = ranges[n_ids:, 0]
-            self.groups_chunked["tile_end"] = ranges[n_ids:, 1]
+            self.groups_chunked["tile_begin"] = c0[n_ids:]
+            self.groups_chunked["tile_end"] = c1[n_ids:]
 
     # -- geometry -------------------------------------------------------------
 
@@ -1041,11 +1046,14 @@ class Plan:
         self.seg_xslot, self.seg_xoff = x_slot, np.where(has_x, xo * x_es, 0)
         self.seg_yslot, self.seg_yoff = y_slot, yo * y_es
         nt = -(-nu // self.tile_units)
-        tile_seg = np.zeros(self.n_tiles, np.int32)
         seg_of_tile = np.repeat(np.arange(n, dtype=np.int32), nt)
-        first = np.repeat(tb - np.concatenate([[0], np.cumsum(nt)[:-1]]), nt)
-        tiles = first + np.arange(len(seg_of_tile), dtype=i64)     # tile index of each (segment, k)
-        tile_seg[tiles] = seg_of_tile
+        starts = np.concatenate([[0], np.cumsum(nt)[:-1]])
+        if len(seg_of_tile) == self.n_tiles and np.array_equal(tb, starts):
+            tile_seg = seg_of_tile                 # tiles handed out back to back (always, today)
+        else:
+            tile_seg = np.zeros(self.n_tiles, np.int32)
+            tiles = np.repeat(tb - starts, nt) + np.arange(len(seg_of_tile), dtype=i64)
+            tile_seg[tiles] = seg_of_tile
         # tile classes: (vector, y dtype, nz, has x, digest), sorted as tuples
         # packed one field per byte (every field < 256), so integer order is
         # the tuples' order
