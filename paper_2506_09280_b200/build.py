@@ -79,7 +79,10 @@ def build_host(force: bool = False, verbose: bool = False) -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    build_host(force=force, verbose=verbose)
+    try:
+        build_host(force=force, verbose=verbose)
+    except Exception as exc:       # optional module: the Python walks stand in for it
+        print(f"warning: _td_host not built ({exc}); the Python record walks will be used", file=sys.stderr)
     if not force and not needs_build():
         return OUTPUT
     tmp = OUTPUT + ".tmp"
